@@ -1,0 +1,260 @@
+/* ldgmg_b200.h -- C ABI of the B200-native multigrid V-cycle core.
+ *
+ * Drop-in boundary for the FP64 block-sparse hot path of the reference
+ * (`ldgmg`, arXiv 2412.12506, /root/reference/proj/include/ldgmg/).  The
+ * reference has no FFI: its "operator API" is the header-only C++ surface in
+ * blockla.hpp / smoothers.hpp / multigrid.hpp.  Every entry point below
+ * replaces one of those functions; the replaced signature is cited per entry.
+ * The C++ wrapper include/ldgmg_b200.hpp re-exposes them with the reference
+ * class names (ldgmg::gpu::{BlockCsr,Smoother,Multigrid}) and maps the status
+ * codes back to the reference's exception types.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or CUDA types in signatures
+ *    (streams are passed as void* = cudaStream_t).
+ *  - Host arrays use the reference layouts: BlockCsr ptr/col int32, blocks
+ *    row-major (inc/blockla.hpp:73-92); vectors element-major (BlockVec::data,
+ *    inc/blockla.hpp:46-58).
+ *  - Functions taking `const double* x` / `double* y` without a _host suffix
+ *    take DEVICE pointers on the context's device; work is enqueued on the
+ *    context stream (asynchronous unless stated).
+ *  - Every function returns LDGMG_OK or an error code; ldgmg_last_error()
+ *    returns the thread-local message, which repeats the reference's exception
+ *    text where one exists (e.g. "spmv: shape mismatch", blockla.hpp:137).
+ *  - No CPU fallback: without a visible CUDA device every compute entry point
+ *    fails with LDGMG_ERR_CUDA.
+ */
+#ifndef LDGMG_B200_H
+#define LDGMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LDGMG_B200_ABI_VERSION 1
+
+/* status codes -> reference exception types (include/ldgmg_b200.hpp) */
+#define LDGMG_OK 0
+#define LDGMG_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument */
+#define LDGMG_ERR_RUNTIME 2          /* std::runtime_error    */
+#define LDGMG_ERR_LOGIC 3            /* std::logic_error      */
+#define LDGMG_ERR_CUDA 4             /* device / driver failure, no device */
+#define LDGMG_ERR_NCCL 5             /* collective failure */
+
+/* enum values mirror the reference enums */
+enum { LDGMG_SWEEP_FORWARD = 0, LDGMG_SWEEP_REVERSE = 1 };               /* smoothers.hpp:19 */
+enum { LDGMG_JACOBI = 0, LDGMG_COLOURED_GS = 1, LDGMG_PROC_BLOCK_GS = 2, /* smoothers.hpp:21 */
+       LDGMG_SAI = 3 };
+enum { LDGMG_SYSTEM_SCALAR = 0, LDGMG_SYSTEM_STOKES = 1 };              /* ldg_core.hpp:40 */
+enum { LDGMG_BC_PERIODIC = 0, LDGMG_BC_DIRICHLET = 1, LDGMG_BC_NEUMANN = 2 }; /* mesh.hpp:28 */
+enum { LDGMG_PHASE_SINGLE = 0, /* one phase (PhaseGeometry::single)                        */
+       LDGMG_PHASE_BOXES = 1,  /* inner box (lo,hi) + background (harness.hpp:58-64)       */
+       LDGMG_PHASE_BALL = 2,   /* centroid inside ball/ellipse (extension A2, re-tested on  */
+       LDGMG_PHASE_ELLIPSE = 3 /*   every level)                              */
+};
+
+/* SmootherConfig (smoothers.hpp:23-58) */
+typedef struct ldgmg_smoother_config {
+    int kind;       /* LDGMG_JACOBI ... LDGMG_SAI */
+    double omega;   /* damping; coloured GS always runs undamped */
+    int partitions; /* processor-block GS only */
+    int level;      /* SAI pattern power */
+    double zeta;    /* SAI pressure balance weight */
+    int cache;      /* SAI least-squares dedupe (bitwise transparent) */
+} ldgmg_smoother_config;
+
+/* MultigridConfig (multigrid.hpp:26-36) */
+typedef struct ldgmg_mg_config {
+    ldgmg_smoother_config smoother;
+    int pre, post; /* LDGMG_SWEEP_* */
+    int nu1, nu2;
+    int bottom_max_elements;
+    double bottom_tol;
+    int min_depth;
+} ldgmg_mg_config;
+
+/* SaiStats (smoothers.hpp:132-138) */
+typedef struct ldgmg_sai_stats {
+    int rank_deficient_columns;
+    int64_t cache_hits, cache_misses;
+    int n_shapes;        /* distinct (row blocks, col blocks) local LS shapes */
+    int shape_rows[8];   /* first 8 shapes, ascending like std::map */
+    int shape_cols[8];
+    int shape_count[8];
+} ldgmg_sai_stats;
+
+/* Problem description for the built-in host setup (mesh chain + LDG assembly
+ * per level).  Mirrors harness.hpp:30-40 plus the BASELINE config knobs.     */
+typedef struct ldgmg_problem_spec {
+    int kind;          /* LDGMG_SYSTEM_SCALAR / _STOKES */
+    int dim;           /* 2 or 3 */
+    int n;             /* elements per axis (power of two) */
+    int degree;        /* polynomial degree p */
+    int bc[6];         /* per side 2*axis+{0 lower,1 upper}: LDGMG_BC_* */
+    double beta;       /* <=0: 4 p^2 (library default, ldg_core.hpp:101) */
+    double beta_p;     /* Stokes pressure penalty scale */
+    double gamma;      /* Stokes form: 0 standard, 1 stress */
+    double delta;      /* Stokes time step; <=0 steady */
+    int phase_shape;   /* LDGMG_PHASE_* */
+    double center[3];  /* ball/ellipse centre, or box lo */
+    double radii[3];   /* ball radius in radii[0] / ellipse semi-axes, or box hi */
+    double mu_in, mu_out, rho_in, rho_out;
+} ldgmg_problem_spec;
+
+typedef struct ldgmg_ctx ldgmg_ctx;
+typedef struct ldgmg_bsr ldgmg_bsr;
+typedef struct ldgmg_smoother ldgmg_smoother;
+typedef struct ldgmg_transfer ldgmg_transfer;
+typedef struct ldgmg_mg ldgmg_mg;
+typedef struct ldgmg_problem ldgmg_problem;
+
+/* ------------------------------------------------------------------ misc */
+const char* ldgmg_last_error(void);
+int ldgmg_abi_version(void);
+/* Number of kernel launches this process issued (all contexts); counter for
+ * bench.py's gpu_launches claim. */
+int64_t ldgmg_launch_count(void);
+
+/* --------------------------------------------------------------- context */
+int ldgmg_ctx_create(int device, ldgmg_ctx** out);
+int ldgmg_ctx_destroy(ldgmg_ctx* ctx);
+int ldgmg_ctx_set_stream(ldgmg_ctx* ctx, void* cuda_stream);
+void* ldgmg_ctx_stream(ldgmg_ctx* ctx);
+int ldgmg_ctx_synchronize(ldgmg_ctx* ctx);
+/* device scratch helpers for C callers without their own allocator */
+int ldgmg_device_alloc(ldgmg_ctx* ctx, size_t bytes, void** ptr);
+int ldgmg_device_free(ldgmg_ctx* ctx, void* ptr);
+int ldgmg_copy_h2d(ldgmg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int ldgmg_copy_d2h(ldgmg_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ------------------------------------------------------------ BSR (L1)
+ * replaces BlockCsr (inc/blockla.hpp:73-92) / BlockBuilder::freeze (:113-132) */
+int ldgmg_bsr_upload(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int col_bs,
+                     const int* ptr, const int* col, const double* val, ldgmg_bsr** out);
+int ldgmg_bsr_shape(const ldgmg_bsr* A, int* brows, int* bcols, int* row_bs, int* col_bs,
+                    int64_t* nnzb);
+/* download back to the reference layout (row-major blocks) */
+int ldgmg_bsr_download(ldgmg_ctx* ctx, const ldgmg_bsr* A, int* ptr, int* col, double* val);
+/* bytes of device memory the operator occupies (values + indices) */
+int64_t ldgmg_bsr_device_bytes(const ldgmg_bsr* A);
+int ldgmg_bsr_destroy(ldgmg_bsr* A);
+
+/* replaces spmv(const BlockCsr&, const BlockVec&, BlockVec&)  blockla.hpp:136-154 */
+int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
+/* replaces spmv_transpose(...)                                 blockla.hpp:157-176 */
+int ldgmg_spmv_transpose(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
+/* r = b - A x (multigrid.hpp:256-258, smoothers.hpp:439-440), fused */
+int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const double* x,
+                   double* r);
+/* BLAS-1 (blockla.hpp:60-71); dot/norm write one double to *out_host (synchronous) */
+int ldgmg_dot(ldgmg_ctx* ctx, int64_t n, const double* a, const double* b, double* out_host);
+int ldgmg_axpy(ldgmg_ctx* ctx, int64_t n, double alpha, const double* x, double* y);
+
+/* ------------------------------------------------------- smoothers (L3)
+ * replaces Smoother(const System&, const SmootherConfig&, SaiCache*)
+ * (smoothers.hpp:377-404).  `system_kind`/`n_velocity` carry the System
+ * fields the smoother reads (ldg_core.hpp:44-59).  Setup (diagonal factors,
+ * colouring, SAI least squares) runs on the GPU. */
+int ldgmg_smoother_create(ldgmg_ctx* ctx, const ldgmg_bsr* A, int system_kind, int n_velocity,
+                          const ldgmg_smoother_config* cfg, ldgmg_smoother** out);
+/* Drop-in variants: adopt setup computed by the caller's reference objects
+ * (factor_diagonal smoothers.hpp:464-494 / build_sai :259-367), host arrays. */
+int ldgmg_smoother_create_with_factors(ldgmg_ctx* ctx, const ldgmg_bsr* A,
+                                       const ldgmg_smoother_config* cfg, const double* V,
+                                       const double* lambda, const double* s,
+                                       ldgmg_smoother** out);
+int ldgmg_smoother_create_with_sai(ldgmg_ctx* ctx, const ldgmg_bsr* A,
+                                   const ldgmg_smoother_config* cfg, const int* Bptr,
+                                   const int* Bcol, const double* Bval, ldgmg_smoother** out);
+/* replaces Smoother::apply(const BlockVec& b, BlockVec& x, Sweep)  smoothers.hpp:406-450 */
+int ldgmg_smoother_apply(ldgmg_ctx* ctx, const ldgmg_smoother* S, const double* b, double* x,
+                         int sweep);
+/* accessors: colours() / n_colours() / sai_matrix() / sai_stats() (smoothers.hpp:452-461) */
+int ldgmg_smoother_colours(const ldgmg_smoother* S, int* colour /* N or NULL */, int* ncolours);
+int ldgmg_smoother_sai_nnzb(const ldgmg_smoother* S, int64_t* nnzb);
+int ldgmg_smoother_sai_matrix(ldgmg_ctx* ctx, const ldgmg_smoother* S, int* ptr, int* col,
+                              double* val);
+int ldgmg_smoother_sai_stats(const ldgmg_smoother* S, ldgmg_sai_stats* out);
+/* per-element diagonal factors V (bs*bs, column-major like Eigen), lambda, s */
+int ldgmg_smoother_diag_factors(ldgmg_ctx* ctx, const ldgmg_smoother* S, double* V,
+                                double* lambda, double* s);
+int ldgmg_smoother_destroy(ldgmg_smoother* S);
+
+/* ---------------------------------------------------- transfers (L4)
+ * parent_of/orthant_of from coarsen() (mesh.hpp:412-457); K = the 2^dim
+ * injection matrices of build_injection() (multigrid.hpp:212-241), each
+ * bs_scalar x bs_scalar row-major. */
+int ldgmg_transfer_create(ldgmg_ctx* ctx, int n_fine, int n_coarse, const int* parent_of,
+                          const int* orthant_of, int dim, int bs_scalar, int n_comp,
+                          const double* K, ldgmg_transfer** out);
+/* replaces Multigrid::restrict_residual (multigrid.hpp:127-149); rc overwritten */
+int ldgmg_restrict(ldgmg_ctx* ctx, const ldgmg_transfer* T, const double* rf, double* rc);
+/* replaces Multigrid::interpolate_add (multigrid.hpp:104-123) */
+int ldgmg_interpolate_add(ldgmg_ctx* ctx, const ldgmg_transfer* T, const double* xc, double* xf);
+int ldgmg_transfer_destroy(ldgmg_transfer* T);
+
+/* ------------------------------------------------- multigrid hierarchy
+ * replaces Multigrid(Mesh, const LevelAssembler&, MultigridConfig)
+ * (multigrid.hpp:49-65) given the already assembled level operators.
+ * A[l] for l < depth; transfers[l] for l < depth-1.  kernel_* are the System
+ * flags of level 0 (ldg_core.hpp:52-53).  When bottom_V/bottom_lambda are NULL
+ * the bottom eigendecomposition is computed on the GPU. */
+int ldgmg_mg_create(ldgmg_ctx* ctx, int depth, const ldgmg_bsr* const* A,
+                    const ldgmg_transfer* const* transfers, int system_kind, int dim, int n_comp,
+                    int bs_scalar, int kernel_constants, int kernel_pressure,
+                    const ldgmg_mg_config* cfg, const double* bottom_V,
+                    const double* bottom_lambda, ldgmg_mg** out);
+/* Adopt per-level drop-in smoothers instead of building them (optional). */
+int ldgmg_mg_set_smoother(ldgmg_mg* mg, int level, ldgmg_smoother* S);
+int ldgmg_mg_smoother(ldgmg_mg* mg, int level, ldgmg_smoother** out);
+int ldgmg_mg_depth(const ldgmg_mg* mg);
+/* replaces Multigrid::cycle(BlockVec& x, const BlockVec& b)  multigrid.hpp:82-85 */
+int ldgmg_mg_cycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b);
+/* replaces Multigrid::apply(const BlockVec& b) -> x           multigrid.hpp:90-101 */
+int ldgmg_mg_apply(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b, double* x);
+/* Run `ncycles` V-cycles (graph-captured after the first call); x in place. */
+int ldgmg_mg_cycles(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b, int ncycles);
+/* Stationary V-cycle solve from HOST buffers (the end-to-end path):
+ * x = 0; repeat cycle until ||b-Ax||/||b|| <= tol or maxit; residual history
+ * (relative, one entry per iteration incl. iteration 0) to `history` (maxit+1
+ * doubles, may be NULL).  Returns iterations in *iters. */
+int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, double* x_host,
+                        double tol, int maxit, double* history, int* iters);
+/* algorithmic DOF-updates and HBM bytes of one V-cycle */
+int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes);
+int ldgmg_mg_destroy(ldgmg_mg* mg);
+
+/* --------------------------------------- built-in host setup (L0/L2)
+ * The product's own mesh chain + LDG assembly (the reference's
+ * build_uniform/coarsen/assemble_scalar/assemble_stokes, mesh.hpp,
+ * ldg_scalar.hpp:83-125, ldg_stokes.hpp:102-280) so the framework runs
+ * standalone.  Host C++, multi-threaded. */
+int ldgmg_problem_create(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements,
+                         ldgmg_problem** out);
+int ldgmg_problem_depth(const ldgmg_problem* P);
+int ldgmg_problem_level_shape(const ldgmg_problem* P, int level, int* n_elements, int* bs,
+                              int64_t* nnzb);
+int ldgmg_problem_level_matrix(const ldgmg_problem* P, int level, int* ptr, int* col,
+                               double* val);
+int ldgmg_problem_level_transfer(const ldgmg_problem* P, int level, int* parent_of,
+                                 int* orthant_of);
+int ldgmg_problem_info(const ldgmg_problem* P, int* dim, int* n_comp, int* bs_scalar,
+                       int* kernel_constants, int* kernel_pressure, int* n_velocity);
+int ldgmg_problem_injection(const ldgmg_problem* P, double* K);
+/* upload the whole hierarchy and build a GPU multigrid in one call */
+int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P,
+                                 const ldgmg_mg_config* cfg, ldgmg_mg** out);
+int ldgmg_problem_destroy(ldgmg_problem* P);
+
+/* seeded measurement right-hand side: random_rhs (krylov.hpp:279-287),
+ * mt19937_64, u = (rng()>>11)*2^-53, v = 2u-1, host buffer */
+int ldgmg_random_rhs(int nblocks, int bs, uint64_t seed, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LDGMG_B200_H */
