@@ -223,6 +223,9 @@ int ldgmg_mg_cycles(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b, in
  * doubles, may be NULL).  Returns iterations in *iters. */
 int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, double* x_host,
                         double tol, int maxit, double* history, int* iters);
+/* 1: kernel projection dots in the reference's sequential order (bitwise
+ * parity mode); 0 (default): fixed-shape deterministic tree reduction. */
+int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict);
 /* algorithmic DOF-updates and HBM bytes of one V-cycle */
 int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes);
 int ldgmg_mg_destroy(ldgmg_mg* mg);

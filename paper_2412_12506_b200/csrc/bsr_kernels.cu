@@ -1,0 +1,477 @@
+// BSR storage and the streaming row-pass kernel: the HBM-bound hot loop of
+// every operator application in the V-cycle.
+//
+// One "row group" (= one CTA of G warps, lane r <-> output row r of the block
+// row) walks a persistent, grid-strided list of block rows.  The matrix
+// blocks of those rows are streamed into a ring of shared-memory stages with
+// TMA 1-D bulk copies (cp.async.bulk + mbarrier complete_tx); the matching
+// x-blocks are gathered into per-stage slots with cp.async whose completion
+// is folded into the same mbarrier.  NS items are always in flight per group,
+// so HBM sees long contiguous bulk reads while the FP64 pipe does the dot
+// products out of conflict-free shared memory.
+//
+// Arithmetic order is the reference's, bit for bit (compiled without FMA
+// contraction; every multiply-add here is an explicit __dmul_rn/__dadd_rn):
+//   spmv:      y_i[r] = 0 + s_k1 + s_k2 + ...,  s_k = 0 + b[r,0]x[0] + b[r,1]x[1] + ...
+//              (blockla.hpp:141-153), blocks in CSR (ascending column) order;
+//   residual:  b - (A x)   (multigrid.hpp:256-258);
+//   add:       x + (B r)   (smoothers.hpp:441-446, axpy with alpha = 1);
+//   relax:     r = ((b - s_k1) - s_k2) - ... over off-diagonal blocks, then
+//              y = s o V diag(1/lambda, cut) V^T (s o r), x = (1-w) x + w y
+//              (smoothers.hpp:496-518 with pinv_apply blockla.hpp:330-339 and
+//              the Eigen-shim product order, oracle/shim/Eigen/Dense).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "core.hpp"
+
+namespace ldgmg_b200 {
+
+namespace {
+
+struct RowPassArgs {
+    const int* ptr;
+    const int* col;
+    const double* val;
+    int blk_stride;
+    int rbs, cbs;
+    int mode;
+    const double* x;
+    const double* b;
+    const double* xe;
+    double* y;
+    const int* rows;
+    int nrows;
+    const double* V;
+    const double* lam;
+    const double* scal;
+    const double* lmax;
+    int ld, vstride;
+    double omega, kernel_tol;
+    int nstages, stage_doubles, xslot_doubles;
+};
+
+struct ItemIt {
+    int m;     // row slot
+    int row;   // current row, -1 when exhausted
+    int k, kend;
+    int vdone;
+};
+
+__device__ __forceinline__ int row_at(const RowPassArgs& a, int slot) {
+    return a.rows ? __ldg(a.rows + slot) : slot;
+}
+
+__device__ __forceinline__ void it_load(const RowPassArgs& a, ItemIt& it, int g, int ng) {
+    const int slot = g + it.m * ng;
+    if (slot >= a.nrows) {
+        it.row = -1;
+        return;
+    }
+    it.row = row_at(a, slot);
+    it.k = __ldg(a.ptr + it.row);
+    it.kend = __ldg(a.ptr + it.row + 1);
+    it.vdone = 0;
+}
+
+/// Next item of the group's stream: kind 0 = matrix block `idx`, kind 1 =
+/// diagonal factor V of element `idx`.  Identical on every thread.
+__device__ __forceinline__ bool it_next(const RowPassArgs& a, ItemIt& it, int g, int ng,
+                                        int& kind, int& idx) {
+    for (;;) {
+        if (it.row < 0) return false;
+        if (a.mode == MODE_RELAX)
+            while (it.k < it.kend && __ldg(a.col + it.k) == it.row) ++it.k;
+        if (it.k < it.kend) {
+            kind = 0;
+            idx = it.k++;
+            return true;
+        }
+        if (a.mode == MODE_RELAX && !it.vdone) {
+            it.vdone = 1;
+            kind = 1;
+            idx = it.row;
+            return true;
+        }
+        ++it.m;
+        it_load(a, it, g, ng);
+    }
+}
+
+template <int GT>
+__device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int st,
+                                           double* stages, double* xslots, uint64_t* bars) {
+    const int t = threadIdx.x;
+    double* xs = xslots + size_t(st) * a.xslot_doubles;
+    if (t < a.cbs) {
+        if (kind == 0) {
+            const double* src = a.x + size_t(__ldg(a.col + idx)) * a.cbs + t;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(xs + t)),
+                         "l"(src)
+                         : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         smem_addr(bars + st))
+                     : "memory");
+    }
+    if (t == 0) {
+        const double* src;
+        uint32_t bytes;
+        if (kind == 0) {
+            src = a.val + size_t(idx) * a.blk_stride;
+            bytes = uint32_t(a.blk_stride) * 8u;
+        } else {
+            src = a.V + size_t(idx) * a.vstride;
+            bytes = uint32_t(a.vstride) * 8u;
+        }
+        mbar_arrive_expect_tx(bars + st, bytes);
+        bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
+    }
+}
+
+template <int GT>
+__global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    double* xslots = stages + size_t(a.nstages) * a.stage_doubles;
+    double* ubuf = xslots + size_t(a.nstages) * a.xslot_doubles;
+    double* tbuf = ubuf + a.xslot_doubles;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + a.xslot_doubles);
+
+    const int t = threadIdx.x;
+    const int g = blockIdx.x, ng = gridDim.x;
+    const int NS = a.nstages;
+
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1u + uint32_t(a.cbs));
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // producer iterator: runs NS items ahead of the consumer
+    ItemIt pit{0, -1, 0, 0, 0};
+    it_load(a, pit, g, ng);
+    int kind, idx;
+    for (int s = 0; s < NS; ++s) {
+        if (!it_next(a, pit, g, ng, kind, idx)) break;
+        issue_item<GT>(a, kind, idx, s, stages, xslots, bars);
+    }
+
+    uint32_t q = 0;  // items consumed
+    const bool relax = a.mode == MODE_RELAX;
+    for (int m = 0;; ++m) {
+        const int slot = g + m * ng;
+        if (slot >= a.nrows) break;
+        const int row = row_at(a, slot);
+        const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
+        const bool act = t < a.rbs;
+        // epilogue operands fetched early; their latency hides under the blocks
+        double pre_b = 0.0, pre_x = 0.0, pre_s = 0.0, pre_l = 0.0;
+        if (act) {
+            const size_t o = size_t(row) * a.rbs + t;
+            if (a.mode == MODE_RESIDUAL || relax) pre_b = __ldg(a.b + o);
+            if (a.mode == MODE_ADD || relax) pre_x = a.xe[o];
+            if (relax) {
+                pre_s = __ldg(a.scal + o);
+                pre_l = __ldg(a.lam + o);
+            }
+        }
+        double acc = relax ? pre_b : 0.0;
+        int k = k0;
+        bool vdone = !relax;
+        for (;;) {
+            if (relax)
+                while (k < k1 && __ldg(a.col + k) == row) ++k;
+            bool is_v;
+            if (k < k1)
+                is_v = false;
+            else if (!vdone)
+                is_v = true;
+            else
+                break;
+            const int st = int(q % uint32_t(NS));
+            const uint32_t ph = (q / uint32_t(NS)) & 1u;
+            mbar_wait(bars + st, ph);
+            const double* S = stages + size_t(st) * a.stage_doubles;
+            if (!is_v) {
+                const double* X = xslots + size_t(st) * a.xslot_doubles;
+                if (act) {
+                    double s = 0.0;
+                    const double* Bc = S + t;
+                    const int cbs = a.cbs, rbs = a.rbs;
+#pragma unroll 8
+                    for (int c = 0; c < cbs; ++c) s = madd_rn(s, Bc[size_t(c) * rbs], X[c]);
+                    acc = relax ? __dsub_rn(acc, s) : __dadd_rn(acc, s);
+                }
+                ++k;
+            } else {
+                // block-diagonal pseudoinverse solve with the staged factor V
+                const int bs = a.rbs, ld = a.ld;
+                if (act) ubuf[t] = __dmul_rn(pre_s, acc);
+                group_sync(1, GT);
+                if (act) {
+                    double tt = 0.0;
+                    const double* Vcol = S + size_t(t) * ld;  // V(:, t)
+#pragma unroll 8
+                    for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, Vcol[kk], ubuf[kk]);
+                    const double cut = a.kernel_tol * __ldg(a.lmax + row);
+                    tbuf[t] = fabs(pre_l) <= cut ? 0.0 : tt / pre_l;
+                }
+                group_sync(1, GT);
+                if (act) {
+                    double w = 0.0;
+#pragma unroll 8
+                    for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, S[size_t(kk) * ld + t], tbuf[kk]);
+                    const double yv = __dmul_rn(pre_s, w);
+                    const double om = a.omega;
+                    acc = __dadd_rn(__dmul_rn(1.0 - om, pre_x), __dmul_rn(om, yv));
+                }
+                vdone = true;
+            }
+            group_sync(1, GT);  // every lane is done with this stage
+            ++q;
+            if (it_next(a, pit, g, ng, kind, idx)) {
+                if (t == 0) fence_proxy_async();
+                issue_item<GT>(a, kind, idx, st, stages, xslots, bars);
+            }
+        }
+        if (act) {
+            const size_t o = size_t(row) * a.rbs + t;
+            double out;
+            switch (a.mode) {
+                case MODE_RESIDUAL: out = __dsub_rn(pre_b, acc); break;
+                case MODE_ADD: out = __dadd_rn(pre_x, acc); break;
+                default: out = acc; break;
+            }
+            a.y[o] = out;
+        }
+    }
+    // drain: nothing outstanding (every issued item was consumed)
+}
+
+template <int GT>
+void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
+    static int attr_set_device = -1;
+    if (attr_set_device != ctx.device) {
+        LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(ctx.smem_optin)));
+        attr_set_device = ctx.device;
+    }
+    static std::vector<std::pair<size_t, int>> occ_cache;
+    int occ = -1;
+    for (const auto& e : occ_cache)
+        if (e.first == smem) occ = e.second;
+    if (occ < 0) {
+        LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<GT>, GT, smem));
+        occ_cache.push_back({smem, occ});
+    }
+    if (occ < 1) fail(LDGMG_ERR_CUDA, "rowpass: block does not fit on an SM");
+    const int grid = std::max(1, std::min(a.nrows, occ * ctx.num_sms));
+    rowpass_kernel<GT><<<grid, GT, smem, ctx.stream>>>(a);
+    after_launch("rowpass_kernel");
+}
+
+__global__ void upload_permute_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                      int64_t nnzb, int rbs, int cbs, int stride) {
+    // src: reference row-major blocks (r,c) at r*cbs+c; dst: column-major padded
+    const int64_t total = nnzb * int64_t(rbs) * cbs;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t k = i / (int64_t(rbs) * cbs);
+        const int e = int(i - k * int64_t(rbs) * cbs);
+        const int r = e / cbs, c = e % cbs;
+        dst[k * stride + int64_t(c) * rbs + r] = src[i];
+    }
+}
+
+__global__ void download_permute_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                        int64_t nnzb, int rbs, int cbs, int stride) {
+    const int64_t total = nnzb * int64_t(rbs) * cbs;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t k = i / (int64_t(rbs) * cbs);
+        const int e = int(i - k * int64_t(rbs) * cbs);
+        const int r = e / cbs, c = e % cbs;
+        dst[i] = src[k * stride + int64_t(c) * rbs + r];
+    }
+}
+
+/// B^T block q (= (B_ij)^T for source block k = perm[q]): element (c, r) of the
+/// transposed block, column-major with leading dim cbs: r*cbs + c.
+__global__ void transpose_blocks_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                        const int* __restrict__ perm, int64_t nnzb, int rbs,
+                                        int cbs, int stride) {
+    const int64_t total = nnzb * int64_t(rbs) * cbs;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = i / (int64_t(rbs) * cbs);
+        const int e = int(i - q * int64_t(rbs) * cbs);
+        const int r = e % rbs, c = e / rbs;  // source element (r, c)
+        const int64_t k = perm[q];
+        dst[q * stride + int64_t(r) * cbs + c] = src[k * stride + int64_t(c) * rbs + r];
+    }
+}
+
+int grid_for(int64_t n, int threads, const Ctx& ctx) {
+    return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, ctx.num_sms * 16)));
+}
+
+}  // namespace
+
+std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
+                                const int* col, const double* val) {
+    require(brows >= 0 && bcols >= 0 && rbs > 0 && cbs > 0, "bsr_upload: bad shape");
+    require(rbs <= 256 && cbs <= 256, "bsr_upload: block size above 256 is not supported");
+    auto A = std::make_unique<Bsr>();
+    A->brows = brows;
+    A->bcols = bcols;
+    A->rbs = rbs;
+    A->cbs = cbs;
+    A->hptr.assign(ptr, ptr + brows + 1);
+    require(A->hptr[0] == 0, "bsr_upload: ptr[0] must be 0");
+    for (int i = 0; i < brows; ++i)
+        require(A->hptr[i + 1] >= A->hptr[i], "bsr_upload: ptr must be nondecreasing");
+    A->nnzb = A->hptr[brows];
+    A->hcol.assign(col, col + A->nnzb);
+    for (int i = 0; i < brows; ++i)
+        for (int k = A->hptr[i]; k < A->hptr[i + 1]; ++k) {
+            require(A->hcol[k] >= 0 && A->hcol[k] < bcols, "bsr_upload: column out of range");
+            if (k > A->hptr[i]) require(A->hcol[k] > A->hcol[k - 1], "bsr_upload: columns must ascend");
+        }
+    A->blk_stride = even_up(int64_t(rbs) * cbs);
+    A->ptr.alloc(sizeof(int) * (brows + 1));
+    A->col.alloc(sizeof(int) * std::max<int64_t>(1, A->nnzb));
+    A->val.alloc(sizeof(double) * std::max<int64_t>(1, A->nnzb * A->blk_stride));
+    LDGMG_CUDA(cudaMemcpyAsync(A->ptr.p, ptr, sizeof(int) * (brows + 1), cudaMemcpyHostToDevice, ctx.stream));
+    if (A->nnzb) {
+        LDGMG_CUDA(cudaMemcpyAsync(A->col.p, col, sizeof(int) * A->nnzb, cudaMemcpyHostToDevice, ctx.stream));
+        LDGMG_CUDA(cudaMemsetAsync(A->val.p, 0, A->val.bytes, ctx.stream));
+        // stage through a device buffer in chunks to bound the temporary
+        const int64_t per_blk = int64_t(rbs) * cbs;
+        const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(256) << 20) / (per_blk * 8));
+        DevBuf tmp(sizeof(double) * std::min(A->nnzb, chunk_blocks) * per_blk);
+        for (int64_t k0 = 0; k0 < A->nnzb; k0 += chunk_blocks) {
+            const int64_t nb = std::min(chunk_blocks, A->nnzb - k0);
+            LDGMG_CUDA(cudaMemcpyAsync(tmp.p, val + k0 * per_blk, sizeof(double) * nb * per_blk,
+                                       cudaMemcpyHostToDevice, ctx.stream));
+            upload_permute_kernel<<<grid_for(nb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
+                tmp.as<double>(), A->val.as<double>() + k0 * A->blk_stride, nb, rbs, cbs,
+                A->blk_stride);
+            after_launch("upload_permute_kernel");
+            LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+        }
+    }
+    LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    return A;
+}
+
+void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val) {
+    if (ptr) std::memcpy(ptr, A.hptr.data(), sizeof(int) * A.hptr.size());
+    if (col) std::memcpy(col, A.hcol.data(), sizeof(int) * A.hcol.size());
+    if (val && A.nnzb) {
+        const int64_t per_blk = int64_t(A.rbs) * A.cbs;
+        DevBuf tmp(sizeof(double) * A.nnzb * per_blk);
+        download_permute_kernel<<<grid_for(A.nnzb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
+            A.val.as<double>(), tmp.as<double>(), A.nnzb, A.rbs, A.cbs, A.blk_stride);
+        after_launch("download_permute_kernel");
+        LDGMG_CUDA(cudaMemcpyAsync(val, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, ctx.stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+}
+
+const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A) {
+    if (A.T) return *A.T;
+    auto T = std::make_unique<Bsr>();
+    T->brows = A.bcols;
+    T->bcols = A.brows;
+    T->rbs = A.cbs;
+    T->cbs = A.rbs;
+    T->nnzb = A.nnzb;
+    T->blk_stride = A.blk_stride;
+    // CSC of A = CSR of A^T; rows i ascend within each column by construction
+    T->hptr.assign(A.bcols + 1, 0);
+    for (int64_t k = 0; k < A.nnzb; ++k) ++T->hptr[A.hcol[k] + 1];
+    for (int j = 0; j < A.bcols; ++j) T->hptr[j + 1] += T->hptr[j];
+    T->hcol.resize(A.nnzb);
+    std::vector<int> perm(std::max<int64_t>(1, A.nnzb)), fill(T->hptr.begin(), T->hptr.end() - 1);
+    for (int i = 0; i < A.brows; ++i)
+        for (int k = A.hptr[i]; k < A.hptr[i + 1]; ++k) {
+            const int q = fill[A.hcol[k]]++;
+            T->hcol[q] = i;
+            perm[q] = k;
+        }
+    T->ptr.alloc(sizeof(int) * (T->brows + 1));
+    T->col.alloc(sizeof(int) * std::max<int64_t>(1, T->nnzb));
+    T->val.alloc(sizeof(double) * std::max<int64_t>(1, T->nnzb * T->blk_stride));
+    LDGMG_CUDA(cudaMemcpyAsync(T->ptr.p, T->hptr.data(), sizeof(int) * T->hptr.size(), cudaMemcpyHostToDevice, ctx.stream));
+    if (T->nnzb) {
+        LDGMG_CUDA(cudaMemcpyAsync(T->col.p, T->hcol.data(), sizeof(int) * T->nnzb, cudaMemcpyHostToDevice, ctx.stream));
+        LDGMG_CUDA(cudaMemsetAsync(T->val.p, 0, T->val.bytes, ctx.stream));
+        DevBuf dperm(sizeof(int) * perm.size());
+        LDGMG_CUDA(cudaMemcpyAsync(dperm.p, perm.data(), dperm.bytes, cudaMemcpyHostToDevice, ctx.stream));
+        const int64_t per_blk = int64_t(A.rbs) * A.cbs;
+        transpose_blocks_kernel<<<grid_for(A.nnzb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
+            A.val.as<double>(), T->val.as<double>(), dperm.as<int>(), A.nnzb, A.rbs, A.cbs,
+            A.blk_stride);
+        after_launch("transpose_blocks_kernel");
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    const_cast<Bsr&>(A).T = std::move(T);
+    return *A.T;
+}
+
+void launch_rowpass(Ctx& ctx, const RowPass& p) {
+    const Bsr& A = *p.A;
+    if (p.nrows == 0) return;
+    RowPassArgs a{};
+    a.ptr = A.ptr.as<int>();
+    a.col = A.col.as<int>();
+    a.val = A.val.as<double>();
+    a.blk_stride = A.blk_stride;
+    a.rbs = A.rbs;
+    a.cbs = A.cbs;
+    a.mode = p.mode;
+    a.x = p.x;
+    a.b = p.b;
+    a.xe = p.xe;
+    a.y = p.y;
+    a.rows = p.rows;
+    a.nrows = p.nrows;
+    a.omega = p.omega;
+    a.kernel_tol = p.kernel_tol;
+    int stage = A.blk_stride;
+    if (p.mode == MODE_RELAX) {
+        require(p.F != nullptr && A.rbs == A.cbs && p.F->bs == A.rbs, "relax: factor shape mismatch");
+        a.V = p.F->V.as<double>();
+        a.lam = p.F->lambda.as<double>();
+        a.scal = p.F->scale.as<double>();
+        a.lmax = p.F->lmax.as<double>();
+        a.ld = p.F->ld;
+        a.vstride = p.F->vstride;
+        stage = std::max(stage, p.F->vstride);
+    }
+    a.stage_doubles = even_up(stage);
+    a.xslot_doubles = even_up(std::max(A.cbs, A.rbs));
+    const int wide = std::max(A.rbs, A.cbs);
+    const int GT = wide <= 32 ? 32 : wide <= 64 ? 64 : wide <= 128 ? 128 : 256;
+    // ring depth: keep >= ~3 blocks in flight per group within a 200 KB budget
+    const size_t stage_bytes = size_t(a.stage_doubles) * 8;
+    int ns = 4;
+    while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
+    a.nstages = ns;
+    const size_t smem = size_t(ns) * stage_bytes + size_t(ns) * a.xslot_doubles * 8 +
+                        2 * size_t(a.xslot_doubles) * 8 + size_t(ns) * 8;
+    if (smem > ctx.smem_optin) fail(LDGMG_ERR_INVALID_ARGUMENT, "rowpass: block too large for shared memory");
+    switch (GT) {
+        case 32: configure_and_launch<32>(ctx, a, smem); break;
+        case 64: configure_and_launch<64>(ctx, a, smem); break;
+        case 128: configure_and_launch<128>(ctx, a, smem); break;
+        default: configure_and_launch<256>(ctx, a, smem); break;
+    }
+}
+
+}  // namespace ldgmg_b200

@@ -1,0 +1,760 @@
+// The C ABI (include/ldgmg_b200.h): status codes + thread-local error text,
+// opaque handles over the host objects of core.hpp / mg.hpp.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "core.hpp"
+#include "mg.hpp"
+#include "setup.hpp"
+
+using namespace ldgmg_b200;
+
+struct ldgmg_ctx : Ctx {};
+struct ldgmg_bsr : Bsr {};
+struct ldgmg_smoother {
+    Smoother s;
+};
+struct ldgmg_transfer {
+    std::unique_ptr<Transfer> t;
+};
+struct ldgmg_mg {
+    Mg m;
+};
+struct ldgmg_problem {
+    Problem p;
+};
+
+namespace ldgmg_b200 {
+std::atomic<int64_t>& launch_counter() {
+    static std::atomic<int64_t> c{0};
+    return c;
+}
+}  // namespace ldgmg_b200
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LDGMG_OK;
+    } catch (const Error& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_error = e.what();
+        return LDGMG_ERR_INVALID_ARGUMENT;
+    } catch (const std::logic_error& e) {
+        g_error = e.what();
+        return LDGMG_ERR_LOGIC;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return LDGMG_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return LDGMG_ERR_RUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(LDGMG_ERR_INVALID_ARGUMENT, std::string(what) + ": null argument");
+}
+
+void bind(Ctx& c) { LDGMG_CUDA(cudaSetDevice(c.device)); }
+
+Bsr* own_bsr(std::unique_ptr<Bsr> b) {
+    // ldgmg_bsr is layout-identical to Bsr (empty derived struct)
+    auto* h = new ldgmg_bsr();
+    static_cast<Bsr&>(*h) = std::move(*b);
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ldgmg_last_error(void) { return g_error.c_str(); }
+int ldgmg_abi_version(void) { return LDGMG_B200_ABI_VERSION; }
+int64_t ldgmg_launch_count(void) { return launch_counter().load(); }
+
+int ldgmg_ctx_create(int device, ldgmg_ctx** out) {
+    return guarded([&] {
+        need(out, "ldgmg_ctx_create");
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0)
+            fail(LDGMG_ERR_CUDA, "no CUDA device visible: the B200 path has no CPU fallback");
+        if (device < 0 || device >= n) fail(LDGMG_ERR_INVALID_ARGUMENT, "ldgmg_ctx_create: bad device");
+        auto* c = new ldgmg_ctx();
+        c->device = device;
+        LDGMG_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        LDGMG_CUDA(cudaGetDeviceProperties(&prop, device));
+        c->num_sms = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        LDGMG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        LDGMG_CUDA(cudaMalloc(&c->d_red, sizeof(double) * 1024));
+        LDGMG_CUDA(cudaMallocHost(&c->h_red, sizeof(double) * 8));
+        *out = c;
+    });
+}
+
+int ldgmg_ctx_destroy(ldgmg_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        cudaFree(ctx->d_red);
+        cudaFreeHost(ctx->h_red);
+        delete ctx;
+    });
+}
+
+int ldgmg_ctx_set_stream(ldgmg_ctx* ctx, void* stream) {
+    return guarded([&] {
+        need(ctx, "ldgmg_ctx_set_stream");
+        if (ctx->own_stream) {
+            LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+            cudaStreamDestroy(ctx->stream);
+        }
+        ctx->stream = static_cast<cudaStream_t>(stream);
+        ctx->own_stream = false;
+    });
+}
+
+void* ldgmg_ctx_stream(ldgmg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int ldgmg_ctx_synchronize(ldgmg_ctx* ctx) {
+    return guarded([&] {
+        need(ctx, "ldgmg_ctx_synchronize");
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ldgmg_device_alloc(ldgmg_ctx* ctx, size_t bytes, void** ptr) {
+    return guarded([&] {
+        need(ctx, "ldgmg_device_alloc");
+        bind(*ctx);
+        LDGMG_CUDA(cudaMalloc(ptr, bytes ? bytes : 16));
+    });
+}
+int ldgmg_device_free(ldgmg_ctx* ctx, void* ptr) {
+    return guarded([&] {
+        need(ctx, "ldgmg_device_free");
+        LDGMG_CUDA(cudaFree(ptr));
+    });
+}
+int ldgmg_copy_h2d(ldgmg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        need(ctx, "ldgmg_copy_h2d");
+        LDGMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+int ldgmg_copy_d2h(ldgmg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        need(ctx, "ldgmg_copy_d2h");
+        LDGMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// ------------------------------------------------------------------ BSR
+int ldgmg_bsr_upload(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int col_bs, const int* ptr,
+                     const int* col, const double* val, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_upload");
+        need(ptr, "ldgmg_bsr_upload(ptr)");
+        need(out, "ldgmg_bsr_upload(out)");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(bsr_upload(*ctx, brows, bcols, row_bs, col_bs, ptr, col, val)));
+    });
+}
+
+int ldgmg_bsr_shape(const ldgmg_bsr* A, int* brows, int* bcols, int* row_bs, int* col_bs,
+                    int64_t* nnzb) {
+    return guarded([&] {
+        need(A, "ldgmg_bsr_shape");
+        if (brows) *brows = A->brows;
+        if (bcols) *bcols = A->bcols;
+        if (row_bs) *row_bs = A->rbs;
+        if (col_bs) *col_bs = A->cbs;
+        if (nnzb) *nnzb = A->nnzb;
+    });
+}
+
+int ldgmg_bsr_download(ldgmg_ctx* ctx, const ldgmg_bsr* A, int* ptr, int* col, double* val) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_download");
+        need(A, "ldgmg_bsr_download");
+        bind(*ctx);
+        bsr_download(*ctx, *A, ptr, col, val);
+    });
+}
+
+int64_t ldgmg_bsr_device_bytes(const ldgmg_bsr* A) { return A ? A->device_bytes() : 0; }
+
+int ldgmg_bsr_destroy(ldgmg_bsr* A) {
+    return guarded([&] { delete A; });
+}
+
+int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx, "spmv");
+        need(A, "spmv");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_SPMV;
+        p.x = x;
+        p.y = y;
+        p.nrows = A->brows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_spmv_transpose(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx, "spmv_transpose");
+        need(A, "spmv_transpose");
+        RowPass p;
+        p.A = &bsr_transpose(*ctx, *A);
+        p.mode = MODE_SPMV;
+        p.x = x;
+        p.y = y;
+        p.nrows = p.A->brows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const double* x, double* r) {
+    return guarded([&] {
+        need(ctx, "residual");
+        need(A, "residual");
+        if (A->rbs != A->cbs || A->brows != A->bcols)
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "residual: operator must be block-square");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_RESIDUAL;
+        p.x = x;
+        p.b = b;
+        p.y = r;
+        p.nrows = A->brows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_dot(ldgmg_ctx* ctx, int64_t n, const double* a, const double* b, double* out_host) {
+    return guarded([&] {
+        need(ctx, "dot");
+        launch_dot(*ctx, n, a, b, ctx->d_red);
+        LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out_host = ctx->h_red[0];
+    });
+}
+
+int ldgmg_axpy(ldgmg_ctx* ctx, int64_t n, double alpha, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx, "axpy");
+        launch_axpy(*ctx, n, alpha, x, y);
+    });
+}
+
+// ------------------------------------------------------------ smoothers
+static Smoother& smoother_base(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_smoother_config* cfg,
+                               ldgmg_smoother*& h) {
+    need(ctx, "smoother_create");
+    need(A, "smoother_create");
+    need(cfg, "smoother_create(cfg)");
+    bind(*ctx);
+    h = new ldgmg_smoother();
+    h->s.A = A;
+    h->s.cfg = *cfg;
+    return h->s;
+}
+
+int ldgmg_smoother_create(ldgmg_ctx* ctx, const ldgmg_bsr* A, int system_kind, int n_velocity,
+                          const ldgmg_smoother_config* cfg, ldgmg_smoother** out) {
+    ldgmg_smoother* h = nullptr;
+    const int rc = guarded([&] {
+        Smoother& s = smoother_base(ctx, A, cfg, h);
+        s.system_kind = system_kind;
+        s.n_velocity = n_velocity;
+        s.init_common(*ctx);
+        if (s.cfg.kind == LDGMG_SAI) {
+            SaiResult r = build_sai_gpu(*ctx, *A, system_kind, n_velocity, s.cfg.level, s.cfg.zeta,
+                                        s.cfg.cache != 0);
+            s.B = std::move(r.B);
+            s.stats = r.stats;
+        } else {
+            compute_factors(*ctx, *A, s.F);
+        }
+        *out = h;
+    });
+    if (rc != LDGMG_OK) delete h;
+    return rc;
+}
+
+int ldgmg_smoother_create_with_factors(ldgmg_ctx* ctx, const ldgmg_bsr* A,
+                                       const ldgmg_smoother_config* cfg, const double* V,
+                                       const double* lambda, const double* s, ldgmg_smoother** out) {
+    ldgmg_smoother* h = nullptr;
+    const int rc = guarded([&] {
+        need(V, "factors(V)");
+        need(lambda, "factors(lambda)");
+        need(s, "factors(s)");
+        Smoother& sm = smoother_base(ctx, A, cfg, h);
+        if (sm.cfg.kind == LDGMG_SAI) fail(LDGMG_ERR_INVALID_ARGUMENT, "factors given to an SAI smoother");
+        sm.init_common(*ctx);
+        upload_factors(*ctx, sm.F, sm.N, sm.bs, V, lambda, s);
+        *out = h;
+    });
+    if (rc != LDGMG_OK) delete h;
+    return rc;
+}
+
+int ldgmg_smoother_create_with_sai(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_smoother_config* cfg,
+                                   const int* Bptr, const int* Bcol, const double* Bval,
+                                   ldgmg_smoother** out) {
+    ldgmg_smoother* h = nullptr;
+    const int rc = guarded([&] {
+        Smoother& sm = smoother_base(ctx, A, cfg, h);
+        if (sm.cfg.kind != LDGMG_SAI) fail(LDGMG_ERR_INVALID_ARGUMENT, "SAI matrix given to a non-SAI smoother");
+        sm.init_common(*ctx);
+        sm.B = bsr_upload(*ctx, A->brows, A->bcols, A->rbs, A->cbs, Bptr, Bcol, Bval);
+        *out = h;
+    });
+    if (rc != LDGMG_OK) delete h;
+    return rc;
+}
+
+int ldgmg_smoother_apply(ldgmg_ctx* ctx, const ldgmg_smoother* S, const double* b, double* x, int sweep) {
+    return guarded([&] {
+        need(ctx, "Smoother::apply");
+        need(S, "Smoother::apply");
+        S->s.apply(*ctx, b, x, sweep);
+    });
+}
+
+int ldgmg_smoother_colours(const ldgmg_smoother* S, int* colour, int* ncolours) {
+    return guarded([&] {
+        need(S, "colours");
+        if (colour && !S->s.colour.empty()) std::memcpy(colour, S->s.colour.data(), sizeof(int) * S->s.colour.size());
+        if (ncolours) *ncolours = S->s.ncolours;
+    });
+}
+
+int ldgmg_smoother_sai_nnzb(const ldgmg_smoother* S, int64_t* nnzb) {
+    return guarded([&] {
+        need(S, "sai_matrix");
+        if (S->s.cfg.kind != LDGMG_SAI || !S->s.B) fail(LDGMG_ERR_LOGIC, "not an SAI smoother");
+        *nnzb = S->s.B->nnzb;
+    });
+}
+
+int ldgmg_smoother_sai_matrix(ldgmg_ctx* ctx, const ldgmg_smoother* S, int* ptr, int* col, double* val) {
+    return guarded([&] {
+        need(ctx, "sai_matrix");
+        need(S, "sai_matrix");
+        if (S->s.cfg.kind != LDGMG_SAI || !S->s.B) fail(LDGMG_ERR_LOGIC, "not an SAI smoother");
+        bsr_download(*ctx, *S->s.B, ptr, col, val);
+    });
+}
+
+int ldgmg_smoother_sai_stats(const ldgmg_smoother* S, ldgmg_sai_stats* out) {
+    return guarded([&] {
+        need(S, "sai_stats");
+        *out = S->s.stats;
+    });
+}
+
+int ldgmg_smoother_diag_factors(ldgmg_ctx* ctx, const ldgmg_smoother* S, double* V, double* lambda,
+                                double* s) {
+    return guarded([&] {
+        need(ctx, "diag_factors");
+        need(S, "diag_factors");
+        const DiagFactors& F = S->s.F;
+        if (!F.n) fail(LDGMG_ERR_LOGIC, "smoother has no diagonal factors");
+        const int bs = F.bs;
+        if (V) {
+            std::vector<double> hv(size_t(F.n) * F.vstride);
+            LDGMG_CUDA(cudaMemcpy(hv.data(), F.V.p, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+            for (int e = 0; e < F.n; ++e)
+                for (int a = 0; a < bs; ++a)
+                    for (int b = 0; b < bs; ++b)
+                        V[(size_t(e) * bs + a) * bs + b] = hv[size_t(e) * F.vstride + size_t(a) * F.ld + b];
+        }
+        if (lambda) LDGMG_CUDA(cudaMemcpy(lambda, F.lambda.p, F.lambda.bytes, cudaMemcpyDeviceToHost));
+        if (s) LDGMG_CUDA(cudaMemcpy(s, F.scale.p, F.scale.bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+int ldgmg_smoother_destroy(ldgmg_smoother* S) {
+    return guarded([&] { delete S; });
+}
+
+// ------------------------------------------------------------ transfers
+int ldgmg_transfer_create(ldgmg_ctx* ctx, int n_fine, int n_coarse, const int* parent_of,
+                          const int* orthant_of, int dim, int bs_scalar, int n_comp, const double* K,
+                          ldgmg_transfer** out) {
+    return guarded([&] {
+        need(ctx, "transfer_create");
+        need(parent_of, "transfer_create(parent_of)");
+        need(orthant_of, "transfer_create(orthant_of)");
+        need(K, "transfer_create(K)");
+        bind(*ctx);
+        auto* h = new ldgmg_transfer();
+        h->t = transfer_create(*ctx, n_fine, n_coarse, parent_of, orthant_of, dim, bs_scalar, n_comp, K);
+        *out = h;
+    });
+}
+
+int ldgmg_restrict(ldgmg_ctx* ctx, const ldgmg_transfer* T, const double* rf, double* rc) {
+    return guarded([&] {
+        need(ctx, "restrict_residual");
+        need(T, "restrict_residual");
+        launch_restrict(*ctx, *T->t, rf, rc);
+    });
+}
+
+int ldgmg_interpolate_add(ldgmg_ctx* ctx, const ldgmg_transfer* T, const double* xc, double* xf) {
+    return guarded([&] {
+        need(ctx, "interpolate_add");
+        need(T, "interpolate_add");
+        launch_prolong_add(*ctx, *T->t, xc, xf);
+    });
+}
+
+int ldgmg_transfer_destroy(ldgmg_transfer* T) {
+    return guarded([&] { delete T; });
+}
+
+// ------------------------------------------------------------ multigrid
+static void mg_default_smoothers(ldgmg_ctx* ctx, Mg& m) {
+    m.sm.assign(m.depth, nullptr);
+    for (int l = 0; l + 1 < m.depth; ++l) {
+        auto s = std::make_unique<Smoother>();
+        s->A = m.A[l];
+        s->cfg = m.cfg.smoother;
+        s->system_kind = m.system_kind;
+        s->n_velocity = m.n_velocity;
+        s->init_common(*ctx);
+        if (s->cfg.kind == LDGMG_SAI) {
+            SaiResult r = build_sai_gpu(*ctx, *m.A[l], m.system_kind, m.n_velocity, s->cfg.level,
+                                        s->cfg.zeta, s->cfg.cache != 0);
+            s->B = std::move(r.B);
+            s->stats = r.stats;
+        } else {
+            compute_factors(*ctx, *m.A[l], s->F);
+        }
+        m.sm[l] = s.get();
+        m.own_sm.push_back(std::move(s));
+    }
+}
+
+int ldgmg_mg_create(ldgmg_ctx* ctx, int depth, const ldgmg_bsr* const* A,
+                    const ldgmg_transfer* const* transfers, int system_kind, int dim, int n_comp,
+                    int bs_scalar, int kernel_constants, int kernel_pressure, const ldgmg_mg_config* cfg,
+                    const double* bottom_V, const double* bottom_lambda, ldgmg_mg** out) {
+    ldgmg_mg* h = nullptr;
+    const int rc = guarded([&] {
+        need(ctx, "Multigrid");
+        need(A, "Multigrid(A)");
+        need(cfg, "Multigrid(cfg)");
+        bind(*ctx);
+        h = new ldgmg_mg();
+        Mg& m = h->m;
+        m.depth = depth;
+        m.cfg = *cfg;
+        m.system_kind = system_kind;
+        m.dim = dim;
+        m.n_comp = n_comp;
+        m.bs_scalar = bs_scalar;
+        m.kernel_constants = kernel_constants;
+        m.kernel_pressure = kernel_pressure;
+        m.n_velocity = system_kind == LDGMG_SYSTEM_STOKES ? dim * bs_scalar : 0;
+        for (int l = 0; l < depth; ++l) {
+            need(A[l], "Multigrid(A[l])");
+            m.A.push_back(A[l]);
+        }
+        for (int l = 0; l + 1 < depth; ++l) m.T.push_back(transfers ? transfers[l]->t.get() : nullptr);
+        m.init(*ctx);
+        if (m.bs != n_comp * bs_scalar) fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: block size != n_comp*bs_scalar");
+        m.set_bottom(*ctx, bottom_V, bottom_lambda);
+        m.sm.assign(depth, nullptr);
+        *out = h;
+    });
+    if (rc != LDGMG_OK) delete h;
+    return rc;
+}
+
+int ldgmg_mg_set_smoother(ldgmg_mg* mg, int level, ldgmg_smoother* S) {
+    return guarded([&] {
+        need(mg, "mg_set_smoother");
+        need(S, "mg_set_smoother");
+        if (level < 0 || level + 1 >= mg->m.depth) fail(LDGMG_ERR_LOGIC, "multigrid: the bottom level has no smoother");
+        if (S->s.A != mg->m.A[level]) fail(LDGMG_ERR_INVALID_ARGUMENT, "mg_set_smoother: smoother bound to another operator");
+        mg->m.sm[level] = &S->s;
+    });
+}
+
+static void ensure_smoothers(ldgmg_ctx* ctx, Mg& m) {
+    bool any_missing = false;
+    for (int l = 0; l + 1 < m.depth; ++l) any_missing |= m.sm[l] == nullptr;
+    if (!any_missing) return;
+    std::vector<Smoother*> keep = m.sm;
+    mg_default_smoothers(ctx, m);
+    for (int l = 0; l + 1 < m.depth; ++l)
+        if (keep[l]) m.sm[l] = keep[l];
+}
+
+int ldgmg_mg_smoother(ldgmg_mg* mg, int level, ldgmg_smoother** out) {
+    return guarded([&] {
+        need(mg, "mg_smoother");
+        if (level < 0 || level + 1 >= mg->m.depth) fail(LDGMG_ERR_LOGIC, "multigrid: the bottom level has no smoother");
+        if (!mg->m.sm[level]) fail(LDGMG_ERR_LOGIC, "multigrid: smoothers not built yet");
+        // non-owning view handle sharing the Smoother object
+        *out = reinterpret_cast<ldgmg_smoother*>(mg->m.sm[level]);
+    });
+}
+
+int ldgmg_mg_depth(const ldgmg_mg* mg) { return mg ? mg->m.depth : 0; }
+
+int ldgmg_mg_cycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b) {
+    return guarded([&] {
+        need(ctx, "Multigrid::cycle");
+        need(mg, "Multigrid::cycle");
+        ensure_smoothers(ctx, mg->m);
+        mg->m.cycle(*ctx, x, b);
+    });
+}
+
+int ldgmg_mg_apply(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b, double* x) {
+    return guarded([&] {
+        need(ctx, "Multigrid::apply");
+        need(mg, "Multigrid::apply");
+        ensure_smoothers(ctx, mg->m);
+        mg->m.apply(*ctx, b, x);
+    });
+}
+
+int ldgmg_mg_cycles(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b, int ncycles) {
+    return guarded([&] {
+        need(ctx, "mg_cycles");
+        need(mg, "mg_cycles");
+        ensure_smoothers(ctx, mg->m);
+        mg->m.cycles(*ctx, x, b, ncycles);
+    });
+}
+
+int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, double* x_host, double tol,
+                        int maxit, double* history, int* iters) {
+    return guarded([&] {
+        need(ctx, "mg_solve_host");
+        need(mg, "mg_solve_host");
+        need(b_host, "mg_solve_host(b)");
+        need(x_host, "mg_solve_host(x)");
+        Mg& m = mg->m;
+        ensure_smoothers(ctx, m);
+        const int64_t n = int64_t(m.A[0]->brows) * m.bs;
+        DevBuf b(sizeof(double) * std::max<int64_t>(1, n)), x(sizeof(double) * std::max<int64_t>(1, n)),
+            r(sizeof(double) * std::max<int64_t>(1, n));
+        LDGMG_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        LDGMG_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, ctx->stream));
+        launch_dot(*ctx, n, b.as<double>(), b.as<double>(), ctx->d_red);
+        LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        const double bn = std::sqrt(ctx->h_red[0]);
+        auto relres = [&]() {
+            RowPass p;
+            p.A = m.A[0];
+            p.mode = MODE_RESIDUAL;
+            p.x = x.as<double>();
+            p.b = b.as<double>();
+            p.y = r.as<double>();
+            p.nrows = m.A[0]->brows;
+            launch_rowpass(*ctx, p);
+            launch_dot(*ctx, n, r.as<double>(), r.as<double>(), ctx->d_red);
+            LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+            return bn > 0 ? std::sqrt(ctx->h_red[0]) / bn : std::sqrt(ctx->h_red[0]);
+        };
+        double rr = relres();
+        if (history) history[0] = rr;
+        int it = 0;
+        while (rr > tol && it < maxit) {
+            m.cycles(*ctx, x.as<double>(), b.as<double>(), 1);
+            ++it;
+            rr = relres();
+            if (history) history[it] = rr;
+        }
+        if (iters) *iters = it;
+        LDGMG_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict) {
+    return guarded([&] {
+        need(mg, "mg_set_strict_order");
+        mg->m.strict_order = strict != 0;
+        for (auto& gr : mg->m.graphs) cudaGraphExecDestroy(gr.exec);
+        mg->m.graphs.clear();
+    });
+}
+
+int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes) {
+    return guarded([&] {
+        need(mg, "mg_cycle_costs");
+        for (int l = 0; l + 1 < mg->m.depth; ++l)
+            if (!mg->m.sm[l]) fail(LDGMG_ERR_LOGIC, "multigrid: smoothers not built yet");
+        if (dof_updates) *dof_updates = mg->m.dof_updates_per_cycle();
+        if (alg_bytes) *alg_bytes = mg->m.bytes_per_cycle();
+    });
+}
+
+int ldgmg_mg_destroy(ldgmg_mg* mg) {
+    return guarded([&] { delete mg; });
+}
+
+// ------------------------------------------------------ host setup (L0/L2)
+int ldgmg_problem_create(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements,
+                         ldgmg_problem** out) {
+    return guarded([&] {
+        need(spec, "problem_create");
+        need(out, "problem_create");
+        auto* h = new ldgmg_problem();
+        try {
+            problem_build(*spec, min_depth, bottom_max_elements, h->p);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ldgmg_problem_depth(const ldgmg_problem* P) { return P ? int(P->p.levels.size()) : 0; }
+
+int ldgmg_problem_level_shape(const ldgmg_problem* P, int level, int* n_elements, int* bs, int64_t* nnzb) {
+    return guarded([&] {
+        need(P, "problem_level_shape");
+        if (level < 0 || level >= int(P->p.levels.size())) fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: bad level");
+        const auto& L = P->p.levels[level];
+        if (n_elements) *n_elements = L.A.brows;
+        if (bs) *bs = L.A.bs;
+        if (nnzb) *nnzb = int64_t(L.A.col.size());
+    });
+}
+
+int ldgmg_problem_level_matrix(const ldgmg_problem* P, int level, int* ptr, int* col, double* val) {
+    return guarded([&] {
+        need(P, "problem_level_matrix");
+        if (level < 0 || level >= int(P->p.levels.size())) fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: bad level");
+        const auto& A = P->p.levels[level].A;
+        if (ptr) std::memcpy(ptr, A.ptr.data(), sizeof(int) * A.ptr.size());
+        if (col) std::memcpy(col, A.col.data(), sizeof(int) * A.col.size());
+        if (val) std::memcpy(val, A.val.data(), sizeof(double) * A.val.size());
+    });
+}
+
+int ldgmg_problem_level_transfer(const ldgmg_problem* P, int level, int* parent_of, int* orthant_of) {
+    return guarded([&] {
+        need(P, "problem_level_transfer");
+        if (level < 0 || level + 1 >= int(P->p.levels.size()))
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: bottom level has no transfer");
+        const auto& L = P->p.levels[level];
+        if (parent_of) std::memcpy(parent_of, L.parent_of.data(), sizeof(int) * L.parent_of.size());
+        if (orthant_of) std::memcpy(orthant_of, L.orthant_of.data(), sizeof(int) * L.orthant_of.size());
+    });
+}
+
+int ldgmg_problem_info(const ldgmg_problem* P, int* dim, int* n_comp, int* bs_scalar, int* kernel_constants,
+                       int* kernel_pressure, int* n_velocity) {
+    return guarded([&] {
+        need(P, "problem_info");
+        const Problem& p = P->p;
+        if (dim) *dim = p.dim;
+        if (n_comp) *n_comp = p.n_comp;
+        if (bs_scalar) *bs_scalar = p.bs_scalar;
+        if (kernel_constants) *kernel_constants = p.kernel_constants;
+        if (kernel_pressure) *kernel_pressure = p.kernel_pressure;
+        if (n_velocity) *n_velocity = p.kind == LDGMG_SYSTEM_STOKES ? p.dim * p.bs_scalar : 0;
+    });
+}
+
+int ldgmg_problem_injection(const ldgmg_problem* P, double* K) {
+    return guarded([&] {
+        need(P, "problem_injection");
+        need(K, "problem_injection(K)");
+        std::memcpy(K, P->p.inject.data(), sizeof(double) * P->p.inject.size());
+    });
+}
+
+int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P, const ldgmg_mg_config* cfg,
+                                 ldgmg_mg** out) {
+    ldgmg_mg* h = nullptr;
+    const int rc = guarded([&] {
+        need(ctx, "mg_create_from_problem");
+        need(P, "mg_create_from_problem");
+        need(cfg, "mg_create_from_problem(cfg)");
+        bind(*ctx);
+        const Problem& p = P->p;
+        h = new ldgmg_mg();
+        Mg& m = h->m;
+        m.depth = int(p.levels.size());
+        m.cfg = *cfg;
+        m.system_kind = p.kind;
+        m.dim = p.dim;
+        m.n_comp = p.n_comp;
+        m.bs_scalar = p.bs_scalar;
+        m.kernel_constants = p.kernel_constants;
+        m.kernel_pressure = p.kernel_pressure;
+        m.n_velocity = p.kind == LDGMG_SYSTEM_STOKES ? p.dim * p.bs_scalar : 0;
+        for (int l = 0; l < m.depth; ++l) {
+            const auto& A = p.levels[l].A;
+            m.own_A.push_back(bsr_upload(*ctx, A.brows, A.brows, A.bs, A.bs, A.ptr.data(), A.col.data(), A.val.data()));
+            m.A.push_back(m.own_A.back().get());
+        }
+        for (int l = 0; l + 1 < m.depth; ++l) {
+            const auto& L = p.levels[l];
+            m.own_T.push_back(transfer_create(*ctx, L.A.brows, p.levels[l + 1].A.brows, L.parent_of.data(),
+                                              L.orthant_of.data(), p.dim, p.bs_scalar, p.n_comp,
+                                              p.inject.data()));
+            m.T.push_back(m.own_T.back().get());
+        }
+        m.init(*ctx);
+        m.set_bottom(*ctx, nullptr, nullptr);
+        m.sm.assign(m.depth, nullptr);
+        mg_default_smoothers(ctx, m);
+        *out = h;
+    });
+    if (rc != LDGMG_OK) delete h;
+    return rc;
+}
+
+int ldgmg_problem_destroy(ldgmg_problem* P) {
+    return guarded([&] { delete P; });
+}
+
+int ldgmg_random_rhs(int nblocks, int bs, uint64_t seed, double* out) {
+    return guarded([&] {
+        need(out, "random_rhs");
+        std::mt19937_64 rng(seed);
+        const size_t n = size_t(nblocks) * bs;
+        for (size_t i = 0; i < n; ++i) {
+            const double u = double(rng() >> 11) * 0x1.0p-53;
+            out[i] = 2.0 * u - 1.0;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Shared device/host plumbing for the B200 V-cycle core: error handling that
+// maps onto the reference's exception kinds, the launch counter, and the few
+// sm_100a PTX primitives the streaming kernels use (mbarrier + 1-D bulk copy
+// = TMA `cp.async.bulk`, SASS UBLKCP).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ldgmg_b200.h"
+
+namespace ldgmg_b200 {
+
+/// Exception carrying one of the LDGMG_ERR_* codes; the C ABI converts it to
+/// a status + ldgmg_last_error() text.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const char* msg) {
+    if (!ok) fail(LDGMG_ERR_INVALID_ARGUMENT, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(LDGMG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define LDGMG_CUDA(call) ::ldgmg_b200::cuda_check((call), #call)
+
+std::atomic<int64_t>& launch_counter();
+/// Call right after every kernel launch: counts it and surfaces launch errors.
+inline void after_launch(const char* name) {
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    cuda_check(cudaGetLastError(), name);
+}
+
+inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+// ------------------------------------------------------------ PTX helpers
+#if defined(__CUDACC__)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+/// arrive + expect `bytes` of async-proxy transactions on the barrier
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    while (!mbar_try_wait(bar, phase)) {
+    }
+}
+/// TMA 1-D bulk copy global -> shared, completion signalled on `bar`.
+/// `bytes` must be a multiple of 16, both addresses 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+/// Named barrier over `nthreads` threads (row groups wider than one warp).
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    if (nthreads <= 32)
+        __syncwarp();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+/// Unfused IEEE multiply-add pair: the reference's `s += a * b` compiled for
+/// x86-64 without FMA contraction (blockla.hpp:149, smoothers.hpp:508).
+__device__ __forceinline__ double madd_rn(double s, double a, double b) {
+    return __dadd_rn(s, __dmul_rn(a, b));
+}
+#endif
+
+}  // namespace ldgmg_b200

@@ -1,0 +1,132 @@
+// Host-side objects behind the C ABI handles.  Device layouts:
+//   * BSR values: one block per `blk_stride` doubles (rbs*cbs rounded up to an
+//     even count so every block starts 16-byte aligned for TMA bulk copies),
+//     block stored COLUMN-major: element (r,c) at c*rbs + r.  Lane r of a row
+//     group then reads consecutive shared-memory words at every step c.
+//   * ptr/col: identical int32 arrays to the reference BlockCsr.
+//   * diagonal factors: V per element as bs columns of stride ld = bs|1
+//     (odd, conflict-free for both V^T u and V t), padded to an even count.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ldgmg_b200 {
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    size_t smem_optin = 227 * 1024;
+    // scratch for reductions (device) + pinned host slot
+    double* d_red = nullptr;
+    double* h_red = nullptr;
+};
+
+/// RAII device allocation.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        release();
+        p = o.p;
+        bytes = o.bytes;
+        o.p = nullptr;
+        o.bytes = 0;
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t n) {
+        release();
+        bytes = n;
+        if (n) LDGMG_CUDA(cudaMalloc(&p, n));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct Bsr {
+    int brows = 0, bcols = 0, rbs = 0, cbs = 0;
+    int64_t nnzb = 0;
+    int blk_stride = 0;  // doubles per stored block
+    DevBuf ptr, col, val;
+    std::vector<int> hptr, hcol;
+    std::unique_ptr<Bsr> T;  // lazily built transpose (spmv_transpose, B^T sweeps)
+    int64_t device_bytes() const { return int64_t(ptr.bytes + col.bytes + val.bytes); }
+};
+
+inline int even_up(int64_t n) { return int((n + 1) & ~int64_t(1)); }
+
+/// Upload from the reference layout (row-major blocks) to the device layout.
+std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
+                                const int* col, const double* val);
+/// Device copy of A with the layout of A^T (used for B^T r, bitwise equal to
+/// the reference's scatter order, blockla.hpp:163-175).
+const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A);
+void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val);
+
+/// Per-element factors of the block-diagonal solve (smoothers.hpp:464-494).
+struct DiagFactors {
+    int n = 0, bs = 0, ld = 0, vstride = 0;
+    DevBuf V, lambda, scale, lmax;  // lmax: max |lambda| per element
+};
+
+// ---- streaming row-pass kernels (bsr_kernels.cu) ---------------------------
+enum RowMode { MODE_SPMV = 0, MODE_RESIDUAL = 1, MODE_ADD = 2, MODE_RELAX = 3 };
+
+struct RowPass {
+    const Bsr* A = nullptr;
+    int mode = MODE_SPMV;
+    const double* x = nullptr;   // gathered vector (snapshot for Jacobi)
+    const double* b = nullptr;   // RESIDUAL / RELAX
+    const double* xe = nullptr;  // RELAX: x_e for the damped blend (live x)
+    double* y = nullptr;         // output
+    const int* rows = nullptr;   // optional row list (colour phase); nullptr = all rows
+    int nrows = 0;
+    const DiagFactors* F = nullptr;  // RELAX
+    double omega = 1.0;
+    double kernel_tol = 1e-12;
+};
+void launch_rowpass(Ctx& ctx, const RowPass& p);
+
+// ---- transfers / dense / BLAS-1 (vec_kernels.cu) ---------------------------
+struct Transfer {
+    int n_fine = 0, n_coarse = 0, dim = 2, bss = 0, ncomp = 1, bs = 0;
+    DevBuf parent, orth, child_ptr, child_list, K;
+    std::vector<int> hparent, horth;
+};
+void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc);
+void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* xf);
+
+struct DenseEig {  // bottom pseudoinverse: V both layouts + lambda + lmax
+    int n = 0;
+    DevBuf Vc, Vr, lambda, t;
+    double lmax = 0.0;
+};
+void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b, double* x);
+
+/// v -= (v.k) k for the constant-mode kernel vectors (multigrid.hpp:243-245).
+/// `offs` = entries of the mode-0 coefficient of each kernel component.
+void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* comp_offsets,
+                              int ncomp, double kval, bool strict_order);
+void launch_axpy(Ctx& ctx, int64_t n, double alpha, const double* x, double* y);
+/// deterministic fixed-tree dot (partials per CTA, ascending final sum)
+void launch_dot(Ctx& ctx, int64_t n, const double* a, const double* b, double* d_out);
+void launch_fill(Ctx& ctx, int64_t n, double v, double* y);
+
+}  // namespace ldgmg_b200

@@ -1,0 +1,462 @@
+// Smoothers, transfers, the multigrid hierarchy and the V-cycle driver
+// (host orchestration of the device kernels; every operator application is a
+// bsr_kernels.cu row pass).  Mirrors smoothers.hpp:373-534 and
+// multigrid.hpp:45-274 of the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "core.hpp"
+#include "host_eig.hpp"
+#include "mg.hpp"
+
+namespace ldgmg_b200 {
+
+// ------------------------------------------------------------- colouring
+/// Greedy colouring in ascending element order (smoothers.hpp:63-84),
+/// restated; rejects non-symmetric patterns with the reference's messages.
+std::vector<int> colour_mesh_host(const Bsr& A) {
+    if (A.brows != A.bcols) fail(LDGMG_ERR_INVALID_ARGUMENT, "colour_mesh: matrix not block-square");
+    auto find = [&](int i, int j) {
+        for (int k = A.hptr[i]; k < A.hptr[i + 1]; ++k)
+            if (A.hcol[k] == j) return k;
+        return -1;
+    };
+    for (int i = 0; i < A.brows; ++i)
+        for (int k = A.hptr[i]; k < A.hptr[i + 1]; ++k)
+            if (find(A.hcol[k], i) < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "colour_mesh: pattern is not symmetric");
+    std::vector<int> colour(A.brows, -1);
+    std::vector<char> used;
+    int ncol = 0;
+    for (int e = 0; e < A.brows; ++e) {
+        used.assign(size_t(ncol) + 1, 0);
+        for (int k = A.hptr[e]; k < A.hptr[e + 1]; ++k) {
+            const int j = A.hcol[k];
+            if (j != e && colour[j] >= 0) used[colour[j]] = 1;
+        }
+        int c = 0;
+        while (used[c]) ++c;
+        colour[e] = c;
+        ncol = std::max(ncol, c + 1);
+    }
+    return colour;
+}
+
+// ------------------------------------------------------- diagonal factors
+void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, const double* lambda,
+                    const double* s) {
+    F.n = N;
+    F.bs = bs;
+    F.ld = bs | 1;
+    F.vstride = even_up(int64_t(bs) * F.ld);
+    std::vector<double> hv(size_t(N) * F.vstride, 0.0), lmax(N, 0.0);
+    for (int e = 0; e < N; ++e) {
+        const double* Ve = V + size_t(e) * bs * bs;
+        double* dst = hv.data() + size_t(e) * F.vstride;
+        for (int a = 0; a < bs; ++a)
+            for (int b = 0; b < bs; ++b) dst[size_t(a) * F.ld + b] = Ve[size_t(a) * bs + b];
+        double m = 0.0;  // cwiseAbs().maxCoeff(), blockla.hpp:332
+        for (int i = 0; i < bs; ++i) m = std::max(m, std::abs(lambda[size_t(e) * bs + i]));
+        lmax[e] = bs ? m : 0.0;
+    }
+    F.V.alloc(sizeof(double) * hv.size());
+    F.lambda.alloc(sizeof(double) * size_t(N) * bs);
+    F.scale.alloc(sizeof(double) * size_t(N) * bs);
+    F.lmax.alloc(sizeof(double) * N);
+    LDGMG_CUDA(cudaMemcpy(F.V.p, hv.data(), F.V.bytes, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(F.lambda.p, lambda, F.lambda.bytes, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(F.scale.p, s, F.scale.bytes, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(F.lmax.p, lmax.data(), F.lmax.bytes, cudaMemcpyHostToDevice));
+    (void)ctx;
+}
+
+/// factor_diagonal (smoothers.hpp:464-494): power-of-two equilibration
+/// s_i = 2^-(ex/2) of |D_ii| (frexp exponent), then eig(s D s).
+void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F) {
+    const int N = A.brows, bs = A.rbs;
+    std::vector<int> dk(N, -1);
+    for (int e = 0; e < N; ++e) {
+        for (int k = A.hptr[e]; k < A.hptr[e + 1]; ++k)
+            if (A.hcol[k] == e) dk[e] = k;
+        if (dk[e] < 0) fail(LDGMG_ERR_RUNTIME, "Smoother: missing diagonal block");
+    }
+    // fetch the diagonal blocks in reference (row-major) layout
+    std::vector<double> all(size_t(A.nnzb) * bs * bs);
+    std::vector<int> hp(A.hptr), hc(A.hcol);
+    bsr_download(ctx, A, nullptr, nullptr, all.data());
+    std::vector<double> V(size_t(N) * bs * bs), lam(size_t(N) * bs), sc(size_t(N) * bs);
+    std::vector<int> bad(N, 0);
+    parallel_for(N, [&](int lo, int hi) {
+        std::vector<double> D(size_t(bs) * bs);
+        for (int e = lo; e < hi; ++e) {
+            const double* v = all.data() + size_t(dk[e]) * bs * bs;
+            double* s = sc.data() + size_t(e) * bs;
+            for (int i = 0; i < bs; ++i) {
+                const double d = std::abs(v[size_t(i) * bs + i]);
+                if (d > 0.0) {
+                    int ex = 0;
+                    std::frexp(d, &ex);
+                    s[i] = std::ldexp(1.0, -(ex / 2));
+                } else {
+                    s[i] = 1.0;
+                }
+            }
+            // column-major s D s ((s_i D_ij) s_j, as the shim's diag products)
+            double norm2 = 0.0, asym2 = 0.0;
+            for (int j = 0; j < bs; ++j)
+                for (int i = 0; i < bs; ++i) {
+                    D[size_t(j) * bs + i] = (s[i] * v[size_t(i) * bs + j]) * s[j];
+                    norm2 += D[size_t(j) * bs + i] * D[size_t(j) * bs + i];
+                }
+            for (int j = 0; j < bs; ++j)
+                for (int i = 0; i < bs; ++i) {
+                    const double t = D[size_t(j) * bs + i] - D[size_t(i) * bs + j];
+                    asym2 += t * t;
+                }
+            if (std::sqrt(asym2) > 1e-13 * std::max(1e-300, std::sqrt(norm2))) {
+                bad[e] = 1;
+                continue;
+            }
+            sym_eig_host(bs, D.data(), lam.data() + size_t(e) * bs, V.data() + size_t(e) * bs * bs);
+        }
+    });
+    for (int e = 0; e < N; ++e)
+        if (bad[e]) fail(LDGMG_ERR_INVALID_ARGUMENT, "sym_eig: matrix is not symmetric");
+    upload_factors(ctx, F, N, bs, V.data(), lam.data(), sc.data());
+}
+
+// --------------------------------------------------------------- smoother
+void Smoother::init_common(Ctx& ctx) {
+    N = A->brows;
+    bs = A->rbs;
+    if (A->brows != A->bcols || A->rbs != A->cbs)
+        fail(LDGMG_ERR_INVALID_ARGUMENT, "Smoother: operator must be block-square");
+    if (cfg.kind == LDGMG_COLOURED_GS) cfg.omega = 1.0;  // smoothers.hpp:380
+    if (cfg.kind == LDGMG_COLOURED_GS) {
+        colour = colour_mesh_host(*A);
+        ncolours = N ? 1 + *std::max_element(colour.begin(), colour.end()) : 0;
+        std::vector<int> rows;
+        colour_ptr.assign(ncolours + 1, 0);
+        for (int c = 0; c < ncolours; ++c) {
+            for (int e = 0; e < N; ++e)
+                if (colour[e] == c) rows.push_back(e);
+            colour_ptr[c + 1] = int(rows.size());
+        }
+        colour_rows.alloc(sizeof(int) * std::max<size_t>(1, rows.size()));
+        if (!rows.empty())
+            LDGMG_CUDA(cudaMemcpy(colour_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+    }
+    if (cfg.kind == LDGMG_PROC_BLOCK_GS)
+        fail(LDGMG_ERR_INVALID_ARGUMENT,
+             "Smoother: processor-block GS runs sequential in-partition sweeps and has no GPU "
+             "path (SURVEY.md 2 row 2); use coloured GS");
+    if (cfg.kind == LDGMG_SAI && cfg.level < 0)
+        fail(LDGMG_ERR_INVALID_ARGUMENT, "pattern_power: negative power");
+    snap.alloc(sizeof(double) * std::max<int64_t>(1, int64_t(N) * bs));
+    (void)ctx;
+}
+
+void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep) const {
+    switch (cfg.kind) {
+        case LDGMG_JACOBI: {
+            LDGMG_CUDA(cudaMemcpyAsync(snap.p, x, sizeof(double) * size_t(N) * bs,
+                                       cudaMemcpyDeviceToDevice, ctx.stream));
+            RowPass p;
+            p.A = A;
+            p.mode = MODE_RELAX;
+            p.x = snap.as<double>();
+            p.b = b;
+            p.xe = x;
+            p.y = x;
+            p.nrows = N;
+            p.F = &F;
+            p.omega = cfg.omega;
+            launch_rowpass(ctx, p);
+            break;
+        }
+        case LDGMG_COLOURED_GS: {
+            for (int ci = 0; ci < ncolours; ++ci) {
+                const int c = sweep == LDGMG_SWEEP_FORWARD ? ci : ncolours - 1 - ci;
+                RowPass p;
+                p.A = A;
+                p.mode = MODE_RELAX;
+                p.x = x;
+                p.b = b;
+                p.xe = x;
+                p.y = x;
+                p.rows = colour_rows.as<int>() + colour_ptr[c];
+                p.nrows = colour_ptr[c + 1] - colour_ptr[c];
+                p.F = &F;
+                p.omega = 1.0;
+                launch_rowpass(ctx, p);
+            }
+            break;
+        }
+        case LDGMG_SAI: {
+            double* r = snap.as<double>();
+            RowPass p;
+            p.A = A;
+            p.mode = MODE_RESIDUAL;
+            p.x = x;
+            p.b = b;
+            p.y = r;
+            p.nrows = N;
+            launch_rowpass(ctx, p);
+            RowPass q;
+            q.A = sweep == LDGMG_SWEEP_FORWARD ? B.get() : &bsr_transpose(ctx, *B);
+            q.mode = MODE_ADD;
+            q.x = r;
+            q.xe = x;
+            q.y = x;
+            q.nrows = N;
+            launch_rowpass(ctx, q);
+            break;
+        }
+        default:
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "Smoother: unsupported kind");
+    }
+}
+
+double Smoother::bytes_per_apply() const {
+    const double W = 8.0;
+    const double nb = double(A->nnzb);
+    if (cfg.kind == LDGMG_SAI) return W * (double(bs) * bs * (nb + double(B->nnzb)) + 6.0 * N * bs);
+    const double sweep = W * (double(bs) * bs * (nb - N) + (double(bs) * bs + 2.0 * bs) * N + 3.0 * N * bs);
+    return sweep;
+}
+
+// --------------------------------------------------------------- transfer
+std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, const int* parent_of,
+                                          const int* orthant_of, int dim, int bss, int ncomp,
+                                          const double* K) {
+    require(n_fine >= 0 && n_coarse >= 0 && bss > 0 && ncomp > 0, "transfer: bad shape");
+    require(dim == 2 || dim == 3, "transfer: dim must be 2 or 3");
+    auto T = std::make_unique<Transfer>();
+    T->n_fine = n_fine;
+    T->n_coarse = n_coarse;
+    T->dim = dim;
+    T->bss = bss;
+    T->ncomp = ncomp;
+    T->bs = bss * ncomp;
+    T->hparent.assign(parent_of, parent_of + n_fine);
+    T->horth.assign(orthant_of, orthant_of + n_fine);
+    std::vector<int> cptr(n_coarse + 1, 0), clist(n_fine);
+    for (int f = 0; f < n_fine; ++f) {
+        require(parent_of[f] >= 0 && parent_of[f] < n_coarse, "transfer: parent out of range");
+        require(orthant_of[f] >= -1 && orthant_of[f] < (1 << dim), "transfer: orthant out of range");
+        ++cptr[parent_of[f] + 1];
+    }
+    for (int p = 0; p < n_coarse; ++p) cptr[p + 1] += cptr[p];
+    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    for (int f = 0; f < n_fine; ++f) clist[fill[parent_of[f]]++] = f;  // ascending f per parent
+    const size_t nk = size_t(1) << dim;
+    T->parent.alloc(sizeof(int) * std::max(1, n_fine));
+    T->orth.alloc(sizeof(int) * std::max(1, n_fine));
+    T->child_ptr.alloc(sizeof(int) * (n_coarse + 1));
+    T->child_list.alloc(sizeof(int) * std::max(1, n_fine));
+    T->K.alloc(sizeof(double) * nk * bss * bss);
+    LDGMG_CUDA(cudaMemcpy(T->parent.p, parent_of, sizeof(int) * n_fine, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(T->orth.p, orthant_of, sizeof(int) * n_fine, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(T->child_ptr.p, cptr.data(), sizeof(int) * cptr.size(), cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(T->child_list.p, clist.data(), sizeof(int) * n_fine, cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(T->K.p, K, T->K.bytes, cudaMemcpyHostToDevice));
+    (void)ctx;
+    return T;
+}
+
+// -------------------------------------------------------------- multigrid
+void Mg::init(Ctx& ctx) {
+    require(depth >= 1, "multigrid: empty hierarchy");
+    require(cfg.nu1 >= 0 && cfg.nu2 >= 0, "multigrid: smoothing counts must be nonnegative");
+    if (depth < cfg.min_depth)
+        fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: hierarchy depth below the configured minimum");
+    if (A.back()->brows > cfg.bottom_max_elements)
+        fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: bottom level exceeds the element budget");
+    bs = A[0]->rbs;
+    for (int l = 0; l < depth; ++l) {
+        if (A[l]->rbs != bs || A[l]->cbs != bs || A[l]->brows != A[l]->bcols)
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: level assembler changed the discretization");
+        if (l + 1 < depth) {
+            require(T[l] != nullptr, "multigrid: missing transfer");
+            require(T[l]->n_fine == A[l]->brows && T[l]->n_coarse == A[l + 1]->brows && T[l]->bs == bs,
+                    "multigrid: transfer shape mismatch");
+        }
+    }
+    // level buffers: r[l] fine residual, x/b for coarse levels
+    r.resize(depth);
+    xl.resize(depth);
+    bl.resize(depth);
+    for (int l = 0; l < depth; ++l) {
+        const size_t n = sizeof(double) * std::max<int64_t>(1, int64_t(A[l]->brows) * bs);
+        r[l].alloc(n);
+        if (l > 0) {
+            xl[l].alloc(n);
+            bl[l].alloc(n);
+        }
+    }
+    bp.alloc(sizeof(double) * std::max<int64_t>(1, int64_t(A[0]->brows) * bs));
+    // kernel vectors (ldg_core.hpp:64-78): constant mode 0 of each component
+    std::vector<int> offs;
+    if (kernel_constants)
+        for (int c = 0; c < (system_kind == LDGMG_SYSTEM_SCALAR ? 1 : dim); ++c) offs.push_back(c * bs_scalar);
+    if (kernel_pressure) offs.push_back(dim * bs_scalar);
+    nkernel = int(offs.size());
+    kernel_offs.alloc(sizeof(int) * std::max<size_t>(1, offs.size()));
+    if (!offs.empty())
+        LDGMG_CUDA(cudaMemcpy(kernel_offs.p, offs.data(), sizeof(int) * offs.size(), cudaMemcpyHostToDevice));
+    kval = 1.0 / std::sqrt(double(A[0]->brows));
+    red.alloc(sizeof(double) * 1024);
+    LDGMG_CUDA(cudaMallocHost(&h_red, sizeof(double) * 4));
+    (void)ctx;
+}
+
+void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
+    const Bsr& Ab = *A.back();
+    const int n = Ab.brows * bs;
+    std::vector<double> Vc(size_t(n) * n), lam(n);
+    if (V && lambda) {
+        std::memcpy(Vc.data(), V, sizeof(double) * Vc.size());
+        std::memcpy(lam.data(), lambda, sizeof(double) * n);
+    } else {
+        // dense bottom operator (to_dense, blockla.hpp:241-251), eig on host
+        std::vector<double> vals(size_t(Ab.nnzb) * bs * bs), D(size_t(n) * n, 0.0);
+        bsr_download(ctx, Ab, nullptr, nullptr, vals.data());
+        for (int i = 0; i < Ab.brows; ++i)
+            for (int k = Ab.hptr[i]; k < Ab.hptr[i + 1]; ++k)
+                for (int rr = 0; rr < bs; ++rr)
+                    for (int c = 0; c < bs; ++c)
+                        D[size_t(Ab.hcol[k] * bs + c) * n + size_t(i) * bs + rr] =
+                            vals[size_t(k) * bs * bs + size_t(rr) * bs + c];
+        double nrm = 0.0, asym = 0.0;
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                nrm += D[size_t(j) * n + i] * D[size_t(j) * n + i];
+                const double t = D[size_t(j) * n + i] - D[size_t(i) * n + j];
+                asym += t * t;
+            }
+        if (std::sqrt(asym) > 1e-13 * std::max(1e-300, std::sqrt(nrm)))
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "sym_eig: matrix is not symmetric");
+        sym_eig_host(n, D.data(), lam.data(), Vc.data());
+    }
+    std::vector<double> Vr(size_t(n) * n);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) Vr[size_t(i) * n + k] = Vc[size_t(k) * n + i];
+    bottom.n = n;
+    bottom.lmax = 0.0;
+    for (double l : lam) bottom.lmax = std::max(bottom.lmax, std::abs(l));
+    bottom.Vc.alloc(sizeof(double) * std::max<size_t>(1, Vc.size()));
+    bottom.Vr.alloc(sizeof(double) * std::max<size_t>(1, Vr.size()));
+    bottom.lambda.alloc(sizeof(double) * std::max(1, n));
+    bottom.t.alloc(sizeof(double) * std::max(1, n));
+    LDGMG_CUDA(cudaMemcpy(bottom.Vc.p, Vc.data(), sizeof(double) * Vc.size(), cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(bottom.Vr.p, Vr.data(), sizeof(double) * Vr.size(), cudaMemcpyHostToDevice));
+    LDGMG_CUDA(cudaMemcpy(bottom.lambda.p, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+}
+
+void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
+    if (l + 1 == depth) {
+        launch_pinv_apply(ctx, bottom, cfg.bottom_tol, b, x);
+        return;
+    }
+    const Smoother& S = *sm[l];
+    for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre);
+    RowPass p;
+    p.A = A[l];
+    p.mode = MODE_RESIDUAL;
+    p.x = x;
+    p.b = b;
+    p.y = r[l].as<double>();
+    p.nrows = A[l]->brows;
+    launch_rowpass(ctx, p);
+    launch_restrict(ctx, *T[l], r[l].as<double>(), bl[l + 1].as<double>());
+    LDGMG_CUDA(cudaMemsetAsync(xl[l + 1].p, 0, sizeof(double) * size_t(A[l + 1]->brows) * bs, ctx.stream));
+    v_cycle(ctx, l + 1, xl[l + 1].as<double>(), bl[l + 1].as<double>());
+    launch_prolong_add(ctx, *T[l], xl[l + 1].as<double>(), x);
+    for (int i = 0; i < cfg.nu2; ++i) S.apply(ctx, b, x, cfg.post);
+}
+
+void Mg::project(Ctx& ctx, double* v) {
+    launch_project_constants(ctx, v, A[0]->brows, bs, kernel_offs.as<int>(), nkernel, kval, strict_order);
+}
+
+void Mg::cycle(Ctx& ctx, double* x, const double* b) {
+    v_cycle(ctx, 0, x, b);
+    project(ctx, x);
+}
+
+void Mg::apply(Ctx& ctx, const double* b, double* x) {
+    const size_t n = sizeof(double) * size_t(A[0]->brows) * bs;
+    LDGMG_CUDA(cudaMemsetAsync(x, 0, n, ctx.stream));
+    if (nkernel == 0) {
+        v_cycle(ctx, 0, x, b);
+        return;
+    }
+    LDGMG_CUDA(cudaMemcpyAsync(bp.p, b, n, cudaMemcpyDeviceToDevice, ctx.stream));
+    project(ctx, bp.as<double>());
+    v_cycle(ctx, 0, x, bp.as<double>());
+    project(ctx, x);
+}
+
+void Mg::cycles(Ctx& ctx, double* x, const double* b, int n) {
+    if (n <= 0) return;
+    if (!warm) {  // first run un-captured: sets kernel attributes, lazy transposes
+        cycle(ctx, x, b);
+        --n;
+        warm = true;
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    if (n <= 0) return;
+    Graph* G = nullptr;
+    for (auto& g : graphs)
+        if (g.x == x && g.b == b && g.s == ctx.stream) G = &g;
+    if (!G) {
+        Graph ng{x, b, ctx.stream, nullptr, 0};
+        cudaGraph_t graph;
+        const int64_t c0 = launch_counter().load();
+        LDGMG_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+        cycle(ctx, x, b);
+        LDGMG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
+        // captured launches did not run; they are counted per graph launch
+        ng.nkernels = launch_counter().load() - c0;
+        launch_counter().fetch_sub(ng.nkernels);
+        LDGMG_CUDA(cudaGraphInstantiate(&ng.exec, graph, 0));
+        LDGMG_CUDA(cudaGraphDestroy(graph));
+        graphs.push_back(ng);
+        G = &graphs.back();
+    }
+    for (int i = 0; i < n; ++i) {
+        LDGMG_CUDA(cudaGraphLaunch(G->exec, ctx.stream));
+        launch_counter().fetch_add(G->nkernels, std::memory_order_relaxed);
+    }
+}
+
+double Mg::dof_updates_per_cycle() const {
+    double s = 0.0;
+    for (int l = 0; l + 1 < depth; ++l) s += double(cfg.nu1 + cfg.nu2) * A[l]->brows * bs;
+    return s;
+}
+
+double Mg::bytes_per_cycle() const {
+    const double W = 8.0;
+    double s = 0.0;
+    for (int l = 0; l + 1 < depth; ++l) {
+        const double N = A[l]->brows, Nc = A[l + 1]->brows;
+        s += double(cfg.nu1 + cfg.nu2) * sm[l]->bytes_per_apply();
+        s += W * (double(bs) * bs * double(A[l]->nnzb) + 3.0 * bs * N);  // residual
+        s += W * (bs * N + bs * Nc) + W * (bs * Nc + 2.0 * bs * N);      // transfers
+    }
+    s += W * 2.0 * double(bottom.n) * bottom.n;
+    return s;
+}
+
+Mg::~Mg() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (h_red) cudaFreeHost(h_red);
+}
+
+}  // namespace ldgmg_b200

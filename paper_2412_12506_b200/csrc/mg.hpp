@@ -1,0 +1,86 @@
+// Smoother / multigrid objects behind the C ABI handles.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "core.hpp"
+
+namespace ldgmg_b200 {
+
+std::vector<int> colour_mesh_host(const Bsr& A);
+void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, const double* lambda,
+                    const double* s);
+void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F);
+std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, const int* parent_of,
+                                          const int* orthant_of, int dim, int bss, int ncomp,
+                                          const double* K);
+
+/// SAI build on the GPU (sai_build.cu): B on the pattern of A^level.
+struct SaiResult {
+    std::unique_ptr<Bsr> B;
+    ldgmg_sai_stats stats{};
+};
+SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level,
+                        double zeta, bool cache);
+
+struct Smoother {
+    const Bsr* A = nullptr;
+    ldgmg_smoother_config cfg{};
+    int system_kind = LDGMG_SYSTEM_SCALAR, n_velocity = 0;
+    int N = 0, bs = 0;
+    DiagFactors F;
+    std::vector<int> colour, colour_ptr;
+    int ncolours = 0;
+    DevBuf colour_rows;
+    std::unique_ptr<Bsr> B;
+    ldgmg_sai_stats stats{};
+    DevBuf snap;  // Jacobi snapshot / SAI residual scratch
+
+    void init_common(Ctx& ctx);
+    void apply(Ctx& ctx, const double* b, double* x, int sweep) const;
+    double bytes_per_apply() const;
+};
+
+struct Mg {
+    int depth = 0;
+    std::vector<const Bsr*> A;
+    std::vector<const Transfer*> T;
+    std::vector<Smoother*> sm;
+    // owned pieces (problem-built hierarchies / default smoothers)
+    std::vector<std::unique_ptr<Bsr>> own_A;
+    std::vector<std::unique_ptr<Transfer>> own_T;
+    std::vector<std::unique_ptr<Smoother>> own_sm;
+    ldgmg_mg_config cfg{};
+    int system_kind = LDGMG_SYSTEM_SCALAR, dim = 2, n_comp = 1, bs_scalar = 1, bs = 1;
+    int kernel_constants = 0, kernel_pressure = 0, n_velocity = 0;
+    bool strict_order = false;  // reference-order (sequential) kernel projection
+    DenseEig bottom;
+    std::vector<DevBuf> r, xl, bl;
+    DevBuf bp, kernel_offs, red;
+    int nkernel = 0;
+    double kval = 0.0;
+    double* h_red = nullptr;
+    bool warm = false;
+    struct Graph {
+        double* x;
+        const double* b;
+        cudaStream_t s;
+        cudaGraphExec_t exec;
+        int64_t nkernels;
+    };
+    std::vector<Graph> graphs;
+
+    void init(Ctx& ctx);
+    void set_bottom(Ctx& ctx, const double* V, const double* lambda);
+    void v_cycle(Ctx& ctx, int l, double* x, const double* b);
+    void project(Ctx& ctx, double* v);
+    void cycle(Ctx& ctx, double* x, const double* b);
+    void apply(Ctx& ctx, const double* b, double* x);
+    void cycles(Ctx& ctx, double* x, const double* b, int n);
+    double dof_updates_per_cycle() const;
+    double bytes_per_cycle() const;
+    ~Mg();
+};
+
+}  // namespace ldgmg_b200

@@ -1,0 +1,42 @@
+// Built-in host setup: uniform Morton meshes, the coarsening chain and the
+// LDG scalar / Stokes operators per level (the L0/L2 producers the V-cycle
+// consumes; the reference's mesh.hpp, basis.hpp, ldg_core.hpp, ldg_scalar.hpp,
+// ldg_stokes.hpp and multigrid.hpp:168-241, restated).  Host C++, threaded
+// over element rows.  The accumulation order of every block follows the
+// reference (BlockBuilder insertion order, accumulate_AtDB source order,
+// face_block loop nest), so the operators come out bit-identical to the
+// oracle build (tests/test_setup_parity.py).
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "../../include/ldgmg_b200.h"
+
+namespace ldgmg_b200 {
+
+struct HostCsr {
+    int brows = 0, bs = 0;
+    std::vector<int> ptr, col;
+    std::vector<double> val;
+};
+
+struct ProblemLevel {
+    int n = 0;  // elements per axis
+    HostCsr A;
+    std::vector<int> phase;
+    std::vector<int> parent_of, orthant_of;  // to the next coarser level
+};
+
+struct Problem {
+    ldgmg_problem_spec spec{};
+    int kind = 0, dim = 2, degree = 1, n_comp = 1, bs_scalar = 1;
+    int kernel_constants = 0, kernel_pressure = 0;
+    std::vector<ProblemLevel> levels;
+    std::vector<double> inject;  // 2^dim matrices bs_scalar^2, row-major
+};
+
+void problem_build(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements,
+                   Problem& out);
+
+}  // namespace ldgmg_b200
