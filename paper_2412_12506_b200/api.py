@@ -49,6 +49,15 @@ class Context:
         check(lib.ldgmg_ctx_create(int(device), C.byref(h)))
         self.h = h
         self.device = device
+        if stream is None:
+            # Device vectors are torch tensors: run on torch's current stream so
+            # the caching allocator's stream-ordered reuse stays race-free.
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device)
+            except ImportError:
+                pass
         if stream is not None:
             self.set_stream(stream)
 

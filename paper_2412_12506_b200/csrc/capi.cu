@@ -291,7 +291,7 @@ int ldgmg_smoother_create(ldgmg_ctx* ctx, const ldgmg_bsr* A, int system_kind, i
         s.init_common(*ctx);
         if (s.cfg.kind == LDGMG_SAI) {
             SaiResult r = build_sai_gpu(*ctx, *A, system_kind, n_velocity, s.cfg.level, s.cfg.zeta,
-                                        s.cfg.cache != 0);
+                                        s.cfg.cache != 0, nullptr);
             s.B = std::move(r.B);
             s.stats = r.stats;
         } else {
@@ -386,14 +386,14 @@ int ldgmg_smoother_diag_factors(ldgmg_ctx* ctx, const ldgmg_smoother* S, double*
         const int bs = F.bs;
         if (V) {
             std::vector<double> hv(size_t(F.n) * F.vstride);
-            LDGMG_CUDA(cudaMemcpy(hv.data(), F.V.p, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+            d2h(*ctx, hv.data(), F.V.p, sizeof(double) * hv.size());
             for (int e = 0; e < F.n; ++e)
                 for (int a = 0; a < bs; ++a)
                     for (int b = 0; b < bs; ++b)
                         V[(size_t(e) * bs + a) * bs + b] = hv[size_t(e) * F.vstride + size_t(a) * F.ld + b];
         }
-        if (lambda) LDGMG_CUDA(cudaMemcpy(lambda, F.lambda.p, F.lambda.bytes, cudaMemcpyDeviceToHost));
-        if (s) LDGMG_CUDA(cudaMemcpy(s, F.scale.p, F.scale.bytes, cudaMemcpyDeviceToHost));
+        if (lambda) d2h(*ctx, lambda, F.lambda.p, F.lambda.bytes);
+        if (s) d2h(*ctx, s, F.scale.p, F.scale.bytes);
     });
 }
 
@@ -440,6 +440,7 @@ int ldgmg_transfer_destroy(ldgmg_transfer* T) {
 // ------------------------------------------------------------ multigrid
 static void mg_default_smoothers(ldgmg_ctx* ctx, Mg& m) {
     m.sm.assign(m.depth, nullptr);
+    if (!m.sai_cache) m.sai_cache = sai_cache_new();
     for (int l = 0; l + 1 < m.depth; ++l) {
         auto s = std::make_unique<Smoother>();
         s->A = m.A[l];
@@ -449,7 +450,7 @@ static void mg_default_smoothers(ldgmg_ctx* ctx, Mg& m) {
         s->init_common(*ctx);
         if (s->cfg.kind == LDGMG_SAI) {
             SaiResult r = build_sai_gpu(*ctx, *m.A[l], m.system_kind, m.n_velocity, s->cfg.level,
-                                        s->cfg.zeta, s->cfg.cache != 0);
+                                        s->cfg.zeta, s->cfg.cache != 0, m.sai_cache);
             s->B = std::move(r.B);
             s->stats = r.stats;
         } else {

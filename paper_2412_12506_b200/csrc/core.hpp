@@ -28,6 +28,19 @@ struct Ctx {
     double* h_red = nullptr;
 };
 
+/// Host<->device copies ordered on the context stream (setup paths; the
+/// legacy-stream cudaMemcpy would race with the non-blocking context stream).
+inline void h2d(Ctx& ctx, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    LDGMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx.stream));
+    LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+inline void d2h(Ctx& ctx, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    LDGMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx.stream));
+    LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
 /// RAII device allocation.
 struct DevBuf {
     void* p = nullptr;

@@ -68,10 +68,10 @@ void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, co
     F.lambda.alloc(sizeof(double) * size_t(N) * bs);
     F.scale.alloc(sizeof(double) * size_t(N) * bs);
     F.lmax.alloc(sizeof(double) * N);
-    LDGMG_CUDA(cudaMemcpy(F.V.p, hv.data(), F.V.bytes, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(F.lambda.p, lambda, F.lambda.bytes, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(F.scale.p, s, F.scale.bytes, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(F.lmax.p, lmax.data(), F.lmax.bytes, cudaMemcpyHostToDevice));
+    h2d(ctx, F.V.p, hv.data(), F.V.bytes);
+    h2d(ctx, F.lambda.p, lambda, F.lambda.bytes);
+    h2d(ctx, F.scale.p, s, F.scale.bytes);
+    h2d(ctx, F.lmax.p, lmax.data(), F.lmax.bytes);
     (void)ctx;
 }
 
@@ -149,7 +149,7 @@ void Smoother::init_common(Ctx& ctx) {
         }
         colour_rows.alloc(sizeof(int) * std::max<size_t>(1, rows.size()));
         if (!rows.empty())
-            LDGMG_CUDA(cudaMemcpy(colour_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+            h2d(ctx, colour_rows.p, rows.data(), sizeof(int) * rows.size());
     }
     if (cfg.kind == LDGMG_PROC_BLOCK_GS)
         fail(LDGMG_ERR_INVALID_ARGUMENT,
@@ -260,11 +260,11 @@ std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, co
     T->child_ptr.alloc(sizeof(int) * (n_coarse + 1));
     T->child_list.alloc(sizeof(int) * std::max(1, n_fine));
     T->K.alloc(sizeof(double) * nk * bss * bss);
-    LDGMG_CUDA(cudaMemcpy(T->parent.p, parent_of, sizeof(int) * n_fine, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(T->orth.p, orthant_of, sizeof(int) * n_fine, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(T->child_ptr.p, cptr.data(), sizeof(int) * cptr.size(), cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(T->child_list.p, clist.data(), sizeof(int) * n_fine, cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(T->K.p, K, T->K.bytes, cudaMemcpyHostToDevice));
+    h2d(ctx, T->parent.p, parent_of, sizeof(int) * n_fine);
+    h2d(ctx, T->orth.p, orthant_of, sizeof(int) * n_fine);
+    h2d(ctx, T->child_ptr.p, cptr.data(), sizeof(int) * cptr.size());
+    h2d(ctx, T->child_list.p, clist.data(), sizeof(int) * n_fine);
+    h2d(ctx, T->K.p, K, T->K.bytes);
     (void)ctx;
     return T;
 }
@@ -308,7 +308,7 @@ void Mg::init(Ctx& ctx) {
     nkernel = int(offs.size());
     kernel_offs.alloc(sizeof(int) * std::max<size_t>(1, offs.size()));
     if (!offs.empty())
-        LDGMG_CUDA(cudaMemcpy(kernel_offs.p, offs.data(), sizeof(int) * offs.size(), cudaMemcpyHostToDevice));
+        h2d(ctx, kernel_offs.p, offs.data(), sizeof(int) * offs.size());
     kval = 1.0 / std::sqrt(double(A[0]->brows));
     red.alloc(sizeof(double) * 1024);
     LDGMG_CUDA(cudaMallocHost(&h_red, sizeof(double) * 4));
@@ -353,9 +353,9 @@ void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
     bottom.Vr.alloc(sizeof(double) * std::max<size_t>(1, Vr.size()));
     bottom.lambda.alloc(sizeof(double) * std::max(1, n));
     bottom.t.alloc(sizeof(double) * std::max(1, n));
-    LDGMG_CUDA(cudaMemcpy(bottom.Vc.p, Vc.data(), sizeof(double) * Vc.size(), cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(bottom.Vr.p, Vr.data(), sizeof(double) * Vr.size(), cudaMemcpyHostToDevice));
-    LDGMG_CUDA(cudaMemcpy(bottom.lambda.p, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    h2d(ctx, bottom.Vc.p, Vc.data(), sizeof(double) * Vc.size());
+    h2d(ctx, bottom.Vr.p, Vr.data(), sizeof(double) * Vr.size());
+    h2d(ctx, bottom.lambda.p, lam.data(), sizeof(double) * n);
 }
 
 void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
@@ -418,9 +418,15 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n) {
         Graph ng{x, b, ctx.stream, nullptr, 0};
         cudaGraph_t graph;
         const int64_t c0 = launch_counter().load();
-        LDGMG_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
-        cycle(ctx, x, b);
-        LDGMG_CUDA(cudaStreamEndCapture(ctx.stream, &graph));
+        // capture on a private non-blocking stream (the context stream may be
+        // the legacy default stream, which cannot be captured)
+        if (!cap_stream) LDGMG_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+        Ctx cctx = ctx;
+        cctx.stream = cap_stream;
+        LDGMG_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+        cycle(cctx, x, b);
+        LDGMG_CUDA(cudaStreamEndCapture(cap_stream, &graph));
         // captured launches did not run; they are counted per graph launch
         ng.nkernels = launch_counter().load() - c0;
         launch_counter().fetch_sub(ng.nkernels);
@@ -457,6 +463,8 @@ double Mg::bytes_per_cycle() const {
 Mg::~Mg() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (h_red) cudaFreeHost(h_red);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (sai_cache) sai_cache_free(sai_cache);
 }
 
 }  // namespace ldgmg_b200

@@ -21,8 +21,11 @@ struct SaiResult {
     std::unique_ptr<Bsr> B;
     ldgmg_sai_stats stats{};
 };
+struct SaiCache;  // least-squares solution cache, shareable across builds
+SaiCache* sai_cache_new();
+void sai_cache_free(SaiCache* c);
 SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level,
-                        double zeta, bool cache);
+                        double zeta, bool cache, SaiCache* shared);
 
 struct Smoother {
     const Bsr* A = nullptr;
@@ -70,6 +73,8 @@ struct Mg {
         int64_t nkernels;
     };
     std::vector<Graph> graphs;
+    cudaStream_t cap_stream = nullptr;
+    SaiCache* sai_cache = nullptr;  // shared across levels (multigrid.hpp:60)
 
     void init(Ctx& ctx);
     void set_bottom(Ctx& ctx, const double* V, const double* lambda);

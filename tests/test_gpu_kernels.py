@@ -67,7 +67,7 @@ def test_spmv_and_transpose_bitwise(ctx, ref, shape):
     assert bits_equal(host(yt), want_t)
     # shape errors raise like the reference (blockla.hpp:137)
     with pytest.raises(g.InvalidArgument, match="shape mismatch"):
-        g.spmv(ctx, A, dev(xt), y)
+        g.spmv(ctx, A, dev(rand(bcols * cbs + 1, 3)), y)
     # round trip of the device layout
     p2, c2, v2 = A.download()
     assert np.array_equal(p2, ptr) and np.array_equal(c2, col) and bits_equal(v2, val)

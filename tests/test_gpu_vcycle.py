@@ -106,8 +106,12 @@ def test_standalone_solve_matches_reference_history(ctx, ref, name):
     xr, hr, itr = R.solve(b, tol=1e-10, maxit=60)
     xg, hg, itg = mg.solve_host(b, tol=1e-10, maxit=60)
     assert itg == itr, (hg, hr)
-    assert np.max(np.abs(hg - hr)) <= 1e-12
-    assert np.linalg.norm(xg - xr) <= 1e-10 * np.linalg.norm(xr)
+    # relative per iteration (some interface configs diverge as *stationary*
+    # iterations in the reference too -- the paper wraps them in GMRES; the
+    # histories must still track each other)
+    assert np.all(np.abs(hg - hr) <= 1e-12 * np.maximum(hr, 1.0)), np.max(np.abs(hg - hr) / np.maximum(hr, 1.0))
+    if hr[-1] <= 1e-10:
+        assert np.linalg.norm(xg - xr) <= 1e-10 * np.linalg.norm(xr)
 
 
 def test_zero_guess_vcycle_is_linear_and_fixes_zero(ctx, ref):
