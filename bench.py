@@ -1,0 +1,300 @@
+"""Benchmark driver (contract in the task statement; workload in DESIGN.md §5).
+
+Headline workload = BASELINE.json configs[1] (C2): 3D Poisson, LDG p=2 on the
+periodic 32^3 Cartesian mesh (27x27 FP64 blocks, 7-block stencil), V-cycle
+with the balanced SAI1 smoother (nu1 = nu2 = 3, pre forward / post reverse,
+down to 2^3), random-init-free: the operator is assembled by the built-in
+setup, the right-hand side is the reference's seeded uniform[-1,1] draw with
+the constant mode removed.
+
+A step is one V-cycle (graph-launched) on device-resident x, b.
+metric = V-cycle DOF-updates/s = sum_{l<L} (nu1+nu2) N_l bs per cycle x cycles / s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 runs under torchrun: every rank runs its own replica of the workload
+(weak scaling), max over ranks of the device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V-cycle DOF-updates/sec"
+UNIT = "DOF-updates/s"
+
+
+def workload(full=True):
+    import paper_2412_12506_b200 as g
+    n = 32 if full else 16
+    spec = g.ProblemSpec(kind=g.SYSTEM_SCALAR, dim=3, n=n, degree=2, bc=(g.BC_PERIODIC,) * 6,
+                         beta=4.0)  # harness default beta = p^2 (harness.hpp:66-68)
+    cfg = g.MultigridConfig(smoother=g.SmootherConfig.sai(1, 0.1), pre=g.SWEEP_FORWARD, post=g.SWEEP_REVERSE,
+                            nu1=3, nu2=3, bottom_max_elements=64, bottom_tol=1e-10, min_depth=2)
+    return spec, cfg
+
+
+def rhs(n, bs, seed=0):
+    import paper_2412_12506_b200 as g
+    b = g.random_rhs(n, bs, seed)
+    idx = np.arange(n) * bs  # constant mode (kernel of the periodic operator)
+    b[idx] -= b[idx].mean()
+    return b
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def cpu_reference(spec_full, cfg, steps, warmup, nthreads, sample_n=16):
+    """The reference's own CPU V-cycle (oracle/_ref built from the unmodified
+    reference headers), run as `nthreads` independent solves in parallel (the
+    reference's run_cells parallelism, harness.hpp:305-327)."""
+    from oracle import ref
+    import paper_2412_12506_b200 as g
+    spec, _ = workload(full=False)
+    spec.n = sample_n
+    R = ref.RefMultigrid(spec, cfg)
+    n, bs, _ = R.shape(0)
+    b = rhs(n, bs)
+    dof = sum((cfg.nu1 + cfg.nu2) * R.shape(l)[0] * R.shape(l)[1] for l in range(R.depth - 1))
+    R.cycles_parallel(b, max(1, warmup), 1)
+    per_step, cyc = [], max(1, steps)
+    secs = R.cycles_parallel(b, cyc, nthreads)
+    value = dof * cyc * nthreads / secs
+    return value, {"sample": f"C2 stencil at {sample_n}^3 (N={n}, p=2, SAI1, nu=3+3), {cyc} V-cycles x "
+                             f"{nthreads} independent solves", "cores": nthreads, "seconds": secs}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    spec, cfg = workload()
+    try:
+        from oracle import ref
+        if not ref.available():
+            raise FileNotFoundError("oracle/_ref not built")
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return
+    nthreads = os.cpu_count() or 1
+    value, info = cpu_reference(spec, cfg, args.steps, args.warmup, nthreads)
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2: 3D Poisson LDG p=2 periodic 32^3, SAI1 V-cycle nu=3+3",
+                   "cpu_sample": info["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                         "sample": info["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_2412_12506_b200 as g
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = g.Context(local, stream=stream)
+
+    spec, cfg = workload()
+    t0 = time.time()
+    P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+    t_asm = time.time() - t0
+    t0 = time.time()
+    mg = g.Multigrid(ctx, cfg, P)
+    torch.cuda.synchronize()
+    t_mg = time.time() - t0
+    n, bs = mg.n, mg.bs
+    dof_cycle, bytes_cycle = mg.cycle_costs()
+    b_host = rhs(n, bs)
+    b = torch.as_tensor(b_host).cuda()
+    x = torch.zeros_like(b)
+
+    # warm-up (also captures the CUDA graph)
+    mg.cycles(x, b, args.warmup)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = g.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        mg.cycles(x, b, args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = g.launch_count() - l0
+    t = e0.elapsed_time(e1) * 1e-3
+    if ws > 1:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    value = dof_cycle * args.steps * ws / t
+
+    # ---- dominant kernel: the level-0 SAI sweep (residual row pass + B r row pass)
+    S0 = mg.smoother(0)
+    A0 = P.level_shape(0)
+    nnzb_a = A0[2]
+    nnzb_b = S0.sai_nnzb()
+    alg = 8.0 * (bs * bs * (nnzb_a + nnzb_b) + 6 * bs * n)
+    xs = torch.rand_like(b)
+    for _ in range(3):
+        S0.apply(b, xs, g.SWEEP_FORWARD)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    k0.record(stream)
+    for _ in range(reps):
+        S0.apply(b, xs, g.SWEEP_FORWARD)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    tk = k0.elapsed_time(k1) * 1e-3 / reps
+    pk = peaks()
+    peak = pk.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("sai_sweep_level0_bytes")
+    except Exception:
+        pass
+
+    # ---- end to end: host buffers through the C ABI (solve to 1e-10)
+    torch.cuda.synchronize()
+    te0 = time.perf_counter()
+    xh, hist, iters = mg.solve_host(b_host, tol=1e-10, maxit=100)
+    te = time.perf_counter() - te0
+    e2e_value = dof_cycle * iters / te
+    e2e_ws = torch.tensor([e2e_value], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        torch.distributed.all_reduce(e2e_ws, op=torch.distributed.ReduceOp.MIN)
+    e2e_value = float(e2e_ws.item()) * ws
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref
+            if ref.available():
+                nthreads = os.cpu_count() or 1
+                cv, info = cpu_reference(spec, cfg, 2, 1, nthreads)
+                cpu = {"value": cv, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                       "sample": info["sample"]}
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: 3D Poisson LDG p=2, periodic 32^3 (N=32768, 27x27 FP64 blocks, 7-block "
+                                   "stencil), SAI1 V-cycle nu=3+3 fwd/rev to 2^3, 5 levels",
+                       "fine_dof": n * bs, "dof_updates_per_cycle": dof_cycle,
+                       "alg_bytes_per_cycle": bytes_cycle, "parallelism": f"replicas x{ws}",
+                       "l2": "no flush: per-cycle working set (A+B+B^T, ~4.6 GB) >> 126 MB L2",
+                       "setup_s": {"assembly": round(t_asm, 2), "hierarchy_gpu": round(t_mg, 2)},
+                       "solve": {"tol": 1e-10, "iterations": iters, "final_relres": float(hist[-1])}},
+            "roofline": {"bound": "hbm", "kernel": "level-0 SAI sweep: residual + B r row passes (rowpass_kernel)",
+                         "achieved": alg / tk / 1e9, "peak": peak, "unit": "GB/s", "frac": alg / tk / 1e9 / peak,
+                         "traffic": traffic, "alg_bytes_per_launch_pair": alg, "ms": tk * 1e3,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+            "vcycle_hbm_GBps": bytes_cycle * args.steps / t / 1e9,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * n * bs),
+                    "d2h_bytes_per_step": int(8 * n * bs + 8 * (iters + 1)),
+                    "step": f"one ldgmg_mg_solve_host call from pageable host buffers to 1e-10 "
+                            f"({iters} V-cycles + residual checks)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -210,6 +210,11 @@ class Smoother:
         check(lib.ldgmg_smoother_colours(self.h, None, C.byref(n)))
         return n.value
 
+    def sai_nnzb(self) -> int:
+        nnzb = C.c_int64()
+        check(lib.ldgmg_smoother_sai_nnzb(self.h, C.byref(nnzb)))
+        return nnzb.value
+
     def sai_matrix(self):
         nnzb = C.c_int64()
         check(lib.ldgmg_smoother_sai_nnzb(self.h, C.byref(nnzb)))
