@@ -337,6 +337,7 @@ std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs
         require(A->hptr[i + 1] >= A->hptr[i], "bsr_upload: ptr must be nondecreasing");
     A->nnzb = A->hptr[brows];
     A->hcol.assign(col, col + A->nnzb);
+    set_max_row(*A);
     for (int i = 0; i < brows; ++i)
         for (int k = A->hptr[i]; k < A->hptr[i + 1]; ++k) {
             require(A->hcol[k] >= 0 && A->hcol[k] < bcols, "bsr_upload: column out of range");
@@ -404,6 +405,7 @@ const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A) {
             T->hcol[q] = i;
             perm[q] = k;
         }
+    set_max_row(*T);
     T->ptr.alloc(sizeof(int) * (T->brows + 1));
     T->col.alloc(sizeof(int) * std::max<int64_t>(1, T->nnzb));
     T->val.alloc(sizeof(double) * std::max<int64_t>(1, T->nnzb * T->blk_stride));
@@ -424,9 +426,136 @@ const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A) {
     return *A.T;
 }
 
+namespace {
+
+/// Split-row variant for SMALL levels (few rows per SM): one CTA per block
+/// row, its blocks spread over the warps (each warp computes whole s_k dot
+/// products for its blocks straight from L2/HBM), then warp 0 combines the
+/// s_k in CSR order -- the same arithmetic, bit for bit, as rowpass_kernel,
+/// with the per-row latency of one block instead of the whole row.
+/// Requires rbs, cbs <= 32.
+__global__ void __launch_bounds__(256) rowsplit_kernel(const RowPassArgs a, int maxlen) {
+    extern __shared__ __align__(16) double ss[];  // maxlen x 32 partial sums, then u, t
+    double* ubuf = ss + size_t(maxlen) * 32;
+    double* tbuf = ubuf + 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    const bool relax = a.mode == MODE_RELAX;
+    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) {
+        const int row = row_at(a, slot);
+        const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
+        for (int k = k0 + warp; k < k1; k += W) {
+            const int j = __ldg(a.col + k);
+            if (relax && j == row) continue;
+            if (lane < a.rbs) {
+                const double* Bc = a.val + size_t(k) * a.blk_stride + lane;
+                const double* xj = a.x + size_t(j) * a.cbs;
+                double s = 0.0;
+#pragma unroll 9
+                for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, __ldg(Bc + size_t(c) * a.rbs), xj[c]);
+                ss[size_t(k - k0) * 32 + lane] = s;
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const bool act = lane < a.rbs;
+            const size_t o = size_t(row) * a.rbs + lane;
+            double acc = 0.0;
+            if (act) {
+                if (relax) {
+                    acc = __ldg(a.b + o);
+                    for (int k = k0; k < k1; ++k)
+                        if (__ldg(a.col + k) != row) acc = __dsub_rn(acc, ss[size_t(k - k0) * 32 + lane]);
+                } else {
+                    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, ss[size_t(k - k0) * 32 + lane]);
+                }
+            }
+            if (relax) {
+                const int bs = a.rbs, ld = a.ld;
+                const double* Ve = a.V + size_t(row) * a.vstride;
+                const double sc = act ? __ldg(a.scal + o) : 0.0;
+                const double lam = act ? __ldg(a.lam + o) : 0.0;
+                const double xe = act ? a.xe[o] : 0.0;
+                if (act) ubuf[lane] = __dmul_rn(sc, acc);
+                __syncwarp();
+                if (act) {
+                    double tt = 0.0;
+                    const double* Vcol = Ve + size_t(lane) * ld;
+                    for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, __ldg(Vcol + kk), ubuf[kk]);
+                    const double cut = a.kernel_tol * __ldg(a.lmax + row);
+                    tbuf[lane] = fabs(lam) <= cut ? 0.0 : tt / lam;
+                }
+                __syncwarp();
+                if (act) {
+                    double w = 0.0;
+                    for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, __ldg(Ve + size_t(kk) * ld + lane), tbuf[kk]);
+                    const double yv = __dmul_rn(sc, w);
+                    acc = __dadd_rn(__dmul_rn(1.0 - a.omega, xe), __dmul_rn(a.omega, yv));
+                }
+            }
+            if (act) {
+                double out;
+                switch (a.mode) {
+                    case MODE_RESIDUAL: out = __dsub_rn(__ldg(a.b + o), acc); break;
+                    case MODE_ADD: out = __dadd_rn(a.xe[o], acc); break;
+                    default: out = acc; break;
+                }
+                a.y[o] = out;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int split_threshold_rows(const Ctx& ctx) {
+    static int env = -2;
+    if (env == -2) {
+        const char* s = getenv("LDGMG_SPLIT_ROWS");
+        env = s ? atoi(s) : -1;
+    }
+    return env >= 0 ? env : 32 * ctx.num_sms;
+}
+
+}  // namespace
+
 void launch_rowpass(Ctx& ctx, const RowPass& p) {
     const Bsr& A = *p.A;
     if (p.nrows == 0) return;
+    if (A.rbs <= 32 && A.cbs <= 32 && p.nrows <= split_threshold_rows(ctx)) {
+        RowPassArgs a{};
+        a.ptr = A.ptr.as<int>();
+        a.col = A.col.as<int>();
+        a.val = A.val.as<double>();
+        a.blk_stride = A.blk_stride;
+        a.rbs = A.rbs;
+        a.cbs = A.cbs;
+        a.mode = p.mode;
+        a.x = p.x;
+        a.b = p.b;
+        a.xe = p.xe;
+        a.y = p.y;
+        a.rows = p.rows;
+        a.nrows = p.nrows;
+        a.omega = p.omega;
+        a.kernel_tol = p.kernel_tol;
+        if (p.mode == MODE_RELAX) {
+            require(p.F != nullptr && A.rbs == A.cbs && p.F->bs == A.rbs, "relax: factor shape mismatch");
+            a.V = p.F->V.as<double>();
+            a.lam = p.F->lambda.as<double>();
+            a.scal = p.F->scale.as<double>();
+            a.lmax = p.F->lmax.as<double>();
+            a.ld = p.F->ld;
+            a.vstride = p.F->vstride;
+        }
+        const int maxlen = std::max(1, A.max_row);
+        const int warps = std::min(8, maxlen);
+        const size_t smem = sizeof(double) * (size_t(maxlen) * 32 + 64);
+        if (smem > 48 * 1024)
+            LDGMG_CUDA(cudaFuncSetAttribute(rowsplit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const int grid = std::min(p.nrows, ctx.num_sms * 16);
+        rowsplit_kernel<<<grid, warps * 32, smem, ctx.stream>>>(a, maxlen);
+        after_launch("rowsplit_kernel");
+        return;
+    }
     RowPassArgs a{};
     a.ptr = A.ptr.as<int>();
     a.col = A.col.as<int>();

@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -77,6 +78,7 @@ struct Bsr {
     int brows = 0, bcols = 0, rbs = 0, cbs = 0;
     int64_t nnzb = 0;
     int blk_stride = 0;  // doubles per stored block
+    int max_row = 0;     // longest block row (split-row kernel scratch)
     DevBuf ptr, col, val;
     std::vector<int> hptr, hcol;
     std::unique_ptr<Bsr> T;  // lazily built transpose (spmv_transpose, B^T sweeps)
@@ -84,6 +86,11 @@ struct Bsr {
 };
 
 inline int even_up(int64_t n) { return int((n + 1) & ~int64_t(1)); }
+
+inline void set_max_row(Bsr& A) {
+    A.max_row = 0;
+    for (int i = 0; i < A.brows; ++i) A.max_row = std::max(A.max_row, A.hptr[i + 1] - A.hptr[i]);
+}
 
 /// Upload from the reference layout (row-major blocks) to the device layout.
 std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
@@ -120,6 +127,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p);
 // ---- transfers / dense / BLAS-1 (vec_kernels.cu) ---------------------------
 struct Transfer {
     int n_fine = 0, n_coarse = 0, dim = 2, bss = 0, ncomp = 1, bs = 0;
+    int max_children = 0;
     DevBuf parent, orth, child_ptr, child_list, K;
     std::vector<int> hparent, horth;
 };

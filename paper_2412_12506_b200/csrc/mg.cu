@@ -254,6 +254,7 @@ std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, co
     for (int p = 0; p < n_coarse; ++p) cptr[p + 1] += cptr[p];
     std::vector<int> fill(cptr.begin(), cptr.end() - 1);
     for (int f = 0; f < n_fine; ++f) clist[fill[parent_of[f]]++] = f;  // ascending f per parent
+    for (int p = 0; p < n_coarse; ++p) T->max_children = std::max(T->max_children, cptr[p + 1] - cptr[p]);
     const size_t nk = size_t(1) << dim;
     T->parent.alloc(sizeof(int) * std::max(1, n_fine));
     T->orth.alloc(sizeof(int) * std::max(1, n_fine));

@@ -738,6 +738,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         B->blk_stride = stride;
         B->hptr = bptr;
         B->hcol = bcol;
+        set_max_row(*B);
         B->ptr.alloc(sizeof(int) * (N + 1));
         B->col.alloc(sizeof(int) * std::max<int64_t>(1, B->nnzb));
         B->val.alloc(sizeof(double) * std::max<int64_t>(1, B->nnzb * stride));

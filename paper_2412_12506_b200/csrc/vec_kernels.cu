@@ -71,6 +71,107 @@ __global__ void prolong_kernel(const int* __restrict__ parent, const int* __rest
     }
 }
 
+/// Restriction, one CTA per coarse element p: the children's residual
+/// blocks are staged in shared memory, thread (c, j) runs the reference's
+/// sequential sums (children ascending, i ascending) with K read through the
+/// read-only path.  Same bits as restrict_kernel, no dependent-load chains.
+__global__ void restrict_cta_kernel(const int* __restrict__ child_ptr, const int* __restrict__ child,
+                                    const int* __restrict__ orth, const double* __restrict__ K,
+                                    const double* __restrict__ rf, double* __restrict__ rc, int n_coarse,
+                                    int bss, int ncomp, int maxch) {
+    extern __shared__ double sh[];  // maxch x BS
+    __shared__ int sch[64], sor[64];
+    const int BS = bss * ncomp;
+    for (int p = blockIdx.x; p < n_coarse; p += gridDim.x) {
+        const int q0 = child_ptr[p], nch = child_ptr[p + 1] - q0;
+        for (int q = threadIdx.x; q < nch; q += blockDim.x) {
+            sch[q] = child[q0 + q];
+            sor[q] = orth[sch[q]];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nch * BS; t += blockDim.x) {
+            const int q = t / BS, e = t - q * BS;
+            sh[t] = rf[size_t(sch[q]) * BS + e];
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < BS; o += blockDim.x) {
+            const int c = o / bss, j = o - c * bss;
+            double acc = 0.0;
+            for (int q = 0; q < nch; ++q) {
+                const double* src = sh + q * BS;
+                const int ot = sor[q];
+                if (ot < 0) {
+                    acc = __dadd_rn(acc, src[o]);
+                    continue;
+                }
+                const double* Ko = K + size_t(ot) * bss * bss + j;
+                double s = 0.0;
+#pragma unroll 9
+                for (int i = 0; i < bss; ++i) s = madd_rn(s, __ldg(Ko + size_t(i) * bss), src[c * bss + i]);
+                acc = __dadd_rn(acc, s);
+            }
+            rc[size_t(p) * BS + o] = acc;
+        }
+        __syncthreads();
+    }
+    (void)maxch;
+}
+
+/// Prolongation, one CTA per coarse element p: xc_p staged in shared memory,
+/// every child f of p updated by thread (f, c, i) (reference order, j ascending).
+__global__ void prolong_cta_kernel(const int* __restrict__ child_ptr, const int* __restrict__ child,
+                                   const int* __restrict__ orth, const double* __restrict__ K,
+                                   const double* __restrict__ xc, double* __restrict__ xf, int n_coarse,
+                                   int bss, int ncomp) {
+    extern __shared__ double sx[];  // BS
+    const int BS = bss * ncomp;
+    for (int p = blockIdx.x; p < n_coarse; p += gridDim.x) {
+        for (int t = threadIdx.x; t < BS; t += blockDim.x) sx[t] = xc[size_t(p) * BS + t];
+        __syncthreads();
+        const int q0 = child_ptr[p], nch = child_ptr[p + 1] - q0;
+        for (int t = threadIdx.x; t < nch * BS; t += blockDim.x) {
+            const int q = t / BS, ii = t - q * BS;
+            const int f = child[q0 + q], ot = orth[f];
+            double* dst = xf + size_t(f) * BS + ii;
+            if (ot < 0) {
+                *dst = __dadd_rn(*dst, sx[ii]);
+                continue;
+            }
+            const int c = ii / bss, i = ii - c * bss;
+            const double* Ko = K + size_t(ot) * bss * bss + size_t(i) * bss;
+            double s = 0.0;
+#pragma unroll 9
+            for (int j = 0; j < bss; ++j) s = madd_rn(s, __ldg(Ko + j), sx[c * bss + j]);
+            *dst = __dadd_rn(*dst, s);
+        }
+        __syncthreads();
+    }
+}
+
+/// Bottom pseudoinverse in one CTA (n <= 4096): b and t in shared memory.
+__global__ void __launch_bounds__(1024) pinv_cta_kernel(const double* __restrict__ Vr, const double* __restrict__ Vc,
+                                                        const double* __restrict__ lam, const double* __restrict__ b,
+                                                        double* __restrict__ x, int n, double cut) {
+    extern __shared__ double sb[];  // b (n) then t (n)
+    double* st = sb + n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = b[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < n; ++k) s = madd_rn(s, __ldg(Vr + size_t(k) * n + i), sb[k]);
+        const double l = lam[i];
+        st[i] = fabs(l) <= cut ? 0.0 : s / l;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < n; ++k) s = madd_rn(s, __ldg(Vc + size_t(k) * n + i), st[k]);
+        x[i] = s;
+    }
+}
+
 /// t_i = cut(sum_k V(k,i) b_k) / lambda_i ; Vr row-major: V(k,i) at k*n+i.
 __global__ void pinv_t_kernel(const double* __restrict__ Vr, const double* __restrict__ lam,
                               const double* __restrict__ b, double* __restrict__ t, int n,
@@ -183,6 +284,15 @@ int grid1(int64_t n, int threads, const Ctx& ctx) {
 void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc) {
     const int64_t total = int64_t(T.n_coarse) * T.bs;
     if (!total) return;
+    if (T.max_children <= 64 && size_t(T.max_children) * T.bs * 8 <= 48 * 1024) {
+        const int threads = T.bs <= 32 ? 32 : T.bs <= 64 ? 64 : T.bs <= 128 ? 128 : 256;
+        restrict_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads,
+                              size_t(T.max_children) * T.bs * 8, ctx.stream>>>(
+            T.child_ptr.as<int>(), T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse,
+            T.bss, T.ncomp, T.max_children);
+        after_launch("restrict_cta_kernel");
+        return;
+    }
     restrict_kernel<<<grid1(total, 256, ctx), 256, 0, ctx.stream>>>(
         T.child_ptr.as<int>(), T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), rf, rc,
         T.n_coarse, T.bss, T.ncomp);
@@ -192,6 +302,14 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc) 
 void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* xf) {
     const int64_t total = int64_t(T.n_fine) * T.bs;
     if (!total) return;
+    if (T.bs * 8 <= 48 * 1024) {
+        const int threads = std::min(256, std::max(32, ((T.max_children * T.bs + 31) / 32) * 32));
+        prolong_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads, size_t(T.bs) * 8,
+                             ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(), T.orth.as<int>(),
+                                           T.K.as<double>(), xc, xf, T.n_coarse, T.bss, T.ncomp);
+        after_launch("prolong_cta_kernel");
+        return;
+    }
     prolong_kernel<<<grid1(total, 256, ctx), 256, 0, ctx.stream>>>(
         T.parent.as<int>(), T.orth.as<int>(), T.K.as<double>(), xc, xf, T.n_fine, T.bss, T.ncomp);
     after_launch("prolong_kernel");
@@ -201,6 +319,12 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
     const int n = E.n;
     if (!n) return;
     const double cut = tol * E.lmax;
+    if (n <= 3072) {
+        pinv_cta_kernel<<<1, 1024, sizeof(double) * 2 * n, ctx.stream>>>(E.Vr.as<double>(), E.Vc.as<double>(),
+                                                                        E.lambda.as<double>(), b, x, n, cut);
+        after_launch("pinv_cta_kernel");
+        return;
+    }
     pinv_t_kernel<<<div_up(n, 128), 128, 0, ctx.stream>>>(E.Vr.as<double>(), E.lambda.as<double>(),
                                                          b, E.t.as<double>(), n, cut);
     after_launch("pinv_t_kernel");
