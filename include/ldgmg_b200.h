@@ -230,6 +230,28 @@ int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict);
 int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes);
 int ldgmg_mg_destroy(ldgmg_mg* mg);
 
+/* ------------------------------------------------ Krylov (L5, krylov.hpp)
+ * The reference's measurement protocol around the V-cycle.  SolveReport
+ * (krylov.hpp:38-47); residuals go to the caller's buffer (capacity >= maxit+1). */
+typedef struct ldgmg_solve_report {
+    double* residuals;
+    int capacity;
+    int n_residuals;
+    int iterations;
+    int converged, breakdown;
+    double rho, eta;
+    int classification; /* 0 fast, 1 slow, 2 nonconvergent (krylov.hpp:25) */
+    int low_confidence;
+} ldgmg_solve_report;
+enum { LDGMG_KRYLOV_CG = 0, LDGMG_KRYLOV_GMRES = 1 };
+/* replaces pcg / gmres_left(A, b, preconditioner(V), tol, maxit)
+ * (krylov.hpp:117-251): A = level-0 operator, V = Multigrid::apply; device b, x */
+int ldgmg_krylov_solve(ldgmg_ctx* ctx, ldgmg_mg* mg, int kind, const double* b, double* x,
+                       double tol, int maxit, ldgmg_solve_report* rep);
+/* replaces estimate_eta(S, V, kind, {tol, maxit, seed}) (krylov.hpp:293-306) */
+int ldgmg_estimate_eta(ldgmg_ctx* ctx, ldgmg_mg* mg, int kind, uint64_t seed, double tol,
+                       int maxit, ldgmg_solve_report* rep);
+
 /* --------------------------------------- built-in host setup (L0/L2)
  * The product's own mesh chain + LDG assembly (the reference's
  * build_uniform/coarsen/assemble_scalar/assemble_stokes, mesh.hpp,

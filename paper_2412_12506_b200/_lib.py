@@ -87,6 +87,15 @@ class ProblemSpec(C.Structure):
                 ("rho_out", C.c_double)]
 
 
+class SolveReportC(C.Structure):
+    _fields_ = [("residuals", C.POINTER(C.c_double)), ("capacity", C.c_int), ("n_residuals", C.c_int),
+                ("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("rho", C.c_double),
+                ("eta", C.c_double), ("classification", C.c_int), ("low_confidence", C.c_int)]
+
+
+KRYLOV_CG, KRYLOV_GMRES = 0, 1
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -152,6 +161,8 @@ _SIGS = {
     "ldgmg_mg_set_strict_order": ([_P, _I], _I),
     "ldgmg_mg_cycle_costs": ([_P, _DP, _DP], _I),
     "ldgmg_mg_destroy": ([_P], _I),
+    "ldgmg_krylov_solve": ([_P, _P, _I, _P, _P, _D, _I, C.POINTER(SolveReportC)], _I),
+    "ldgmg_estimate_eta": ([_P, _P, _I, C.c_uint64, _D, _I, C.POINTER(SolveReportC)], _I),
     "ldgmg_problem_create": ([C.POINTER(ProblemSpec), _I, _I, C.POINTER(_P)], _I),
     "ldgmg_problem_depth": ([_P], _I),
     "ldgmg_problem_level_shape": ([_P, _I, _IP, _IP, C.POINTER(_I64)], _I),

@@ -440,6 +440,27 @@ class Multigrid:
                                       hist.ctypes.data, C.byref(it)))
         return x, hist[: it.value + 1], it.value
 
+    def _report(self, fn, maxit):
+        buf = np.empty(maxit + 2)
+        rep = L.SolveReportC()
+        rep.residuals = buf.ctypes.data_as(C.POINTER(C.c_double))
+        rep.capacity = maxit + 2
+        check(fn(C.byref(rep)))
+        return {"residuals": buf[: rep.n_residuals].copy(), "iterations": rep.iterations,
+                "converged": bool(rep.converged), "breakdown": bool(rep.breakdown), "rho": rep.rho,
+                "eta": rep.eta, "classification": ["fast", "slow", "nonconvergent"][rep.classification],
+                "low_confidence": bool(rep.low_confidence)}
+
+    def krylov_solve(self, b, x, kind=L.KRYLOV_GMRES, tol=1e-12, maxit=60):
+        """pcg / gmres_left with this V-cycle as preconditioner (krylov.hpp:117-251)."""
+        return self._report(lambda r: lib.ldgmg_krylov_solve(self.ctx.h, self.h, int(kind), _ptr(b), _ptr(x),
+                                                             float(tol), int(maxit), r), maxit)
+
+    def estimate_eta(self, kind=L.KRYLOV_GMRES, seed=0, tol=1e-12, maxit=60):
+        """The paper-protocol measurement (krylov.hpp:293-306)."""
+        return self._report(lambda r: lib.ldgmg_estimate_eta(self.ctx.h, self.h, int(kind), int(seed), float(tol),
+                                                             int(maxit), r), maxit)
+
     def cycle_costs(self):
         d, b = C.c_double(), C.c_double()
         check(lib.ldgmg_mg_cycle_costs(self.h, C.byref(d), C.byref(b)))

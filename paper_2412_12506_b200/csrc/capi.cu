@@ -9,6 +9,7 @@
 
 #include "core.hpp"
 #include "mg.hpp"
+#include "krylov.hpp"
 #include "setup.hpp"
 
 using namespace ldgmg_b200;
@@ -624,6 +625,46 @@ int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_by
 
 int ldgmg_mg_destroy(ldgmg_mg* mg) {
     return guarded([&] { delete mg; });
+}
+
+// ---------------------------------------------------------------- Krylov
+static void report_out(const SolveReport& r, ldgmg_solve_report* rep) {
+    rep->n_residuals = int(r.residuals.size());
+    if (rep->residuals) {
+        if (rep->capacity < rep->n_residuals) fail(LDGMG_ERR_INVALID_ARGUMENT, "solve report: residual buffer too small");
+        std::memcpy(rep->residuals, r.residuals.data(), sizeof(double) * r.residuals.size());
+    }
+    rep->iterations = r.iterations;
+    rep->converged = r.converged;
+    rep->breakdown = r.breakdown;
+    rep->rho = r.rho;
+    rep->eta = r.eta;
+    rep->classification = r.classification;
+    rep->low_confidence = r.low_confidence;
+}
+
+int ldgmg_krylov_solve(ldgmg_ctx* ctx, ldgmg_mg* mg, int kind, const double* b, double* x, double tol, int maxit,
+                       ldgmg_solve_report* rep) {
+    return guarded([&] {
+        need(ctx, "krylov_solve");
+        need(mg, "krylov_solve");
+        need(rep, "krylov_solve(report)");
+        ensure_smoothers(ctx, mg->m);
+        const SolveReport r = kind == LDGMG_KRYLOV_CG ? pcg(*ctx, mg->m, b, x, tol, maxit)
+                                                      : gmres_left(*ctx, mg->m, b, x, tol, maxit);
+        report_out(r, rep);
+    });
+}
+
+int ldgmg_estimate_eta(ldgmg_ctx* ctx, ldgmg_mg* mg, int kind, uint64_t seed, double tol, int maxit,
+                       ldgmg_solve_report* rep) {
+    return guarded([&] {
+        need(ctx, "estimate_eta");
+        need(mg, "estimate_eta");
+        need(rep, "estimate_eta(report)");
+        ensure_smoothers(ctx, mg->m);
+        report_out(estimate_eta(*ctx, mg->m, kind, seed, tol, maxit), rep);
+    });
 }
 
 // ------------------------------------------------------ host setup (L0/L2)

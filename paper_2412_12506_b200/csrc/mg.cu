@@ -307,6 +307,7 @@ void Mg::init(Ctx& ctx) {
         for (int c = 0; c < (system_kind == LDGMG_SYSTEM_SCALAR ? 1 : dim); ++c) offs.push_back(c * bs_scalar);
     if (kernel_pressure) offs.push_back(dim * bs_scalar);
     nkernel = int(offs.size());
+    kernel_offsets_host = offs;
     kernel_offs.alloc(sizeof(int) * std::max<size_t>(1, offs.size()));
     if (!offs.empty())
         h2d(ctx, kernel_offs.p, offs.data(), sizeof(int) * offs.size());

@@ -58,6 +58,9 @@ struct Mg {
     int system_kind = LDGMG_SYSTEM_SCALAR, dim = 2, n_comp = 1, bs_scalar = 1, bs = 1;
     int kernel_constants = 0, kernel_pressure = 0, n_velocity = 0;
     bool strict_order = false;  // reference-order (sequential) kernel projection
+    std::vector<int> kernel_offsets_host;
+    /// symmetric_plan (multigrid.hpp:41-43)
+    bool symmetric() const { return cfg.smoother.kind == LDGMG_JACOBI || cfg.pre != cfg.post; }
     DenseEig bottom;
     std::vector<DevBuf> r, xl, bl;
     DevBuf bp, kernel_offs, red;
