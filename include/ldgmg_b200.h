@@ -274,6 +274,11 @@ int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P,
                                  const ldgmg_mg_config* cfg, ldgmg_mg** out);
 int ldgmg_problem_destroy(ldgmg_problem* P);
 
+/* the 2^dim polynomial-injection matrices of build_injection
+ * (multigrid.hpp:212-241) for a (dim, degree) tensor Legendre basis,
+ * row-major ((p+1)^dim)^2 each; host, no device needed */
+int ldgmg_injection_matrices(int dim, int degree, double* K);
+
 /* seeded measurement right-hand side: random_rhs (krylov.hpp:279-287),
  * mt19937_64, u = (rng()>>11)*2^-53, v = 2u-1, host buffer */
 int ldgmg_random_rhs(int nblocks, int bs, uint64_t seed, double* out);

@@ -173,6 +173,7 @@ _SIGS = {
     "ldgmg_mg_create_from_problem": ([_P, _P, C.POINTER(MgConfig), C.POINTER(_P)], _I),
     "ldgmg_problem_destroy": ([_P], _I),
     "ldgmg_random_rhs": ([_I, _I, C.c_uint64, _P], _I),
+    "ldgmg_injection_matrices": ([_I, _I, _P], _I),
 }
 
 for _name, (_args, _res) in _SIGS.items():

@@ -787,6 +787,15 @@ int ldgmg_problem_destroy(ldgmg_problem* P) {
     return guarded([&] { delete P; });
 }
 
+int ldgmg_injection_matrices(int dim, int degree, double* K) {
+    return guarded([&] {
+        need(K, "injection_matrices");
+        if (dim != 2 && dim != 3) fail(LDGMG_ERR_INVALID_ARGUMENT, "basis: dim must be 2 or 3");
+        const std::vector<double> v = injection_matrices(dim, degree);
+        std::memcpy(K, v.data(), sizeof(double) * v.size());
+    });
+}
+
 int ldgmg_random_rhs(int nblocks, int bs, uint64_t seed, double* out) {
     return guarded([&] {
         need(out, "random_rhs");

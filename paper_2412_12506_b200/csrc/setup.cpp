@@ -779,7 +779,13 @@ void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_el
         P.kernel_pressure = !has_kind(fine, LDGMG_BC_NEUMANN);
     }
 
-    // injection (multigrid.hpp:212-241)
+    P.inject = injection_matrices(s.dim, s.degree);
+}
+
+/// build_injection (multigrid.hpp:212-241): 1D maps T[s]_ij = sum_q w_q P_i(x_q)
+/// P_j((x_q + 2s - 1)/2), Kronecker products over the child orthants.
+std::vector<double> injection_matrices(int dim, int degree) {
+    const Basis B(degree, dim);
     const int p1 = B.p1, bs = B.bs;
     std::array<std::vector<double>, 2> T;
     for (int sd = 0; sd < 2; ++sd) {
@@ -792,18 +798,19 @@ void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_el
                 T[sd][size_t(i) * p1 + j] = acc;
             }
     }
-    const int nk = 1 << s.dim;
-    P.inject.assign(size_t(nk) * bs * bs, 0.0);
+    const int nk = 1 << dim;
+    std::vector<double> K(size_t(nk) * bs * bs, 0.0);
     for (int o = 0; o < nk; ++o)
         for (int i = 0; i < bs; ++i) {
             const auto ix = B.decompose(i);
             for (int j = 0; j < bs; ++j) {
                 const auto jx = B.decompose(j);
                 double v = 1.0;
-                for (int a = 0; a < s.dim; ++a) v *= T[(o >> a) & 1][size_t(ix[a]) * p1 + jx[a]];
-                P.inject[(size_t(o) * bs + i) * bs + j] = v;
+                for (int a = 0; a < dim; ++a) v *= T[(o >> a) & 1][size_t(ix[a]) * p1 + jx[a]];
+                K[(size_t(o) * bs + i) * bs + j] = v;
             }
         }
+    return K;
 }
 
 }  // namespace ldgmg_b200

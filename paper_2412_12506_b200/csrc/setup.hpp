@@ -39,4 +39,6 @@ struct Problem {
 void problem_build(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements,
                    Problem& out);
 
+std::vector<double> injection_matrices(int dim, int degree);
+
 }  // namespace ldgmg_b200
