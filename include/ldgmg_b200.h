@@ -142,6 +142,15 @@ int ldgmg_bsr_download(ldgmg_ctx* ctx, const ldgmg_bsr* A, int* ptr, int* col, d
 int64_t ldgmg_bsr_device_bytes(const ldgmg_bsr* A);
 int ldgmg_bsr_destroy(ldgmg_bsr* A);
 
+/* Upload a rank-local slice whose column indices are renumbered (owned
+ * columns first, then ghost slots): block order inside each row must stay
+ * the global ascending order, so columns need not ascend locally.
+ * flags: LDGMG_BSR_UNSORTED_COLUMNS. */
+#define LDGMG_BSR_UNSORTED_COLUMNS 1
+int ldgmg_bsr_upload_ex(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int col_bs,
+                        const int* ptr, const int* col, const double* val, int flags,
+                        ldgmg_bsr** out);
+
 /* replaces spmv(const BlockCsr&, const BlockVec&, BlockVec&)  blockla.hpp:136-154 */
 int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
 /* replaces spmv_transpose(...)                                 blockla.hpp:157-176 */
@@ -149,6 +158,40 @@ int ldgmg_spmv_transpose(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, do
 /* r = b - A x (multigrid.hpp:256-258, smoothers.hpp:439-440), fused */
 int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const double* x,
                    double* r);
+/* y += A x  (the SAI update x += B r, smoothers.hpp:441-446, as one pass) */
+int ldgmg_spmv_add(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
+
+/* Block-diagonal relaxation of every row of a (possibly rank-local,
+ * rectangular) operator with caller-held factors: x_out[e] = (1-w) x_live[e]
+ * + w s o pinv(V, lambda)(s o (b_e - sum_{j != e} A_ej x_src[j]))
+ * (smoothers.hpp:496-518).  Row e's diagonal block is the one whose column
+ * index equals diag_col_offset + e. */
+typedef struct ldgmg_factors ldgmg_factors;
+int ldgmg_factors_upload(ldgmg_ctx* ctx, int n, int bs, const double* V, const double* lambda,
+                         const double* s, ldgmg_factors** out);
+int ldgmg_factors_destroy(ldgmg_factors* F);
+int ldgmg_relax(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, const double* b,
+                const double* x_src, const double* x_live, double* x_out, double omega);
+
+/* out[i*bs .. i*bs+bs) = x[idx[i]*bs ..]  (ghost-exchange packing; idx on the device) */
+int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out);
+
+/* Partition plan of one level for `nranks` contiguous element ranges
+ * [p*N/P, (p+1)*N/P) (partition_ranges, smoothers.hpp:87-94).  Host-only.
+ * Phase 1 (local_col / send_idx NULL): sizes.  Phase 2: fills
+ *   local_col[nnz_local]   : columns of the owned rows renumbered (owned j -> j-r0,
+ *                            ghost j -> n_owned + slot), block order unchanged
+ *   ghost_gid[n_ghost]     : global ids of the ghost slots, grouped by owner rank,
+ *                            ascending inside each group
+ *   recv_count[nranks]     : ghost slots received from each rank (consecutive)
+ *   send_count[nranks]     : owned elements each rank needs from us
+ *   send_idx[n_send]       : their local (owned) indices, grouped by rank, ascending gid
+ * The ghost set of rank p is the column set of its rows (A pattern); the send
+ * lists are derived from the other ranks' rows (structurally symmetric or not). */
+int ldgmg_partition_level(int N, const int* ptr, const int* col, int nranks, int rank, int* r0,
+                          int* r1, int* n_ghost, int* n_send, int* local_col, int* ghost_gid,
+                          int* recv_count, int* send_count, int* send_idx);
+
 /* BLAS-1 (blockla.hpp:60-71); dot/norm write one double to *out_host (synchronous) */
 int ldgmg_dot(ldgmg_ctx* ctx, int64_t n, const double* a, const double* b, double* out_host);
 int ldgmg_axpy(ldgmg_ctx* ctx, int64_t n, double alpha, const double* x, double* y);
@@ -213,6 +256,9 @@ int ldgmg_mg_smoother(ldgmg_mg* mg, int level, ldgmg_smoother** out);
 int ldgmg_mg_depth(const ldgmg_mg* mg);
 /* replaces Multigrid::cycle(BlockVec& x, const BlockVec& b)  multigrid.hpp:82-85 */
 int ldgmg_mg_cycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b);
+/* the bare recursive v_cycle(0, x, b) (multigrid.hpp:247-264), no kernel
+ * projection -- the coarse-grid solve of a mesh-partitioned hierarchy */
+int ldgmg_mg_vcycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b);
 /* replaces Multigrid::apply(const BlockVec& b) -> x           multigrid.hpp:90-101 */
 int ldgmg_mg_apply(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b, double* x);
 /* Run `ncycles` V-cycles (graph-captured after the first call); x in place. */

@@ -131,6 +131,13 @@ _SIGS = {
     "ldgmg_bsr_download": ([_P, _P, _P, _P, _P], _I),
     "ldgmg_bsr_device_bytes": ([_P], _I64),
     "ldgmg_bsr_destroy": ([_P], _I),
+    "ldgmg_bsr_upload_ex": ([_P, _I, _I, _I, _I, _P, _P, _P, _I, C.POINTER(_P)], _I),
+    "ldgmg_spmv_add": ([_P, _P, _P, _P], _I),
+    "ldgmg_factors_upload": ([_P, _I, _I, _P, _P, _P, C.POINTER(_P)], _I),
+    "ldgmg_factors_destroy": ([_P], _I),
+    "ldgmg_relax": ([_P, _P, _P, _P, _P, _P, _P, _D], _I),
+    "ldgmg_gather_blocks": ([_P, _P, _P, _I, _I, _P], _I),
+    "ldgmg_partition_level": ([_I, _P, _P, _I, _I, _IP, _IP, _IP, _IP, _P, _P, _P, _P, _P], _I),
     "ldgmg_spmv": ([_P, _P, _P, _P], _I),
     "ldgmg_spmv_transpose": ([_P, _P, _P, _P], _I),
     "ldgmg_residual": ([_P, _P, _P, _P, _P], _I),
@@ -156,6 +163,7 @@ _SIGS = {
     "ldgmg_mg_depth": ([_P], _I),
     "ldgmg_mg_cycle": ([_P, _P, _P, _P], _I),
     "ldgmg_mg_apply": ([_P, _P, _P, _P], _I),
+    "ldgmg_mg_vcycle": ([_P, _P, _P, _P], _I),
     "ldgmg_mg_cycles": ([_P, _P, _P, _P, _I], _I),
     "ldgmg_mg_solve_host": ([_P, _P, _P, _P, _D, _I, _P, _IP], _I),
     "ldgmg_mg_set_strict_order": ([_P, _I], _I),

@@ -427,6 +427,10 @@ class Multigrid:
     def apply(self, b, x) -> None:
         check(lib.ldgmg_mg_apply(self.ctx.h, self.h, _ptr(b), _ptr(x)))
 
+    def vcycle(self, x, b) -> None:
+        """Bare v_cycle(0, x, b) without kernel projection (multigrid.hpp:247-264)."""
+        check(lib.ldgmg_mg_vcycle(self.ctx.h, self.h, _ptr(x), _ptr(b)))
+
     def cycles(self, x, b, n: int) -> None:
         check(lib.ldgmg_mg_cycles(self.ctx.h, self.h, _ptr(x), _ptr(b), int(n)))
 

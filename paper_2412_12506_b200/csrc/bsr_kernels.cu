@@ -323,7 +323,7 @@ int grid_for(int64_t n, int threads, const Ctx& ctx) {
 }  // namespace
 
 std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
-                                const int* col, const double* val) {
+                                const int* col, const double* val, bool require_sorted) {
     require(brows >= 0 && bcols >= 0 && rbs > 0 && cbs > 0, "bsr_upload: bad shape");
     require(rbs <= 256 && cbs <= 256, "bsr_upload: block size above 256 is not supported");
     auto A = std::make_unique<Bsr>();
@@ -341,7 +341,8 @@ std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs
     for (int i = 0; i < brows; ++i)
         for (int k = A->hptr[i]; k < A->hptr[i + 1]; ++k) {
             require(A->hcol[k] >= 0 && A->hcol[k] < bcols, "bsr_upload: column out of range");
-            if (k > A->hptr[i]) require(A->hcol[k] > A->hcol[k - 1], "bsr_upload: columns must ascend");
+            if (require_sorted && k > A->hptr[i])
+                require(A->hcol[k] > A->hcol[k - 1], "bsr_upload: columns must ascend");
         }
     A->blk_stride = even_up(int64_t(rbs) * cbs);
     A->ptr.alloc(sizeof(int) * (brows + 1));

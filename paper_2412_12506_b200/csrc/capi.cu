@@ -6,6 +6,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <unordered_map>
 
 #include "core.hpp"
 #include "mg.hpp"
@@ -239,8 +240,9 @@ int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const do
     return guarded([&] {
         need(ctx, "residual");
         need(A, "residual");
-        if (A->rbs != A->cbs || A->brows != A->bcols)
-            fail(LDGMG_ERR_INVALID_ARGUMENT, "residual: operator must be block-square");
+        // square blocks; a rank-local slice may have more (ghost) columns than rows
+        if (A->rbs != A->cbs || A->bcols < A->brows)
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "residual: operator must have square blocks");
         RowPass p;
         p.A = A;
         p.mode = MODE_RESIDUAL;
@@ -249,6 +251,157 @@ int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const do
         p.y = r;
         p.nrows = A->brows;
         launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_bsr_upload_ex(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int col_bs, const int* ptr, const int* col,
+                        const double* val, int flags, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_upload_ex");
+        need(ptr, "ldgmg_bsr_upload_ex(ptr)");
+        need(out, "ldgmg_bsr_upload_ex(out)");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(bsr_upload(*ctx, brows, bcols, row_bs, col_bs, ptr, col, val,
+                                                          (flags & LDGMG_BSR_UNSORTED_COLUMNS) == 0)));
+    });
+}
+
+int ldgmg_spmv_add(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y) {
+    return guarded([&] {
+        need(ctx, "spmv_add");
+        need(A, "spmv_add");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_ADD;
+        p.x = x;
+        p.xe = y;
+        p.y = y;
+        p.nrows = A->brows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+struct ldgmg_factors {
+    DiagFactors f;
+};
+
+int ldgmg_factors_upload(ldgmg_ctx* ctx, int n, int bs, const double* V, const double* lambda, const double* s,
+                         ldgmg_factors** out) {
+    return guarded([&] {
+        need(ctx, "factors_upload");
+        need(V, "factors_upload(V)");
+        need(lambda, "factors_upload(lambda)");
+        need(s, "factors_upload(s)");
+        bind(*ctx);
+        auto* h = new ldgmg_factors();
+        upload_factors(*ctx, h->f, n, bs, V, lambda, s);
+        *out = h;
+    });
+}
+
+int ldgmg_factors_destroy(ldgmg_factors* F) {
+    return guarded([&] { delete F; });
+}
+
+int ldgmg_relax(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, const double* b, const double* x_src,
+                const double* x_live, double* x_out, double omega) {
+    return guarded([&] {
+        need(ctx, "relax");
+        need(A, "relax");
+        need(F, "relax(factors)");
+        if (F->f.n != A->brows) fail(LDGMG_ERR_INVALID_ARGUMENT, "relax: factor count != block rows");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_RELAX;
+        p.x = x_src;
+        p.b = b;
+        p.xe = x_live;
+        p.y = x_out;
+        p.nrows = A->brows;
+        p.F = &F->f;
+        p.omega = omega;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out) {
+    return guarded([&] {
+        need(ctx, "gather_blocks");
+        launch_gather_blocks(*ctx, x, idx, n, bs, out);
+    });
+}
+
+int ldgmg_partition_level(int N, const int* ptr, const int* col, int nranks, int rank, int* r0, int* r1, int* n_ghost,
+                          int* n_send, int* local_col, int* ghost_gid, int* recv_count, int* send_count,
+                          int* send_idx) {
+    return guarded([&] {
+        need(ptr, "partition_level(ptr)");
+        if (nranks < 1 || nranks > N) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition_ranges: partition count must lie in [1, N]");
+        if (rank < 0 || rank >= nranks) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition_level: bad rank");
+        auto lo = [&](int p) { return int((long long)p * N / nranks); };
+        auto owner = [&](int j) {
+            int p = int((long long)j * nranks / N);
+            while (p + 1 < nranks && lo(p + 1) <= j) ++p;
+            while (p > 0 && lo(p) > j) --p;
+            return p;
+        };
+        const int a = lo(rank), b = lo(rank + 1), nown = b - a;
+        // ghost set: non-owned columns of our rows, grouped by owner, ascending gid
+        std::vector<std::vector<int>> by(nranks);
+        {
+            std::vector<char> seen(N, 0);
+            for (int i = a; i < b; ++i)
+                for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+                    const int j = col[k];
+                    if ((j < a || j >= b) && !seen[j]) {
+                        seen[j] = 1;
+                        by[owner(j)].push_back(j);
+                    }
+                }
+        }
+        std::vector<int> ghosts;
+        std::vector<int> rc(nranks, 0);
+        for (int p = 0; p < nranks; ++p) {
+            std::sort(by[p].begin(), by[p].end());
+            rc[p] = int(by[p].size());
+            ghosts.insert(ghosts.end(), by[p].begin(), by[p].end());
+        }
+        // send lists: for every other rank q, the owned columns q's rows reference
+        std::vector<std::vector<int>> sends(nranks);
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            std::vector<char> seen(size_t(nown), 0);
+            for (int i = lo(q); i < lo(q + 1); ++i)
+                for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+                    const int j = col[k];
+                    if (j >= a && j < b && !seen[j - a]) {
+                        seen[j - a] = 1;
+                        sends[q].push_back(j - a);
+                    }
+                }
+            std::sort(sends[q].begin(), sends[q].end());
+        }
+        int ns = 0;
+        for (auto& s : sends) ns += int(s.size());
+        *r0 = a;
+        *r1 = b;
+        *n_ghost = int(ghosts.size());
+        *n_send = ns;
+        if (!local_col) return;
+        std::unordered_map<int, int> slot;
+        for (size_t g = 0; g < ghosts.size(); ++g) slot[ghosts[g]] = nown + int(g);
+        for (int i = a, o = 0; i < b; ++i)
+            for (int k = ptr[i]; k < ptr[i + 1]; ++k, ++o) {
+                const int j = col[k];
+                local_col[o] = (j >= a && j < b) ? j - a : slot.at(j);
+            }
+        if (ghost_gid) std::memcpy(ghost_gid, ghosts.data(), sizeof(int) * ghosts.size());
+        if (recv_count) std::memcpy(recv_count, rc.data(), sizeof(int) * nranks);
+        if (send_count)
+            for (int q = 0; q < nranks; ++q) send_count[q] = int(sends[q].size());
+        if (send_idx)
+            for (int q = 0, o = 0; q < nranks; ++q)
+                for (int v : sends[q]) send_idx[o++] = v;
     });
 }
 
@@ -536,6 +689,15 @@ int ldgmg_mg_cycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b) {
         need(mg, "Multigrid::cycle");
         ensure_smoothers(ctx, mg->m);
         mg->m.cycle(*ctx, x, b);
+    });
+}
+
+int ldgmg_mg_vcycle(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b) {
+    return guarded([&] {
+        need(ctx, "mg_vcycle");
+        need(mg, "mg_vcycle");
+        ensure_smoothers(ctx, mg->m);
+        mg->m.v_cycle(*ctx, 0, x, b);
     });
 }
 

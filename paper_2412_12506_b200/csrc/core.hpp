@@ -94,7 +94,9 @@ inline void set_max_row(Bsr& A) {
 
 /// Upload from the reference layout (row-major blocks) to the device layout.
 std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
-                                const int* col, const double* val);
+                                const int* col, const double* val, bool require_sorted = true);
+/// out[i] = x block idx[i] (ghost-exchange packing)
+void launch_gather_blocks(Ctx& ctx, const double* x, const int* idx, int n, int bs, double* out);
 /// Device copy of A with the layout of A^T (used for B^T r, bitwise equal to
 /// the reference's scatter order, blockla.hpp:163-175).
 const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A);

@@ -275,6 +275,15 @@ __global__ void dot_final_kernel(const double* __restrict__ part, int np, double
     }
 }
 
+__global__ void gather_blocks_kernel(const double* __restrict__ x, const int* __restrict__ idx, int n, int bs,
+                                     double* __restrict__ out) {
+    const int64_t total = int64_t(n) * bs;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(t / bs), e = int(t - int64_t(i) * bs);
+        out[t] = x[size_t(idx[i]) * bs + e];
+    }
+}
+
 int grid1(int64_t n, int threads, const Ctx& ctx) {
     return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, int64_t(ctx.num_sms) * 32)));
 }
@@ -342,6 +351,12 @@ void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* com
         project_fast_kernel<<<ncomp, 1024, 0, ctx.stream>>>(v, N, bs, comp_offsets, ncomp, kval);
         after_launch("project_fast_kernel");
     }
+}
+
+void launch_gather_blocks(Ctx& ctx, const double* x, const int* idx, int n, int bs, double* out) {
+    if (n <= 0) return;
+    gather_blocks_kernel<<<grid1(int64_t(n) * bs, 256, ctx), 256, 0, ctx.stream>>>(x, idx, n, bs, out);
+    after_launch("gather_blocks_kernel");
 }
 
 void launch_axpy(Ctx& ctx, int64_t n, double alpha, const double* x, double* y) {

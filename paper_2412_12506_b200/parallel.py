@@ -1,0 +1,403 @@
+"""Mesh-partitioned multi-GPU V-cycle.
+
+One process per GPU.  Rank p owns the contiguous Morton element range
+[p*N/P, (p+1)*N/P) of every distributed level (partition_ranges,
+smoothers.hpp:87-94); for uniform meshes the children of coarse element c are
+8c..8c+7, so the ranges are nested and restriction / prolongation are
+rank-local.  Each operator application gathers one ghost layer of its input
+(x before the residual / relaxation, r before B r or B^T r) with
+torch.distributed point-to-point ops (NCCL over NVLink on B200, gloo in the
+CPU tests); the kernel projection reduces in the reference's sequential order
+over all elements (all-gather of the per-element products), so results are
+independent of the rank count and bit-identical to the single-GPU strict
+mode.  Levels with fewer than `min_rows_per_rank * P` elements are
+agglomerated: every rank gathers the coarse right-hand side and runs the rest
+of the V-cycle redundantly (identical bits everywhere).
+
+All local compute is in the C ABI's sm_100a kernels (GpuOps); the ops object
+is injectable only so that the partition / exchange / agglomeration logic can
+be tested on CPU against the reference (tests/test_parallel_gloo.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check, lib
+
+
+@dataclass
+class Plan:
+    """Partition plan of one operator's rows on one rank (ldgmg_partition_level)."""
+    r0: int
+    r1: int
+    n_own: int
+    n_ghost: int
+    local_col: np.ndarray
+    ghost_gid: np.ndarray
+    recv_count: np.ndarray
+    send_count: np.ndarray
+    send_idx: np.ndarray
+
+    @property
+    def recv_off(self):
+        return np.concatenate([[0], np.cumsum(self.recv_count)])
+
+    @property
+    def send_off(self):
+        return np.concatenate([[0], np.cumsum(self.send_count)])
+
+
+def partition_level(ptr, col, N, nranks, rank) -> Plan:
+    ptr = np.ascontiguousarray(ptr, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    r0, r1, ng, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(lib.ldgmg_partition_level(N, ptr.ctypes.data, col.ctypes.data, nranks, rank, C.byref(r0), C.byref(r1),
+                                    C.byref(ng), C.byref(ns), None, None, None, None, None))
+    nnz_loc = int(ptr[r1.value] - ptr[r0.value])
+    lc = np.empty(max(nnz_loc, 1), np.int32)
+    gg = np.empty(max(ng.value, 1), np.int32)
+    rc = np.empty(nranks, np.int32)
+    sc = np.empty(nranks, np.int32)
+    si = np.empty(max(ns.value, 1), np.int32)
+    check(lib.ldgmg_partition_level(N, ptr.ctypes.data, col.ctypes.data, nranks, rank, C.byref(r0), C.byref(r1),
+                                    C.byref(ng), C.byref(ns), lc.ctypes.data, gg.ctypes.data, rc.ctypes.data,
+                                    sc.ctypes.data, si.ctypes.data))
+    return Plan(r0.value, r1.value, r1.value - r0.value, ng.value, lc[:nnz_loc], gg[:ng.value], rc, sc,
+                si[:ns.value])
+
+
+def local_rows(ptr, col, val, bs_r, bs_c, plan: Plan):
+    """Rows [r0, r1) of a global BSR with the plan's renumbered columns."""
+    ptr = np.asarray(ptr)
+    lptr = (ptr[plan.r0:plan.r1 + 1] - ptr[plan.r0]).astype(np.int32)
+    k0, k1 = int(ptr[plan.r0]), int(ptr[plan.r1])
+    lval = np.asarray(val)[k0 * bs_r * bs_c:k1 * bs_r * bs_c]
+    return lptr, plan.local_col, lval
+
+
+def transpose_csr(ptr, col, val, n_rows, n_cols, bs):
+    """Host transpose of a square-block BSR (B^T for the reverse sweep):
+    block (j, i) of the result = (B_ij)^T, rows i ascending per column j."""
+    ptr, col = np.asarray(ptr), np.asarray(col)
+    B = np.asarray(val).reshape(-1, bs, bs)
+    rows = np.repeat(np.arange(n_rows), np.diff(ptr))
+    order = np.lexsort((rows, col))
+    tptr = np.zeros(n_cols + 1, np.int32)
+    np.add.at(tptr, col + 1, 1)
+    tptr = np.cumsum(tptr).astype(np.int32)
+    return tptr, rows[order].astype(np.int32), np.ascontiguousarray(B[order].transpose(0, 2, 1)).reshape(-1)
+
+
+class GpuOps:
+    """Local compute through the C ABI (the product path)."""
+
+    def __init__(self, ctx):
+        import torch
+        self.torch = torch
+        self.ctx = ctx
+
+    def tensor(self, n):
+        return self.torch.zeros(int(n), dtype=self.torch.float64, device="cuda")
+
+    def itensor(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, np.int32)).cuda()
+
+    def upload(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, np.float64)).cuda()
+
+    def matrix(self, brows, bcols, bs, ptr, col, val):
+        h = C.c_void_p()
+        p = np.ascontiguousarray(ptr, np.int32)
+        c = np.ascontiguousarray(col, np.int32)
+        v = np.ascontiguousarray(val, np.float64)
+        check(lib.ldgmg_bsr_upload_ex(self.ctx.h, int(brows), int(bcols), bs, bs, p.ctypes.data, c.ctypes.data,
+                                      v.ctypes.data, 1, C.byref(h)))  # LDGMG_BSR_UNSORTED_COLUMNS
+        return _Handle(h, lib.ldgmg_bsr_destroy)
+
+    def factors(self, n, bs, V, lam, s):
+        h = C.c_void_p()
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (V, lam, s)]
+        check(lib.ldgmg_factors_upload(self.ctx.h, int(n), int(bs), *(a.ctypes.data for a in arrs), C.byref(h)))
+        return _Handle(h, lib.ldgmg_factors_destroy)
+
+    def transfer(self, n_fine, n_coarse, parent, orth, dim, bss, ncomp, K):
+        from .api import Transfer
+        return Transfer(self.ctx, n_fine, n_coarse, parent, orth, dim, bss, ncomp, K)
+
+    def residual(self, A, b, x_ext, r):
+        check(lib.ldgmg_residual(self.ctx.h, A.h, b.data_ptr(), x_ext.data_ptr(), r.data_ptr()))
+
+    def spmv_add(self, B, r_ext, x_own):
+        check(lib.ldgmg_spmv_add(self.ctx.h, B.h, r_ext.data_ptr(), x_own.data_ptr()))
+
+    def relax(self, A, F, b, x_src, x_live, x_out, omega):
+        check(lib.ldgmg_relax(self.ctx.h, A.h, F.h, b.data_ptr(), x_src.data_ptr(), x_live.data_ptr(),
+                              x_out.data_ptr(), float(omega)))
+
+    def restrict(self, T, rf, rc):
+        T.restrict(rf, rc)
+
+    def prolong(self, T, xc, xf):
+        T.interpolate_add(xc, xf)
+
+    def gather(self, x, idx, n, bs, out):
+        check(lib.ldgmg_gather_blocks(self.ctx.h, x.data_ptr(), idx.data_ptr(), int(n), int(bs), out.data_ptr()))
+
+    def to_host(self, t):
+        return t.detach().cpu().numpy()
+
+
+class _Handle:
+    def __init__(self, h, dtor):
+        self.h, self._dtor = h, dtor
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._dtor(self.h)
+            self.h = None
+
+
+class Exchanger:
+    """Ghost exchange of one plan: pack owned blocks the neighbours need,
+    point-to-point send / receive straight into the ghost slots."""
+
+    def __init__(self, plan: Plan, bs: int, ops, dist, group, rank):
+        self.plan, self.bs, self.ops, self.dist, self.group, self.rank = plan, bs, ops, dist, group, rank
+        self.idx = ops.itensor(plan.send_idx if len(plan.send_idx) else np.zeros(1, np.int32))
+        self.sendbuf = ops.tensor(max(1, len(plan.send_idx)) * bs)
+        self.so, self.ro = plan.send_off, plan.recv_off
+
+    def __call__(self, x_ext):
+        p, bs = self.plan, self.bs
+        if p.n_ghost == 0 and len(p.send_idx) == 0:
+            return
+        self.ops.gather(x_ext, self.idx, len(p.send_idx), bs, self.sendbuf)
+        P2P = self.dist.P2POp
+        reqs = []
+        for q in range(len(p.send_count)):
+            if q == self.rank:
+                continue
+            if p.send_count[q]:
+                reqs.append(P2P(self.dist.isend, self.sendbuf[self.so[q] * bs:self.so[q + 1] * bs], q, self.group))
+            if p.recv_count[q]:
+                g0 = (p.n_own + self.ro[q]) * bs
+                reqs.append(P2P(self.dist.irecv, x_ext[g0:g0 + int(p.recv_count[q]) * bs], q, self.group))
+        if reqs:
+            for w in self.dist.batch_isend_irecv(reqs):
+                w.wait()
+
+
+class DistMultigrid:
+    """The V-cycle over P ranks (see module docstring).
+
+    `levels[l]` (global, host numpy): dict with A=(ptr, col, val), n, bs and,
+    for smoothed levels, B=(ptr,col,val) for SAI or factors=(V, lam, s) for
+    Jacobi; `transfers[l]` = (parent_of, orthant_of); K injection matrices;
+    `coarse` = an object with .vcycle(x, b) on full coarse vectors (the
+    agglomerated tail, e.g. an api.Multigrid over levels >= ld)."""
+
+    def __init__(self, ops, dist, cfg, levels, transfers, K, dim, bss, ncomp, kernel_offsets, coarse_factory,
+                 group=None, min_rows_per_rank=64):
+        self.ops, self.dist, self.cfg, self.group = ops, dist, cfg, group
+        self.rank = dist.get_rank(group)
+        self.P = dist.get_world_size(group)
+        self.bs = levels[0]["bs"]
+        self.koffs = list(kernel_offsets)
+        self.N0 = levels[0]["n"]
+        depth = len(levels)
+        ld = 0
+        while ld < depth - 1 and levels[ld]["n"] >= self.P * min_rows_per_rank:
+            ld += 1
+        self.ld = max(ld, 1) if depth > 1 else 0
+        if self.ld == 0:
+            raise ValueError("distributed V-cycle needs at least one partitioned level")
+        bs = self.bs
+        self.L = []
+        for l in range(self.ld):
+            lv = levels[l]
+            n = lv["n"]
+            pa = partition_level(*lv["A"][:2], n, self.P, self.rank)
+            d = {"n": n, "plan": pa, "A": ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs,
+                                                     *local_rows(*lv["A"], bs, bs, pa)),
+                 "xA": Exchanger(pa, bs, ops, dist, group, self.rank)}
+            if "B" in lv:
+                Bg = lv["B"]
+                BTg = transpose_csr(*Bg, n, n, bs)
+                for key, M in (("B", Bg), ("BT", BTg)):
+                    pb = partition_level(M[0], M[1], n, self.P, self.rank)
+                    d[key] = ops.matrix(pb.n_own, pb.n_own + pb.n_ghost, bs, *local_rows(*M, bs, bs, pb))
+                    d["x" + key] = Exchanger(pb, bs, ops, dist, group, self.rank)
+                    d["ng" + key] = pb.n_ghost
+            if "factors" in lv:
+                V, lam, s = lv["factors"]
+                a, b = pa.r0, pa.r1
+                d["F"] = ops.factors(pa.n_own, bs, V[a * bs * bs:b * bs * bs], lam[a * bs:b * bs], s[a * bs:b * bs])
+            # transfer to level l+1, rank-local (nested ranges)
+            parent, orth = transfers[l]
+            nc = levels[l + 1]["n"]
+            c0, c1 = self.rank * nc // self.P, (self.rank + 1) * nc // self.P
+            lp = np.asarray(parent[pa.r0:pa.r1])
+            bounds = [q * n // self.P for q in range(self.P + 1)]
+            if any(int(parent[bq - 1]) == int(parent[bq]) for bq in bounds[1:-1] if 0 < bq < n):
+                raise ValueError("a rank boundary splits a sibling group; use P dividing N/2^dim")
+            if l + 1 < self.ld and (lp.min(initial=c0) < c0 or lp.max(initial=c0) >= c1):
+                raise ValueError("partition ranges are not nested across levels")
+            # children-induced coarse ranges of every rank (agglomeration gather)
+            d["cranges"] = [(int(parent[bounds[q]]) if bounds[q] < n else nc,
+                             int(parent[bounds[q + 1] - 1]) + 1 if bounds[q + 1] > bounds[q] else int(parent[bounds[q]]))
+                            for q in range(self.P)]
+            d["c0"], d["c1"], d["nc"] = c0, c1, nc
+            d["T"] = ops.transfer(pa.n_own, c1 - c0 if l + 1 < self.ld else nc, lp - (c0 if l + 1 < self.ld else 0),
+                                  orth[pa.r0:pa.r1], dim, bss, ncomp, K)
+            d["x"] = ops.tensor((pa.n_own + pa.n_ghost) * bs)
+            d["snap"] = ops.tensor((pa.n_own + pa.n_ghost) * bs)
+            d["r"] = ops.tensor(pa.n_own * bs)
+            d["rext"] = ops.tensor((pa.n_own + max(d.get("ngB", 0), d.get("ngBT", 0))) * bs)
+            d["b"] = ops.tensor(pa.n_own * bs)
+            self.L.append(d)
+        # agglomerated tail: levels >= ld on every rank
+        self.coarse = coarse_factory(self.ld)
+        nct = levels[self.ld]["n"]
+        self.rc_full = ops.tensor(nct * bs)
+        self.xc_full = ops.tensor(nct * bs)
+        self.rc_part = ops.tensor(nct * bs)  # this rank's restriction contribution
+
+    # ---------------------------------------------------------------- smoothing
+    def smooth(self, l, b, sweep):
+        d, bs = self.L[l], self.bs
+        n_own = d["plan"].n_own
+        x_ext = d["x"]
+        kind = self.cfg.smoother.kind
+        if kind == L.SAI:
+            d["xA"](x_ext)
+            rext = d["rext"]
+            self.ops.residual(d["A"], b, x_ext, rext[:n_own * bs])
+            key = "B" if sweep == L.SWEEP_FORWARD else "BT"
+            d["x" + key](rext)
+            self.ops.spmv_add(d[key], rext, x_ext[:n_own * bs])
+        elif kind == L.JACOBI:
+            d["xA"](x_ext)
+            snap = d["snap"]
+            snap.copy_(x_ext)
+            self.ops.relax(d["A"], d["F"], b, snap, snap[:n_own * bs], x_ext[:n_own * bs], self.cfg.smoother.omega)
+        else:
+            raise ValueError("distributed V-cycle supports the Jacobi and SAI smoothers")
+
+    # ---------------------------------------------------------------- V-cycle
+    def _vcycle(self, l, b):
+        """x lives in self.L[l]['x'][:own]; b is the owned right-hand side."""
+        d, bs = self.L[l], self.bs
+        n_own = d["plan"].n_own
+        x_ext = d["x"]
+        for _ in range(self.cfg.nu1):
+            self.smooth(l, b, self.cfg.pre)
+        d["xA"](x_ext)
+        self.ops.residual(d["A"], b, x_ext, d["r"])
+        if l + 1 < self.ld:
+            nxt = self.L[l + 1]
+            self.ops.restrict(d["T"], d["r"], nxt["b"])
+            nxt["x"].zero_()
+            self._vcycle(l + 1, nxt["b"])
+            self.ops.prolong(d["T"], nxt["x"][:nxt["plan"].n_own * bs], x_ext[:n_own * bs])
+        else:
+            # agglomerate: every rank restricts its children into the full
+            # coarse vector (disjoint parents), all-reduce assembles it exactly
+            self.rc_part.zero_()
+            self.ops.restrict(d["T"], d["r"], self.rc_part)
+            self._allgather_coarse(l)
+            self.xc_full.zero_()
+            self.coarse.vcycle(self.xc_full, self.rc_full)
+            self.ops.prolong(d["T"], self.xc_full, x_ext[:n_own * bs])
+        for _ in range(self.cfg.nu2):
+            self.smooth(l, b, self.cfg.post)
+
+    def _allgather(self, mine, sizes):
+        """all_gather of unevenly sized slices (padded to the largest)."""
+        m = max(sizes)
+        buf = self.ops.tensor(m)
+        buf[:mine.numel()] = mine
+        parts = [self.ops.tensor(m) for _ in sizes]
+        self.dist.all_gather(parts, buf, group=self.group)
+        return [p[:sz] for p, sz in zip(parts, sizes)]
+
+    def _allgather_coarse(self, l):
+        d, bs = self.L[l], self.bs
+        cr = d["cranges"]
+        a, b = cr[self.rank]
+        parts = self._allgather(self.rc_part[a * bs:b * bs], [(y - x) * bs for x, y in cr])
+        for (x, y), part in zip(cr, parts):
+            self.rc_full[x * bs:y * bs] = part
+
+    def project(self, v_own):
+        """multigrid.hpp:243-245 with the dot in the reference's sequential
+        order over all elements (P-independent, = single-GPU strict mode)."""
+        if not self.koffs:
+            return
+        bs, n_own = self.bs, self.L[0]["plan"].n_own
+        kval = 1.0 / np.sqrt(float(self.N0))
+        sizes = [(q + 1) * self.N0 // self.P - q * self.N0 // self.P for q in range(self.P)]
+        for off in self.koffs:
+            own = v_own[off::bs][:n_own] * kval
+            parts = self._allgather(own.contiguous(), sizes)
+            prods = np.concatenate([self.ops.to_host(p) for p in parts])
+            dsum = float(np.add.accumulate(np.concatenate([[0.0], prods]))[-1])
+            v_own[off::bs][:n_own] += (-dsum) * kval
+
+    def cycle(self, x_own, b_own):
+        """Multigrid::cycle on the owned slices (multigrid.hpp:82-85)."""
+        d, bs = self.L[0], self.bs
+        n_own = d["plan"].n_own
+        d["x"][:n_own * bs] = x_own
+        self._vcycle(0, b_own)
+        x_own.copy_(d["x"][:n_own * bs])
+        self.project(x_own)
+
+    def owned_range(self, level=0):
+        p = self.L[level]["plan"]
+        return p.r0, p.r1
+
+
+def from_problem(ctx, problem, cfg, dist, group=None, min_rows_per_rank=64):
+    """Distributed hierarchy from the built-in setup.  Setup data (SAI B,
+    factors) come from a replicated single-GPU hierarchy on each rank."""
+    from .api import DeviceBsr, Multigrid, MultigridConfig, Transfer
+    full = Multigrid(ctx, cfg, problem)
+    depth = problem.depth
+    levels, transfers = [], []
+    for l in range(depth):
+        n, bs, _ = problem.level_shape(l)
+        lv = {"n": n, "bs": bs, "A": problem.level_matrix(l)}
+        if l + 1 < depth:
+            S = full.smoother(l)
+            if cfg.smoother.kind == L.SAI:
+                lv["B"] = S.sai_matrix()
+            else:
+                lv["factors"] = S.diag_factors()
+            transfers.append(problem.level_transfer(l))
+        levels.append(lv)
+    K = problem.injection()
+
+    def coarse_factory(ld):
+        As = [DeviceBsr(ctx, levels[l]["n"], levels[l]["n"], levels[l]["bs"], levels[l]["bs"], *levels[l]["A"])
+              for l in range(ld, depth)]
+        Ts = [Transfer(ctx, levels[l]["n"], levels[l + 1]["n"], *transfers[l], problem.dim, problem.bs_scalar,
+                       problem.n_comp, K) for l in range(ld, depth - 1)]
+        ccfg = MultigridConfig(smoother=cfg.smoother, pre=cfg.pre, post=cfg.post, nu1=cfg.nu1, nu2=cfg.nu2,
+                               bottom_max_elements=cfg.bottom_max_elements, bottom_tol=cfg.bottom_tol, min_depth=1)
+        return Multigrid(ctx, ccfg, levels=As, transfers=Ts,
+                         system_kind=L.SYSTEM_STOKES if problem.n_comp > 1 else L.SYSTEM_SCALAR, dim=problem.dim,
+                         n_comp=problem.n_comp, bs_scalar=problem.bs_scalar)
+
+    offs = []
+    if problem.kernel_constants:
+        offs += [c * problem.bs_scalar for c in range(1 if problem.n_comp == 1 else problem.dim)]
+    if problem.kernel_pressure:
+        offs.append(problem.dim * problem.bs_scalar)
+    dm = DistMultigrid(GpuOps(ctx), dist, cfg, levels, transfers, K, problem.dim, problem.bs_scalar,
+                       problem.n_comp, offs, coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank)
+    dm._full = full
+    return dm

@@ -1,0 +1,112 @@
+"""Worker for tests/test_parallel_gloo.py (spawned; must be importable).
+
+Runs the product's partitioned V-cycle (paper_2412_12506_b200.parallel:
+partition plans from the C ABI, ghost exchange / agglomeration /
+P-independent projection over torch.distributed gloo) with a CPU compute
+double -- the numpy oracle port -- and writes this rank's owned slice of x
+after a few cycles."""
+import os
+import sys
+
+import numpy as np
+
+
+class CpuOps:
+    """Test double for GpuOps: the same local operations on torch CPU tensors,
+    computed by the oracle port (oracle/port.py)."""
+
+    def __init__(self):
+        import torch
+        from oracle import port
+        self.torch, self.port = torch, port
+
+    def tensor(self, n):
+        return self.torch.zeros(int(n), dtype=self.torch.float64)
+
+    def itensor(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, np.int64))
+
+    def matrix(self, brows, bcols, bs, ptr, col, val):
+        return (np.asarray(ptr), np.asarray(col), np.asarray(val), int(brows), int(bcols), int(bs))
+
+    def factors(self, n, bs, V, lam, s):
+        return (np.asarray(V), np.asarray(lam), np.asarray(s))
+
+    def transfer(self, n_fine, n_coarse, parent, orth, dim, bss, ncomp, K):
+        return (np.asarray(parent), np.asarray(orth), np.asarray(K), bss, ncomp, int(n_coarse))
+
+    def residual(self, A, b, x_ext, r):
+        ptr, col, val, _, _, bs = A
+        r.copy_(self.torch.as_tensor(b.numpy() - self.port.spmv(ptr, col, val, bs, bs, x_ext.numpy())))
+
+    def spmv_add(self, B, r_ext, x_own):
+        ptr, col, val, _, _, bs = B
+        x_own.copy_(self.torch.as_tensor(x_own.numpy() + self.port.spmv(ptr, col, val, bs, bs, r_ext.numpy())))
+
+    def relax(self, A, F, b, x_src, x_live, x_out, omega):
+        ptr, col, val, n, _, bs = A
+        out = self.port.relax_rows(np.arange(n), ptr, col, val, bs, b.numpy(), x_src.numpy(), x_live.numpy(), *F,
+                                   omega)
+        x_out.copy_(self.torch.as_tensor(out.reshape(-1)))
+
+    def restrict(self, T, rf, rc):
+        parent, orth, K, bss, ncomp, nc = T
+        rc.copy_(self.torch.as_tensor(self.port.restrict(parent, orth, K, bss, ncomp, nc, rf.numpy())))
+
+    def prolong(self, T, xc, xf):
+        parent, orth, K, bss, ncomp, nc = T
+        xf.copy_(self.torch.as_tensor(self.port.interpolate_add(parent, orth, K, bss, ncomp, xc.numpy(),
+                                                                xf.numpy())))
+
+    def gather(self, x, idx, n, bs, out):
+        out[:n * bs] = x.view(-1, bs)[idx[:n]].reshape(-1)
+
+    def to_host(self, t):
+        return t.numpy()
+
+
+def worker(rank, world, port_no, case, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    from oracle import port, ref
+    from paper_2412_12506_b200 import parallel
+    from tests import cases as K
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spec, cfg, min_rows = {
+        "sai-scalar2d-periodic": (K.scalar(16, 2, K.P, degree=1), K.cfg("sai", level=1, nu=2), 16),
+        "sai-scalar2d-dirichlet-p2": (K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=1), 8),
+        "jacobi-scalar2d-periodic": (K.scalar(16, 2, K.P, degree=1), K.cfg("jacobi", omega=0.7, nu=2), 16),
+        "sai-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=1), K.cfg("sai", level=1, zeta=0.13, nu=1), 8),
+        "sai-scalar3d-periodic": (K.scalar(8, 3, K.P, degree=1), K.cfg("sai", level=1, nu=1), 32),
+    }[case]
+    R = ref.RefMultigrid(spec, cfg)
+    P = port.from_reference(R, cfg)
+    levels = P.levels
+    transfers = P.transfers
+
+    def coarse_factory(ld):
+        tail = port.PortMultigrid(levels[ld:], transfers[ld:], P.K, P.bottom, cfg, P.bss, P.ncomp, [])
+
+        class Coarse:
+            def vcycle(self, x, b):
+                x.copy_(torch.as_tensor(tail.v_cycle(0, np.zeros(x.numel()), b.numpy())))
+        return Coarse()
+
+    dm = parallel.DistMultigrid(CpuOps(), dist, cfg, levels, transfers, P.K, R.dim, P.bss, P.ncomp, P.koffs,
+                                coarse_factory, min_rows_per_rank=min_rows)
+    n, bs = levels[0]["n"], levels[0]["bs"]
+    rng = np.random.default_rng(5)
+    b = rng.uniform(-1, 1, n * bs)
+    r0, r1 = dm.owned_range()
+    x_own = torch.zeros((r1 - r0) * bs, dtype=torch.float64)
+    b_own = torch.as_tensor(b[r0 * bs:r1 * bs].copy())
+    for _ in range(2):
+        dm.cycle(x_own, b_own)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), x=x_own.numpy(), r0=r0, r1=r1, ld=dm.ld)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -1,0 +1,51 @@
+"""The partitioned V-cycle's GPU path (GpuOps over the C ABI, NCCL process
+group) at world size 1 equals the single-GPU hierarchy in strict-order mode
+bit for bit.  The multi-rank logic is covered on CPU by
+tests/test_parallel_gloo.py (2 and 4 ranks, bit-exact)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2412_12506_b200 as g
+from tests import cases as K
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dist1():
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+
+
+@pytest.mark.parametrize("name,spec,cfg,min_rows", [
+    ("sai-3d", K.scalar(8, 3, K.P, degree=2, beta=4.0), K.cfg("sai", level=1), 64),
+    ("sai-2d-dirichlet", K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=2), 16),
+    ("jacobi-2d", K.scalar(16, 2, K.P, degree=3, beta=9.0), K.cfg("jacobi", omega=0.7, nu=2), 16),
+])
+def test_partitioned_path_world1_bitwise(ctx, dist1, name, spec, cfg, min_rows):
+    from paper_2412_12506_b200 import parallel
+    P = g.Problem(spec, min_depth=cfg.min_depth)
+    dm = parallel.from_problem(ctx, P, cfg, dist1, min_rows_per_rank=min_rows)
+    full = dm._full
+    full.set_strict_order(True)
+    n, bs = full.n, full.bs
+    b = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, n * bs)).cuda()
+    xd = torch.zeros_like(b)
+    xf = torch.zeros_like(b)
+    for _ in range(2):
+        dm.cycle(xd, b)
+        full.cycle(xf, b)
+    torch.cuda.synchronize()
+    assert np.array_equal(xd.cpu().numpy(), xf.cpu().numpy())
