@@ -132,7 +132,49 @@ __device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int i
     }
 }
 
-template <int GT>
+/// s = 0 + B[t,0] X[0] + B[t,1] X[1] + ... from a column-major stage (lane t
+/// holds Bc = stage + t); BS compile-time for the common block sizes (fully
+/// unrolled, immediate offsets), 0 = runtime (any rbs x cbs).
+template <int BS>
+__device__ __forceinline__ double bdot(const double* __restrict__ Bc, const double* __restrict__ X, int cbs,
+                                       int rbs) {
+    double s = 0.0;
+    if constexpr (BS > 0) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) s = madd_rn(s, Bc[c * BS], X[c]);
+    } else {
+#pragma unroll 8
+        for (int c = 0; c < cbs; ++c) s = madd_rn(s, Bc[size_t(c) * rbs], X[c]);
+    }
+    return s;
+}
+
+/// Two independent block dot products interleaved: the sequential FP64 add
+/// chain of one block is what bounds a warp, two chains double its ILP while
+/// every s_k keeps the reference's order.
+template <int BS>
+__device__ __forceinline__ void bdot2(const double* __restrict__ B1, const double* __restrict__ X1,
+                                      const double* __restrict__ B2, const double* __restrict__ X2, int cbs, int rbs,
+                                      double& s1, double& s2) {
+    double u = 0.0, v = 0.0;
+    if constexpr (BS > 0) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            u = madd_rn(u, B1[c * BS], X1[c]);
+            v = madd_rn(v, B2[c * BS], X2[c]);
+        }
+    } else {
+#pragma unroll 4
+        for (int c = 0; c < cbs; ++c) {
+            u = madd_rn(u, B1[size_t(c) * rbs], X1[c]);
+            v = madd_rn(v, B2[size_t(c) * rbs], X2[c]);
+        }
+    }
+    s1 = u;
+    s2 = v;
+}
+
+template <int GT, int BS>
 __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* stages = reinterpret_cast<double*>(smem_raw);
@@ -144,6 +186,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     const int t = threadIdx.x;
     const int g = blockIdx.x, ng = gridDim.x;
     const int NS = a.nstages;
+    const int rbs = BS > 0 ? BS : a.rbs, cbs = BS > 0 ? BS : a.cbs;
 
     if (t == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1u + uint32_t(a.cbs));
@@ -162,16 +205,17 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
 
     uint32_t q = 0;  // items consumed
     const bool relax = a.mode == MODE_RELAX;
+    const bool pairs = NS >= 3;
     for (int m = 0;; ++m) {
         const int slot = g + m * ng;
         if (slot >= a.nrows) break;
         const int row = row_at(a, slot);
         const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
-        const bool act = t < a.rbs;
+        const bool act = t < rbs;
         // epilogue operands fetched early; their latency hides under the blocks
         double pre_b = 0.0, pre_x = 0.0, pre_s = 0.0, pre_l = 0.0;
         if (act) {
-            const size_t o = size_t(row) * a.rbs + t;
+            const size_t o = size_t(row) * rbs + t;
             if (a.mode == MODE_RESIDUAL || relax) pre_b = __ldg(a.b + o);
             if (a.mode == MODE_ADD || relax) pre_x = a.xe[o];
             if (relax) {
@@ -185,31 +229,42 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
         for (;;) {
             if (relax)
                 while (k < k1 && __ldg(a.col + k) == row) ++k;
-            bool is_v;
-            if (k < k1)
-                is_v = false;
-            else if (!vdone)
-                is_v = true;
-            else
+            int nblk = 0, k2 = k;
+            if (k < k1) {
+                nblk = 1;
+                k2 = k + 1;
+                if (relax)
+                    while (k2 < k1 && __ldg(a.col + k2) == row) ++k2;
+                if (pairs && k2 < k1) nblk = 2;
+            } else if (vdone) {
                 break;
+            }
             const int st = int(q % uint32_t(NS));
-            const uint32_t ph = (q / uint32_t(NS)) & 1u;
-            mbar_wait(bars + st, ph);
+            mbar_wait(bars + st, (q / uint32_t(NS)) & 1u);
             const double* S = stages + size_t(st) * a.stage_doubles;
-            if (!is_v) {
-                const double* X = xslots + size_t(st) * a.xslot_doubles;
+            const double* X = xslots + size_t(st) * a.xslot_doubles;
+            int used = 1;
+            if (nblk == 2) {
+                const int st2 = int((q + 1) % uint32_t(NS));
+                mbar_wait(bars + st2, ((q + 1) / uint32_t(NS)) & 1u);
                 if (act) {
-                    double s = 0.0;
-                    const double* Bc = S + t;
-                    const int cbs = a.cbs, rbs = a.rbs;
-#pragma unroll 8
-                    for (int c = 0; c < cbs; ++c) s = madd_rn(s, Bc[size_t(c) * rbs], X[c]);
+                    double s1, s2;
+                    bdot2<BS>(S + t, X, stages + size_t(st2) * a.stage_doubles + t,
+                              xslots + size_t(st2) * a.xslot_doubles, cbs, rbs, s1, s2);
+                    acc = relax ? __dsub_rn(acc, s1) : __dadd_rn(acc, s1);
+                    acc = relax ? __dsub_rn(acc, s2) : __dadd_rn(acc, s2);
+                }
+                k = k2 + 1;
+                used = 2;
+            } else if (nblk == 1) {
+                if (act) {
+                    const double s = bdot<BS>(S + t, X, cbs, rbs);
                     acc = relax ? __dsub_rn(acc, s) : __dadd_rn(acc, s);
                 }
-                ++k;
+                k = k + 1;
             } else {
                 // block-diagonal pseudoinverse solve with the staged factor V
-                const int bs = a.rbs, ld = a.ld;
+                const int bs = rbs, ld = a.ld;
                 if (act) ubuf[t] = __dmul_rn(pre_s, acc);
                 group_sync(1, GT);
                 if (act) {
@@ -231,15 +286,18 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                 }
                 vdone = true;
             }
-            group_sync(1, GT);  // every lane is done with this stage
-            ++q;
-            if (it_next(a, pit, g, ng, kind, idx)) {
-                if (t == 0) fence_proxy_async();
-                issue_item<GT>(a, kind, idx, st, stages, xslots, bars);
+            group_sync(1, GT);  // every lane is done with these stages
+            for (int u = 0; u < used; ++u) {
+                const int su = int(q % uint32_t(NS));
+                ++q;
+                if (it_next(a, pit, g, ng, kind, idx)) {
+                    if (t == 0) fence_proxy_async();
+                    issue_item<GT>(a, kind, idx, su, stages, xslots, bars);
+                }
             }
         }
         if (act) {
-            const size_t o = size_t(row) * a.rbs + t;
+            const size_t o = size_t(row) * rbs + t;
             double out;
             switch (a.mode) {
                 case MODE_RESIDUAL: out = __dsub_rn(pre_b, acc); break;
@@ -252,12 +310,11 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     // drain: nothing outstanding (every issued item was consumed)
 }
 
-template <int GT>
+template <int GT, int BS>
 void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
     static int attr_set_device = -1;
     if (attr_set_device != ctx.device) {
-        LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(ctx.smem_optin)));
         attr_set_device = ctx.device;
     }
@@ -266,12 +323,12 @@ void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
     for (const auto& e : occ_cache)
         if (e.first == smem) occ = e.second;
     if (occ < 0) {
-        LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<GT>, GT, smem));
+        LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<GT, BS>, GT, smem));
         occ_cache.push_back({smem, occ});
     }
     if (occ < 1) fail(LDGMG_ERR_CUDA, "rowpass: block does not fit on an SM");
     const int grid = std::max(1, std::min(a.nrows, occ * ctx.num_sms));
-    rowpass_kernel<GT><<<grid, GT, smem, ctx.stream>>>(a);
+    rowpass_kernel<GT, BS><<<grid, GT, smem, ctx.stream>>>(a);
     after_launch("rowpass_kernel");
 }
 
@@ -590,17 +647,28 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
     const int GT = wide <= 32 ? 32 : wide <= 64 ? 64 : wide <= 128 ? 128 : 256;
     // ring depth: keep >= ~3 blocks in flight per group within a 200 KB budget
     const size_t stage_bytes = size_t(a.stage_doubles) * 8;
-    int ns = 4;
+    static int ns_env = -2;
+    if (ns_env == -2) {
+        const char* e = getenv("LDGMG_NS");
+        ns_env = e ? atoi(e) : -1;
+    }
+    int ns = ns_env > 1 ? ns_env : 4;
     while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
     a.nstages = ns;
     const size_t smem = size_t(ns) * stage_bytes + size_t(ns) * a.xslot_doubles * 8 +
                         2 * size_t(a.xslot_doubles) * 8 + size_t(ns) * 8;
     if (smem > ctx.smem_optin) fail(LDGMG_ERR_INVALID_ARGUMENT, "rowpass: block too large for shared memory");
-    switch (GT) {
-        case 32: configure_and_launch<32>(ctx, a, smem); break;
-        case 64: configure_and_launch<64>(ctx, a, smem); break;
-        case 128: configure_and_launch<128>(ctx, a, smem); break;
-        default: configure_and_launch<256>(ctx, a, smem); break;
+    const bool sq = A.rbs == A.cbs;
+    if (sq && A.rbs == 16) configure_and_launch<32, 16>(ctx, a, smem);
+    else if (sq && A.rbs == 25) configure_and_launch<32, 25>(ctx, a, smem);
+    else if (sq && A.rbs == 27) configure_and_launch<32, 27>(ctx, a, smem);
+    else if (sq && A.rbs == 48) configure_and_launch<64, 48>(ctx, a, smem);
+    else if (sq && A.rbs == 108) configure_and_launch<128, 108>(ctx, a, smem);
+    else switch (GT) {
+        case 32: configure_and_launch<32, 0>(ctx, a, smem); break;
+        case 64: configure_and_launch<64, 0>(ctx, a, smem); break;
+        case 128: configure_and_launch<128, 0>(ctx, a, smem); break;
+        default: configure_and_launch<256, 0>(ctx, a, smem); break;
     }
 }
 
