@@ -44,6 +44,18 @@ def configs(c5n):
                   mg(g.SmootherConfig.coloured_gs(), 3), "normal"),
         "C3-SAI": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=16.0, **ball3),
                    mg(g.SmootherConfig.sai(1), 3), "normal"),
+        # reference-native conforming interface (catalogue box (1/4,3/4)^2,
+        # harness.hpp:57-64): the hierarchy stops before phase mixing (4x4)
+        "C3-box-GS": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=16.0,
+                                    phase_shape=g.PHASE_BOXES, center=(0.25, 0.25, 0.25), radii=(0.75, 0.75, 0.75),
+                                    mu_in=1e4, mu_out=1.0),
+                      mg(g.SmootherConfig.coloured_gs(), 3), "normal"),
+        "C3-box-SAI": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=16.0,
+                                     phase_shape=g.PHASE_BOXES, center=(0.25, 0.25, 0.25), radii=(0.75, 0.75, 0.75),
+                                     mu_in=1e4, mu_out=1.0),
+                       mg(g.SmootherConfig.sai(1), 3), "normal"),
+        "C3-beta4p2-GS": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=64.0, **ball3),
+                          mg(g.SmootherConfig.coloured_gs(), 3), "normal"),
         "C4": (g.ProblemSpec(kind=T, dim=2, n=128, degree=3, bc=(P_,) * 6, beta=9.0, beta_p=1 / 16, gamma=0.0, **ell),
                mg(g.SmootherConfig.sai(1, 0.0990), 3), "uniform"),
         "C5": (g.ProblemSpec(kind=T, dim=3, n=c5n, degree=2, bc=(P_,) * 6, beta=4.0, beta_p=1 / 16, gamma=0.0,
