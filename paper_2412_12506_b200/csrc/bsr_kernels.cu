@@ -27,32 +27,11 @@
 #include <vector>
 
 #include "core.hpp"
+#include "row_ops.cuh"
 
 namespace ldgmg_b200 {
 
 namespace {
-
-struct RowPassArgs {
-    const int* ptr;
-    const int* col;
-    const double* val;
-    int blk_stride;
-    int rbs, cbs;
-    int mode;
-    const double* x;
-    const double* b;
-    const double* xe;
-    double* y;
-    const int* rows;
-    int nrows;
-    const double* V;
-    const double* lam;
-    const double* scal;
-    const double* lmax;
-    int ld, vstride;
-    double omega, kernel_tol;
-    int nstages, stage_doubles, xslot_doubles;
-};
 
 struct ItemIt {
     int m;     // row slot
@@ -60,10 +39,6 @@ struct ItemIt {
     int k, kend;
     int vdone;
 };
-
-__device__ __forceinline__ int row_at(const RowPassArgs& a, int slot) {
-    return a.rows ? __ldg(a.rows + slot) : slot;
-}
 
 __device__ __forceinline__ void it_load(const RowPassArgs& a, ItemIt& it, int g, int ng) {
     const int slot = g + it.m * ng;
@@ -494,74 +469,7 @@ namespace {
 /// Requires rbs, cbs <= 32.
 __global__ void __launch_bounds__(256) rowsplit_kernel(const RowPassArgs a, int maxlen) {
     extern __shared__ __align__(16) double ss[];  // maxlen x 32 partial sums, then u, t
-    double* ubuf = ss + size_t(maxlen) * 32;
-    double* tbuf = ubuf + 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
-    const bool relax = a.mode == MODE_RELAX;
-    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) {
-        const int row = row_at(a, slot);
-        const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
-        for (int k = k0 + warp; k < k1; k += W) {
-            const int j = __ldg(a.col + k);
-            if (relax && j == row) continue;
-            if (lane < a.rbs) {
-                const double* Bc = a.val + size_t(k) * a.blk_stride + lane;
-                const double* xj = a.x + size_t(j) * a.cbs;
-                double s = 0.0;
-#pragma unroll 9
-                for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, __ldg(Bc + size_t(c) * a.rbs), xj[c]);
-                ss[size_t(k - k0) * 32 + lane] = s;
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const bool act = lane < a.rbs;
-            const size_t o = size_t(row) * a.rbs + lane;
-            double acc = 0.0;
-            if (act) {
-                if (relax) {
-                    acc = __ldg(a.b + o);
-                    for (int k = k0; k < k1; ++k)
-                        if (__ldg(a.col + k) != row) acc = __dsub_rn(acc, ss[size_t(k - k0) * 32 + lane]);
-                } else {
-                    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, ss[size_t(k - k0) * 32 + lane]);
-                }
-            }
-            if (relax) {
-                const int bs = a.rbs, ld = a.ld;
-                const double* Ve = a.V + size_t(row) * a.vstride;
-                const double sc = act ? __ldg(a.scal + o) : 0.0;
-                const double lam = act ? __ldg(a.lam + o) : 0.0;
-                const double xe = act ? a.xe[o] : 0.0;
-                if (act) ubuf[lane] = __dmul_rn(sc, acc);
-                __syncwarp();
-                if (act) {
-                    double tt = 0.0;
-                    const double* Vcol = Ve + size_t(lane) * ld;
-                    for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, __ldg(Vcol + kk), ubuf[kk]);
-                    const double cut = a.kernel_tol * __ldg(a.lmax + row);
-                    tbuf[lane] = fabs(lam) <= cut ? 0.0 : tt / lam;
-                }
-                __syncwarp();
-                if (act) {
-                    double w = 0.0;
-                    for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, __ldg(Ve + size_t(kk) * ld + lane), tbuf[kk]);
-                    const double yv = __dmul_rn(sc, w);
-                    acc = __dadd_rn(__dmul_rn(1.0 - a.omega, xe), __dmul_rn(a.omega, yv));
-                }
-            }
-            if (act) {
-                double out;
-                switch (a.mode) {
-                    case MODE_RESIDUAL: out = __dsub_rn(__ldg(a.b + o), acc); break;
-                    case MODE_ADD: out = __dadd_rn(a.xe[o], acc); break;
-                    default: out = acc; break;
-                }
-                a.y[o] = out;
-            }
-        }
-        __syncthreads();
-    }
+    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) split_row_task(a, row_at(a, slot), maxlen, ss);
 }
 
 int split_threshold_rows(const Ctx& ctx) {

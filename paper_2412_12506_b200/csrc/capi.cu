@@ -658,17 +658,31 @@ int ldgmg_mg_set_smoother(ldgmg_mg* mg, int level, ldgmg_smoother* S) {
         if (level < 0 || level + 1 >= mg->m.depth) fail(LDGMG_ERR_LOGIC, "multigrid: the bottom level has no smoother");
         if (S->s.A != mg->m.A[level]) fail(LDGMG_ERR_INVALID_ARGUMENT, "mg_set_smoother: smoother bound to another operator");
         mg->m.sm[level] = &S->s;
+        mg->m.coarse_dirty = true;
     });
 }
 
 static void ensure_smoothers(ldgmg_ctx* ctx, Mg& m) {
     bool any_missing = false;
     for (int l = 0; l + 1 < m.depth; ++l) any_missing |= m.sm[l] == nullptr;
-    if (!any_missing) return;
-    std::vector<Smoother*> keep = m.sm;
-    mg_default_smoothers(ctx, m);
-    for (int l = 0; l + 1 < m.depth; ++l)
-        if (keep[l]) m.sm[l] = keep[l];
+    if (any_missing) {
+        std::vector<Smoother*> keep = m.sm;
+        mg_default_smoothers(ctx, m);
+        for (int l = 0; l + 1 < m.depth; ++l)
+            if (keep[l]) m.sm[l] = keep[l];
+    }
+    if (m.coarse_dirty) {
+        static int env = -2;
+        if (env == -2) {
+            const char* s = getenv("LDGMG_COARSE_ROWS");
+            env = s ? atoi(s) : -1;
+        }
+        if (env >= 0) m.coarse_rows = env;
+        m.build_coarse_program(*ctx);
+        m.coarse_dirty = false;
+        for (auto& gr : m.graphs) cudaGraphExecDestroy(gr.exec);
+        m.graphs.clear();
+    }
 }
 
 int ldgmg_mg_smoother(ldgmg_mg* mg, int level, ldgmg_smoother** out) {

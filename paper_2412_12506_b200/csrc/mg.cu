@@ -365,6 +365,10 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
         launch_pinv_apply(ctx, bottom, cfg.bottom_tol, b, x);
         return;
     }
+    if (l > 0 && l == coarse_level && x == xl[l].as<double>() && b == bl[l].as<double>()) {
+        launch_coarse_program(ctx);  // the rest of the V-cycle in one cooperative kernel
+        return;
+    }
     const Smoother& S = *sm[l];
     for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre);
     RowPass p;

@@ -77,6 +77,15 @@ struct Mg {
     };
     std::vector<Graph> graphs;
     cudaStream_t cap_stream = nullptr;
+    // persistent cooperative program for the small levels (coarse_program.cu)
+    int coarse_rows = 2048;  // levels with at most this many elements
+    int coarse_level = -1;   // first level run by the program (-1: none)
+    bool coarse_dirty = true;
+    DevBuf coarse_prog;
+    int coarse_nops = 0, coarse_maxlen = 1, coarse_grid = 0;
+    size_t coarse_smem = 0;
+    void build_coarse_program(Ctx& ctx);
+    void launch_coarse_program(Ctx& ctx);
     SaiCache* sai_cache = nullptr;  // shared across levels (multigrid.hpp:60)
 
     void init(Ctx& ctx);

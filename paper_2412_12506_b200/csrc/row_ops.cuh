@@ -1,0 +1,177 @@
+// Device-side pieces shared by the row-pass kernels (bsr_kernels.cu) and the
+// persistent coarse-level program (coarse_program.cu).  Every function keeps
+// the reference's evaluation order (see bsr_kernels.cu header).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "core.hpp"
+
+namespace ldgmg_b200 {
+
+struct RowPassArgs {
+    const int* ptr;
+    const int* col;
+    const double* val;
+    int blk_stride;
+    int rbs, cbs;
+    int mode;
+    const double* x;
+    const double* b;
+    const double* xe;
+    double* y;
+    const int* rows;
+    int nrows;
+    const double* V;
+    const double* lam;
+    const double* scal;
+    const double* lmax;
+    int ld, vstride;
+    double omega, kernel_tol;
+    int nstages, stage_doubles, xslot_doubles;
+};
+
+__device__ __forceinline__ int row_at(const RowPassArgs& a, int slot) {
+    return a.rows ? __ldg(a.rows + slot) : slot;
+}
+
+/// One block row processed by a whole CTA (rbs, cbs <= 32): the row's blocks
+/// spread over the warps (each computes s_k = 0 + b[r,0]x[0] + ... for its
+/// blocks), warp 0 combines them in CSR order and runs the epilogue (relax:
+/// the block-diagonal pseudoinverse with V read from global memory).
+/// `ss` holds maxlen x 32 partial sums + 64 doubles.  All CTA threads call it.
+__device__ __forceinline__ void split_row_task(const RowPassArgs& a, int row, int maxlen, double* ss) {
+    double* ubuf = ss + size_t(maxlen) * 32;
+    double* tbuf = ubuf + 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    const bool relax = a.mode == MODE_RELAX;
+    const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
+    for (int k = k0 + warp; k < k1; k += W) {
+        const int j = __ldg(a.col + k);
+        if (relax && j == row) continue;
+        if (lane < a.rbs) {
+            const double* Bc = a.val + size_t(k) * a.blk_stride + lane;
+            const double* xj = a.x + size_t(j) * a.cbs;
+            double s = 0.0;
+#pragma unroll 9
+            for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, __ldg(Bc + size_t(c) * a.rbs), xj[c]);
+            ss[size_t(k - k0) * 32 + lane] = s;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const bool act = lane < a.rbs;
+        const size_t o = size_t(row) * a.rbs + lane;
+        double acc = 0.0;
+        if (act) {
+            if (relax) {
+                acc = __ldg(a.b + o);
+                for (int k = k0; k < k1; ++k)
+                    if (__ldg(a.col + k) != row) acc = __dsub_rn(acc, ss[size_t(k - k0) * 32 + lane]);
+            } else {
+                for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, ss[size_t(k - k0) * 32 + lane]);
+            }
+        }
+        if (relax) {
+            const int bs = a.rbs, ld = a.ld;
+            const double* Ve = a.V + size_t(row) * a.vstride;
+            const double sc = act ? __ldg(a.scal + o) : 0.0;
+            const double lam = act ? __ldg(a.lam + o) : 0.0;
+            const double xe = act ? a.xe[o] : 0.0;
+            if (act) ubuf[lane] = __dmul_rn(sc, acc);
+            __syncwarp();
+            if (act) {
+                double tt = 0.0;
+                const double* Vcol = Ve + size_t(lane) * ld;
+                for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, __ldg(Vcol + kk), ubuf[kk]);
+                const double cut = a.kernel_tol * __ldg(a.lmax + row);
+                tbuf[lane] = fabs(lam) <= cut ? 0.0 : tt / lam;
+            }
+            __syncwarp();
+            if (act) {
+                double w = 0.0;
+                for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, __ldg(Ve + size_t(kk) * ld + lane), tbuf[kk]);
+                const double yv = __dmul_rn(sc, w);
+                acc = __dadd_rn(__dmul_rn(1.0 - a.omega, xe), __dmul_rn(a.omega, yv));
+            }
+        }
+        if (act) {
+            double out;
+            switch (a.mode) {
+                case MODE_RESIDUAL: out = __dsub_rn(__ldg(a.b + o), acc); break;
+                case MODE_ADD: out = __dadd_rn(a.xe[o], acc); break;
+                default: out = acc; break;
+            }
+            a.y[o] = out;
+        }
+    }
+    __syncthreads();
+}
+
+/// Restriction of coarse element p (multigrid.hpp:127-149 order); `sh` holds
+/// the children's blocks (<= 64 children x BS).  All CTA threads call it.
+__device__ __forceinline__ void restrict_parent_task(const int* __restrict__ child_ptr, const int* __restrict__ child,
+                                                     const int* __restrict__ orth, const double* __restrict__ K,
+                                                     const double* __restrict__ rf, double* __restrict__ rc, int p,
+                                                     int bss, int ncomp, double* sh, int* sch, int* sor) {
+    const int BS = bss * ncomp;
+    const int q0 = child_ptr[p], nch = child_ptr[p + 1] - q0;
+    for (int q = threadIdx.x; q < nch; q += blockDim.x) {
+        sch[q] = child[q0 + q];
+        sor[q] = orth[sch[q]];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nch * BS; t += blockDim.x) {
+        const int q = t / BS, e = t - q * BS;
+        sh[t] = rf[size_t(sch[q]) * BS + e];
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < BS; o += blockDim.x) {
+        const int c = o / bss, j = o - c * bss;
+        double acc = 0.0;
+        for (int q = 0; q < nch; ++q) {
+            const double* src = sh + q * BS;
+            const int ot = sor[q];
+            if (ot < 0) {
+                acc = __dadd_rn(acc, src[o]);
+                continue;
+            }
+            const double* Ko = K + size_t(ot) * bss * bss + j;
+            double s = 0.0;
+#pragma unroll 9
+            for (int i = 0; i < bss; ++i) s = madd_rn(s, __ldg(Ko + size_t(i) * bss), src[c * bss + i]);
+            acc = __dadd_rn(acc, s);
+        }
+        rc[size_t(p) * BS + o] = acc;
+    }
+    __syncthreads();
+}
+
+/// Prolongation onto the children of coarse element p (multigrid.hpp:104-123).
+__device__ __forceinline__ void prolong_parent_task(const int* __restrict__ child_ptr, const int* __restrict__ child,
+                                                    const int* __restrict__ orth, const double* __restrict__ K,
+                                                    const double* __restrict__ xc, double* __restrict__ xf, int p,
+                                                    int bss, int ncomp, double* sx) {
+    const int BS = bss * ncomp;
+    for (int t = threadIdx.x; t < BS; t += blockDim.x) sx[t] = xc[size_t(p) * BS + t];
+    __syncthreads();
+    const int q0 = child_ptr[p], nch = child_ptr[p + 1] - q0;
+    for (int t = threadIdx.x; t < nch * BS; t += blockDim.x) {
+        const int q = t / BS, ii = t - q * BS;
+        const int f = child[q0 + q], ot = orth[f];
+        double* dst = xf + size_t(f) * BS + ii;
+        if (ot < 0) {
+            *dst = __dadd_rn(*dst, sx[ii]);
+            continue;
+        }
+        const int c = ii / bss, i = ii - c * bss;
+        const double* Ko = K + size_t(ot) * bss * bss + size_t(i) * bss;
+        double s = 0.0;
+#pragma unroll 9
+        for (int j = 0; j < bss; ++j) s = madd_rn(s, __ldg(Ko + j), sx[c * bss + j]);
+        *dst = __dadd_rn(*dst, s);
+    }
+    __syncthreads();
+}
+
+}  // namespace ldgmg_b200
