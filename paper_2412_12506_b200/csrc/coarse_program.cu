@@ -49,11 +49,20 @@ namespace {
 __global__ void __launch_bounds__(256) coarse_program_kernel(const CoarseOp* __restrict__ ops, int nops, int maxlen) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int sch[64], sor[64];
+    __shared__ CoarseOp sop;
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     const int64_t nth = int64_t(gridDim.x) * blockDim.x;
     for (int i = 0; i < nops; ++i) {
-        const CoarseOp& op = ops[i];
+        // stage the op descriptor once per CTA (one coalesced read, then smem)
+        {
+            const int nw = int(sizeof(CoarseOp) / sizeof(int));
+            const int* src = reinterpret_cast<const int*>(ops + i);
+            int* dst = reinterpret_cast<int*>(&sop);
+            for (int w = threadIdx.x; w < nw; w += blockDim.x) dst[w] = src[w];
+            __syncthreads();
+        }
+        const CoarseOp& op = sop;
         switch (op.type) {
             case OP_ROWS:
                 for (int slot = blockIdx.x; slot < op.rows.nrows; slot += gridDim.x)
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(256) coarse_program_kernel(const CoarseOp* __r
                 }
                 break;
         }
-        grid.sync();
+        grid.sync();  // also orders the next descriptor load after this op's smem reads
     }
 }
 
@@ -235,7 +244,12 @@ void Mg::build_coarse_program(Ctx& ctx) {
     int occ = 0;
     LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coarse_program_kernel, 256, coarse_smem));
     if (occ < 1) return;
-    coarse_grid = ctx.num_sms * std::min(occ, 2);
+    static int env_grid = -2;
+    if (env_grid == -2) {
+        const char* e = getenv("LDGMG_COARSE_CTAS_PER_SM");
+        env_grid = e ? atoi(e) : -1;
+    }
+    coarse_grid = ctx.num_sms * std::max(1, std::min(occ, env_grid > 0 ? env_grid : 1));
     coarse_level = lc;
 }
 
