@@ -143,7 +143,7 @@ CoarseOp rows_op(const Bsr& A, int mode, const double* x, const double* b, const
 void Mg::build_coarse_program(Ctx& ctx) {
     coarse_level = -1;
     int lc = -1;
-    for (int l = 1; l + 1 < depth; ++l)
+    for (int l = 1; l + 1 < depth && coarse_rows > 0; ++l)
         if (A[l]->brows <= coarse_rows) {
             lc = l;
             break;

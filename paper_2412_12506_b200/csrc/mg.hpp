@@ -78,7 +78,10 @@ struct Mg {
     std::vector<Graph> graphs;
     cudaStream_t cap_stream = nullptr;
     // persistent cooperative program for the small levels (coarse_program.cu)
-    int coarse_rows = 2048;  // levels with at most this many elements
+    // Off by default: measured slower than graph-launched passes on B200 (C2
+    // 3.46 -> 3.89 ms, grid-wide barriers cost more than graph node launches);
+    // LDGMG_COARSE_ROWS=n enables it for levels with <= n elements.
+    int coarse_rows = 0;
     int coarse_level = -1;   // first level run by the program (-1: none)
     bool coarse_dirty = true;
     DevBuf coarse_prog;
