@@ -228,6 +228,155 @@ __global__ void __launch_bounds__(NT) qr_ls_kernel(double* __restrict__ Ms, cons
     if (tid == 0) deficient[p] = def;
 }
 
+/// Blocked Householder QR least squares (compact WY, panels of NB columns
+/// factored in shared memory).  Same contract as qr_ls_kernel.  The trailing
+/// matrix and the right-hand sides are read twice and written once per
+/// PANEL instead of per column, an NB-fold cut of the L2 traffic that bounds
+/// the unblocked kernel.  Requires m * NB doubles of shared memory.
+template <int NT, int NB>
+__global__ void __launch_bounds__(NT) qr_blocked_kernel(double* __restrict__ Ms, const int64_t* __restrict__ moff,
+                                                        double* __restrict__ Ws, const int64_t* __restrict__ woff,
+                                                        double* __restrict__ Xs, const int64_t* __restrict__ xoff,
+                                                        const int* __restrict__ ni, const int* __restrict__ nj, int bs,
+                                                        int* __restrict__ deficient) {
+    extern __shared__ __align__(16) double Vp[];  // (m) x NB panel, column-major (rows j0.. stored from 0)
+    __shared__ double red[NT / 32];
+    __shared__ double sT[NB * NB], stau[NB], sh_nrm, sh_beta;
+    const int p = blockIdx.x;
+    const int m = ni[p] * bs, n = nj[p] * bs, k = bs;
+    double* M = Ms + moff[p];
+    double* W = Ws + woff[p];
+    double* X = Xs + xoff[p];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc = 0.0;
+    for (int64_t t = tid; t < int64_t(m) * k; t += NT) {
+        const int c = int(t / m), r = int(t - int64_t(c) * m);
+        W[t] = r == c ? 1.0 : 0.0;
+    }
+    for (int64_t t = tid; t < int64_t(m) * n; t += NT) acc += M[t] * M[t];
+    acc = block_sum<NT>(acc, red);
+    if (tid == 0) sh_nrm = sqrt(acc);
+    __syncthreads();
+    const double tol = 1e-12 * sh_nrm;
+    int def = 0;
+    for (int j0 = 0; j0 < n; j0 += NB) {
+        const int nb = min(NB, n - j0), mr = m - j0;
+        // 1. panel -> shared memory
+        for (int t = tid; t < mr * nb; t += NT) {
+            const int c = t / mr, r = t - c * mr;
+            Vp[size_t(c) * mr + r] = M[size_t(j0 + c) * m + j0 + r];
+        }
+        __syncthreads();
+        // 2. unblocked factorisation of the panel in shared memory
+        for (int jj = 0; jj < nb; ++jj) {
+            double* cj = Vp + size_t(jj) * mr;
+            double s = 0.0;
+            for (int i = jj + 1 + tid; i < mr; i += NT) s += cj[i] * cj[i];
+            s = block_sum<NT>(s, red);
+            const double alpha = cj[jj];
+            double tau = 0.0, beta = alpha;
+            if (s != 0.0) {
+                const double nrm = sqrt(alpha * alpha + s);
+                beta = alpha >= 0.0 ? -nrm : nrm;
+                tau = (beta - alpha) / beta;
+                const double scal = 1.0 / (alpha - beta);
+                for (int i = jj + 1 + tid; i < mr; i += NT) cj[i] *= scal;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                cj[jj] = 1.0;  // implicit unit head of v, R_jj kept in sh_beta
+                stau[jj] = tau;
+                sh_beta = beta;
+            }
+            __syncthreads();
+            const double bj = sh_beta;
+            if (!(fabs(bj) > tol)) def = 1;
+            // apply to the remaining panel columns (one warp per column)
+            for (int c = jj + 1 + warp; c < nb; c += NT / 32) {
+                double* ct = Vp + size_t(c) * mr;
+                double w = 0.0;
+                for (int i = jj + lane; i < mr; i += 32) w += cj[i] * ct[i];
+                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+                w *= tau;
+                for (int i = jj + lane; i < mr; i += 32) ct[i] -= w * cj[i];
+            }
+            __syncthreads();
+            if (tid == 0) M[size_t(j0 + jj) * m + j0 + jj] = bj;  // R diagonal
+            // R above the diagonal of this panel column comes from the panel
+            for (int i = tid; i < jj; i += NT) M[size_t(j0 + jj) * m + j0 + i] = Vp[size_t(jj) * mr + i];
+            __syncthreads();
+        }
+        // 3. T of the compact WY form H_0 ... H_{nb-1} = I - V T V^T (T upper)
+        if (tid < nb) sT[tid * NB + tid] = stau[tid];
+        __syncthreads();
+        for (int i = 1; i < nb; ++i) {
+            // z = V(:,0:i)^T v_i (one warp per entry)
+            for (int c = warp; c < i; c += NT / 32) {
+                double w = 0.0;
+                for (int r = i + lane; r < mr; r += 32) w += Vp[size_t(c) * mr + r] * Vp[size_t(i) * mr + r];
+                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+                if (lane == 0) sT[c * NB + i] = w;  // stash z_c in column i
+            }
+            __syncthreads();
+            if (tid == 0) {  // T(0:i, i) = -tau_i T(0:i,0:i) z
+                double tmp[NB];
+                for (int a = 0; a < i; ++a) {
+                    double s = 0.0;
+                    for (int b2 = a; b2 < i; ++b2) s += sT[a * NB + b2] * sT[b2 * NB + i];
+                    tmp[a] = -stau[i] * s;
+                }
+                for (int a = 0; a < i; ++a) sT[a * NB + i] = tmp[a];
+            }
+            __syncthreads();
+        }
+        // 4. trailing update of M[:, j0+nb:] and W: C -= V T^T V^T C, a warp per column
+        const int ncols = (n - j0 - nb) + k;
+        for (int t = warp; t < ncols; t += NT / 32) {
+            double* ct = t < n - j0 - nb ? M + size_t(j0 + nb + t) * m + j0 : W + size_t(t - (n - j0 - nb)) * m + j0;
+            double y[NB];
+#pragma unroll
+            for (int a = 0; a < NB; ++a) y[a] = 0.0;
+            for (int r = lane; r < mr; r += 32) {
+                const double cv = ct[r];
+#pragma unroll
+                for (int a = 0; a < NB; ++a)
+                    if (a < nb && r >= a) y[a] += Vp[size_t(a) * mr + r] * cv;
+            }
+#pragma unroll
+            for (int a = 0; a < NB; ++a)
+                for (int o = 16; o > 0; o >>= 1) y[a] += __shfl_xor_sync(0xffffffffu, y[a], o);
+            double z[NB];  // z = T^T y
+#pragma unroll
+            for (int a = 0; a < NB; ++a) {
+                double s = 0.0;
+                for (int b2 = 0; b2 <= a && b2 < nb; ++b2) s += sT[b2 * NB + a] * y[b2];
+                z[a] = a < nb ? s : 0.0;
+            }
+            for (int r = lane; r < mr; r += 32) {
+                double d = 0.0;
+#pragma unroll
+                for (int a = 0; a < NB; ++a)
+                    if (a < nb && r >= a) d += Vp[size_t(a) * mr + r] * z[a];
+                ct[r] -= d;
+            }
+        }
+        __syncthreads();
+    }
+    if (!def)
+        for (int c = warp; c < k; c += NT / 32) {
+            const double* wc = W + size_t(c) * m;
+            double* xc = X + size_t(c) * n;
+            for (int i = n - 1; i >= 0; --i) {
+                double s = 0.0;
+                for (int l = i + 1 + lane; l < n; l += 32) s += M[size_t(l) * m + i] * xc[l];
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) xc[i] = (wc[i] - s) / M[size_t(i) * m + i];
+                __syncwarp();
+            }
+        }
+    if (tid == 0) deficient[p] = def;
+}
+
 /// Minimum-norm least squares by one-sided Jacobi SVD (dgelsd semantics,
 /// singular values <= rcond * s_max dropped).  U = M (m x n) in place,
 /// V (n x n) workspace.
@@ -667,11 +816,35 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                                                          d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                          d_moff.as<int64_t>(), d_M.as<double>());
             after_launch("assemble_m_kernel");
-            qr_ls_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
-                                                          d_woff.as<int64_t>(), d_X.as<double>(),
-                                                          d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
-                                                          d_def.as<int>());
-            after_launch("qr_ls_kernel");
+            int max_m = 0;
+            for (int v : hni) max_m = std::max(max_m, v * bs);
+            const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
+            static int qr_env = -2;
+            if (qr_env == -2) {
+                const char* e = getenv("LDGMG_QR_UNBLOCKED");
+                qr_env = e ? atoi(e) : 0;
+            }
+            if (!qr_env && smem8 <= 200 * 1024) {
+                LDGMG_CUDA(cudaFuncSetAttribute(qr_blocked_kernel<256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(smem8)));
+                qr_blocked_kernel<256, 8><<<nb, 256, smem8, ctx.stream>>>(
+                    d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
+                    d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
+                after_launch("qr_blocked_kernel");
+            } else if (!qr_env && smem4 <= 200 * 1024) {
+                LDGMG_CUDA(cudaFuncSetAttribute(qr_blocked_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(smem4)));
+                qr_blocked_kernel<256, 4><<<nb, 256, smem4, ctx.stream>>>(
+                    d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
+                    d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
+                after_launch("qr_blocked_kernel");
+            } else {
+                qr_ls_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
+                                                              d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
+                                                              d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
+                                                              d_def.as<int>());
+                after_launch("qr_ls_kernel");
+            }
             std::vector<int> def(nb);
             d2h(ctx, def.data(), d_def.p, sizeof(int) * nb);
             // rank-deficient problems: minimum-norm refit from a fresh copy of M
