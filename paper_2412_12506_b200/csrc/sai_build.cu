@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -228,153 +229,416 @@ __global__ void __launch_bounds__(NT) qr_ls_kernel(double* __restrict__ Ms, cons
     if (tid == 0) deficient[p] = def;
 }
 
-/// Blocked Householder QR least squares (compact WY, panels of NB columns
-/// factored in shared memory).  Same contract as qr_ls_kernel.  The trailing
-/// matrix and the right-hand sides are read twice and written once per
-/// PANEL instead of per column, an NB-fold cut of the L2 traffic that bounds
-/// the unblocked kernel.  Requires m * NB doubles of shared memory.
-template <int NT, int NB>
-__global__ void __launch_bounds__(NT) qr_blocked_kernel(double* __restrict__ Ms, const int64_t* __restrict__ moff,
-                                                        double* __restrict__ Ws, const int64_t* __restrict__ woff,
-                                                        double* __restrict__ Xs, const int64_t* __restrict__ xoff,
-                                                        const int* __restrict__ ni, const int* __restrict__ nj, int bs,
-                                                        int* __restrict__ deficient) {
-    extern __shared__ __align__(16) double Vp[];  // (m) x NB panel, column-major (rows j0.. stored from 0)
+// ---------------------------------------------------------------------------
+// Blocked Householder QR least squares across the whole batch (compact WY).
+// Same contract as qr_ls_kernel, split into launches so that the trailing
+// update -- all of the flops and all of the traffic -- runs on thousands of
+// CTAs instead of one CTA per problem:
+//   qr_init_kernel      W = E, ||M||_F, deficient = 0          (CTA / problem)
+//   per panel j0 (host loop over j0 = 0, NB, 2NB, ...):
+//     qr_panel_kernel   factor M[j0:, j0:j0+NB] in shared memory, write the
+//                       reflectors V (explicit unit heads, zeros above) and the
+//                       upper-triangular T of H_0..H_{nb-1} = I - V T V^T
+//     qr_trailing_kernel  C -= V T^T V^T C on every trailing column of M and
+//                       of W; one warp per CPW columns, (tiles x problems) grid
+//   qr_backsub_kernel   R X = (Q^T E)[0:n], blocked by 32 rows   (CTAs / problem)
+// Per panel the trailing block is read twice and written once: 24 B per
+// element, NB-fold less than the unblocked column-by-column kernel.
+// ---------------------------------------------------------------------------
+template <int NT>
+__global__ void __launch_bounds__(NT) qr_init_kernel(const double* __restrict__ Ms, const int64_t* __restrict__ moff,
+                                                     double* __restrict__ Ws, const int64_t* __restrict__ woff,
+                                                     const int* __restrict__ ni, const int* __restrict__ nj, int bs,
+                                                     double* __restrict__ tol_out, int* __restrict__ deficient) {
     __shared__ double red[NT / 32];
-    __shared__ double sT[NB * NB], stau[NB], sh_nrm, sh_beta;
     const int p = blockIdx.x;
     const int m = ni[p] * bs, n = nj[p] * bs, k = bs;
-    double* M = Ms + moff[p];
+    const double* M = Ms + moff[p];
     double* W = Ws + woff[p];
-    double* X = Xs + xoff[p];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double acc = 0.0;
-    for (int64_t t = tid; t < int64_t(m) * k; t += NT) {
+    for (int64_t t = threadIdx.x; t < int64_t(m) * k; t += NT) {
         const int c = int(t / m), r = int(t - int64_t(c) * m);
         W[t] = r == c ? 1.0 : 0.0;
     }
-    for (int64_t t = tid; t < int64_t(m) * n; t += NT) acc += M[t] * M[t];
+    double acc = 0.0;
+    for (int64_t t = threadIdx.x; t < int64_t(m) * n; t += NT) acc += M[t] * M[t];
     acc = block_sum<NT>(acc, red);
-    if (tid == 0) sh_nrm = sqrt(acc);
-    __syncthreads();
-    const double tol = 1e-12 * sh_nrm;
+    if (threadIdx.x == 0) {
+        tol_out[p] = 1e-12 * sqrt(acc);
+        deficient[p] = 0;
+    }
+}
+
+template <int NT, int NB>
+__global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, const int64_t* __restrict__ moff,
+                                                      const int* __restrict__ ni, const int* __restrict__ nj, int bs,
+                                                      int j0, const double* __restrict__ tolv, double* __restrict__ Vg,
+                                                      const int64_t* __restrict__ voff, double* __restrict__ Tg,
+                                                      int* __restrict__ deficient) {
+    extern __shared__ __align__(16) double Vp[];  // mr x NB panel, column-major (row j0 stored at 0)
+    __shared__ double red[NT / 32];
+    __shared__ double sT[NB * NB], stau[NB], sh_beta;
+    const int p = blockIdx.x;
+    const int m = ni[p] * bs, n = nj[p] * bs;
+    if (j0 >= n) return;
+    double* M = Ms + moff[p];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = min(NB, n - j0), mr = m - j0;
+    const double tol = tolv[p];
     int def = 0;
-    for (int j0 = 0; j0 < n; j0 += NB) {
-        const int nb = min(NB, n - j0), mr = m - j0;
-        // 1. panel -> shared memory
-        for (int t = tid; t < mr * nb; t += NT) {
-            const int c = t / mr, r = t - c * mr;
-            Vp[size_t(c) * mr + r] = M[size_t(j0 + c) * m + j0 + r];
+    for (int t = tid; t < mr * nb; t += NT) {
+        const int c = t / mr, r = t - c * mr;
+        Vp[size_t(c) * mr + r] = M[size_t(j0 + c) * m + j0 + r];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < nb; ++jj) {
+        double* cj = Vp + size_t(jj) * mr;
+        double s = 0.0;
+        for (int i = jj + 1 + tid; i < mr; i += NT) s += cj[i] * cj[i];
+        s = block_sum<NT>(s, red);
+        const double alpha = cj[jj];
+        double tau = 0.0, beta = alpha;
+        if (s != 0.0) {
+            const double nrm = sqrt(alpha * alpha + s);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+            const double scal = 1.0 / (alpha - beta);
+            for (int i = jj + 1 + tid; i < mr; i += NT) cj[i] *= scal;
         }
         __syncthreads();
-        // 2. unblocked factorisation of the panel in shared memory
-        for (int jj = 0; jj < nb; ++jj) {
-            double* cj = Vp + size_t(jj) * mr;
-            double s = 0.0;
-            for (int i = jj + 1 + tid; i < mr; i += NT) s += cj[i] * cj[i];
-            s = block_sum<NT>(s, red);
-            const double alpha = cj[jj];
-            double tau = 0.0, beta = alpha;
-            if (s != 0.0) {
-                const double nrm = sqrt(alpha * alpha + s);
-                beta = alpha >= 0.0 ? -nrm : nrm;
-                tau = (beta - alpha) / beta;
-                const double scal = 1.0 / (alpha - beta);
-                for (int i = jj + 1 + tid; i < mr; i += NT) cj[i] *= scal;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                cj[jj] = 1.0;  // implicit unit head of v, R_jj kept in sh_beta
-                stau[jj] = tau;
-                sh_beta = beta;
-            }
-            __syncthreads();
-            const double bj = sh_beta;
-            if (!(fabs(bj) > tol)) def = 1;
-            // apply to the remaining panel columns (one warp per column)
-            for (int c = jj + 1 + warp; c < nb; c += NT / 32) {
-                double* ct = Vp + size_t(c) * mr;
-                double w = 0.0;
-                for (int i = jj + lane; i < mr; i += 32) w += cj[i] * ct[i];
-                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-                w *= tau;
-                for (int i = jj + lane; i < mr; i += 32) ct[i] -= w * cj[i];
-            }
-            __syncthreads();
-            if (tid == 0) M[size_t(j0 + jj) * m + j0 + jj] = bj;  // R diagonal
-            // R above the diagonal of this panel column comes from the panel
-            for (int i = tid; i < jj; i += NT) M[size_t(j0 + jj) * m + j0 + i] = Vp[size_t(jj) * mr + i];
-            __syncthreads();
+        if (tid == 0) {
+            cj[jj] = 1.0;  // implicit unit head of v; R_jj goes straight to M
+            stau[jj] = tau;
+            sh_beta = beta;
         }
-        // 3. T of the compact WY form H_0 ... H_{nb-1} = I - V T V^T (T upper)
-        if (tid < nb) sT[tid * NB + tid] = stau[tid];
         __syncthreads();
-        for (int i = 1; i < nb; ++i) {
-            // z = V(:,0:i)^T v_i (one warp per entry)
-            for (int c = warp; c < i; c += NT / 32) {
-                double w = 0.0;
-                for (int r = i + lane; r < mr; r += 32) w += Vp[size_t(c) * mr + r] * Vp[size_t(i) * mr + r];
-                for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-                if (lane == 0) sT[c * NB + i] = w;  // stash z_c in column i
-            }
-            __syncthreads();
-            if (tid == 0) {  // T(0:i, i) = -tau_i T(0:i,0:i) z
-                double tmp[NB];
-                for (int a = 0; a < i; ++a) {
-                    double s = 0.0;
-                    for (int b2 = a; b2 < i; ++b2) s += sT[a * NB + b2] * sT[b2 * NB + i];
-                    tmp[a] = -stau[i] * s;
-                }
-                for (int a = 0; a < i; ++a) sT[a * NB + i] = tmp[a];
-            }
-            __syncthreads();
+        const double bj = sh_beta;
+        if (!(fabs(bj) > tol)) def = 1;
+        for (int c = jj + 1 + warp; c < nb; c += NT / 32) {
+            double* ct = Vp + size_t(c) * mr;
+            double w = 0.0;
+            for (int i = jj + lane; i < mr; i += 32) w += cj[i] * ct[i];
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            w *= tau;
+            for (int i = jj + lane; i < mr; i += 32) ct[i] -= w * cj[i];
         }
-        // 4. trailing update of M[:, j0+nb:] and W: C -= V T^T V^T C, a warp per column
-        const int ncols = (n - j0 - nb) + k;
-        for (int t = warp; t < ncols; t += NT / 32) {
-            double* ct = t < n - j0 - nb ? M + size_t(j0 + nb + t) * m + j0 : W + size_t(t - (n - j0 - nb)) * m + j0;
-            double y[NB];
-#pragma unroll
-            for (int a = 0; a < NB; ++a) y[a] = 0.0;
-            for (int r = lane; r < mr; r += 32) {
-                const double cv = ct[r];
-#pragma unroll
-                for (int a = 0; a < NB; ++a)
-                    if (a < nb && r >= a) y[a] += Vp[size_t(a) * mr + r] * cv;
-            }
-#pragma unroll
-            for (int a = 0; a < NB; ++a)
-                for (int o = 16; o > 0; o >>= 1) y[a] += __shfl_xor_sync(0xffffffffu, y[a], o);
-            double z[NB];  // z = T^T y
-#pragma unroll
-            for (int a = 0; a < NB; ++a) {
+        __syncthreads();
+        if (tid == 0) M[size_t(j0 + jj) * m + j0 + jj] = bj;
+        for (int i = tid; i < jj; i += NT) M[size_t(j0 + jj) * m + j0 + i] = Vp[size_t(jj) * mr + i];
+    }
+    __syncthreads();
+    // T of H_0 ... H_{nb-1} = I - V T V^T (upper triangular)
+    for (int t = tid; t < NB * NB; t += NT) sT[t] = 0.0;
+    __syncthreads();
+    if (tid < nb) sT[tid * NB + tid] = stau[tid];
+    __syncthreads();
+    for (int i = 1; i < nb; ++i) {
+        for (int c = warp; c < i; c += NT / 32) {  // z_c = v_c^T v_i over rows >= i
+            double w = 0.0;
+            for (int r = i + lane; r < mr; r += 32) w += Vp[size_t(c) * mr + r] * Vp[size_t(i) * mr + r];
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            if (lane == 0) sT[c * NB + i] = w;
+        }
+        __syncthreads();
+        if (tid == 0) {  // T(0:i, i) = -tau_i T(0:i,0:i) z
+            double tmp[NB];
+            for (int a = 0; a < i; ++a) {
                 double s = 0.0;
-                for (int b2 = 0; b2 <= a && b2 < nb; ++b2) s += sT[b2 * NB + a] * y[b2];
-                z[a] = a < nb ? s : 0.0;
+                for (int b2 = a; b2 < i; ++b2) s += sT[a * NB + b2] * sT[b2 * NB + i];
+                tmp[a] = -stau[i] * s;
             }
-            for (int r = lane; r < mr; r += 32) {
-                double d = 0.0;
-#pragma unroll
-                for (int a = 0; a < NB; ++a)
-                    if (a < nb && r >= a) d += Vp[size_t(a) * mr + r] * z[a];
-                ct[r] -= d;
-            }
+            for (int a = 0; a < i; ++a) sT[a * NB + i] = tmp[a];
         }
         __syncthreads();
     }
-    if (!def)
-        for (int c = warp; c < k; c += NT / 32) {
-            const double* wc = W + size_t(c) * m;
-            double* xc = X + size_t(c) * n;
-            for (int i = n - 1; i >= 0; --i) {
-                double s = 0.0;
-                for (int l = i + 1 + lane; l < n; l += 32) s += M[size_t(l) * m + i] * xc[l];
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0) xc[i] = (wc[i] - s) / M[size_t(i) * m + i];
-                __syncwarp();
+    // V with explicit zeros above the unit heads (padded to NB columns)
+    double* V = Vg + voff[p];
+    for (int t = tid; t < mr * NB; t += NT) {
+        const int c = t / mr, r = t - c * mr;
+        V[t] = (c < nb && r >= c) ? Vp[size_t(c) * mr + r] : 0.0;
+    }
+    for (int t = tid; t < NB * NB; t += NT) Tg[size_t(p) * NB * NB + t] = sT[t];
+    if (def && tid == 0) deficient[p] = 1;
+}
+
+template <int NB, int CPW>
+__global__ void __launch_bounds__(256) qr_trailing_kernel(double* __restrict__ Ms, const int64_t* __restrict__ moff,
+                                                          double* __restrict__ Ws, const int64_t* __restrict__ woff,
+                                                          const int* __restrict__ ni, const int* __restrict__ nj,
+                                                          int bs, int j0, const double* __restrict__ Vg,
+                                                          const int64_t* __restrict__ voff,
+                                                          const double* __restrict__ Tg) {
+    const int p = blockIdx.y;
+    const int m = ni[p] * bs, n = nj[p] * bs;
+    if (j0 >= n) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nb = min(NB, n - j0), mr = m - j0;
+    const int nm = n - j0 - nb, ncols = nm + bs;
+    const int c0 = (blockIdx.x * 8 + warp) * CPW;
+    if (c0 >= ncols) return;
+    double* cp[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+        const int t = min(c0 + c, ncols - 1);  // clamped duplicates are never written
+        cp[c] = t < nm ? Ms + moff[p] + size_t(j0 + nb + t) * m + j0 : Ws + woff[p] + size_t(t - nm) * m + j0;
+    }
+    const double* V = Vg + voff[p];
+    double y[CPW][NB];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int a = 0; a < NB; ++a) y[c][a] = 0.0;
+#pragma unroll 2
+    for (int r = lane; r < mr; r += 32) {
+        double v[NB], cv[CPW];
+#pragma unroll
+        for (int a = 0; a < NB; ++a) v[a] = __ldg(V + size_t(a) * mr + r);
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) cv[c] = cp[c][r];
+#pragma unroll
+        for (int c = 0; c < CPW; ++c)
+#pragma unroll
+            for (int a = 0; a < NB; ++a) y[c][a] = fma(v[a], cv[c], y[c][a]);
+    }
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int a = 0; a < NB; ++a)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) y[c][a] += __shfl_xor_sync(0xffffffffu, y[c][a], o);
+    const double* T = Tg + size_t(p) * NB * NB;
+    double z[CPW][NB];  // z = T^T y
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+        double ta[NB];
+#pragma unroll
+        for (int b2 = 0; b2 < NB; ++b2) ta[b2] = b2 <= a ? __ldg(T + b2 * NB + a) : 0.0;
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int b2 = 0; b2 < NB; ++b2) s = fma(ta[b2], y[c][b2], s);
+            z[c][a] = s;
+        }
+    }
+#pragma unroll 2
+    for (int r = lane; r < mr; r += 32) {
+        double v[NB];
+#pragma unroll
+        for (int a = 0; a < NB; ++a) v[a] = __ldg(V + size_t(a) * mr + r);
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) {
+            if (c0 + c >= ncols) continue;
+            double d = 0.0;
+#pragma unroll
+            for (int a = 0; a < NB; ++a) d = fma(v[a], z[c][a], d);
+            cp[c][r] -= d;
+        }
+    }
+}
+
+/// Trailing update with the CPW-column tile staged in shared memory by TMA
+/// bulk copies: every element of the trailing block crosses HBM once in each
+/// direction per panel (16 B), against 24 B and register-bound latency for
+/// qr_trailing_kernel.  Rows are split over all 8 warps; the reflectors V
+/// (mr x NB, shared by every tile of the problem) stream from L2.
+/// Columns start at arbitrary double offsets, so each copy starts at the
+/// 16-byte-aligned element below and covers an even element count; the
+/// buffers carry two doubles of tail padding for the over-read.
+template <int NB, int CPW>
+__global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict__ Ms,
+                                                              const int64_t* __restrict__ moff,
+                                                              double* __restrict__ Ws,
+                                                              const int64_t* __restrict__ woff,
+                                                              const int* __restrict__ ni, const int* __restrict__ nj,
+                                                              int bs, int j0, const double* __restrict__ Vg,
+                                                              const int64_t* __restrict__ voff,
+                                                              const double* __restrict__ Tg) {
+    extern __shared__ __align__(16) double sC[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ double sy[8][CPW * NB];
+    __shared__ double sz[CPW * NB];
+    const int p = blockIdx.y;
+    const int m = ni[p] * bs, n = nj[p] * bs;
+    if (j0 >= n) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = min(NB, n - j0), mr = m - j0;
+    const int nm = n - j0 - nb, ncols = nm + bs;
+    const int c0 = blockIdx.x * CPW;
+    if (c0 >= ncols) return;
+    const int nc = min(CPW, ncols - c0);
+    const int ld = ((mr + 1) & ~1) + 2;
+    double* colp[CPW];
+    int off[CPW];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+        const int t = min(c0 + c, ncols - 1);
+        const int64_t g = t < nm ? moff[p] + int64_t(j0 + nb + t) * m + j0 : woff[p] + int64_t(t - nm) * m + j0;
+        double* base = t < nm ? Ms : Ws;
+        colp[c] = base + g;
+        off[c] = int(g & 1);
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t total = 0;
+        for (int c = 0; c < nc; ++c) total += uint32_t(((off[c] + mr + 1) & ~1) * sizeof(double));
+        mbar_arrive_expect_tx(&bar, total);
+        for (int c = 0; c < nc; ++c)
+            bulk_g2s(sC + size_t(c) * ld, colp[c] - off[c], uint32_t(((off[c] + mr + 1) & ~1) * sizeof(double)),
+                     &bar);
+    }
+    const double* V = Vg + voff[p];
+    mbar_wait(&bar, 0);
+    double y[CPW][NB];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int a = 0; a < NB; ++a) y[c][a] = 0.0;
+    // RU rows per thread per step: all RU*NB reflector loads issue before use
+    constexpr int RU = CPW >= 8 ? 2 : 4;
+    for (int r0 = tid; r0 < mr; r0 += 256 * RU) {
+        double v[RU][NB];
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+#pragma unroll
+            for (int a = 0; a < NB; ++a) {
+                const int r = r0 + u * 256;
+                v[u][a] = r < mr ? __ldg(V + size_t(a) * mr + r) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int r = min(r0 + u * 256, mr - 1);
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                const double cv = c < nc ? sC[size_t(c) * ld + off[c] + r] : 0.0;
+#pragma unroll
+                for (int a = 0; a < NB; ++a) y[c][a] = fma(v[u][a], cv, y[c][a]);
             }
         }
-    if (tid == 0) deficient[p] = def;
+    }
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int a = 0; a < NB; ++a) {
+            double w = y[c][a];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            if (lane == 0) sy[warp][c * NB + a] = w;
+        }
+    __syncthreads();
+    if (tid < CPW * NB) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += sy[w][tid];
+        sy[0][tid] = s;
+    }
+    __syncthreads();
+    if (tid < CPW * NB) {  // z = T^T y
+        const int c = tid / NB, a = tid - c * NB;
+        const double* T = Tg + size_t(p) * NB * NB;
+        double s = 0.0;
+        for (int b2 = 0; b2 <= a; ++b2) s = fma(__ldg(T + b2 * NB + a), sy[0][c * NB + b2], s);
+        sz[tid] = s;
+    }
+    __syncthreads();
+    double z[CPW][NB];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c)
+#pragma unroll
+        for (int a = 0; a < NB; ++a) z[c][a] = sz[c * NB + a];
+    for (int r0 = tid; r0 < mr; r0 += 256 * RU) {
+        double v[RU][NB];
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+#pragma unroll
+            for (int a = 0; a < NB; ++a) {
+                const int r = r0 + u * 256;
+                v[u][a] = r < mr ? __ldg(V + size_t(a) * mr + r) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int r = r0 + u * 256;
+            if (r >= mr) break;
+#pragma unroll
+            for (int c = 0; c < CPW; ++c) {
+                if (c >= nc) continue;
+                double d = 0.0;
+#pragma unroll
+                for (int a = 0; a < NB; ++a) d = fma(v[u][a], z[c][a], d);
+                colp[c][r] = sC[size_t(c) * ld + off[c] + r] - d;
+            }
+        }
+    }
+}
+
+/// X = R^{-1} (Q^T E)[0:n] for CB right-hand sides per CTA, blocked by 32
+/// rows: solve the 32x32 diagonal block, then update every row above it.
+template <int CB>
+__global__ void __launch_bounds__(256) qr_backsub_kernel(const double* __restrict__ Ms,
+                                                         const int64_t* __restrict__ moff,
+                                                         const double* __restrict__ Ws,
+                                                         const int64_t* __restrict__ woff, double* __restrict__ Xs,
+                                                         const int64_t* __restrict__ xoff,
+                                                         const int* __restrict__ ni, const int* __restrict__ nj,
+                                                         int bs, const int* __restrict__ deficient) {
+    __shared__ double sR[32][33];
+    __shared__ double sx[32][CB];
+    const int p = blockIdx.y;
+    if (deficient[p]) return;
+    const int m = ni[p] * bs, n = nj[p] * bs;
+    const int cb0 = blockIdx.x * CB, nc = min(CB, bs - cb0);
+    if (nc <= 0) return;
+    const double* M = Ms + moff[p];
+    const double* W = Ws + woff[p];
+    double* X = Xs + xoff[p];
+    const int tid = threadIdx.x;
+    for (int t = tid; t < n * nc; t += 256) {
+        const int c = t / n, i = t - c * n;
+        X[size_t(cb0 + c) * n + i] = W[size_t(cb0 + c) * m + i];
+    }
+    __syncthreads();
+    for (int i1 = n; i1 > 0; i1 -= 32) {
+        const int i0 = max(0, i1 - 32), h = i1 - i0;
+        for (int t = tid; t < 32 * 32; t += 256) {
+            const int l = t >> 5, i = t & 31;  // R(i0+i, i0+l), column-major
+            sR[i][l] = (i < h && l < h) ? M[size_t(i0 + l) * m + i0 + i] : 0.0;
+        }
+        for (int t = tid; t < 32 * CB; t += 256) {
+            const int c = t / 32, i = t & 31;
+            sx[i][c] = (i < h && c < nc) ? X[size_t(cb0 + c) * n + i0 + i] : 0.0;
+        }
+        __syncthreads();
+        if (tid < nc) {
+            const int c = tid;
+            for (int i = h - 1; i >= 0; --i) {
+                double s = sx[i][c];
+                for (int l = i + 1; l < h; ++l) s -= sR[i][l] * sx[l][c];
+                sx[i][c] = s / sR[i][i];
+            }
+        }
+        __syncthreads();
+        for (int t = tid; t < h * nc; t += 256) {
+            const int c = t / h, i = t - c * h;
+            X[size_t(cb0 + c) * n + i0 + i] = sx[i][c];
+        }
+        for (int i = tid; i < i0; i += 256) {
+            double acc[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+            for (int l = 0; l < h; ++l) {
+                const double r = M[size_t(i0 + l) * m + i];
+#pragma unroll
+                for (int c = 0; c < CB; ++c) acc[c] = fma(r, sx[l][c], acc[c]);
+            }
+#pragma unroll
+            for (int c = 0; c < CB; ++c)
+                if (c < nc) X[size_t(cb0 + c) * n + i] -= acc[c];
+        }
+        __syncthreads();
+    }
 }
 
 /// Minimum-norm least squares by one-sided Jacobi SVD (dgelsd semantics,
@@ -525,6 +789,72 @@ struct SaiCache {
 SaiCache* sai_cache_new() { return new SaiCache(); }
 void sai_cache_free(SaiCache* c) { delete c; }
 
+/// Host driver of the blocked batch QR (see qr_init_kernel).
+template <int NB>
+void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_X,
+                      DevBuf& d_xoff, DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, const std::vector<int>& hni, int bs,
+                      int nb, int max_m, int max_n) {
+    constexpr int CPW = 4;
+    std::vector<int64_t> voff(nb + 1, 0);
+    for (int i = 0; i < nb; ++i) voff[i + 1] = voff[i] + int64_t(hni[i]) * bs * NB;
+    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, voff[nb])), d_voff(sizeof(int64_t) * (nb + 1)),
+        d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb);
+    h2d(ctx, d_voff.p, voff.data(), d_voff.bytes);
+    qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
+                                                    d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
+                                                    d_tol.as<double>(), d_def.as<int>());
+    after_launch("qr_init_kernel");
+    const size_t smem = sizeof(double) * size_t(max_m) * NB;
+    LDGMG_CUDA(cudaFuncSetAttribute(qr_panel_kernel<256, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // TMA-staged trailing tiles of tcpw columns (needs the 2-double tail pad
+    // on M and W that build_sai_gpu allocates).  Wider tiles re-read the
+    // reflectors from L2 fewer times; the widest tile that fits is used.
+    static int tma_env = -2, tcpw_env = -2;
+    if (tma_env == -2) {
+        const char* e = getenv("LDGMG_QR_TMA");
+        tma_env = e ? atoi(e) : 1;
+        e = getenv("LDGMG_QR_TCPW");
+        tcpw_env = e ? atoi(e) : 0;
+    }
+    const size_t col_bytes = sizeof(double) * size_t(((max_m + 1) & ~1) + 2);
+    int tcpw = 0;
+    for (int c : {8, 4, 2})
+        if (!tcpw && col_bytes * c <= 200 * 1024 && (tcpw_env == 0 || tcpw_env == c)) tcpw = c;
+    const bool tma = tma_env != 0 && tcpw > 0;
+    const size_t tsmem = col_bytes * tcpw;
+    auto tma_kernel = tcpw == 8 ? qr_trailing_tma_kernel<NB, 8>
+                                : tcpw == 4 ? qr_trailing_tma_kernel<NB, 4> : qr_trailing_tma_kernel<NB, 2>;
+    if (tma)
+        LDGMG_CUDA(cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem)));
+    for (int j0 = 0; j0 < max_n; j0 += NB) {
+        qr_panel_kernel<256, NB><<<nb, 256, smem, ctx.stream>>>(
+            d_M.as<double>(), d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(),
+            d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), d_def.as<int>());
+        after_launch("qr_panel_kernel");
+        const int ncols = std::max(0, max_n - j0 - NB) + bs;
+        if (tma) {
+            const dim3 g(div_up(ncols, tcpw), nb);
+            tma_kernel<<<g, 256, tsmem, ctx.stream>>>(
+                d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_ni.as<int>(),
+                d_nj.as<int>(), bs, j0, d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>());
+        } else {
+            const dim3 g(div_up(ncols, 8 * CPW), nb);
+            qr_trailing_kernel<NB, CPW><<<g, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
+                                                                   d_W.as<double>(), d_woff.as<int64_t>(),
+                                                                   d_ni.as<int>(), d_nj.as<int>(), bs, j0,
+                                                                   d_V.as<double>(), d_voff.as<int64_t>(),
+                                                                   d_T.as<double>());
+        }
+        after_launch("qr_trailing_kernel");
+    }
+    constexpr int CB = 16;
+    qr_backsub_kernel<CB><<<dim3(div_up(bs, CB), nb), 256, 0, ctx.stream>>>(
+        d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
+        d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
+    after_launch("qr_backsub_kernel");
+    (void)d_X;
+}
+
 SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level, double zeta,
                         bool use_cache, SaiCache* shared) {
     const int N = A.brows, bs = A.rbs;
@@ -537,6 +867,16 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     const int64_t nnzb = A.nnzb;
     SaiCache own;
     SaiCache* cache = use_cache ? (shared ? shared : &own) : nullptr;
+    static const bool timing = getenv("LDGMG_SAI_TIMING") && atoi(getenv("LDGMG_SAI_TIMING"));
+    auto t_last = std::chrono::steady_clock::now();
+    auto stamp = [&](const char* what) {
+        if (!timing) return;
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sai N=%d bs=%d] %-22s %9.3f s\n", N, bs, what,
+                std::chrono::duration<double>(now - t_last).count());
+        t_last = now;
+    };
 
     // ---- 1. balance vector
     std::vector<int> dk(N, -1), rowof(std::max<int64_t>(1, nnzb));
@@ -577,6 +917,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     std::vector<uint64_t> hash(2 * std::max<int64_t>(1, nnzb));
     d2h(ctx, hash.data(), d_hash.p, sizeof(uint64_t) * 2 * nnzb);
 
+    stamp("balance+scale+hash");
     // ---- 4. memcmp ranks of the distinct block contents
     std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, int>>> by_h1;
     std::vector<int> distinct_of(std::max<int64_t>(1, nnzb)), reps;
@@ -624,6 +965,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     };
     auto rank_blk = [&](int k) { return k < 0 ? -1 : rank_of_distinct[distinct_of[k]]; };
 
+    stamp("distinct-block ranks");
     // ---- 5. patterns (pattern_power, blockla.hpp:197-226) and per-column plans
     std::vector<std::vector<int>> pat(N);
     parallel_for(N, [&](int lo, int hi) {
@@ -716,6 +1058,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         }
     });
 
+    stamp("patterns+plans");
     // cache semantics in column order (smoothers.hpp:327-355)
     SaiResult res;
     res.stats = ldgmg_sai_stats{};
@@ -769,6 +1112,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         }
     }
 
+    stamp("cache lookup");
     // ---- 6. solve the unique local problems on the GPU (batched)
     const int np = int(probs.size());
     std::vector<int64_t> xoff(np + 1, 0);
@@ -776,34 +1120,54 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     DevBuf d_X(sizeof(double) * std::max<int64_t>(1, xoff[np]));
     std::vector<int> deficient(np, 0);
     {
-        int p0 = 0;
-        const size_t budget = size_t(2) << 30;
-        while (p0 < np) {
+        // batches of similar shape (problems are independent, so the order
+        // only affects how well the smem-sized kernels fit); the workspace is
+        // allocated once for the largest batch
+        std::vector<int> bord(np);
+        for (int i = 0; i < np; ++i) bord[i] = i;
+        std::stable_sort(bord.begin(), bord.end(), [&](int a, int b) {
+            return probs[a].ni != probs[b].ni ? probs[a].ni < probs[b].ni : probs[a].nj < probs[b].nj;
+        });
+        const size_t budget = size_t(4) << 30;
+        std::vector<std::pair<int, int>> batches;
+        size_t max_mn = 0, max_mk = 0;
+        for (int p0 = 0; p0 < np;) {
             int p1 = p0;
-            size_t need = 0;
-            std::vector<int64_t> moff(1, 0), woff(1, 0), boff(1, 0);
-            std::vector<int> hni, hnj, hblk;
+            size_t need = 0, mn = 0, mk = 0;
             while (p1 < np) {
-                const int64_t m = int64_t(probs[p1].ni) * bs, n = int64_t(probs[p1].nj) * bs;
+                const int64_t m = int64_t(probs[bord[p1]].ni) * bs, n = int64_t(probs[bord[p1]].nj) * bs;
                 const size_t add = sizeof(double) * size_t(m * n + m * bs);
                 if (p1 > p0 && (need + add > budget || p1 - p0 >= 4 * ctx.num_sms)) break;
                 need += add;
-                hni.push_back(probs[p1].ni);
-                hnj.push_back(probs[p1].nj);
-                const ColumnPlan& P = plan[probs[p1].column];
+                mn += size_t(m * n);
+                mk += size_t(m * bs);
+                ++p1;
+            }
+            batches.push_back({p0, p1});
+            max_mn = std::max(max_mn, mn);
+            max_mk = std::max(max_mk, mk);
+            p0 = p1;
+        }
+        DevBuf d_M(sizeof(double) * (max_mn + 2)), d_W(sizeof(double) * (max_mk + 2));
+        for (auto [p0, p1] : batches) {
+            std::vector<int64_t> moff(1, 0), woff(1, 0), boff(1, 0), xo;
+            std::vector<int> hni, hnj, hblk;
+            for (int q = p0; q < p1; ++q) {
+                const int pid = bord[q];
+                const int64_t m = int64_t(probs[pid].ni) * bs, n = int64_t(probs[pid].nj) * bs;
+                hni.push_back(probs[pid].ni);
+                hnj.push_back(probs[pid].nj);
+                const ColumnPlan& P = plan[probs[pid].column];
                 hblk.insert(hblk.end(), P.blk.begin(), P.blk.end());
                 moff.push_back(moff.back() + m * n);
                 woff.push_back(woff.back() + m * bs);
                 boff.push_back(boff.back() + int64_t(P.blk.size()));
-                ++p1;
+                xo.push_back(xoff[pid]);
             }
             const int nb = p1 - p0;
-            DevBuf d_M(sizeof(double) * std::max<int64_t>(1, moff.back())),
-                d_W(sizeof(double) * std::max<int64_t>(1, woff.back())), d_moff(sizeof(int64_t) * moff.size()),
-                d_woff(sizeof(int64_t) * woff.size()), d_boff(sizeof(int64_t) * boff.size()),
-                d_blk(sizeof(int) * std::max<size_t>(1, hblk.size())), d_ni(sizeof(int) * nb), d_nj(sizeof(int) * nb),
-                d_xoff(sizeof(int64_t) * nb), d_def(sizeof(int) * nb);
-            std::vector<int64_t> xo(xoff.begin() + p0, xoff.begin() + p1);
+            DevBuf d_moff(sizeof(int64_t) * moff.size()), d_woff(sizeof(int64_t) * woff.size()),
+                d_boff(sizeof(int64_t) * boff.size()), d_blk(sizeof(int) * std::max<size_t>(1, hblk.size())),
+                d_ni(sizeof(int) * nb), d_nj(sizeof(int) * nb), d_xoff(sizeof(int64_t) * nb), d_def(sizeof(int) * nb);
             h2d(ctx, d_moff.p, moff.data(), d_moff.bytes);
             h2d(ctx, d_woff.p, woff.data(), d_woff.bytes);
             h2d(ctx, d_boff.p, boff.data(), d_boff.bytes);
@@ -816,35 +1180,32 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                                                          d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                          d_moff.as<int64_t>(), d_M.as<double>());
             after_launch("assemble_m_kernel");
-            int max_m = 0;
-            for (int v : hni) max_m = std::max(max_m, v * bs);
-            const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
+            stamp("assemble M");
+            int max_m = 0, max_n = 0;
+            for (int i = 0; i < nb; ++i) {
+                max_m = std::max(max_m, hni[i] * bs);
+                max_n = std::max(max_n, hnj[i] * bs);
+            }
             static int qr_env = -2;
             if (qr_env == -2) {
                 const char* e = getenv("LDGMG_QR_UNBLOCKED");
                 qr_env = e ? atoi(e) : 0;
             }
-            if (!qr_env && smem8 <= 200 * 1024) {
-                LDGMG_CUDA(cudaFuncSetAttribute(qr_blocked_kernel<256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(smem8)));
-                qr_blocked_kernel<256, 8><<<nb, 256, smem8, ctx.stream>>>(
-                    d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
-                    d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
-                after_launch("qr_blocked_kernel");
-            } else if (!qr_env && smem4 <= 200 * 1024) {
-                LDGMG_CUDA(cudaFuncSetAttribute(qr_blocked_kernel<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(smem4)));
-                qr_blocked_kernel<256, 4><<<nb, 256, smem4, ctx.stream>>>(
-                    d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
-                    d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
-                after_launch("qr_blocked_kernel");
-            } else {
+            const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
+            if (!qr_env && smem8 <= 200 * 1024)
+                qr_blocked_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
+                                    max_n);
+            else if (!qr_env && smem4 <= 200 * 1024)
+                qr_blocked_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
+                                    max_n);
+            else {
                 qr_ls_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
                                                               d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
                                                               d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
                                                               d_def.as<int>());
                 after_launch("qr_ls_kernel");
             }
+            stamp("QR least squares");
             std::vector<int> def(nb);
             d2h(ctx, def.data(), d_def.p, sizeof(int) * nb);
             // rank-deficient problems: minimum-norm refit from a fresh copy of M
@@ -879,9 +1240,10 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                     d_x2.as<int64_t>(), d_ni2.as<int>(), d_nj2.as<int>(), bs, 1e-12);
                 after_launch("svd_minnorm_kernel");
                 LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+                if (timing) fprintf(stderr, "[sai] %d rank-deficient problems of %d\n", nd, nb);
+                stamp("SVD min-norm refit");
             }
-            for (int i = 0; i < nb; ++i) deficient[p0 + i] = def[i];
-            p0 = p1;
+            for (int i = 0; i < nb; ++i) deficient[bord[p0 + i]] = def[i];
         }
     }
 
@@ -980,6 +1342,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         }
         LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
     }
+    stamp("scatter");
     res.stats.n_shapes = int(ls_dims.size());
     int i = 0;
     for (const auto& [shape, count] : ls_dims) {
