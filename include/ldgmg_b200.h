@@ -142,6 +142,18 @@ int ldgmg_bsr_download(ldgmg_ctx* ctx, const ldgmg_bsr* A, int* ptr, int* col, d
 int64_t ldgmg_bsr_device_bytes(const ldgmg_bsr* A);
 int ldgmg_bsr_destroy(ldgmg_bsr* A);
 
+/* Block-coordinate text format (replaces dump_block_coo, blockla.hpp:253-268;
+ * the load side is the BlockBuilder round trip of tests/test_blockla.cpp:207-230:
+ * duplicates summed in file order, ascending columns).  Device variants
+ * download / upload; the _host variants touch no GPU.  coo_read_host is
+ * two-phase: with ptr == NULL it only reports the shape and nnzb. */
+int ldgmg_bsr_dump_coo(ldgmg_ctx* ctx, const ldgmg_bsr* A, const char* path);
+int ldgmg_bsr_load_coo(ldgmg_ctx* ctx, const char* path, ldgmg_bsr** out);
+int ldgmg_coo_write_host(const char* path, int brows, int bcols, int row_bs, int col_bs, const int* ptr,
+                         const int* col, const double* val);
+int ldgmg_coo_read_host(const char* path, int* brows, int* bcols, int* row_bs, int* col_bs, int64_t* nnzb,
+                        int* ptr, int* col, double* val);
+
 /* Upload a rank-local slice whose column indices are renumbered (owned
  * columns first, then ghost slots): block order inside each row must stay
  * the global ascending order, so columns need not ascend locally.

@@ -66,6 +66,7 @@ def lib():
             "ref_random_rhs": ([I, I, C.c_ulonglong, P], I),
             "ref_eta": ([P, I, C.c_ulonglong, D, I, P, IP, IP, IP, C.POINTER(D), C.POINTER(D)], I),
             "ref_bsr_spmv": ([I, I, I, I, P, P, P, P, P, I, C.POINTER(C.c_ulonglong)], I),
+            "ref_dump_block_coo": ([I, I, I, I, P, P, P, C.c_char_p], I),
             "ref_pattern_power_nnz": ([I, P, P, I, LLP], I),
             "ref_pattern_power": ([I, P, P, I, P, P], I),
             "ref_dense_lstsq": ([I, I, I, P, P, P, IP], I),
@@ -254,6 +255,14 @@ def random_rhs(nblocks, bs, seed=0):
     out = np.empty(nblocks * bs)
     _chk(lib().ref_random_rhs(nblocks, bs, seed, _p(out)))
     return out
+
+
+def dump_block_coo(brows, bcols, rbs, cbs, ptr, col, val, path):
+    """The reference's dump_block_coo (blockla.hpp:253-268) written to `path`."""
+    ptr = np.ascontiguousarray(ptr, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    _chk(lib().ref_dump_block_coo(brows, bcols, rbs, cbs, _p(ptr), _p(col), _p(val), str(path).encode()))
 
 
 def bsr_spmv(brows, bcols, rbs, cbs, ptr, col, val, x, transpose=False):

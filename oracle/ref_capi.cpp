@@ -23,6 +23,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <string>
 #include <thread>
@@ -525,6 +526,17 @@ int ref_bsr_spmv(int brows, int bcols, int rbs, int cbs, const int* ptr, const i
             spmv(A, xv, yv);
         if (mults) *mults = block_mult_counter();
         std::memcpy(y, yv.data.data(), sizeof(double) * yv.data.size());
+    });
+}
+
+/// dump_block_coo (blockla.hpp:253-268) of a raw matrix to `path`.
+int ref_dump_block_coo(int brows, int bcols, int rbs, int cbs, const int* ptr, const int* col,
+                       const double* val, const char* path) {
+    return guard([&] {
+        const BlockCsr A = csr_in(brows, bcols, rbs, cbs, ptr, col, val);
+        std::ofstream os(path);
+        if (!os) throw std::runtime_error("ref_dump_block_coo: cannot open output");
+        dump_block_coo(A, os);
     });
 }
 

@@ -130,6 +130,10 @@ _SIGS = {
     "ldgmg_bsr_shape": ([_P, _IP, _IP, _IP, _IP, C.POINTER(_I64)], _I),
     "ldgmg_bsr_download": ([_P, _P, _P, _P, _P], _I),
     "ldgmg_bsr_device_bytes": ([_P], _I64),
+    "ldgmg_bsr_dump_coo": ([_P, _P, C.c_char_p], _I),
+    "ldgmg_bsr_load_coo": ([_P, C.c_char_p, _P], _I),
+    "ldgmg_coo_write_host": ([C.c_char_p, _I, _I, _I, _I, _P, _P, _P], _I),
+    "ldgmg_coo_read_host": ([C.c_char_p, _P, _P, _P, _P, _P, _P, _P, _P], _I),
     "ldgmg_bsr_destroy": ([_P], _I),
     "ldgmg_bsr_upload_ex": ([_P, _I, _I, _I, _I, _P, _P, _P, _I, C.POINTER(_P)], _I),
     "ldgmg_spmv_add": ([_P, _P, _P, _P], _I),

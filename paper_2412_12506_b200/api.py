@@ -114,10 +114,50 @@ class DeviceBsr:
     def device_bytes(self) -> int:
         return int(lib.ldgmg_bsr_device_bytes(self.h))
 
+    def dump_coo(self, path) -> None:
+        """Block-coordinate text dump (the reference's dump_block_coo, blockla.hpp:253-268)."""
+        check(lib.ldgmg_bsr_dump_coo(self.ctx.h, self.h, str(path).encode()))
+
+    @classmethod
+    def load_coo(cls, ctx: Context, path) -> "DeviceBsr":
+        """Upload a block-coordinate dump (duplicates summed, columns ascending)."""
+        obj = cls.__new__(cls)
+        obj.ctx = ctx
+        h = C.c_void_p()
+        check(lib.ldgmg_bsr_load_coo(ctx.h, str(path).encode(), C.byref(h)))
+        obj.h = h
+        br, bc, rb, cb, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+        check(lib.ldgmg_bsr_shape(h, C.byref(br), C.byref(bc), C.byref(rb), C.byref(cb), C.byref(nz)))
+        obj.brows, obj.bcols, obj.row_bs, obj.col_bs, obj.nnzb = br.value, bc.value, rb.value, cb.value, nz.value
+        return obj
+
     def __del__(self):
         if getattr(self, "h", None):
             lib.ldgmg_bsr_destroy(self.h)
             self.h = None
+
+
+def coo_write(path, brows, bcols, row_bs, col_bs, ptr, col, val) -> None:
+    """Host-only block-coordinate writer (same text as dump_block_coo)."""
+    ptr = _np(ptr, np.int32)
+    col = _np(col, np.int32)
+    val = _np(val, np.float64)
+    check(lib.ldgmg_coo_write_host(str(path).encode(), int(brows), int(bcols), int(row_bs), int(col_bs),
+                                   ptr.ctypes.data, col.ctypes.data, val.ctypes.data))
+
+
+def coo_read(path):
+    """Host-only block-coordinate reader -> (brows, bcols, row_bs, col_bs, ptr, col, val)."""
+    br, bc, rb, cb, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+    p = str(path).encode()
+    check(lib.ldgmg_coo_read_host(p, C.byref(br), C.byref(bc), C.byref(rb), C.byref(cb), C.byref(nz),
+                                  None, None, None))
+    ptr = np.empty(br.value + 1, np.int32)
+    col = np.empty(max(nz.value, 1), np.int32)
+    val = np.empty(max(nz.value * rb.value * cb.value, 1), np.float64)
+    check(lib.ldgmg_coo_read_host(p, None, None, None, None, None, ptr.ctypes.data, col.ctypes.data,
+                                  val.ctypes.data))
+    return (br.value, bc.value, rb.value, cb.value, ptr, col[: nz.value], val[: nz.value * rb.value * cb.value])
 
 
 def spmv(ctx: Context, A: DeviceBsr, x, y) -> None:

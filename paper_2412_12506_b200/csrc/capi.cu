@@ -9,6 +9,7 @@
 #include <unordered_map>
 
 #include "core.hpp"
+#include "formats.hpp"
 #include "mg.hpp"
 #include "krylov.hpp"
 #include "setup.hpp"
@@ -206,6 +207,56 @@ int64_t ldgmg_bsr_device_bytes(const ldgmg_bsr* A) { return A ? A->device_bytes(
 
 int ldgmg_bsr_destroy(ldgmg_bsr* A) {
     return guarded([&] { delete A; });
+}
+
+int ldgmg_bsr_dump_coo(ldgmg_ctx* ctx, const ldgmg_bsr* A, const char* path) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_dump_coo");
+        need(A, "ldgmg_bsr_dump_coo");
+        need(path, "ldgmg_bsr_dump_coo(path)");
+        bind(*ctx);
+        std::vector<int> ptr(A->brows + 1), col(std::max<int64_t>(1, A->nnzb));
+        std::vector<double> val(std::max<int64_t>(1, A->nnzb * A->rbs * A->cbs));
+        bsr_download(*ctx, *A, ptr.data(), col.data(), val.data());
+        coo_write(path, A->brows, A->bcols, A->rbs, A->cbs, ptr.data(), col.data(), val.data());
+    });
+}
+
+int ldgmg_bsr_load_coo(ldgmg_ctx* ctx, const char* path, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_load_coo");
+        need(path, "ldgmg_bsr_load_coo(path)");
+        need(out, "ldgmg_bsr_load_coo(out)");
+        bind(*ctx);
+        const CooMatrix M = coo_read(path);
+        *out = static_cast<ldgmg_bsr*>(
+            own_bsr(bsr_upload(*ctx, M.brows, M.bcols, M.rbs, M.cbs, M.ptr.data(), M.col.data(), M.val.data())));
+    });
+}
+
+int ldgmg_coo_write_host(const char* path, int brows, int bcols, int row_bs, int col_bs, const int* ptr,
+                         const int* col, const double* val) {
+    return guarded([&] {
+        need(ptr, "ldgmg_coo_write_host(ptr)");
+        coo_write(path, brows, bcols, row_bs, col_bs, ptr, col, val);
+    });
+}
+
+int ldgmg_coo_read_host(const char* path, int* brows, int* bcols, int* row_bs, int* col_bs, int64_t* nnzb,
+                        int* ptr, int* col, double* val) {
+    return guarded([&] {
+        const CooMatrix M = coo_read(path);
+        if (brows) *brows = M.brows;
+        if (bcols) *bcols = M.bcols;
+        if (row_bs) *row_bs = M.rbs;
+        if (col_bs) *col_bs = M.cbs;
+        if (nnzb) *nnzb = int64_t(M.col.size());
+        if (ptr) {
+            std::memcpy(ptr, M.ptr.data(), sizeof(int) * M.ptr.size());
+            if (col) std::memcpy(col, M.col.data(), sizeof(int) * M.col.size());
+            if (val) std::memcpy(val, M.val.data(), sizeof(double) * M.val.size());
+        }
+    });
 }
 
 int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y) {

@@ -90,12 +90,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("names", nargs="*", default=["C1", "C1-512", "C2", "C3-GS", "C3-SAI", "C4", "C5"])
     ap.add_argument("--c5n", type=int, default=16)
+    ap.add_argument("--csv", default=None, help="also write reference-format CSV rows (+perf columns)")
     ap.add_argument("--cycles", type=int, default=20)
     a = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = g.Context(0, stream=stream)
     cfgs = configs(a.c5n)
+    rows = []
     for name in a.names:
         spec, cfg, rk = cfgs[name]
         t0 = time.time()
@@ -139,7 +141,23 @@ def main():
             rec["gmres"] = {"iterations": rep["iterations"], "converged": rep["converged"],
                             "eta": rep["eta"], "seconds": round(time.perf_counter() - t0, 4)}
         print(json.dumps(rec), flush=True)
+        if a.csv:
+            from paper_2412_12506_b200 import report as R
+            sm = cfg.smoother
+            fam = {g.JACOBI: "J", g.COLOURED_GS: "GS", g.SAI: f"SAI{sm.level}"}[sm.kind]
+            sweeps = "" if sm.kind == g.JACOBI else "-" + "".join("f" if s_ == g.SWEEP_FORWARD else "r"
+                                                                 for s_ in (cfg.pre, cfg.post))
+            et = mg.estimate_eta(g._lib.KRYLOV_GMRES, seed=0)
+            rows.append(R.CellRow(name, spec.dim, spec.degree, spec.n, f"GMRES-{fam}{sweeps}", rho=et["rho"],
+                                  eta=et["eta"], iterations=et["iterations"],
+                                  classification=R.CLASSIFICATIONS.index(et["classification"]),
+                                  perf={"setup_s": t_asm + t_mg, "vcycle_ms": tc * 1e3,
+                                        "dof_updates_per_s": dof / tc, "alg_gbps": byts / tc / 1e9}))
         del mg, P
+    if a.csv:
+        from paper_2412_12506_b200 import report as R
+        with open(a.csv, "w") as f:
+            R.write_csv(f, rows)
 
 
 if __name__ == "__main__":
