@@ -187,6 +187,29 @@ def gs_sweep(ptr, col, val, bs, b, x, V, lam, scal, colour, reverse=False):
     return x.reshape(-1)
 
 
+def pgs_sweep(ptr, col, val, bs, b, x, V, lam, scal, omega, partitions, reverse=False):
+    """Processor-block GS (smoothers.hpp:426-436): each partition of
+    partition_ranges(N, P) (:87-94) sweeps its elements in order (reverse:
+    descending), in-partition neighbours read live, the rest from the
+    snapshot.  Element-by-element (pure restatement; small cases only)."""
+    N = len(ptr) - 1
+    if partitions < 1 or partitions > N:
+        raise ValueError("partition_ranges: partition count must lie in [1, N]")
+    part = np.empty(N, np.int64)
+    for p in range(partitions):
+        part[p * N // partitions:(p + 1) * N // partitions] = p
+    snap = np.array(x, copy=True)
+    live = np.array(x, copy=True).reshape(-1, bs)
+    for p in range(partitions):
+        s0, s1 = p * N // partitions, (p + 1) * N // partitions
+        order = range(s1 - 1, s0 - 1, -1) if reverse else range(s0, s1)
+        for e in order:
+            # neighbour source per block: live x inside the partition, snapshot outside
+            src = np.where(np.repeat(part == part[e], bs), live.reshape(-1), snap)
+            live[e] = relax_rows([e], ptr, col, val, bs, b, src, live.reshape(-1), V, lam, scal, omega)[0]
+    return live.reshape(-1)
+
+
 def sai_sweep(A, B, bs, b, x, reverse=False):
     ax = spmv(A[0], A[1], A[2], bs, bs, x)
     r = np.asarray(b) - ax
@@ -261,6 +284,9 @@ class PortMultigrid:
             return jacobi_sweep(*L["A"], bs, b, x, *L["factors"], self.cfg.smoother.omega)
         if kind == 1:
             return gs_sweep(*L["A"], bs, b, x, *L["factors"], L["colour"], reverse=sweep == 1)
+        if kind == 2:
+            return pgs_sweep(*L["A"], bs, b, x, *L["factors"], self.cfg.smoother.omega,
+                             self.cfg.smoother.partitions, reverse=sweep == 1)
         if kind == 3:
             return sai_sweep(L["A"], L["B"], bs, b, x, reverse=sweep == 1)
         raise ValueError("unsupported smoother")

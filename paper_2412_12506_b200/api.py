@@ -198,6 +198,10 @@ class SmootherConfig:
         return SmootherConfig(kind=L.COLOURED_GS, omega=1.0)
 
     @staticmethod
+    def proc_block_gs(partitions: int, omega: float = 0.8) -> "SmootherConfig":
+        return SmootherConfig(kind=L.PROC_BLOCK_GS, omega=omega, partitions=partitions)
+
+    @staticmethod
     def sai(level: int, zeta: float = 0.1, cache: bool = True) -> "SmootherConfig":
         return SmootherConfig(kind=L.SAI, level=level, zeta=zeta, cache=cache)
 

@@ -77,13 +77,14 @@ __device__ __forceinline__ bool it_next(const RowPassArgs& a, ItemIt& it, int g,
 }
 
 template <int GT>
-__device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int st,
+__device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int row, int st,
                                            double* stages, double* xslots, uint64_t* bars) {
     const int t = threadIdx.x;
     double* xs = xslots + size_t(st) * a.xslot_doubles;
     if (t < a.cbs) {
         if (kind == 0) {
-            const double* src = a.x + size_t(__ldg(a.col + idx)) * a.cbs + t;
+            const int j = __ldg(a.col + idx);
+            const double* src = x_source(a, row, j) + size_t(j) * a.cbs + t;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(xs + t)),
                          "l"(src)
                          : "memory");
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     int kind, idx;
     for (int s = 0; s < NS; ++s) {
         if (!it_next(a, pit, g, ng, kind, idx)) break;
-        issue_item<GT>(a, kind, idx, s, stages, xslots, bars);
+        issue_item<GT>(a, kind, idx, pit.row, s, stages, xslots, bars);
     }
 
     uint32_t q = 0;  // items consumed
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                 ++q;
                 if (it_next(a, pit, g, ng, kind, idx)) {
                     if (t == 0) fence_proxy_async();
-                    issue_item<GT>(a, kind, idx, su, stages, xslots, bars);
+                    issue_item<GT>(a, kind, idx, pit.row, su, stages, xslots, bars);
                 }
             }
         }
@@ -498,6 +499,8 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         a.cbs = A.cbs;
         a.mode = p.mode;
         a.x = p.x;
+        a.part = p.part;
+        a.x_alt = p.x_alt;
         a.b = p.b;
         a.xe = p.xe;
         a.y = p.y;
@@ -533,6 +536,8 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
     a.cbs = A.cbs;
     a.mode = p.mode;
     a.x = p.x;
+    a.part = p.part;
+    a.x_alt = p.x_alt;
     a.b = p.b;
     a.xe = p.xe;
     a.y = p.y;

@@ -2,7 +2,10 @@
 // opaque handles over the host objects of core.hpp / mg.hpp.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -643,6 +646,26 @@ int ldgmg_transfer_destroy(ldgmg_transfer* T) {
 }
 
 // ------------------------------------------------------------ multigrid
+/// Wall-clock setup phases on stderr when LDGMG_SETUP_TIMING=1 (stream-synchronised).
+struct SetupTimer {
+    const char* what;
+    cudaStream_t s;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    SetupTimer(const char* w, cudaStream_t st) : what(w), s(st) {
+        const char* e = getenv("LDGMG_SETUP_TIMING");
+        on = e && atoi(e);
+        t = std::chrono::steady_clock::now();
+    }
+    void stamp(const char* phase) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[setup %s] %-22s %9.3f s\n", what, phase, std::chrono::duration<double>(now - t).count());
+        t = now;
+    }
+};
+
 static void mg_default_smoothers(ldgmg_ctx* ctx, Mg& m) {
     m.sm.assign(m.depth, nullptr);
     if (!m.sai_cache) m.sai_cache = sai_cache_new();
@@ -653,13 +676,16 @@ static void mg_default_smoothers(ldgmg_ctx* ctx, Mg& m) {
         s->system_kind = m.system_kind;
         s->n_velocity = m.n_velocity;
         s->init_common(*ctx);
+        SetupTimer tm("smoother", ctx->stream);
         if (s->cfg.kind == LDGMG_SAI) {
             SaiResult r = build_sai_gpu(*ctx, *m.A[l], m.system_kind, m.n_velocity, s->cfg.level,
                                         s->cfg.zeta, s->cfg.cache != 0, m.sai_cache);
             s->B = std::move(r.B);
             s->stats = r.stats;
+            tm.stamp(l == 0 ? "SAI build level 0" : "SAI build coarse");
         } else {
             compute_factors(*ctx, *m.A[l], s->F);
+            tm.stamp(l == 0 ? "diag factors level 0" : "diag factors coarse");
         }
         m.sm[l] = s.get();
         m.own_sm.push_back(std::move(s));
@@ -988,11 +1014,13 @@ int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P, const l
         m.kernel_constants = p.kernel_constants;
         m.kernel_pressure = p.kernel_pressure;
         m.n_velocity = p.kind == LDGMG_SYSTEM_STOKES ? p.dim * p.bs_scalar : 0;
+        SetupTimer tm("mg_create_from_problem", ctx->stream);
         for (int l = 0; l < m.depth; ++l) {
             const auto& A = p.levels[l].A;
             m.own_A.push_back(bsr_upload(*ctx, A.brows, A.brows, A.bs, A.bs, A.ptr.data(), A.col.data(), A.val.data()));
             m.A.push_back(m.own_A.back().get());
         }
+        tm.stamp("operator upload");
         for (int l = 0; l + 1 < m.depth; ++l) {
             const auto& L = p.levels[l];
             m.own_T.push_back(transfer_create(*ctx, L.A.brows, p.levels[l + 1].A.brows, L.parent_of.data(),
@@ -1000,10 +1028,14 @@ int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P, const l
                                               p.inject.data()));
             m.T.push_back(m.own_T.back().get());
         }
+        tm.stamp("transfers");
         m.init(*ctx);
+        tm.stamp("level scratch");
         m.set_bottom(*ctx, nullptr, nullptr);
+        tm.stamp("bottom pseudoinverse");
         m.sm.assign(m.depth, nullptr);
         mg_default_smoothers(ctx, m);
+        tm.stamp("smoothers");
         *out = h;
     });
     if (rc != LDGMG_OK) delete h;

@@ -155,6 +155,7 @@ void Mg::build_coarse_program(Ctx& ctx) {
     int maxlen = 1;
     for (int l = lc; l < depth; ++l) {
         if (A[l]->rbs > 32) return;  // split-row ops need bs <= 32
+        if (l + 1 < depth && sm[l]->cfg.kind == LDGMG_PROC_BLOCK_GS) return;  // not recorded
         maxlen = std::max(maxlen, A[l]->max_row);
         if (l + 1 < depth && T[l]->max_children > 64) return;
     }

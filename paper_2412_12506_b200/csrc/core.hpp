@@ -121,6 +121,8 @@ struct RowPass {
     const int* rows = nullptr;   // optional row list (colour phase); nullptr = all rows
     int nrows = 0;
     const DiagFactors* F = nullptr;  // RELAX
+    const int* part = nullptr;       // RELAX, processor-block GS: partition of each element
+    const double* x_alt = nullptr;   //   neighbours in other partitions read from here
     double omega = 1.0;
     double kernel_tol = 1e-12;
 };

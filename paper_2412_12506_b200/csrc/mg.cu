@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -75,9 +76,21 @@ void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, co
     (void)ctx;
 }
 
+void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F) {
+    static int host = -1;
+    if (host < 0) {
+        const char* e = getenv("LDGMG_HOST_FACTORS");
+        host = e && atoi(e) ? 1 : 0;
+    }
+    if (host)
+        compute_factors_host(ctx, A, F);
+    else
+        compute_factors_gpu(ctx, A, F);
+}
+
 /// factor_diagonal (smoothers.hpp:464-494): power-of-two equilibration
 /// s_i = 2^-(ex/2) of |D_ii| (frexp exponent), then eig(s D s).
-void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F) {
+void compute_factors_host(Ctx& ctx, const Bsr& A, DiagFactors& F) {
     const int N = A.brows, bs = A.rbs;
     std::vector<int> dk(N, -1);
     for (int e = 0; e < N; ++e) {
@@ -151,10 +164,49 @@ void Smoother::init_common(Ctx& ctx) {
         if (!rows.empty())
             h2d(ctx, colour_rows.p, rows.data(), sizeof(int) * rows.size());
     }
-    if (cfg.kind == LDGMG_PROC_BLOCK_GS)
-        fail(LDGMG_ERR_INVALID_ARGUMENT,
-             "Smoother: processor-block GS runs sequential in-partition sweeps and has no GPU "
-             "path (SURVEY.md 2 row 2); use coloured GS");
+    if (cfg.kind == LDGMG_PROC_BLOCK_GS) {
+        // partition_ranges (smoothers.hpp:87-94) and part_of (:383-386)
+        const int P = cfg.partitions;
+        if (P < 1 || P > N)
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "partition_ranges: partition count must lie in [1, N]");
+        std::vector<int> part_of(N);
+        for (int p = 0; p < P; ++p)
+            for (int e = int(int64_t(p) * N / P); e < int(int64_t(p + 1) * N / P); ++e) part_of[e] = p;
+        part.alloc(sizeof(int) * std::max(1, N));
+        h2d(ctx, part.p, part_of.data(), sizeof(int) * N);
+        // The reference sweeps every partition sequentially (forward:
+        // ascending, reverse: descending), reading in-partition neighbours
+        // live and the others from a snapshot (smoothers.hpp:426-436).  An
+        // element therefore depends only on its in-partition neighbours that
+        // precede it in the sweep; relaxing the wavefronts of that DAG one
+        // launch at a time reproduces the sequential result bit for bit.
+        for (int d = 0; d < 2; ++d) {
+            std::vector<int> lev(N, 0);
+            int nlev = N ? 1 : 0;
+            for (int i = 0; i < N; ++i) {
+                const int e = d == 0 ? i : N - 1 - i;
+                int l = 0;
+                for (int k = A->hptr[e]; k < A->hptr[e + 1]; ++k) {
+                    const int j = A->hcol[k];
+                    if (j == e || part_of[j] != part_of[e]) continue;
+                    if (d == 0 ? j < e : j > e) l = std::max(l, lev[j] + 1);
+                }
+                lev[e] = l;
+                nlev = std::max(nlev, l + 1);
+            }
+            std::vector<int> rows;
+            rows.reserve(N);
+            sched_ptr[d].assign(nlev + 1, 0);
+            std::vector<int> cnt(nlev, 0);
+            for (int e = 0; e < N; ++e) ++cnt[lev[e]];
+            for (int l = 0; l < nlev; ++l) sched_ptr[d][l + 1] = sched_ptr[d][l] + cnt[l];
+            rows.resize(N);
+            std::vector<int> fill(sched_ptr[d].begin(), sched_ptr[d].end() - 1);
+            for (int e = 0; e < N; ++e) rows[fill[lev[e]]++] = e;
+            sched_rows[d].alloc(sizeof(int) * std::max(1, N));
+            if (N) h2d(ctx, sched_rows[d].p, rows.data(), sizeof(int) * N);
+        }
+    }
     if (cfg.kind == LDGMG_SAI && cfg.level < 0)
         fail(LDGMG_ERR_INVALID_ARGUMENT, "pattern_power: negative power");
     snap.alloc(sizeof(double) * std::max<int64_t>(1, int64_t(N) * bs));
@@ -193,6 +245,28 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep) const {
                 p.nrows = colour_ptr[c + 1] - colour_ptr[c];
                 p.F = &F;
                 p.omega = 1.0;
+                launch_rowpass(ctx, p);
+            }
+            break;
+        }
+        case LDGMG_PROC_BLOCK_GS: {
+            LDGMG_CUDA(cudaMemcpyAsync(snap.p, x, sizeof(double) * size_t(N) * bs,
+                                       cudaMemcpyDeviceToDevice, ctx.stream));
+            const int d = sweep == LDGMG_SWEEP_FORWARD ? 0 : 1;
+            for (size_t l = 0; l + 1 < sched_ptr[d].size(); ++l) {
+                RowPass p;
+                p.A = A;
+                p.mode = MODE_RELAX;
+                p.x = x;
+                p.x_alt = snap.as<double>();
+                p.part = part.as<int>();
+                p.b = b;
+                p.xe = x;
+                p.y = x;
+                p.rows = sched_rows[d].as<int>() + sched_ptr[d][l];
+                p.nrows = sched_ptr[d][l + 1] - sched_ptr[d][l];
+                p.F = &F;
+                p.omega = cfg.omega;
                 launch_rowpass(ctx, p);
             }
             break;

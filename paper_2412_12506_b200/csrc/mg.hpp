@@ -11,7 +11,9 @@ namespace ldgmg_b200 {
 std::vector<int> colour_mesh_host(const Bsr& A);
 void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, const double* lambda,
                     const double* s);
-void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F);
+void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F);      // GPU (factors.cu) unless LDGMG_HOST_FACTORS=1
+void compute_factors_host(Ctx& ctx, const Bsr& A, DiagFactors& F);  // host eig, multithreaded
+void compute_factors_gpu(Ctx& ctx, const Bsr& A, DiagFactors& F);
 std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, const int* parent_of,
                                           const int* orthant_of, int dim, int bss, int ncomp,
                                           const double* K);
@@ -38,7 +40,11 @@ struct Smoother {
     DevBuf colour_rows;
     std::unique_ptr<Bsr> B;
     ldgmg_sai_stats stats{};
-    DevBuf snap;  // Jacobi snapshot / SAI residual scratch
+    DevBuf snap;  // Jacobi / processor-block GS snapshot, SAI residual scratch
+    // processor-block GS: partition of each element, wavefront schedules
+    // (rows grouped by level) for the forward [0] and reverse [1] sweeps
+    DevBuf part, sched_rows[2];
+    std::vector<int> sched_ptr[2];
 
     void init_common(Ctx& ctx);
     void apply(Ctx& ctx, const double* b, double* x, int sweep) const;

@@ -29,7 +29,15 @@ struct RowPassArgs {
     int ld, vstride;
     double omega, kernel_tol;
     int nstages, stage_doubles, xslot_doubles;
+    // processor-block GS (smoothers.hpp:426-436): neighbour j of row e is read
+    // from x when part[j] == part[e], else from x_alt (the sweep's snapshot)
+    const int* part;
+    const double* x_alt;
 };
+
+__device__ __forceinline__ const double* x_source(const RowPassArgs& a, int row, int j) {
+    return (a.part && __ldg(a.part + j) != __ldg(a.part + row)) ? a.x_alt : a.x;
+}
 
 __device__ __forceinline__ int row_at(const RowPassArgs& a, int slot) {
     return a.rows ? __ldg(a.rows + slot) : slot;
@@ -51,7 +59,7 @@ __device__ __forceinline__ void split_row_task(const RowPassArgs& a, int row, in
         if (relax && j == row) continue;
         if (lane < a.rbs) {
             const double* Bc = a.val + size_t(k) * a.blk_stride + lane;
-            const double* xj = a.x + size_t(j) * a.cbs;
+            const double* xj = x_source(a, row, j) + size_t(j) * a.cbs;
             double s = 0.0;
 #pragma unroll 9
             for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, __ldg(Bc + size_t(c) * a.rbs), xj[c]);

@@ -72,7 +72,7 @@ def parse_combo(text: str, zeta: float = 0.131) -> SolverSpec:
         P = 4 if len(fam) == 3 else digits(fam[3:])
         if P < 1:
             fail("partition count must be positive")
-        out.smoother = SmootherConfig(kind=L.PROC_BLOCK_GS, omega=0.8, partitions=P)
+        out.smoother = SmootherConfig.proc_block_gs(P)
         fam_name = f"PGS{P}"
     elif fam.startswith("SAI"):
         if len(fam) == 3:

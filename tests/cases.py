@@ -18,11 +18,13 @@ def stokes(n, dim, bc=P, gamma=0.0, degree=1, beta_p=1.0, delta=0.0, beta=-1.0, 
 
 
 def cfg(kind="jacobi", omega=0.8, nu=3, level=1, zeta=0.1, pre=g.SWEEP_FORWARD, post=g.SWEEP_REVERSE,
-        min_depth=2, bottom_max=64):
+        min_depth=2, bottom_max=64, partitions=4):
     if kind == "jacobi":
         sm = g.SmootherConfig.jacobi(omega)
     elif kind == "gs":
         sm = g.SmootherConfig.coloured_gs()
+    elif kind == "pgs":
+        sm = g.SmootherConfig.proc_block_gs(partitions, omega)
     else:
         sm = g.SmootherConfig.sai(level, zeta)
     return g.MultigridConfig(smoother=sm, pre=pre, post=post, nu1=nu, nu2=nu, min_depth=min_depth,

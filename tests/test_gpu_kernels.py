@@ -157,6 +157,33 @@ def test_coloured_gs_bitwise_and_colouring(ctx, ref, name):
             assert bits_equal(host(xd), x)
 
 
+@pytest.mark.parametrize("name", sorted(SYSTEMS))
+@pytest.mark.parametrize("P", [1, 3, 4])
+def test_proc_block_gs_bitwise(ctx, ref, name, P):
+    """Processor-block GS (smoothers.hpp:426-436) run as wavefronts of the
+    in-partition dependency DAG: bit-identical to the sequential sweeps."""
+    R, cfg = level_system(ref, SYSTEMS[name], "pgs", partitions=P, omega=0.7)
+    n, bs, _ = R.shape(0)
+    A = g.DeviceBsr(ctx, n, n, bs, bs, *R.matrix(0))
+    S = g.Smoother(ctx, A, cfg.smoother, factors=R.diag_factors(0))
+    b = rand(n * bs, 31)
+    for sweep in (g.SWEEP_FORWARD, g.SWEEP_REVERSE):
+        x = rand(n * bs, 32)
+        xd = dev(x)
+        for _ in range(2):
+            S.apply(dev(b), xd, sweep)
+            x = R.smoother_apply(0, b, x, sweep)
+            assert bits_equal(host(xd), x)
+
+
+def test_proc_block_gs_rejects_too_many_partitions(ctx, ref):
+    R, _ = level_system(ref, SYSTEMS["scalar2d-dirichlet-p1-mu1.3"])
+    n, bs, _ = R.shape(0)
+    A = g.DeviceBsr(ctx, n, n, bs, bs, *R.matrix(0))
+    with pytest.raises(g.InvalidArgument, match="partition count must lie in"):
+        g.Smoother(ctx, A, g.SmootherConfig.proc_block_gs(n + 1), factors=R.diag_factors(0))
+
+
 def test_gs_ignores_damping(ctx, ref):
     R, _ = level_system(ref, SYSTEMS["scalar2d-dirichlet-p1-mu1.3"], "gs")
     n, bs, _ = R.shape(0)

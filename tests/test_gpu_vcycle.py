@@ -60,6 +60,8 @@ DROPIN = {
     "gs-scalar2d-dirichlet-p2": (K.scalar(16, 2, K.D, degree=2), K.cfg("gs")),
     "sai1-scalar2d-dirichlet-p2": (K.scalar(8, 2, K.D, degree=2), K.cfg("sai", level=1)),
     "sai1-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=2), K.cfg("sai", level=1, zeta=0.13)),
+    "pgs4-scalar2d-periodic-p2": (K.scalar(16, 2, K.P, degree=2), K.cfg("pgs", partitions=4)),
+    "pgs3-stokes2d-rf": (K.stokes(8, 2, K.P, degree=1), K.cfg("pgs", partitions=3, omega=0.7, pre=1, post=0)),
 }
 DROPIN.update({f"baseline-{k}": v for k, v in K.baseline_configs().items()})
 
@@ -137,8 +139,8 @@ def test_zero_guess_vcycle_is_linear_and_fixes_zero(ctx, ref):
 
 
 @pytest.mark.parametrize("kind,pre,post,symmetric", [
-    ("jacobi", 0, 0, True), ("gs", 0, 1, True), ("sai", 0, 1, True), ("sai", 1, 0, True),
-    ("gs", 0, 0, False), ("sai", 0, 0, False), ("sai", 1, 1, False)])
+    ("jacobi", 0, 0, True), ("gs", 0, 1, True), ("sai", 0, 1, True), ("sai", 1, 0, True), ("pgs", 0, 1, True),
+    ("gs", 0, 0, False), ("sai", 0, 0, False), ("sai", 1, 1, False), ("pgs", 0, 0, False)])
 def test_symmetric_plans_are_self_adjoint(ctx, ref, kind, pre, post, symmetric):
     spec = K.scalar(8, 2, K.D, degree=2)
     mg = g.Multigrid(ctx, K.cfg(kind, pre=pre, post=post), g.Problem(spec))

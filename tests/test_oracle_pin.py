@@ -90,7 +90,7 @@ def test_port_bitwise_on_golden_fixtures(path):
     assert eq(P.apply(b), z["want_apply"])
 
 
-@pytest.mark.parametrize("case", ["periodic-jacobi", "dirichlet-gs-p2", "stokes-sai", "3d-sai"])
+@pytest.mark.parametrize("case", ["periodic-jacobi", "dirichlet-gs-p2", "stokes-sai", "3d-sai", "pgs3-2d", "pgs2-stokes"])
 def test_port_bitwise_live_against_reference(ref, case):
     from tests import cases as K
     spec, cfg = {
@@ -98,6 +98,9 @@ def test_port_bitwise_live_against_reference(ref, case):
         "dirichlet-gs-p2": (K.scalar(8, 2, K.D, degree=2), K.cfg("gs")),
         "stokes-sai": (K.stokes(4, 2, K.P, gamma=1.0, degree=2), K.cfg("sai", level=1, zeta=0.13)),
         "3d-sai": (K.scalar(4, 3, K.P, degree=2), K.cfg("sai", level=1)),
+        "pgs3-2d": (K.scalar(8, 2, K.D, degree=1), K.cfg("pgs", partitions=3, nu=2)),
+        "pgs2-stokes": (K.stokes(4, 2, K.P, degree=1), K.cfg("pgs", partitions=2, omega=0.7, nu=1,
+                                                           pre=1, post=0)),
     }[case]
     R = ref.RefMultigrid(spec, cfg)
     P = port.from_reference(R, cfg)

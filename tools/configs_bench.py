@@ -54,6 +54,10 @@ def configs(c5n):
                                      phase_shape=g.PHASE_BOXES, center=(0.25, 0.25, 0.25), radii=(0.75, 0.75, 0.75),
                                      mu_in=1e4, mu_out=1.0),
                        mg(g.SmootherConfig.sai(1), 3), "normal"),
+        "C3-box-PGS4": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=16.0,
+                                      phase_shape=g.PHASE_BOXES, center=(0.25, 0.25, 0.25), radii=(0.75, 0.75, 0.75),
+                                      mu_in=1e4, mu_out=1.0),
+                        mg(g.SmootherConfig.proc_block_gs(4), 3), "normal"),
         "C3-beta4p2-GS": (g.ProblemSpec(kind=S, dim=2, n=256, degree=4, bc=(D_,) * 6, beta=64.0, **ball3),
                           mg(g.SmootherConfig.coloured_gs(), 3), "normal"),
         "C4": (g.ProblemSpec(kind=T, dim=2, n=128, degree=3, bc=(P_,) * 6, beta=9.0, beta_p=1 / 16, gamma=0.0, **ell),
@@ -144,7 +148,8 @@ def main():
         if a.csv:
             from paper_2412_12506_b200 import report as R
             sm = cfg.smoother
-            fam = {g.JACOBI: "J", g.COLOURED_GS: "GS", g.SAI: f"SAI{sm.level}"}[sm.kind]
+            fam = {g.JACOBI: "J", g.COLOURED_GS: "GS", g.SAI: f"SAI{sm.level}",
+                   g.PROC_BLOCK_GS: f"PGS{sm.partitions}"}[sm.kind]
             sweeps = "" if sm.kind == g.JACOBI else "-" + "".join("f" if s_ == g.SWEEP_FORWARD else "r"
                                                                  for s_ in (cfg.pre, cfg.post))
             et = mg.estimate_eta(g._lib.KRYLOV_GMRES, seed=0)
