@@ -292,6 +292,7 @@ void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
     if (attr_set_device != ctx.device) {
         LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(ctx.smem_optin)));
+        max_carveout(rowpass_kernel<GT, BS>);
         attr_set_device = ctx.device;
     }
     static std::vector<std::pair<size_t, int>> occ_cache;
@@ -521,8 +522,10 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         const int warps = std::min(8, maxlen);
         const size_t smem = sizeof(double) * (size_t(maxlen) * 32 + 64);
         if (smem > 48 * 1024)
-            LDGMG_CUDA(cudaFuncSetAttribute(rowsplit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            ensure_dyn_smem(rowsplit_kernel, size_t(smem));
         const int grid = std::min(p.nrows, ctx.num_sms * 16);
+        static bool once = (max_carveout(rowsplit_kernel), true);
+        (void)once;
         rowsplit_kernel<<<grid, warps * 32, smem, ctx.stream>>>(a, maxlen);
         after_launch("rowsplit_kernel");
         return;

@@ -8,8 +8,10 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/ldgmg_b200.h"
 
@@ -41,6 +43,52 @@ inline void after_launch(const char* name) {
 }
 
 inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+/// Raise a kernel's dynamic shared-memory limit only when `bytes` exceeds
+/// what was already set on this device: cudaFuncSetAttribute on every launch
+/// costs ~15 us of GPU time per following launch (measured), so the
+/// attribute is cached per (kernel, device).
+template <class K>
+inline void ensure_dyn_smem(K* kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    struct Entry {
+        const void* f;
+        int dev;
+        size_t bytes;
+    };
+    static std::vector<Entry> set;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const void* f = reinterpret_cast<const void*>(kernel);
+    for (auto& e : set)
+        if (e.f == f && e.dev == dev) {
+            if (e.bytes >= bytes) return;
+            cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
+                       "cudaFuncSetAttribute");
+            e.bytes = bytes;
+            return;
+        }
+    cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
+               "cudaFuncSetAttribute");
+    set.push_back({f, dev, bytes});
+}
+
+/// Pin a kernel's shared-memory carveout to the maximum (once per kernel).
+/// The V-cycle alternates the TMA row pass (large carveout) with small
+/// kernels; letting the driver pick a smaller carveout for those forces an
+/// SM reconfiguration (L1 drain) at every switch, which measured as a
+/// ~15 us bubble per small launch on B200.  LDGMG_CARVEOUT=0 disables.
+template <class K>
+inline void max_carveout(K* kernel) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("LDGMG_CARVEOUT");
+        env = e ? std::atoi(e) : 1;
+    }
+    if (env) cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+                        "carveout");
+}
 
 // ------------------------------------------------------------ PTX helpers
 #if defined(__CUDACC__)

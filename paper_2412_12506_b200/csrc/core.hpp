@@ -147,8 +147,9 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
 
 /// v -= (v.k) k for the constant-mode kernel vectors (multigrid.hpp:243-245).
 /// `offs` = entries of the mode-0 coefficient of each kernel component.
+/// `scratch` (>= 256 * ncomp doubles) enables the multi-CTA fast path.
 void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* comp_offsets,
-                              int ncomp, double kval, bool strict_order);
+                              int ncomp, double kval, bool strict_order, double* scratch = nullptr);
 void launch_axpy(Ctx& ctx, int64_t n, double alpha, const double* x, double* y);
 /// deterministic fixed-tree dot (partials per CTA, ascending final sum)
 void launch_dot(Ctx& ctx, int64_t n, const double* a, const double* b, double* d_out);

@@ -425,8 +425,9 @@ void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
     bottom.n = n;
     bottom.lmax = 0.0;
     for (double l : lam) bottom.lmax = std::max(bottom.lmax, std::abs(l));
-    bottom.Vc.alloc(sizeof(double) * std::max<size_t>(1, Vc.size()));
-    bottom.Vr.alloc(sizeof(double) * std::max<size_t>(1, Vr.size()));
+    // +2: tail padding for the even-sized bulk copies of pinv_stream_kernel
+    bottom.Vc.alloc(sizeof(double) * (Vc.size() + 2));
+    bottom.Vr.alloc(sizeof(double) * (Vr.size() + 2));
     bottom.lambda.alloc(sizeof(double) * std::max(1, n));
     bottom.t.alloc(sizeof(double) * std::max(1, n));
     h2d(ctx, bottom.Vc.p, Vc.data(), sizeof(double) * Vc.size());
@@ -461,7 +462,8 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
 }
 
 void Mg::project(Ctx& ctx, double* v) {
-    launch_project_constants(ctx, v, A[0]->brows, bs, kernel_offs.as<int>(), nkernel, kval, strict_order);
+    launch_project_constants(ctx, v, A[0]->brows, bs, kernel_offs.as<int>(), nkernel, kval, strict_order,
+                             red.as<double>());
 }
 
 void Mg::cycle(Ctx& ctx, double* x, const double* b) {

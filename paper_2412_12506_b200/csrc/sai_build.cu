@@ -825,7 +825,7 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
     auto tma_kernel = tcpw == 8 ? qr_trailing_tma_kernel<NB, 8>
                                 : tcpw == 4 ? qr_trailing_tma_kernel<NB, 4> : qr_trailing_tma_kernel<NB, 2>;
     if (tma)
-        LDGMG_CUDA(cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem)));
+        ensure_dyn_smem(tma_kernel, size_t(tsmem));
     for (int j0 = 0; j0 < max_n; j0 += NB) {
         qr_panel_kernel<256, NB><<<nb, 256, smem, ctx.stream>>>(
             d_M.as<double>(), d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(),

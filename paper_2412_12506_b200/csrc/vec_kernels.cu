@@ -148,6 +148,274 @@ __global__ void prolong_cta_kernel(const int* __restrict__ child_ptr, const int*
     }
 }
 
+/// Copies the 2^d injection matrices (nK doubles, nK even) into shared
+/// memory with one TMA bulk copy: a single memory round trip per CTA.
+__device__ __forceinline__ void stage_K_bulk(double* sK, const double* K, int nK, uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, uint32_t(nK) * 8u);
+        bulk_g2s(sK, K, uint32_t(nK) * 8u, bar);
+    }
+    mbar_wait(bar, 0);
+}
+
+/// Restriction, one WARP per coarse element p with the injection matrices in
+/// shared memory.  Every global access of a parent is issued in batches
+/// (children ids, orthants, then all child residual blocks) so a parent costs
+/// ~3 memory round trips; lane (c, j) then computes the per-child sums s_f
+/// as independent chains (ILP across children) and accumulates them in the
+/// reference order acc = 0 + s_f1 + s_f2 + ... (copies for orthant -1).
+/// Same bits as restrict_kernel.
+template <int MAXCH>
+__global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restrict__ child_ptr,
+                                                            const int* __restrict__ child,
+                                                            const int* __restrict__ orth,
+                                                            const double* __restrict__ K,
+                                                            const double* __restrict__ rf, double* __restrict__ rc,
+                                                            int n_coarse, int bss, int ncomp, int nK) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int sch[8][MAXCH], sor[8][MAXCH];
+    __shared__ __align__(8) uint64_t bar;
+    const int BS = bss * ncomp, bb = bss * bss;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    double* sK = sm;
+    double* src = sm + nK + size_t(warp) * MAXCH * BS;
+    stage_K_bulk(sK, K, nK, &bar);
+    for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
+        const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
+        int f = 0;
+        if (lane < nch) f = __ldg(child + q0 + lane);
+        if (lane < nch) {
+            sch[warp][lane] = f;
+            sor[warp][lane] = __ldg(orth + f);
+        }
+        __syncwarp();
+        const int total = nch * BS;
+        for (int t0 = lane; t0 < total; t0 += 32 * 8) {
+            double tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * 32;
+                tmp[u] = 0.0;
+                if (t < total) {
+                    const int q = t / BS, e = t - q * BS;
+                    tmp[u] = rf[size_t(sch[warp][q]) * BS + e];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (t0 + u * 32 < total) src[t0 + u * 32] = tmp[u];
+        }
+        __syncwarp();
+        for (int o = lane; o < BS; o += 32) {
+            const int c = o / bss, j = o - c * bss;
+            // every chain runs unconditionally on valid addresses (inactive
+            // ones read K_0 / child 0 and are discarded): no branches in the
+            // loop, so the 2*MAXCH shared loads of a step issue back to back
+            double sq[MAXCH];
+            int ko[MAXCH], so[MAXCH];
+#pragma unroll
+            for (int q = 0; q < MAXCH; ++q) {
+                sq[q] = 0.0;
+                const bool act = q < nch && sor[warp][q] >= 0;
+                ko[q] = (act ? sor[warp][q] * bb : 0) + j;
+                so[q] = (q < nch ? q * BS : 0) + c * bss;
+            }
+            for (int i = 0; i < bss; ++i) {
+                double kv[MAXCH], xv[MAXCH];
+#pragma unroll
+                for (int q = 0; q < MAXCH; ++q) {
+                    kv[q] = sK[ko[q] + i * bss];
+                    xv[q] = src[so[q] + i];
+                }
+#pragma unroll
+                for (int q = 0; q < MAXCH; ++q) sq[q] = madd_rn(sq[q], kv[q], xv[q]);
+            }
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < MAXCH; ++q)
+                if (q < nch) acc = __dadd_rn(acc, sor[warp][q] < 0 ? src[q * BS + o] : sq[q]);
+            rc[size_t(p) * BS + o] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+/// Prolongation, one WARP per coarse element with the injection matrices
+/// staged (bulk copy, then transposed in shared memory so lanes = consecutive
+/// fine rows i read consecutive words).  Per parent: children/orthants and
+/// xc_p in two batched round trips, then RU outputs per lane in flight with
+/// their xf read-modify-writes issued together.  Same bits as prolong_kernel.
+__global__ void __launch_bounds__(256) prolong_warp_kernel(const int* __restrict__ child_ptr,
+                                                           const int* __restrict__ child,
+                                                           const int* __restrict__ orth,
+                                                           const double* __restrict__ K,
+                                                           const double* __restrict__ xc, double* __restrict__ xf,
+                                                           int n_coarse, int bss, int ncomp, int nK) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int sch[8][8], sor[8][8];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr int RU = 8;
+    const int BS = bss * ncomp, bb = bss * bss;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    double* sKt = sm;        // [o][j][i]
+    double* sK = sm + nK;    // bulk-copied K, [o][i][j]
+    double* sx = sm + 2 * size_t(nK) + size_t(warp) * BS;
+    stage_K_bulk(sK, K, nK, &bar);
+    for (int t = threadIdx.x; t < nK; t += blockDim.x) {
+        const int o = t / bb, r = t - o * bb, i = r / bss, j = r - i * bss;
+        sKt[size_t(o) * bb + size_t(j) * bss + i] = sK[t];
+    }
+    __syncthreads();
+    for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
+        const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
+        int f = 0;
+        if (lane < nch) f = __ldg(child + q0 + lane);
+        for (int t = lane; t < BS; t += 32) sx[t] = xc[size_t(p) * BS + t];
+        if (lane < nch) {
+            sch[warp][lane] = f;
+            sor[warp][lane] = __ldg(orth + f);
+        }
+        __syncwarp();
+        const int total = nch * BS;
+        for (int t0 = lane; t0 < total; t0 += 32 * RU) {
+            double sv[RU], old[RU];
+            int kb[RU], xb[RU];
+            double* dst[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int t = t0 + u * 32;
+                sv[u] = 0.0;
+                old[u] = 0.0;
+                kb[u] = -2;  // inactive
+                dst[u] = xf;
+                xb[u] = 0;
+                if (t < total) {
+                    const int q = t / BS, ii = t - q * BS;
+                    const int ot = sor[warp][q];
+                    dst[u] = xf + size_t(sch[warp][q]) * BS + ii;
+                    old[u] = *dst[u];
+                    if (ot < 0) {
+                        kb[u] = -1;
+                        xb[u] = ii;
+                    } else {
+                        const int c = ii / bss, i = ii - c * bss;
+                        kb[u] = ot * bb + i;
+                        xb[u] = c * bss;
+                    }
+                }
+            }
+            // branch-free chains (inactive ones read K_0 and are discarded)
+            int kk[RU], xx[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                kk[u] = kb[u] >= 0 ? kb[u] : 0;
+                xx[u] = kb[u] >= 0 ? xb[u] : 0;
+            }
+            for (int j = 0; j < bss; ++j) {
+                double kv[RU], xv[RU];
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    kv[u] = sKt[kk[u] + j * bss];
+                    xv[u] = sx[xx[u] + j];
+                }
+#pragma unroll
+                for (int u = 0; u < RU; ++u) sv[u] = madd_rn(sv[u], kv[u], xv[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                if (kb[u] == -2) continue;
+                const double add = kb[u] == -1 ? sx[xb[u]] : sv[u];
+                *dst[u] = __dadd_rn(old[u], add);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+/// Bottom pseudoinverse streaming V through shared memory: KC rows of the
+/// row-major Vr (then of Vc) per TMA bulk copy, double buffered; thread i
+/// keeps its sequential k-ascending chain (reference order) for up to 3
+/// columns.  The V arrays carry tail padding for the even-size copies.
+__global__ void __launch_bounds__(1024) pinv_stream_kernel(const double* __restrict__ Vr,
+                                                           const double* __restrict__ Vc,
+                                                           const double* __restrict__ lam,
+                                                           const double* __restrict__ b, double* __restrict__ x,
+                                                           int n, double cut, int KC) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int nv = (n + 1) & ~1;
+    double* sb = sm;            // b, then reused for nothing
+    double* st = sm + nv;       // t
+    double* ring = st + nv;     // 2 x KC x n
+    const size_t chunk = size_t(KC) * n;
+    const int nchunks = (n + KC - 1) / KC;
+    if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        fence_mbar_init();
+    }
+    for (int i = tid; i < n; i += NT) sb[i] = b[i];
+    __syncthreads();
+    uint32_t phases = 0u;  // bit s: parity to wait for on bars[s]
+    for (int pass = 0; pass < 2; ++pass) {
+        const double* Vm = pass == 0 ? Vr : Vc;
+        const double* vin = pass == 0 ? sb : st;
+        auto issue = [&](int c) {
+            const int rows = min(KC, n - c * KC);
+            const uint32_t bytes = uint32_t(((size_t(rows) * n + 1) & ~size_t(1)) * sizeof(double));
+            double* dst = ring + size_t(c & 1) * chunk;
+            mbar_arrive_expect_tx(bars + (c & 1), bytes);
+            bulk_g2s(dst, Vm + size_t(c) * chunk, bytes, bars + (c & 1));
+        };
+        if (tid == 0) {
+            fence_proxy_async();
+            issue(0);
+            if (nchunks > 1) issue(1);
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < nchunks; ++c) {
+            const int slot = c & 1;
+            mbar_wait(bars + slot, (phases >> slot) & 1u);
+            phases ^= 1u << slot;
+            const double* rows = ring + size_t(slot) * chunk;
+            const int k0 = c * KC, kr = min(KC, n - k0);
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int i = tid + u * NT;
+                if (i < n) {
+                    double s = acc[u];
+                    for (int k = 0; k < kr; ++k) s = madd_rn(s, rows[size_t(k) * n + i], vin[k0 + k]);
+                    acc[u] = s;
+                }
+            }
+            __syncthreads();  // every thread is done with this slot
+            if (tid == 0 && c + 2 < nchunks) {
+                fence_proxy_async();
+                issue(c + 2);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            const int i = tid + u * NT;
+            if (i < n) {
+                if (pass == 0) {
+                    const double l = lam[i];
+                    st[i] = fabs(l) <= cut ? 0.0 : acc[u] / l;
+                } else {
+                    x[i] = acc[u];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 /// Bottom pseudoinverse in one CTA (n <= 4096): b and t in shared memory.
 __global__ void __launch_bounds__(1024) pinv_cta_kernel(const double* __restrict__ Vr, const double* __restrict__ Vc,
                                                         const double* __restrict__ lam, const double* __restrict__ b,
@@ -244,6 +512,52 @@ __global__ void axpy_kernel(int64_t n, double alpha, const double* __restrict__ 
         y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
 }
 
+/// Fast projection over the whole GPU with a fixed shape (kProjParts
+/// contiguous element ranges, fixed trees), so the result is deterministic
+/// and independent of the device: partials, then every CTA re-sums the
+/// partials in the same order and applies the update to its range.
+constexpr int kProjParts = 256;
+__global__ void __launch_bounds__(256) project_partial_kernel(const double* __restrict__ v, int N, int bs,
+                                                              const int* __restrict__ offs, double kval,
+                                                              double* __restrict__ part) {
+    __shared__ double red[8];
+    const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
+    const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
+    double s = 0.0;
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) s = madd_rn(s, v[size_t(e) * bs + off], kval);
+    for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t = __dadd_rn(t, red[w]);
+        part[c * kProjParts + k] = t;
+    }
+}
+__global__ void __launch_bounds__(256) project_apply_kernel(double* __restrict__ v, int N, int bs,
+                                                            const int* __restrict__ offs, double kval,
+                                                            const double* __restrict__ part) {
+    __shared__ double red[8];
+    __shared__ double md;
+    const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
+    double s = part[c * kProjParts + threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t = __dadd_rn(t, red[w]);
+        md = -t;
+    }
+    __syncthreads();
+    const double m = md;
+    const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        double& xv = v[size_t(e) * bs + off];
+        xv = __dadd_rn(xv, __dmul_rn(m, kval));
+    }
+}
+
 __global__ void fill_kernel(int64_t n, double v, double* __restrict__ y) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -290,9 +604,27 @@ int grid1(int64_t n, int threads, const Ctx& ctx) {
 
 }  // namespace
 
+namespace {
+int transfer_nK(const Transfer& T) { return (1 << T.dim) * T.bss * T.bss; }
+}  // namespace
+
 void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc) {
     const int64_t total = int64_t(T.n_coarse) * T.bs;
     if (!total) return;
+    const int nK = transfer_nK(T);
+    const size_t smem_w = sizeof(double) * (size_t(nK) + size_t(8) * 8 * T.bs);
+    if (T.max_children <= 8 && smem_w <= 200 * 1024) {
+        if (smem_w > 48 * 1024)
+            ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
+        const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
+        static bool once = (max_carveout(restrict_warp_kernel<8>), true);
+        (void)once;
+        restrict_warp_kernel<8><<<grid, 256, smem_w, ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(),
+                                                                   T.orth.as<int>(), T.K.as<double>(), rf, rc,
+                                                                   T.n_coarse, T.bss, T.ncomp, nK);
+        after_launch("restrict_warp_kernel");
+        return;
+    }
     if (T.max_children <= 64 && size_t(T.max_children) * T.bs * 8 <= 48 * 1024) {
         const int threads = T.bs <= 32 ? 32 : T.bs <= 64 ? 64 : T.bs <= 128 ? 128 : 256;
         restrict_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads,
@@ -311,6 +643,20 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc) 
 void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* xf) {
     const int64_t total = int64_t(T.n_fine) * T.bs;
     if (!total) return;
+    const int nK = transfer_nK(T);
+    const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
+    if (T.max_children <= 8 && smem_w <= 200 * 1024) {
+        if (smem_w > 48 * 1024)
+            ensure_dyn_smem(prolong_warp_kernel, size_t(smem_w));
+        const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
+        static bool once = (max_carveout(prolong_warp_kernel), true);
+        (void)once;
+        prolong_warp_kernel<<<grid, 256, smem_w, ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(),
+                                                               T.orth.as<int>(), T.K.as<double>(), xc, xf,
+                                                               T.n_coarse, T.bss, T.ncomp, nK);
+        after_launch("prolong_warp_kernel");
+        return;
+    }
     if (T.bs * 8 <= 48 * 1024) {
         const int threads = std::min(256, std::max(32, ((T.max_children * T.bs + 31) / 32) * 32));
         prolong_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads, size_t(T.bs) * 8,
@@ -329,6 +675,20 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
     if (!n) return;
     const double cut = tol * E.lmax;
     if (n <= 3072) {
+        // KC rows of V per stage, two stages, within ~200 KB of shared memory
+        const size_t vec = size_t((n + 1) & ~1) * 2;
+        int KC = int(std::min<size_t>(size_t(n), ((200 * 1024 / 8 - vec - 2) / (2 * size_t(n)))));
+        KC &= ~1;
+        if (KC >= 2) {
+            const size_t smem = sizeof(double) * (vec + size_t(2) * KC * n + 2);
+            ensure_dyn_smem(pinv_stream_kernel, size_t(smem));
+            static bool once = (max_carveout(pinv_stream_kernel), true);
+            (void)once;
+            pinv_stream_kernel<<<1, 1024, smem, ctx.stream>>>(E.Vr.as<double>(), E.Vc.as<double>(),
+                                                              E.lambda.as<double>(), b, x, n, cut, KC);
+            after_launch("pinv_stream_kernel");
+            return;
+        }
         pinv_cta_kernel<<<1, 1024, sizeof(double) * 2 * n, ctx.stream>>>(E.Vr.as<double>(), E.Vc.as<double>(),
                                                                         E.lambda.as<double>(), b, x, n, cut);
         after_launch("pinv_cta_kernel");
@@ -342,11 +702,20 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
 }
 
 void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* comp_offsets,
-                              int ncomp, double kval, bool strict_order) {
+                              int ncomp, double kval, bool strict_order, double* scratch) {
     if (!ncomp) return;
     if (strict_order) {
         project_strict_kernel<<<1, 32, 0, ctx.stream>>>(v, N, bs, comp_offsets, ncomp, kval);
         after_launch("project_strict_kernel");
+    } else if (scratch && N >= kProjParts) {
+        static bool once = (max_carveout(project_partial_kernel), max_carveout(project_apply_kernel), true);
+        (void)once;
+        project_partial_kernel<<<dim3(kProjParts, ncomp), 256, 0, ctx.stream>>>(v, N, bs, comp_offsets, kval,
+                                                                               scratch);
+        after_launch("project_partial_kernel");
+        project_apply_kernel<<<dim3(kProjParts, ncomp), 256, 0, ctx.stream>>>(v, N, bs, comp_offsets, kval,
+                                                                             scratch);
+        after_launch("project_apply_kernel");
     } else {
         project_fast_kernel<<<ncomp, 1024, 0, ctx.stream>>>(v, N, bs, comp_offsets, ncomp, kval);
         after_launch("project_fast_kernel");
