@@ -170,13 +170,22 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
     spec, cfg = workload()
     spec.n = 64
     t0 = time.time()
-    P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
-    t_asm = time.time() - t0
-    t0 = time.time()
-    dm = parallel.from_problem(ctx, P, cfg, dist, min_rows_per_rank=512)
+    if args.replicated_setup:
+        P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+        t_asm = time.time() - t0
+        t0 = time.time()
+        dm = parallel.from_problem(ctx, P, cfg, dist, min_rows_per_rank=512)
+    else:
+        # distributed setup: this rank's rows + SAI halo only (host assembly and
+        # GPU SAI build both ~1/P of the replicated cost)
+        t_asm = 0.0
+        dm = parallel.from_problem_partial(ctx, spec, cfg, dist, min_rows_per_rank=512)
+        P = dm._problem
     torch.cuda.synchronize()
     t_mg = time.time() - t0
-    dof_cycle, bytes_cycle = dm._full.cycle_costs()
+    cc = torch.tensor(dm.cycle_costs(), device="cuda", dtype=torch.float64)
+    dist.all_reduce(cc)
+    dof_cycle, bytes_cycle = float(cc[0]), float(cc[1])
     n, bs = P.level_shape(0)[:2]
     b_host = rhs(n, bs)
     r0, r1 = dm.owned_range()
@@ -231,7 +240,9 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
                        "partitioned_levels": dm.ld,
                        "l2": "no flush: per-rank working set >> 126 MB L2",
                        "setup_s": {"assembly": round(t_asm, 2), "hierarchy_gpu": round(t_mg, 2),
-                                   "note": "setup replicated per rank (round 1)"}},
+                                   "distributed": not args.replicated_setup,
+                                   "note": ("replicated per rank" if args.replicated_setup else
+                                            "each rank assembles its rows + SAI halo and solves its SAI columns")}},
             "vcycle_hbm_GBps_total": bytes_cycle * args.steps / t / 1e9,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * (r1 - r0) * bs),
                     "d2h_bytes_per_step": int(8 * (r1 - r0) * bs),
@@ -250,6 +261,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true", help="force the mesh-partitioned path at N=1 (testing)")
+    ap.add_argument("--replicated-setup", action="store_true",
+                    help="N>1: build the whole hierarchy on every rank (default: distributed setup)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -386,7 +399,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 

@@ -233,6 +233,12 @@ int ldgmg_smoother_sai_nnzb(const ldgmg_smoother* S, int64_t* nnzb);
 int ldgmg_smoother_sai_matrix(ldgmg_ctx* ctx, const ldgmg_smoother* S, int* ptr, int* col,
                               double* val);
 int ldgmg_smoother_sai_stats(const ldgmg_smoother* S, ldgmg_sai_stats* out);
+/* replaces build_sai(System, level, zeta, SaiCache*, SaiStats*) (smoothers.hpp:259-367)
+ * on a device operator: B on the pattern of A^level.  `col_mask` (NULL or
+ * N ints) restricts the least-squares solves to the columns with a nonzero
+ * entry (distributed setup); the other columns of B stay zero. */
+int ldgmg_sai_build(ldgmg_ctx* ctx, const ldgmg_bsr* A, int system_kind, int n_velocity, int level,
+                    double zeta, int cache, const int* col_mask, ldgmg_bsr** B, ldgmg_sai_stats* stats);
 /* per-element diagonal factors V (bs*bs, column-major like Eigen), lambda, s */
 int ldgmg_smoother_diag_factors(ldgmg_ctx* ctx, const ldgmg_smoother* S, double* V,
                                 double* lambda, double* s);
@@ -285,6 +291,9 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
  * parity mode); 0 (default): fixed-shape deterministic tree reduction. */
 int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict);
 /* algorithmic DOF-updates and HBM bytes of one V-cycle */
+/* build every smoother not set by the caller (otherwise done lazily by the
+ * first cycle): the rest of the reference constructor's setup, multigrid.hpp:49-65 */
+int ldgmg_mg_setup(ldgmg_ctx* ctx, ldgmg_mg* mg);
 int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes);
 int ldgmg_mg_destroy(ldgmg_mg* mg);
 
@@ -317,6 +326,16 @@ int ldgmg_estimate_eta(ldgmg_ctx* ctx, ldgmg_mg* mg, int kind, uint64_t seed, do
  * standalone.  Host C++, multi-threaded. */
 int ldgmg_problem_create(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements,
                          ldgmg_problem** out);
+/* Distributed setup: as ldgmg_problem_create, but every level
+ * with >= nranks * min_rows_per_rank elements (except the last) assembles
+ * only rank `rank`'s element range [rank*N/P, (rank+1)*N/P) (partition_ranges,
+ * smoothers.hpp:87-94) plus `halo_hops` face layers; the other rows are left
+ * empty.  Each assembled row is bit-identical to the full assembly. */
+int ldgmg_problem_create_partial(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements,
+                                 int nranks, int rank, int halo_hops, int min_rows_per_rank,
+                                 ldgmg_problem** out);
+/* 1 when the level was assembled partially (rank rows + halo) */
+int ldgmg_problem_level_partial(const ldgmg_problem* P, int level);
 int ldgmg_problem_depth(const ldgmg_problem* P);
 int ldgmg_problem_level_shape(const ldgmg_problem* P, int level, int* n_elements, int* bs,
                               int64_t* nnzb);

@@ -9,6 +9,6 @@ from ._lib import (BC_DIRICHLET, BC_NEUMANN, BC_PERIODIC, COLOURED_GS, JACOBI, P
                    SYSTEM_SCALAR, SYSTEM_STOKES, CudaError, InvalidArgument, LdgmgError, LdgmgRuntimeError,
                    LogicError, launch_count)
 from .api import (Context, DeviceBsr, Multigrid, MultigridConfig, Problem, ProblemSpec, Smoother,
-                  SmootherConfig, Transfer, coo_read, coo_write, random_rhs, residual, spmv, spmv_transpose)
+                  SmootherConfig, Transfer, coo_read, coo_write, random_rhs, sai_build, residual, spmv, spmv_transpose)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

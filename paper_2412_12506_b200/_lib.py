@@ -155,6 +155,7 @@ _SIGS = {
     "ldgmg_smoother_sai_nnzb": ([_P, C.POINTER(_I64)], _I),
     "ldgmg_smoother_sai_matrix": ([_P, _P, _P, _P, _P], _I),
     "ldgmg_smoother_sai_stats": ([_P, C.POINTER(SaiStats)], _I),
+    "ldgmg_sai_build": ([_P, _P, _I, _I, _I, _D, _I, _P, C.POINTER(_P), C.POINTER(SaiStats)], _I),
     "ldgmg_smoother_diag_factors": ([_P, _P, _P, _P, _P], _I),
     "ldgmg_smoother_destroy": ([_P], _I),
     "ldgmg_transfer_create": ([_P, _I, _I, _P, _P, _I, _I, _I, _P, C.POINTER(_P)], _I),
@@ -171,11 +172,14 @@ _SIGS = {
     "ldgmg_mg_cycles": ([_P, _P, _P, _P, _I], _I),
     "ldgmg_mg_solve_host": ([_P, _P, _P, _P, _D, _I, _P, _IP], _I),
     "ldgmg_mg_set_strict_order": ([_P, _I], _I),
+    "ldgmg_mg_setup": ([_P, _P], _I),
     "ldgmg_mg_cycle_costs": ([_P, _DP, _DP], _I),
     "ldgmg_mg_destroy": ([_P], _I),
     "ldgmg_krylov_solve": ([_P, _P, _I, _P, _P, _D, _I, C.POINTER(SolveReportC)], _I),
     "ldgmg_estimate_eta": ([_P, _P, _I, C.c_uint64, _D, _I, C.POINTER(SolveReportC)], _I),
     "ldgmg_problem_create": ([C.POINTER(ProblemSpec), _I, _I, C.POINTER(_P)], _I),
+    "ldgmg_problem_create_partial": ([C.POINTER(ProblemSpec), _I, _I, _I, _I, _I, _I, C.POINTER(_P)], _I),
+    "ldgmg_problem_level_partial": ([_P, _I], _I),
     "ldgmg_problem_depth": ([_P], _I),
     "ldgmg_problem_level_shape": ([_P, _I, _IP, _IP, C.POINTER(_I64)], _I),
     "ldgmg_problem_level_matrix": ([_P, _I, _P, _P, _P], _I),

@@ -375,6 +375,10 @@ class Problem:
         h = C.c_void_p()
         check(lib.ldgmg_problem_create(C.byref(cs), int(min_depth), int(bottom_max_elements), C.byref(h)))
         self.h = h
+        self._init_info()
+
+    def _init_info(self):
+        h = self.h
         self.depth = int(lib.ldgmg_problem_depth(h))
         dim, nc, bss, kc, kp, nv = (C.c_int() for _ in range(6))
         check(lib.ldgmg_problem_info(h, C.byref(dim), C.byref(nc), C.byref(bss), C.byref(kc), C.byref(kp),
@@ -382,6 +386,25 @@ class Problem:
         self.dim, self.n_comp, self.bs_scalar = dim.value, nc.value, bss.value
         self.kernel_constants, self.kernel_pressure, self.n_velocity = kc.value, kp.value, nv.value
         self.bs = self.n_comp * self.bs_scalar
+
+    @classmethod
+    def partial(cls, spec: ProblemSpec, nranks: int, rank: int, halo_hops: int, min_rows_per_rank: int = 64,
+                min_depth=2, bottom_max_elements=64) -> "Problem":
+        """Distributed setup (ldgmg_problem_create_partial): levels with >=
+        nranks*min_rows_per_rank elements assemble only this rank's rows plus
+        `halo_hops` face layers (other rows empty, global numbering kept)."""
+        obj = cls.__new__(cls)
+        obj.spec = spec
+        cs = spec.c()
+        h = C.c_void_p()
+        check(lib.ldgmg_problem_create_partial(C.byref(cs), int(min_depth), int(bottom_max_elements), int(nranks),
+                                               int(rank), int(halo_hops), int(min_rows_per_rank), C.byref(h)))
+        obj.h = h
+        obj._init_info()
+        return obj
+
+    def level_partial(self, l) -> bool:
+        return bool(lib.ldgmg_problem_level_partial(self.h, int(l)))
 
     def level_shape(self, l):
         n, bs, nnzb = C.c_int(), C.c_int(), C.c_int64()
@@ -509,7 +532,12 @@ class Multigrid:
         return self._report(lambda r: lib.ldgmg_estimate_eta(self.ctx.h, self.h, int(kind), int(seed), float(tol),
                                                              int(maxit), r), maxit)
 
+    def setup(self) -> None:
+        """Build the smoothers not set by set_smoother (else the first cycle does)."""
+        check(lib.ldgmg_mg_setup(self.ctx.h, self.h))
+
     def cycle_costs(self):
+        self.setup()
         d, b = C.c_double(), C.c_double()
         check(lib.ldgmg_mg_cycle_costs(self.h, C.byref(d), C.byref(b)))
         return d.value, b.value
@@ -518,6 +546,27 @@ class Multigrid:
         if getattr(self, "h", None):
             lib.ldgmg_mg_destroy(self.h)
             self.h = None
+
+
+def sai_build(ctx: Context, A: DeviceBsr, system_kind=L.SYSTEM_SCALAR, n_velocity=0, level=1, zeta=0.1,
+              cache=True, col_mask=None):
+    """build_sai (smoothers.hpp:259-367) on a device operator -> (DeviceBsr B, SaiStats).
+    `col_mask` (N bools) restricts the solved columns (the others stay zero)."""
+    st = L.SaiStats()
+    h = C.c_void_p()
+    m = None
+    if col_mask is not None:
+        m = np.ascontiguousarray(np.asarray(col_mask) != 0, np.int32)
+        if m.size != A.brows:
+            raise L.InvalidArgument("build_sai: column mask size mismatch")
+    check(lib.ldgmg_sai_build(ctx.h, A.h, int(system_kind), int(n_velocity), int(level), float(zeta), int(bool(cache)),
+                              m.ctypes.data if m is not None else None, C.byref(h), C.byref(st)))
+    B = DeviceBsr.__new__(DeviceBsr)
+    B.ctx, B.h = ctx, h
+    br, bc, rb, cb, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+    check(lib.ldgmg_bsr_shape(h, C.byref(br), C.byref(bc), C.byref(rb), C.byref(cb), C.byref(nz)))
+    B.brows, B.bcols, B.row_bs, B.col_bs, B.nnzb = br.value, bc.value, rb.value, cb.value, nz.value
+    return B, st
 
 
 def random_rhs(nblocks: int, bs: int, seed: int = 0) -> np.ndarray:

@@ -866,6 +866,15 @@ int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict) {
     });
 }
 
+int ldgmg_mg_setup(ldgmg_ctx* ctx, ldgmg_mg* mg) {
+    return guarded([&] {
+        need(ctx, "mg_setup");
+        need(mg, "mg_setup");
+        bind(*ctx);
+        ensure_smoothers(ctx, mg->m);
+    });
+}
+
 int ldgmg_mg_cycle_costs(const ldgmg_mg* mg, double* dof_updates, double* alg_bytes) {
     return guarded([&] {
         need(mg, "mg_cycle_costs");
@@ -934,6 +943,48 @@ int ldgmg_problem_create(const ldgmg_problem_spec* spec, int min_depth, int bott
             throw;
         }
         *out = h;
+    });
+}
+
+int ldgmg_problem_create_partial(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements,
+                                 int nranks, int rank, int halo_hops, int min_rows_per_rank,
+                                 ldgmg_problem** out) {
+    return guarded([&] {
+        need(spec, "problem_create_partial");
+        need(out, "problem_create_partial");
+        auto* h = new ldgmg_problem();
+        try {
+            problem_build_partial(*spec, min_depth, bottom_max_elements, nranks, rank, halo_hops, min_rows_per_rank,
+                                  h->p);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ldgmg_problem_level_partial(const ldgmg_problem* P, int level) {
+    if (!P || level < 0 || level >= int(P->p.levels.size())) return 0;
+    return P->p.levels[level].partial ? 1 : 0;
+}
+
+int ldgmg_sai_build(ldgmg_ctx* ctx, const ldgmg_bsr* A, int system_kind, int n_velocity, int level, double zeta,
+                    int cache, const int* col_mask, ldgmg_bsr** B, ldgmg_sai_stats* stats) {
+    return guarded([&] {
+        need(ctx, "build_sai");
+        need(A, "build_sai");
+        need(B, "build_sai(B)");
+        bind(*ctx);
+        std::vector<char> mask;
+        if (col_mask) {
+            mask.resize(A->brows);
+            for (int j = 0; j < A->brows; ++j) mask[j] = col_mask[j] != 0;
+        }
+        SaiResult r = build_sai_gpu(*ctx, *A, system_kind, n_velocity, level, zeta, cache != 0, nullptr,
+                                    col_mask ? &mask : nullptr);
+        if (stats) *stats = r.stats;
+        *B = static_cast<ldgmg_bsr*>(own_bsr(std::move(r.B)));
     });
 }
 

@@ -26,8 +26,10 @@ struct SaiResult {
 struct SaiCache;  // least-squares solution cache, shareable across builds
 SaiCache* sai_cache_new();
 void sai_cache_free(SaiCache* c);
+/// `colmask` (optional, N entries): solve only the columns with a nonzero
+/// entry (distributed setup: the rank's columns); the others stay empty.
 SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level,
-                        double zeta, bool cache, SaiCache* shared);
+                        double zeta, bool cache, SaiCache* shared, const std::vector<char>* colmask = nullptr);
 
 struct Smoother {
     const Bsr* A = nullptr;

@@ -856,7 +856,7 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
 }
 
 SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level, double zeta,
-                        bool use_cache, SaiCache* shared) {
+                        bool use_cache, SaiCache* shared, const std::vector<char>* colmask) {
     const int N = A.brows, bs = A.rbs;
     if (A.bcols != N || A.cbs != bs) fail(LDGMG_ERR_INVALID_ARGUMENT, "build_sai: matrix not block-square");
     if (level < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "pattern_power: negative power");
@@ -996,6 +996,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         std::vector<int> mark(N, -1), seen(N, -1), I, cand;
         for (int j = lo; j < hi; ++j) {
             ColumnPlan& P = plan[j];
+            if (colmask && !(*colmask)[j]) continue;  // column not requested
             const std::vector<int>& J = pat[j];
             I.clear();
             for (int k : J)
@@ -1075,6 +1076,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     std::vector<std::pair<int, Key>> inserts;  // (problem id, key) to insert after solving
     size_t pending_bytes = cache ? cache->bytes : 0;
     for (int j = 0; j < N; ++j) {
+        if (colmask && !(*colmask)[j]) continue;
         const ColumnPlan& P = plan[j];
         ++ls_dims[{P.ni, P.nj}];
         if (cache) {
@@ -1307,6 +1309,11 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         sxoff.push_back(cxoff[i]);
     }
     for (int j = 0; j < N; ++j) {
+        if (colmask && !(*colmask)[j]) {  // not requested: empty column
+            sprob[j] = 0;
+            coff[j + 1] = int(jc.size());
+            continue;
+        }
         const ColumnPlan& P = plan[j];
         bool def;
         if (col_entry[j]) {

@@ -243,6 +243,13 @@ struct Ctx {
     int dim, bs, p1;
     double beta;
     std::vector<double> msc, mu, rho;
+    // row-restricted assembly (distributed setup): rows of the operator to
+    // build (`rows`), and the rows of G / E they need (`grows` = rows plus
+    // their face neighbours).  Empty vectors = every row.  Each built row is
+    // bit-identical to the full assembly (same per-row accumulation).
+    std::vector<char> rows, grows;
+    bool want(int e) const { return rows.empty() || rows[e]; }
+    bool want_g(int e) const { return grows.empty() || grows[e]; }
 
     int donor(const Face& f) const { return mu[f.right] > mu[f.left] ? f.right : f.left; }
     double penalty_tau(const Face& f) const {
@@ -384,6 +391,7 @@ void gradient_rows(const Ctx& c, std::array<Rows, 3>& G) {
         std::vector<Face> faces;
         std::vector<double> VE, VD, M;
         for (int e = lo; e < hi; ++e) {
+            if (!c.want_g(e)) continue;
             std::array<Row, 3> rows;
             const double scal = 2.0 / c.mesh->h;
             for (int k = 0; k < c.dim; ++k) {
@@ -432,6 +440,7 @@ void penalty_rows(const Ctx& c, bool pressure, double beta_p, double delta, Rows
         std::vector<Face> faces;
         std::vector<double> VE, VO, M;
         for (int e = lo; e < hi; ++e) {
+            if (!c.want(e)) continue;
             Row row;
             c.mesh->faces_of(e, faces);
             for (const Face& f : faces) {
@@ -544,6 +553,7 @@ void assemble_scalar(const Ctx& c, HostCsr& A) {
     parallel_for(N, [&](int lo, int hi) {
         std::vector<double> tmp;
         for (int e = lo; e < hi; ++e) {
+            if (!c.want(e)) continue;
             Row row;
             for (int k = 0; k < c.dim; ++k) at_d_b_row(e, src[k][e], G[k], G[k], dmu, bs, row, tmp);
             for (int kk = 0; kk < int(E.cols[e].size()); ++kk) row.add(E.cols[e][kk], E.block(e, kk), 1.0, bs * bs);
@@ -577,6 +587,7 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
     parallel_for(N, [&](int lo, int hi) {
         std::vector<double> tmp;
         for (int e = lo; e < hi; ++e) {
+            if (!c.want(e)) continue;
             Row row;
             for (int k = 0; k < dim; ++k) at_d_b_row(e, src[k][e], G[k], G[k], dmu, bsv, row, tmp);
             for (int kk = 0; kk < int(Ev.cols[e].size()); ++kk)
@@ -601,6 +612,7 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
     parallel_for(N, [&](int lo, int hi) {
         std::vector<double> tr(size_t(bsv) * bsv);
         for (int r0 = lo; r0 < hi; ++r0) {
+            if (!c.want(r0)) continue;
             Row row;
             auto add_sub = [&](int E2, int ci, int cj, const double* small, double s) {
                 double* dst = row.at(E2, BS * BS);
@@ -646,7 +658,56 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
 
 }  // namespace
 
+namespace {
+/// Rows within `hops` face-graph steps of the element range [r0, r1).
+std::vector<char> halo_rows(const LevelMesh& m, int r0, int r1, int hops) {
+    const int N = m.n_elements();
+    std::vector<char> in(N, 0);
+    std::vector<int> frontier, next;
+    for (int e = r0; e < r1; ++e) {
+        in[e] = 1;
+        frontier.push_back(e);
+    }
+    std::vector<Face> faces;
+    for (int h = 0; h < hops && !frontier.empty(); ++h) {
+        next.clear();
+        for (int e : frontier) {
+            m.faces_of(e, faces);
+            for (const Face& f : faces) {
+                if (f.kind != F_INTERIOR) continue;
+                const int o = f.left == e ? f.right : f.left;
+                if (!in[o]) {
+                    in[o] = 1;
+                    next.push_back(o);
+                }
+            }
+        }
+        frontier.swap(next);
+    }
+    return in;
+}
+/// rows plus their face neighbours (the G / E rows an operator row needs)
+std::vector<char> with_neighbours(const LevelMesh& m, const std::vector<char>& rows) {
+    std::vector<char> g(rows);
+    std::vector<Face> faces;
+    for (int e = 0; e < m.n_elements(); ++e) {
+        if (!rows[e]) continue;
+        m.faces_of(e, faces);
+        for (const Face& f : faces)
+            if (f.kind == F_INTERIOR) g[f.left == e ? f.right : f.left] = 1;
+    }
+    return g;
+}
+}  // namespace
+
 void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_elements, Problem& P) {
+    problem_build_partial(s, min_depth, bottom_max_elements, 1, 0, 0, 0, P);
+}
+
+void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int bottom_max_elements, int nranks,
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& P) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: bad rank / rank count");
+    if (halo_hops < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: negative halo");
     if (s.dim != 2 && s.dim != 3) fail(LDGMG_ERR_INVALID_ARGUMENT, "mesh: dim must be 2 or 3");
     if (s.kind != LDGMG_SYSTEM_SCALAR && s.kind != LDGMG_SYSTEM_STOKES)
         fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: unknown system kind");
@@ -751,6 +812,15 @@ void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_el
         ProblemLevel& L = P.levels[l];
         L.n = m.n;
         L.phase = m.phase;
+        L.partial = false;
+        // distributed levels (the same rule as parallel.DistMultigrid): the
+        // rank's range plus `halo_hops` face layers; smaller levels in full
+        if (nranks > 1 && N >= nranks * min_rows_per_rank && l + 1 < meshes.size()) {
+            const int r0 = int(int64_t(rank) * N / nranks), r1 = int(int64_t(rank + 1) * N / nranks);
+            c.rows = halo_rows(m, r0, r1, halo_hops);
+            c.grows = with_neighbours(m, c.rows);
+            L.partial = true;
+        }
         if (s.kind == LDGMG_SYSTEM_SCALAR) {
             assemble_scalar(c, L.A);
         } else {

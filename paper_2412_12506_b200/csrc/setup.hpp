@@ -26,6 +26,7 @@ struct ProblemLevel {
     HostCsr A;
     std::vector<int> phase;
     std::vector<int> parent_of, orthant_of;  // to the next coarser level
+    bool partial = false;  // only the rank's rows + halo assembled (others empty)
 };
 
 struct Problem {
@@ -38,6 +39,12 @@ struct Problem {
 
 void problem_build(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements,
                    Problem& out);
+/// Distributed setup: levels with >= nranks*min_rows_per_rank elements (all
+/// but the last) assemble only the rows of rank `rank`'s contiguous range
+/// [rank*N/P, (rank+1)*N/P) plus `halo_hops` face layers; every assembled
+/// row is bit-identical to problem_build's.  Smaller levels are complete.
+void problem_build_partial(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements, int nranks,
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& out);
 
 std::vector<double> injection_matrices(int dim, int degree);
 

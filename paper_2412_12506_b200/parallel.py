@@ -203,6 +203,7 @@ class DistMultigrid:
     def __init__(self, ops, dist, cfg, levels, transfers, K, dim, bss, ncomp, kernel_offsets, coarse_factory,
                  group=None, min_rows_per_rank=64):
         self.ops, self.dist, self.cfg, self.group = ops, dist, cfg, group
+        self.dim = dim
         self.rank = dist.get_rank(group)
         self.P = dist.get_world_size(group)
         self.bs = levels[0]["bs"]
@@ -221,15 +222,17 @@ class DistMultigrid:
             lv = levels[l]
             n = lv["n"]
             pa = partition_level(*lv["A"][:2], n, self.P, self.rank)
-            d = {"n": n, "plan": pa, "A": ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs,
-                                                     *local_rows(*lv["A"], bs, bs, pa)),
-                 "xA": Exchanger(pa, bs, ops, dist, group, self.rank)}
+            lrA = local_rows(*lv["A"], bs, bs, pa)
+            d = {"n": n, "plan": pa, "A": ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs, *lrA),
+                 "xA": Exchanger(pa, bs, ops, dist, group, self.rank), "nnzA": int(lrA[0][-1])}
             if "B" in lv:
                 Bg = lv["B"]
                 BTg = transpose_csr(*Bg, n, n, bs)
                 for key, M in (("B", Bg), ("BT", BTg)):
                     pb = partition_level(M[0], M[1], n, self.P, self.rank)
-                    d[key] = ops.matrix(pb.n_own, pb.n_own + pb.n_ghost, bs, *local_rows(*M, bs, bs, pb))
+                    lr = local_rows(*M, bs, bs, pb)
+                    d[key] = ops.matrix(pb.n_own, pb.n_own + pb.n_ghost, bs, *lr)
+                    d["nnz" + key] = int(lr[0][-1])
                     d["x" + key] = Exchanger(pb, bs, ops, dist, group, self.rank)
                     d["ng" + key] = pb.n_ghost
             if "factors" in lv:
@@ -356,6 +359,32 @@ class DistMultigrid:
         x_own.copy_(d["x"][:n_own * bs])
         self.project(x_own)
 
+    def cycle_costs(self):
+        """(DOF-updates, algorithmic HBM bytes) of one cycle on THIS rank: its
+        rows of the partitioned levels (SURVEY.md §8d formulas on the local
+        operators) plus, on rank 0 only, the agglomerated tail (replicated
+        work is counted once).  Sum over ranks = the whole job."""
+        W, bs = 8.0, self.bs
+        dof = byts = 0.0
+        nu1, nu2 = self.cfg.nu1, self.cfg.nu2
+        for l, d in enumerate(self.L):
+            n = d["plan"].n_own
+            dof += (nu1 + nu2) * n * bs
+            if self.cfg.smoother.kind == L.SAI:
+                sweep = lambda key: W * (bs * bs * (d["nnzA"] + d["nnz" + key]) + 6.0 * n * bs)  # noqa: E731
+                byts += nu1 * sweep("B" if self.cfg.pre == L.SWEEP_FORWARD else "BT")
+                byts += nu2 * sweep("B" if self.cfg.post == L.SWEEP_FORWARD else "BT")
+            else:
+                byts += (nu1 + nu2) * W * (bs * bs * (d["nnzA"] - n) + (bs * bs + 2.0 * bs) * n + 3.0 * n * bs)
+            byts += W * (bs * bs * d["nnzA"] + 3.0 * n * bs)  # residual
+            nc = d["c1"] - d["c0"] if l + 1 < self.ld else n // (1 << self.dim)
+            byts += W * (bs * n + bs * nc) + W * (bs * nc + 2.0 * bs * n)  # restrict + prolong
+        if self.rank == 0:
+            td, tb = self.coarse.cycle_costs()
+            dof += td
+            byts += tb
+        return dof, byts
+
     def owned_range(self, level=0):
         p = self.L[level]["plan"]
         return p.r0, p.r1
@@ -400,4 +429,153 @@ def from_problem(ctx, problem, cfg, dist, group=None, min_rows_per_rank=64):
     dm = DistMultigrid(GpuOps(ctx), dist, cfg, levels, transfers, K, problem.dim, problem.bs_scalar,
                        problem.n_comp, offs, coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank)
     dm._full = full
+    return dm
+
+
+# --------------------------------------------------------- distributed setup
+def sai_halo_hops(spec, smoother) -> int:
+    """Face-graph layers a rank must assemble around its range so that every
+    SAI column its B / B^T rows need is solved exactly: B row i needs the
+    columns c in pattern^l(i), whose least-squares rows reach
+    pattern^(2l+1) of the range; one operator hop is one face layer, two for
+    the stress-form Stokes operator (its G_j^T G_i cross terms couple
+    diagonal neighbours).  Non-SAI smoothers need the rank's rows only."""
+    if smoother.kind != L.SAI:
+        return 0
+    r_a = 2 if (spec.kind == L.SYSTEM_STOKES and spec.gamma != 0.0) else 1
+    return (2 * smoother.level + 1) * r_a
+
+
+def csr_ring(ptr, col, seed_mask, hops):
+    """Rows within `hops` steps of the seed rows on the block pattern."""
+    ptr, col = np.asarray(ptr), np.asarray(col)
+    mask = np.asarray(seed_mask, bool).copy()
+    frontier = np.nonzero(mask)[0]
+    for _ in range(hops):
+        if frontier.size == 0:
+            break
+        idx = np.concatenate([col[ptr[r]:ptr[r + 1]] for r in frontier]) if frontier.size else np.zeros(0, int)
+        new = np.unique(idx[~mask[idx]])
+        mask[new] = True
+        frontier = new
+    return mask
+
+
+def local_sai(ptr, col, val, n, bs, r0, r1, level, build):
+    """B columns for the rank's SAI rows from its assembled rows only.
+
+    (ptr, col, val) is the rank's global-numbered level operator with the
+    rows of its range plus halo assembled (the others empty).  The operator
+    restricted to the assembled rows H is renumbered locally; `build(lptr,
+    lcol, lval, nH, col_mask)` returns the local B (any solver of the
+    reference's build_sai); the columns pattern^level(range) -- all B / B^T
+    rows of the range need -- are solved.  Returns B in global numbering
+    (rows of H, global-shaped CSR).  Every returned entry of the range's
+    rows and columns equals the global build's (tests/test_distributed_setup.py)."""
+    ptr, col, val = np.asarray(ptr), np.asarray(col), np.asarray(val)
+    H = np.nonzero(np.diff(ptr) > 0)[0]
+    loc = np.full(n, -1, np.int64)
+    loc[H] = np.arange(H.size)
+    keep = loc[col] >= 0
+    rows_of = np.repeat(np.arange(n), np.diff(ptr))
+    kk = np.nonzero(keep)[0]
+    lrows = loc[rows_of[kk]]
+    lptr = np.zeros(H.size + 1, np.int32)
+    np.add.at(lptr, lrows + 1, 1)
+    lptr = np.cumsum(lptr).astype(np.int32)
+    lcol = loc[col[kk]].astype(np.int32)
+    lval = val.reshape(-1, bs * bs)[kk].reshape(-1)
+    own = np.zeros(n, bool)
+    own[r0:r1] = True
+    want = csr_ring(ptr, col, own, level)
+    if not np.all(np.diff(ptr)[want] > 0):
+        raise ValueError("distributed setup: halo too small for the SAI columns of this range")
+    Bp, Bc, Bv = build(lptr, lcol, lval, int(H.size), want[H])
+    Bp, Bc = np.asarray(Bp), np.asarray(Bc)
+    gptr = np.zeros(n + 1, np.int64)
+    gptr[H + 1] = np.diff(Bp)
+    gptr = np.cumsum(gptr).astype(np.int32)
+    return gptr, H[Bc].astype(np.int32), np.asarray(Bv)
+
+
+def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_fn):
+    """Per-level data for DistMultigrid from a Problem.partial: global-shaped
+    operators (assembled rows only), transfers, and for the distributed
+    levels the rank's SAI matrix (local_sai with `sai_fn`) or diagonal
+    factors (`factors_fn(diag_blocks) -> (V, lam, s)` of the rank's rows)."""
+    depth = prob.depth
+    shapes = [prob.level_shape(l) for l in range(depth)]
+    ld = 0
+    while ld < depth - 1 and shapes[ld][0] >= nranks * min_rows_per_rank:
+        ld += 1
+    ld = max(ld, 1)
+    levels, transfers = [], []
+    for l in range(depth):
+        n, bs, _ = shapes[l]
+        lv = {"n": n, "bs": bs, "A": prob.level_matrix(l)}
+        if l + 1 < depth:
+            transfers.append(prob.level_transfer(l))
+            if l < ld:
+                r0, r1 = rank * n // nranks, (rank + 1) * n // nranks
+                if cfg.smoother.kind == L.SAI:
+                    lv["B"] = local_sai(*lv["A"], n, bs, r0, r1, cfg.smoother.level, sai_fn)
+                else:
+                    ptr, col, val = lv["A"]
+                    dk = np.array([ptr[e] + int(np.nonzero(col[ptr[e]:ptr[e + 1]] == e)[0][0])
+                                   for e in range(r0, r1)], np.int64)
+                    D = np.asarray(val).reshape(-1, bs * bs)[dk].reshape(-1)
+                    V, lam, s = factors_fn(r1 - r0, bs, D)
+                    Vg, lg, sg = np.zeros(n * bs * bs), np.zeros(n * bs), np.zeros(n * bs)
+                    Vg[r0 * bs * bs:r1 * bs * bs], lg[r0 * bs:r1 * bs], sg[r0 * bs:r1 * bs] = V, lam, s
+                    lv["factors"] = (Vg, lg, sg)
+        levels.append(lv)
+    return levels, transfers
+
+
+def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64):
+    """Distributed hierarchy with DISTRIBUTED setup: each rank assembles only
+    its rows plus the SAI halo (Problem.partial), solves only the SAI columns
+    its rows need (column-masked GPU build), and computes the diagonal
+    factors of its own rows on the GPU.  The agglomerated tail is set up in
+    full on every rank (it is small).  Results are identical to
+    from_problem (tests/test_distributed_setup.py)."""
+    from .api import DeviceBsr, Multigrid, MultigridConfig, Problem, Smoother, SmootherConfig, Transfer, sai_build
+    rank, P = dist.get_rank(group), dist.get_world_size(group)
+    prob = Problem.partial(spec, P, rank, sai_halo_hops(spec, cfg.smoother), min_rows_per_rank,
+                           min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+    depth = prob.depth
+    kind = L.SYSTEM_STOKES if prob.n_comp > 1 else L.SYSTEM_SCALAR
+
+    def gpu_sai(lptr, lcol, lval, nH, mask):
+        A = DeviceBsr(ctx, nH, nH, prob.bs, prob.bs, lptr, lcol, lval)
+        B, _ = sai_build(ctx, A, kind, prob.n_velocity, cfg.smoother.level, cfg.smoother.zeta,
+                         cfg.smoother.cache, col_mask=mask)
+        return B.download()
+
+    def gpu_factors(n_own, bs, D):
+        Ad = DeviceBsr(ctx, n_own, n_own, bs, bs, np.arange(n_own + 1, dtype=np.int32),
+                       np.arange(n_own, dtype=np.int32), D)
+        return Smoother(ctx, Ad, SmootherConfig.jacobi(cfg.smoother.omega)).diag_factors()
+
+    levels, transfers = partial_levels(prob, cfg, P, rank, min_rows_per_rank, gpu_sai, gpu_factors)
+    K = prob.injection()
+
+    def coarse_factory(ld_):
+        As = [DeviceBsr(ctx, levels[l]["n"], levels[l]["n"], levels[l]["bs"], levels[l]["bs"], *levels[l]["A"])
+              for l in range(ld_, depth)]
+        Ts = [Transfer(ctx, levels[l]["n"], levels[l + 1]["n"], *transfers[l], prob.dim, prob.bs_scalar,
+                       prob.n_comp, K) for l in range(ld_, depth - 1)]
+        ccfg = MultigridConfig(smoother=cfg.smoother, pre=cfg.pre, post=cfg.post, nu1=cfg.nu1, nu2=cfg.nu2,
+                               bottom_max_elements=cfg.bottom_max_elements, bottom_tol=cfg.bottom_tol, min_depth=1)
+        return Multigrid(ctx, ccfg, levels=As, transfers=Ts, system_kind=kind, dim=prob.dim, n_comp=prob.n_comp,
+                         bs_scalar=prob.bs_scalar)
+
+    offs = []
+    if prob.kernel_constants:
+        offs += [c * prob.bs_scalar for c in range(1 if prob.n_comp == 1 else prob.dim)]
+    if prob.kernel_pressure:
+        offs.append(prob.dim * prob.bs_scalar)
+    dm = DistMultigrid(GpuOps(ctx), dist, cfg, levels, transfers, K, prob.dim, prob.bs_scalar, prob.n_comp, offs,
+                       coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank)
+    dm._problem = prob
     return dm

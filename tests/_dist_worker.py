@@ -65,7 +65,7 @@ class CpuOps:
         return t.numpy()
 
 
-def worker(rank, world, port_no, case, outdir):
+def worker(rank, world, port_no, case, outdir, partial=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_no)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -97,8 +97,25 @@ def worker(rank, world, port_no, case, outdir):
                 x.copy_(torch.as_tensor(tail.v_cycle(0, np.zeros(x.numel()), b.numpy())))
         return Coarse()
 
-    dm = parallel.DistMultigrid(CpuOps(), dist, cfg, levels, transfers, P.K, R.dim, P.bss, P.ncomp, P.koffs,
-                                coarse_factory, min_rows_per_rank=min_rows)
+    if partial:
+        # distributed setup: this rank's rows + halo only, SAI columns solved
+        # by the reference's own build_sai on the rank's partial operator
+        import paper_2412_12506_b200 as g
+        prob = g.Problem.partial(spec, world, rank, parallel.sai_halo_hops(spec, cfg.smoother), min_rows)
+        kind = g.SYSTEM_STOKES if prob.n_comp > 1 else g.SYSTEM_SCALAR
+
+        def ref_build(lptr, lcol, lval, nl, mask):
+            (bp, bc, bv), _ = ref.sai_build(kind, prob.dim, prob.n_comp, prob.bs_scalar, nl, lptr, lcol, lval,
+                                            cfg.smoother.level, cfg.smoother.zeta)
+            return bp, bc, bv
+        plevels, ptransfers = parallel.partial_levels(prob, cfg, world, rank, min_rows, ref_build, None)
+        # the agglomerated tail keeps the reference's full data (identical by construction)
+        dm = parallel.DistMultigrid(CpuOps(), dist, cfg, plevels, ptransfers, prob.injection(), prob.dim,
+                                    prob.bs_scalar, prob.n_comp, P.koffs, coarse_factory,
+                                    min_rows_per_rank=min_rows)
+    else:
+        dm = parallel.DistMultigrid(CpuOps(), dist, cfg, levels, transfers, P.K, R.dim, P.bss, P.ncomp, P.koffs,
+                                    coarse_factory, min_rows_per_rank=min_rows)
     n, bs = levels[0]["n"], levels[0]["bs"]
     rng = np.random.default_rng(5)
     b = rng.uniform(-1, 1, n * bs)

@@ -26,7 +26,10 @@ def dist1():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    yield dist
+        yield dist
+        dist.destroy_process_group()
+    else:
+        yield dist
 
 
 @pytest.mark.parametrize("name,spec,cfg,min_rows", [
@@ -49,3 +52,26 @@ def test_partitioned_path_world1_bitwise(ctx, dist1, name, spec, cfg, min_rows):
         full.cycle(xf, b)
     torch.cuda.synchronize()
     assert np.array_equal(xd.cpu().numpy(), xf.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,spec,cfg,min_rows", [
+    ("sai-2d-dirichlet", K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=2), 16),
+    ("jacobi-2d", K.scalar(16, 2, K.P, degree=3, beta=9.0), K.cfg("jacobi", omega=0.7, nu=2), 16),
+])
+def test_distributed_setup_world1_matches_replicated(ctx, dist1, name, spec, cfg, min_rows):
+    """from_problem_partial (distributed setup path, GPU SAI / GPU factors on
+    the rank's rows) gives the same cycles as the replicated setup."""
+    from paper_2412_12506_b200 import parallel
+    a = parallel.from_problem(ctx, g.Problem(spec, min_depth=cfg.min_depth), cfg, dist1, min_rows_per_rank=min_rows)
+    b = parallel.from_problem_partial(ctx, spec, cfg, dist1, min_rows_per_rank=min_rows)
+    n, bs = a._full.n, a._full.bs
+    rhs = torch.as_tensor(np.random.default_rng(4).uniform(-1, 1, n * bs)).cuda()
+    xa, xb = torch.zeros_like(rhs), torch.zeros_like(rhs)
+    for _ in range(2):
+        a.cycle(xa, rhs)
+        b.cycle(xb, rhs)
+    torch.cuda.synchronize()
+    assert np.array_equal(xa.cpu().numpy(), xb.cpu().numpy())
+    da, ba = a.cycle_costs()
+    db, bb = b.cycle_costs()
+    assert da == db and ba == bb

@@ -22,15 +22,18 @@ def free_port():
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", ["sai-scalar2d-periodic", "sai-scalar2d-dirichlet-p2", "jacobi-scalar2d-periodic",
-                                  "sai-stokes2d-stress", "sai-scalar3d-periodic"])
-def test_partitioned_vcycle_matches_reference(ref, tmp_path, case, world):
+@pytest.mark.parametrize("case,partial", [
+    ("sai-scalar2d-periodic", False), ("sai-scalar2d-dirichlet-p2", False), ("jacobi-scalar2d-periodic", False),
+    ("sai-stokes2d-stress", False), ("sai-scalar3d-periodic", False),
+    # distributed setup (each rank assembles its rows + halo, solves its SAI columns)
+    ("sai-scalar2d-periodic", True), ("sai-scalar2d-dirichlet-p2", True), ("sai-stokes2d-stress", True)])
+def test_partitioned_vcycle_matches_reference(ref, tmp_path, case, partial, world):
     import torch.multiprocessing as mp
     from oracle import port
     from tests import _dist_worker
     from tests import cases as K
 
-    mp.start_processes(_dist_worker.worker, args=(world, free_port(), case, str(tmp_path)), nprocs=world,
+    mp.start_processes(_dist_worker.worker, args=(world, free_port(), case, str(tmp_path), partial), nprocs=world,
                        join=True, start_method="spawn")
     spec, cfg = {
         "sai-scalar2d-periodic": (K.scalar(16, 2, K.P, degree=1), K.cfg("sai", level=1, nu=2)),
