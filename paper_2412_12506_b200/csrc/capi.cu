@@ -820,9 +820,25 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         Mg& m = mg->m;
         ensure_smoothers(ctx, m);
         const int64_t n = int64_t(m.A[0]->brows) * m.bs;
-        DevBuf b(sizeof(double) * std::max<int64_t>(1, n)), x(sizeof(double) * std::max<int64_t>(1, n)),
-            r(sizeof(double) * std::max<int64_t>(1, n));
-        LDGMG_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        // device vectors and a pinned staging buffer cached on the hierarchy:
+        // the same pointers every call keep the captured V-cycle graph valid
+        if (m.solve_b.bytes < sizeof(double) * size_t(std::max<int64_t>(1, n))) {
+            m.solve_b.alloc(sizeof(double) * std::max<int64_t>(1, n));
+            m.solve_x.alloc(sizeof(double) * std::max<int64_t>(1, n));
+            m.solve_r.alloc(sizeof(double) * std::max<int64_t>(1, n));
+            if (m.h_stage) cudaFreeHost(m.h_stage);
+            m.h_stage = nullptr;
+            LDGMG_CUDA(cudaMallocHost(&m.h_stage, sizeof(double) * std::max<int64_t>(1, n)));
+        }
+        DevBuf &b = m.solve_b, &x = m.solve_x, &r = m.solve_r;
+        // pageable -> pinned copies in chunks, each chunk's DMA overlapping the next memcpy
+        constexpr int64_t kChunk = 1 << 17;  // doubles (1 MiB)
+        for (int64_t o = 0; o < n; o += kChunk) {
+            const int64_t c = std::min(kChunk, n - o);
+            std::memcpy(m.h_stage + o, b_host + o, sizeof(double) * c);
+            LDGMG_CUDA(cudaMemcpyAsync(b.as<double>() + o, m.h_stage + o, sizeof(double) * c,
+                                       cudaMemcpyHostToDevice, ctx->stream));
+        }
         LDGMG_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, ctx->stream));
         launch_dot(*ctx, n, b.as<double>(), b.as<double>(), ctx->d_red);
         LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -852,8 +868,25 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
             if (history) history[it] = rr;
         }
         if (iters) *iters = it;
-        LDGMG_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        // device -> pinned in chunks; the host copy of chunk k overlaps the DMA of chunk k+1
+        std::vector<cudaEvent_t> done;
+        for (int64_t o = 0; o < n; o += kChunk) {
+            const int64_t c = std::min(kChunk, n - o);
+            LDGMG_CUDA(cudaMemcpyAsync(m.h_stage + o, x.as<double>() + o, sizeof(double) * c,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+            cudaEvent_t ev;
+            LDGMG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            LDGMG_CUDA(cudaEventRecord(ev, ctx->stream));
+            done.push_back(ev);
+        }
+        int64_t o = 0;
+        for (cudaEvent_t ev : done) {
+            LDGMG_CUDA(cudaEventSynchronize(ev));
+            const int64_t c = std::min(kChunk, n - o);
+            std::memcpy(x_host + o, m.h_stage + o, sizeof(double) * c);
+            o += c;
+            cudaEventDestroy(ev);
+        }
     });
 }
 

@@ -545,6 +545,7 @@ double Mg::bytes_per_cycle() const {
 Mg::~Mg() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (h_red) cudaFreeHost(h_red);
+    if (h_stage) cudaFreeHost(h_stage);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (sai_cache) sai_cache_free(sai_cache);
 }

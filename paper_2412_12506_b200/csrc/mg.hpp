@@ -98,6 +98,9 @@ struct Mg {
     void build_coarse_program(Ctx& ctx);
     void launch_coarse_program(Ctx& ctx);
     SaiCache* sai_cache = nullptr;  // shared across levels (multigrid.hpp:60)
+    // ldgmg_mg_solve_host scratch (cached so the graph of (x, b) is reused)
+    DevBuf solve_b, solve_x, solve_r;
+    double* h_stage = nullptr;  // pinned staging for host <-> device
 
     void init(Ctx& ctx);
     void set_bottom(Ctx& ctx, const double* V, const double* lambda);
