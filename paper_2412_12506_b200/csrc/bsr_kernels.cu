@@ -170,9 +170,12 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     }
     __syncthreads();
 
-    // producer iterator: runs NS items ahead of the consumer
+    // producer iterator: runs NS items ahead of the consumer (row lists and
+    // row pointers are immutable: read before the PDL wait)
     ItemIt pit{0, -1, 0, 0, 0};
     it_load(a, pit, g, ng);
+    pdl_wait();
+    pdl_trigger();
     int kind, idx;
     for (int s = 0; s < NS; ++s) {
         if (!it_next(a, pit, g, ng, kind, idx)) break;
@@ -305,7 +308,7 @@ void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
     }
     if (occ < 1) fail(LDGMG_ERR_CUDA, "rowpass: block does not fit on an SM");
     const int grid = std::max(1, std::min(a.nrows, occ * ctx.num_sms));
-    rowpass_kernel<GT, BS><<<grid, GT, smem, ctx.stream>>>(a);
+    launch_pdl(rowpass_kernel<GT, BS>, dim3(grid), dim3(GT), smem, ctx.stream, a);
     after_launch("rowpass_kernel");
 }
 
@@ -471,6 +474,8 @@ namespace {
 /// Requires rbs, cbs <= 32.
 __global__ void __launch_bounds__(256) rowsplit_kernel(const RowPassArgs a, int maxlen) {
     extern __shared__ __align__(16) double ss[];  // maxlen x 32 partial sums, then u, t
+    pdl_wait();
+    pdl_trigger();
     for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) split_row_task(a, row_at(a, slot), maxlen, ss);
 }
 
@@ -526,7 +531,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         const int grid = std::min(p.nrows, ctx.num_sms * 16);
         static bool once = (max_carveout(rowsplit_kernel), true);
         (void)once;
-        rowsplit_kernel<<<grid, warps * 32, smem, ctx.stream>>>(a, maxlen);
+        launch_pdl(rowsplit_kernel, dim3(grid), dim3(warps * 32), smem, ctx.stream, a, maxlen);
         after_launch("rowsplit_kernel");
         return;
     }

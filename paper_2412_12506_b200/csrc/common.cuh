@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/ldgmg_b200.h"
@@ -43,6 +44,40 @@ inline void after_launch(const char* name) {
 }
 
 inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+/// Programmatic dependent launch (PDL, sm_90+), opt-in with LDGMG_PDL=1:
+/// kernels launched with programmatic stream serialization wait for their
+/// predecessor (griddepcontrol.wait) only before touching mutable memory, so
+/// launch processing and the immutable prologue (barrier init, row pointers,
+/// TMA staging of the injection matrices) overlap the previous kernel.
+/// Measured on the graph-replayed C2 V-cycle: an early launch_dependents
+/// trigger made it 5-10 % SLOWER (dependent CTAs parked on the SMs), the
+/// implicit trigger at grid end is neutral (3.295 vs 3.300 ms), so it is off
+/// by default and the device-side trigger is not issued.
+inline bool pdl_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("LDGMG_PDL");
+        env = e ? std::atoi(e) : 0;
+    }
+    return env != 0;
+}
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
 
 /// Raise a kernel's dynamic shared-memory limit only when `bytes` exceeds
 /// what was already set on this device: cudaFuncSetAttribute on every launch
@@ -134,6 +169,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+/// PDL device side: let the next kernel in the stream launch now / wait for
+/// the previous kernel's completion and memory (no-ops without PDL).
+__device__ __forceinline__ void pdl_trigger() {}  // implicit at grid end (see pdl_enabled)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 /// Named barrier over `nthreads` threads (row groups wider than one warp).
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
     if (nthreads <= 32)

@@ -135,7 +135,8 @@ struct Transfer {
     DevBuf parent, orth, child_ptr, child_list, K;
     std::vector<int> hparent, horth;
 };
-void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc);
+/// `zero_xc` (optional): also zero this coarse vector (the V-cycle's x_{l+1}).
+void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, double* zero_xc = nullptr);
 void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* xf);
 
 struct DenseEig {  // bottom pseudoinverse: V both layouts + lambda + lmax

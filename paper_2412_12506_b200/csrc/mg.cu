@@ -454,8 +454,7 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
     p.y = r[l].as<double>();
     p.nrows = A[l]->brows;
     launch_rowpass(ctx, p);
-    launch_restrict(ctx, *T[l], r[l].as<double>(), bl[l + 1].as<double>());
-    LDGMG_CUDA(cudaMemsetAsync(xl[l + 1].p, 0, sizeof(double) * size_t(A[l + 1]->brows) * bs, ctx.stream));
+    launch_restrict(ctx, *T[l], r[l].as<double>(), bl[l + 1].as<double>(), xl[l + 1].as<double>());
     v_cycle(ctx, l + 1, xl[l + 1].as<double>(), bl[l + 1].as<double>());
     launch_prolong_add(ctx, *T[l], xl[l + 1].as<double>(), x);
     for (int i = 0; i < cfg.nu2; ++i) S.apply(ctx, b, x, cfg.post);

@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restric
                                                             const int* __restrict__ orth,
                                                             const double* __restrict__ K,
                                                             const double* __restrict__ rf, double* __restrict__ rc,
-                                                            int n_coarse, int bss, int ncomp, int nK) {
+                                                            int n_coarse, int bss, int ncomp, int nK,
+                                                            double* __restrict__ zero_xc) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int sch[8][MAXCH], sor[8][MAXCH];
     __shared__ __align__(8) uint64_t bar;
@@ -184,7 +185,9 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restric
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
     double* sK = sm;
     double* src = sm + nK + size_t(warp) * MAXCH * BS;
-    stage_K_bulk(sK, K, nK, &bar);
+    stage_K_bulk(sK, K, nK, &bar);  // immutable: overlaps the previous kernel
+    pdl_wait();
+    pdl_trigger();
     for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
         const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
         int f = 0;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restric
             for (int q = 0; q < MAXCH; ++q)
                 if (q < nch) acc = __dadd_rn(acc, sor[warp][q] < 0 ? src[q * BS + o] : sq[q]);
             rc[size_t(p) * BS + o] = acc;
+            if (zero_xc) zero_xc[size_t(p) * BS + o] = 0.0;  // the coarse iterate starts at 0
         }
         __syncwarp();
     }
@@ -265,12 +269,14 @@ __global__ void __launch_bounds__(256) prolong_warp_kernel(const int* __restrict
     double* sKt = sm;        // [o][j][i]
     double* sK = sm + nK;    // bulk-copied K, [o][i][j]
     double* sx = sm + 2 * size_t(nK) + size_t(warp) * BS;
-    stage_K_bulk(sK, K, nK, &bar);
+    stage_K_bulk(sK, K, nK, &bar);  // immutable: overlaps the previous kernel
     for (int t = threadIdx.x; t < nK; t += blockDim.x) {
         const int o = t / bb, r = t - o * bb, i = r / bss, j = r - i * bss;
         sKt[size_t(o) * bb + size_t(j) * bss + i] = sK[t];
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
     for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
         const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
         int f = 0;
@@ -360,6 +366,8 @@ __global__ void __launch_bounds__(1024) pinv_stream_kernel(const double* __restr
         mbar_init(bars + 1, 1);
         fence_mbar_init();
     }
+    pdl_wait();
+    pdl_trigger();
     for (int i = tid; i < n; i += NT) sb[i] = b[i];
     __syncthreads();
     uint32_t phases = 0u;  // bit s: parity to wait for on bars[s]
@@ -521,6 +529,8 @@ __global__ void __launch_bounds__(256) project_partial_kernel(const double* __re
                                                               const int* __restrict__ offs, double kval,
                                                               double* __restrict__ part) {
     __shared__ double red[8];
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
     const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
     double s = 0.0;
@@ -539,6 +549,8 @@ __global__ void __launch_bounds__(256) project_apply_kernel(double* __restrict__
                                                             const double* __restrict__ part) {
     __shared__ double red[8];
     __shared__ double md;
+    pdl_wait();
+    pdl_trigger();
     const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
     double s = part[c * kProjParts + threadIdx.x];
     for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
@@ -608,20 +620,25 @@ namespace {
 int transfer_nK(const Transfer& T) { return (1 << T.dim) * T.bss * T.bss; }
 }  // namespace
 
-void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc) {
+void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, double* zero_xc) {
     const int64_t total = int64_t(T.n_coarse) * T.bs;
     if (!total) return;
     const int nK = transfer_nK(T);
     const size_t smem_w = sizeof(double) * (size_t(nK) + size_t(8) * 8 * T.bs);
-    if (T.max_children <= 8 && smem_w <= 200 * 1024) {
+    const bool warp_ok = T.max_children <= 8 && smem_w <= 200 * 1024;
+    if (zero_xc && !warp_ok) {  // the fallback kernels do not zero
+        LDGMG_CUDA(cudaMemsetAsync(zero_xc, 0, sizeof(double) * size_t(total), ctx.stream));
+        zero_xc = nullptr;
+    }
+    if (warp_ok) {
         if (smem_w > 48 * 1024)
             ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(restrict_warp_kernel<8>), true);
         (void)once;
-        restrict_warp_kernel<8><<<grid, 256, smem_w, ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(),
-                                                                   T.orth.as<int>(), T.K.as<double>(), rf, rc,
-                                                                   T.n_coarse, T.bss, T.ncomp, nK);
+        launch_pdl(restrict_warp_kernel<8>, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
+                   T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse, T.bss, T.ncomp,
+                   nK, zero_xc);
         after_launch("restrict_warp_kernel");
         return;
     }
@@ -651,9 +668,9 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(prolong_warp_kernel), true);
         (void)once;
-        prolong_warp_kernel<<<grid, 256, smem_w, ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(),
-                                                               T.orth.as<int>(), T.K.as<double>(), xc, xf,
-                                                               T.n_coarse, T.bss, T.ncomp, nK);
+        launch_pdl(prolong_warp_kernel, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
+                   T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), xc, xf, T.n_coarse, T.bss, T.ncomp,
+                   nK);
         after_launch("prolong_warp_kernel");
         return;
     }
@@ -684,8 +701,8 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
             ensure_dyn_smem(pinv_stream_kernel, size_t(smem));
             static bool once = (max_carveout(pinv_stream_kernel), true);
             (void)once;
-            pinv_stream_kernel<<<1, 1024, smem, ctx.stream>>>(E.Vr.as<double>(), E.Vc.as<double>(),
-                                                              E.lambda.as<double>(), b, x, n, cut, KC);
+            launch_pdl(pinv_stream_kernel, dim3(1), dim3(1024), smem, ctx.stream, E.Vr.as<double>(),
+                       E.Vc.as<double>(), E.lambda.as<double>(), b, x, n, cut, KC);
             after_launch("pinv_stream_kernel");
             return;
         }
@@ -710,11 +727,11 @@ void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* com
     } else if (scratch && N >= kProjParts) {
         static bool once = (max_carveout(project_partial_kernel), max_carveout(project_apply_kernel), true);
         (void)once;
-        project_partial_kernel<<<dim3(kProjParts, ncomp), 256, 0, ctx.stream>>>(v, N, bs, comp_offsets, kval,
-                                                                               scratch);
+        launch_pdl(project_partial_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream,
+                   static_cast<const double*>(v), N, bs, comp_offsets, kval, scratch);
         after_launch("project_partial_kernel");
-        project_apply_kernel<<<dim3(kProjParts, ncomp), 256, 0, ctx.stream>>>(v, N, bs, comp_offsets, kval,
-                                                                             scratch);
+        launch_pdl(project_apply_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream, v, N, bs, comp_offsets,
+                   kval, static_cast<const double*>(scratch));
         after_launch("project_apply_kernel");
     } else {
         project_fast_kernel<<<ncomp, 1024, 0, ctx.stream>>>(v, N, bs, comp_offsets, ncomp, kval);
