@@ -479,6 +479,22 @@ __global__ void __launch_bounds__(256) rowsplit_kernel(const RowPassArgs a, int 
     for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) split_row_task(a, row_at(a, slot), maxlen, ss);
 }
 
+/// rowsplit_kernel with TMA-staged rows (split_row_task_tma).
+__global__ void __launch_bounds__(256) rowsplit_tma_kernel(const RowPassArgs a, int maxlen) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    uint32_t phase = 0;
+    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x)
+        split_row_task_tma(a, row_at(a, slot), maxlen, sm, &bar, phase);
+}
+
 int split_threshold_rows(const Ctx& ctx) {
     static int env = -2;
     if (env == -2) {
@@ -525,6 +541,23 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         }
         const int maxlen = std::max(1, A.max_row);
         const int warps = std::min(8, maxlen);
+        static int tma_env = -1;
+        if (tma_env < 0) {
+            const char* e = getenv("LDGMG_SPLIT_TMA");
+            tma_env = e ? atoi(e) : 1;
+        }
+        const size_t smem_tma =
+            sizeof(double) * split_row_tma_doubles(maxlen, A.blk_stride, p.mode == MODE_RELAX ? p.F->vstride : 0, A.cbs);
+        if (tma_env && smem_tma <= 120 * 1024) {
+            ensure_dyn_smem(rowsplit_tma_kernel, smem_tma);
+            const int grid = std::min(p.nrows, ctx.num_sms * 16);
+            static bool once = (max_carveout(rowsplit_tma_kernel), true);
+            (void)once;
+            const int threads = std::max(warps * 32, std::min(256, ((maxlen * A.cbs + 31) / 32) * 32));
+            launch_pdl(rowsplit_tma_kernel, dim3(grid), dim3(threads), smem_tma, ctx.stream, a, maxlen);
+            after_launch("rowsplit_tma_kernel");
+            return;
+        }
         const size_t smem = sizeof(double) * (size_t(maxlen) * 32 + 64);
         if (smem > 48 * 1024)
             ensure_dyn_smem(rowsplit_kernel, size_t(smem));

@@ -116,6 +116,120 @@ __device__ __forceinline__ void split_row_task(const RowPassArgs& a, int row, in
     __syncthreads();
 }
 
+/// split_row_task with the row's operands staged in shared memory first:
+/// the row's blocks (contiguous in CSR order) and, for relax, the element's
+/// factor V arrive by TMA bulk copies on `bar`, while the threads gather the
+/// x-blocks and the epilogue operands with all loads in flight at once.  A
+/// row then costs ~3 dependent memory round trips (row pointers -> column
+/// ids -> x) instead of one per 9-step chunk of every block product; the
+/// arithmetic (and so the bits) is split_row_task's.
+/// smem layout (doubles): blocks maxlen*blk_stride | V vstride | x maxlen*xs |
+/// partial sums maxlen*32 | u 32 | t 32 | epilogue 4*32.  All threads call it.
+__device__ __forceinline__ void split_row_task_tma(const RowPassArgs& a, int row, int maxlen, double* sm,
+                                                   uint64_t* bar, uint32_t& phase) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
+    const bool relax = a.mode == MODE_RELAX;
+    const int xs = (a.cbs + 1) & ~1;
+    double* sB = sm;
+    double* sV = sB + size_t(maxlen) * a.blk_stride;
+    double* sX = sV + (relax ? a.vstride : 0);
+    double* ss = sX + size_t(maxlen) * xs;
+    double* ubuf = ss + size_t(maxlen) * 32;
+    double* tbuf = ubuf + 32;
+    double* ep = tbuf + 32;  // b, xe, scal, lam
+    const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1), nk = k1 - k0;
+    if (tid == 0) {
+        fence_proxy_async();  // the previous row's generic reads of sB/sV precede these async writes
+        const uint32_t bb = uint32_t(nk) * uint32_t(a.blk_stride) * 8u;
+        const uint32_t vb = relax ? uint32_t(a.vstride) * 8u : 0u;
+        mbar_arrive_expect_tx(bar, bb + vb);
+        if (bb) bulk_g2s(sB, a.val + size_t(k0) * a.blk_stride, bb, bar);
+        if (vb) bulk_g2s(sV, a.V + size_t(row) * a.vstride, vb, bar);
+    }
+    // x-blocks: thread t -> (block q, entry c), every load issued before use
+    for (int t = tid; t < nk * a.cbs; t += blockDim.x) {
+        const int q = t / a.cbs, c = t - q * a.cbs;
+        const int j = __ldg(a.col + k0 + q);
+        sX[size_t(q) * xs + c] = x_source(a, row, j)[size_t(j) * a.cbs + c];
+    }
+    if (tid < a.rbs) {
+        const size_t o = size_t(row) * a.rbs + tid;
+        if (a.mode == MODE_RESIDUAL || relax) ep[tid] = __ldg(a.b + o);
+        if (relax || a.mode == MODE_ADD) ep[32 + tid] = a.xe[o];
+        if (relax) {
+            ep[64 + tid] = __ldg(a.scal + o);
+            ep[96 + tid] = __ldg(a.lam + o);
+        }
+    }
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    for (int q = warp; q < nk; q += W) {
+        if (relax && __ldg(a.col + k0 + q) == row) continue;
+        if (lane < a.rbs) {
+            const double* Bc = sB + size_t(q) * a.blk_stride + lane;
+            const double* xq = sX + size_t(q) * xs;
+            double s = 0.0;
+#pragma unroll 9
+            for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, Bc[size_t(c) * a.rbs], xq[c]);
+            ss[size_t(q) * 32 + lane] = s;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const bool act = lane < a.rbs;
+        const size_t o = size_t(row) * a.rbs + lane;
+        double acc = 0.0;
+        if (act) {
+            if (relax) {
+                acc = ep[lane];
+                for (int q = 0; q < nk; ++q)
+                    if (__ldg(a.col + k0 + q) != row) acc = __dsub_rn(acc, ss[size_t(q) * 32 + lane]);
+            } else {
+                for (int q = 0; q < nk; ++q) acc = __dadd_rn(acc, ss[size_t(q) * 32 + lane]);
+            }
+        }
+        if (relax) {
+            const int bs = a.rbs, ld = a.ld;
+            const double sc = act ? ep[64 + lane] : 0.0;
+            const double lam = act ? ep[96 + lane] : 0.0;
+            const double xe = act ? ep[32 + lane] : 0.0;
+            if (act) ubuf[lane] = __dmul_rn(sc, acc);
+            __syncwarp();
+            if (act) {
+                double tt = 0.0;
+                const double* Vcol = sV + size_t(lane) * ld;
+                for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, Vcol[kk], ubuf[kk]);
+                const double cut = a.kernel_tol * __ldg(a.lmax + row);
+                tbuf[lane] = fabs(lam) <= cut ? 0.0 : tt / lam;
+            }
+            __syncwarp();
+            if (act) {
+                double w = 0.0;
+                for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, sV[size_t(kk) * ld + lane], tbuf[kk]);
+                const double yv = __dmul_rn(sc, w);
+                acc = __dadd_rn(__dmul_rn(1.0 - a.omega, xe), __dmul_rn(a.omega, yv));
+            }
+        }
+        if (act) {
+            double out;
+            switch (a.mode) {
+                case MODE_RESIDUAL: out = __dsub_rn(ep[lane], acc); break;
+                case MODE_ADD: out = __dadd_rn(ep[32 + lane], acc); break;
+                default: out = acc; break;
+            }
+            a.y[o] = out;
+        }
+    }
+    __syncthreads();
+}
+
+/// shared-memory doubles split_row_task_tma needs
+__host__ __device__ inline size_t split_row_tma_doubles(int maxlen, int blk_stride, int vstride, int cbs) {
+    return size_t(maxlen) * blk_stride + size_t(vstride) + size_t(maxlen) * ((cbs + 1) & ~1) + size_t(maxlen) * 32 +
+           64 + 128;
+}
+
 /// Restriction of coarse element p (multigrid.hpp:127-149 order); `sh` holds
 /// the children's blocks (<= 64 children x BS).  All CTA threads call it.
 __device__ __forceinline__ void restrict_parent_task(const int* __restrict__ child_ptr, const int* __restrict__ child,
