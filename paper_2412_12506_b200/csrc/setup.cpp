@@ -9,6 +9,9 @@
 #include "setup.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <stdexcept>
@@ -255,6 +258,25 @@ struct Ctx {
     double penalty_tau(const Face& f) const {
         const double m = f.right >= 0 ? std::min(mu[f.left], mu[f.right]) : mu[f.left];
         return beta * m / f.size;
+    }
+};
+
+/// LDGMG_SETUP_TIMING=1: wall time of the assembly phases on stderr.
+struct PhaseTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    const char* what;
+    explicit PhaseTimer(const char* w) : what(w) {
+        const char* e = std::getenv("LDGMG_SETUP_TIMING");
+        on = e && std::atoi(e);
+        t = std::chrono::steady_clock::now();
+    }
+    void stamp(const char* phase) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[assembly %s] %-18s %8.3f s\n", what, phase,
+                     std::chrono::duration<double>(now - t).count());
+        t = now;
     }
 };
 
@@ -540,10 +562,13 @@ bool has_kind(const LevelMesh& m, int bc_kind) {
 /// assemble_scalar (ldg_scalar.hpp:83-125), operator part
 void assemble_scalar(const Ctx& c, HostCsr& A) {
     const int N = c.mesh->n_elements(), bs = c.bs;
+    PhaseTimer tm("scalar");
     std::array<Rows, 3> G;
     gradient_rows(c, G);
+    tm.stamp("gradient rows");
     Rows E;
     penalty_rows(c, false, 0.0, 0.0, E);
+    tm.stamp("penalty rows");
     std::vector<double> dmu(N);
     for (int e = 0; e < N; ++e) dmu[e] = c.mu[e] * c.msc[e];
     std::array<std::vector<std::vector<std::pair<int, int>>>, 3> src;
@@ -560,7 +585,9 @@ void assemble_scalar(const Ctx& c, HostCsr& A) {
             out.freeze_row(e, row);
         }
     });
+    tm.stamp("G^T D G + E");
     rows_to_csr(out, N, A);
+    tm.stamp("csr");
 }
 
 /// assemble_stokes (ldg_stokes.hpp:102-192), operator part
@@ -568,11 +595,14 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
     const int N = c.mesh->n_elements(), bsv = c.bs, dim = c.dim;
     const int BS = (dim + 1) * bsv;
     const bool unsteady = delta > 0;
+    PhaseTimer tm("stokes");
     std::array<Rows, 3> G;
     gradient_rows(c, G);
+    tm.stamp("gradient rows");
     Rows Ev, Ep;
     penalty_rows(c, false, 0.0, 0.0, Ev);
     penalty_rows(c, true, beta_p, delta, Ep);
+    tm.stamp("penalty rows");
     std::vector<double> dmu(N);
     for (int e = 0; e < N; ++e) dmu[e] = c.mu[e] * c.msc[e];
     std::array<std::vector<std::vector<std::pair<int, int>>>, 3> src;
@@ -602,6 +632,7 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
                     }
         }
     });
+    tm.stamp("G^T D G (+cross)");
     // Scatter into the saddle layout, per destination row, in the
     // reference's global insertion order (ldg_stokes.hpp:149-191).
     // Pressure-velocity blocks come from G_i columns: (cc, r) gets -(G_i^T)msc_r.
@@ -653,7 +684,9 @@ void assemble_stokes(const Ctx& c, double gamma, double beta_p, double delta, Ho
             out.freeze_row(r0, row);
         }
     });
+    tm.stamp("saddle scatter");
     rows_to_csr(out, N, A);
+    tm.stamp("csr");
 }
 
 }  // namespace

@@ -9,16 +9,40 @@
 #pragma once
 
 #include <array>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "../../include/ldgmg_b200.h"
 
 namespace ldgmg_b200 {
 
+/// std::allocator that default-initialises (no zero fill on resize): the
+/// operator values are written exactly once by the (threaded) assembly, so
+/// zeroing gigabytes first only costs a serial memset and the page faults.
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = DefaultInitAlloc<U>;
+    };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+
 struct HostCsr {
     int brows = 0, bs = 0;
     std::vector<int> ptr, col;
-    std::vector<double> val;
+    std::vector<double, DefaultInitAlloc<double>> val;
 };
 
 struct ProblemLevel {
