@@ -9,7 +9,11 @@
 #pragma once
 
 #include <array>
+#include <sys/mman.h>
+
+#include <cstdlib>
 #include <memory>
+#include <new>
 #include <utility>
 #include <vector>
 
@@ -36,6 +40,23 @@ struct DefaultInitAlloc : std::allocator<T> {
     template <class U, class... Args>
     void construct(U* p, Args&&... args) {
         ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+    /// large arrays: 2 MiB-aligned and advised for transparent huge pages
+    /// (first-touch faults of multi-GB operators dominate the CSR fill)
+    T* allocate(size_t n) {
+        const size_t bytes = n * sizeof(T);
+        if (bytes < (size_t(64) << 20)) return std::allocator<T>::allocate(n);
+        const size_t huge = size_t(2) << 20;
+        void* p = std::aligned_alloc(huge, (bytes + huge - 1) / huge * huge);
+        if (!p) throw std::bad_alloc();
+        madvise(p, (bytes + huge - 1) / huge * huge, MADV_HUGEPAGE);
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t n) {
+        if (n * sizeof(T) < (size_t(64) << 20))
+            std::allocator<T>::deallocate(p, n);
+        else
+            std::free(p);
     }
 };
 
