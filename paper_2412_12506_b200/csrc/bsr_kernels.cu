@@ -23,10 +23,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
 #include "core.hpp"
+#include "host_eig.hpp"
 #include "row_ops.cuh"
 
 namespace ldgmg_b200 {
@@ -359,6 +362,62 @@ int grid_for(int64_t n, int threads, const Ctx& ctx) {
 
 }  // namespace
 
+void h2d_staged(Ctx& ctx, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    constexpr size_t kSlot = size_t(64) << 20;
+    if (bytes < (size_t(8) << 20)) {
+        h2d(ctx, dst, src, bytes);
+        return;
+    }
+    if (!ctx.pin[0]) {
+        for (int i = 0; i < 2; ++i) {
+            LDGMG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx.pin[i]), kSlot));
+            LDGMG_CUDA(cudaEventCreateWithFlags(&ctx.pin_ev[i], cudaEventDisableTiming));
+            LDGMG_CUDA(cudaEventRecord(ctx.pin_ev[i], ctx.stream));
+        }
+        ctx.pin_bytes = kSlot;
+    }
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    static const bool timing = getenv("LDGMG_SETUP_TIMING") && atoi(getenv("LDGMG_SETUP_TIMING"));
+    const auto t0 = std::chrono::steady_clock::now();
+    double t_copy = 0.0, t_wait = 0.0;
+    int slot = 0;
+    for (size_t off = 0; off < bytes; off += kSlot, slot ^= 1) {
+        const size_t n = std::min(kSlot, bytes - off);
+        auto ta = std::chrono::steady_clock::now();
+        LDGMG_CUDA(cudaEventSynchronize(ctx.pin_ev[slot]));  // the slot's previous DMA is done
+        auto tb = std::chrono::steady_clock::now();
+        unsigned char* buf = ctx.pin[slot];
+        const int parts = 8;
+        parallel_for(parts, [&](int lo, int hi) {
+            for (int q = lo; q < hi; ++q) {
+                const size_t a = n * q / parts, b = n * (q + 1) / parts;
+                std::memcpy(buf + a, s + off + a, b - a);
+            }
+        });
+        auto tc = std::chrono::steady_clock::now();
+        t_wait += std::chrono::duration<double>(tb - ta).count();
+        t_copy += std::chrono::duration<double>(tc - tb).count();
+        LDGMG_CUDA(cudaMemcpyAsync(d + off, buf, n, cudaMemcpyHostToDevice, ctx.stream));
+        LDGMG_CUDA(cudaEventRecord(ctx.pin_ev[slot], ctx.stream));
+    }
+    LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (timing)
+        fprintf(stderr, "[h2d_staged] %.1f MB in %.3f s (memcpy %.3f s, dma waits %.3f s)\n", bytes / 1e6,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), t_copy, t_wait);
+}
+
+void ctx_release_staging(Ctx& ctx) {
+    for (int i = 0; i < 2; ++i) {
+        if (ctx.pin[i]) cudaFreeHost(ctx.pin[i]);
+        if (ctx.pin_ev[i]) cudaEventDestroy(ctx.pin_ev[i]);
+        ctx.pin[i] = nullptr;
+        ctx.pin_ev[i] = nullptr;
+    }
+    ctx.pin_bytes = 0;
+}
+
 std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs, const int* ptr,
                                 const int* col, const double* val, bool require_sorted) {
     require(brows >= 0 && bcols >= 0 && rbs > 0 && cbs > 0, "bsr_upload: bad shape");
@@ -395,8 +454,7 @@ std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs
         DevBuf tmp(sizeof(double) * std::min(A->nnzb, chunk_blocks) * per_blk);
         for (int64_t k0 = 0; k0 < A->nnzb; k0 += chunk_blocks) {
             const int64_t nb = std::min(chunk_blocks, A->nnzb - k0);
-            LDGMG_CUDA(cudaMemcpyAsync(tmp.p, val + k0 * per_blk, sizeof(double) * nb * per_blk,
-                                       cudaMemcpyHostToDevice, ctx.stream));
+            h2d_staged(ctx, tmp.p, val + k0 * per_blk, sizeof(double) * nb * per_blk);
             upload_permute_kernel<<<grid_for(nb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
                 tmp.as<double>(), A->val.as<double>() + k0 * A->blk_stride, nb, rbs, cbs,
                 A->blk_stride);

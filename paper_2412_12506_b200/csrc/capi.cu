@@ -120,6 +120,7 @@ int ldgmg_ctx_destroy(ldgmg_ctx* ctx) {
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         cudaFree(ctx->d_red);
         cudaFreeHost(ctx->h_red);
+        ctx_release_staging(*ctx);
         delete ctx;
     });
 }

@@ -27,7 +27,18 @@ struct Ctx {
     // scratch for reductions (device) + pinned host slot
     double* d_red = nullptr;
     double* h_red = nullptr;
+    // pinned double buffer for large host->device uploads (h2d_staged)
+    unsigned char* pin[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    size_t pin_bytes = 0;
 };
+
+/// Large pageable host -> device copy: threaded memcpy into a pinned double
+/// buffer, each slot's DMA overlapping the fill of the other (pageable
+/// cudaMemcpy runs at ~2 GB/s on the box; this reaches the PCIe rate).
+/// Returns after the copy completed.
+void h2d_staged(Ctx& ctx, void* dst, const void* src, size_t bytes);
+void ctx_release_staging(Ctx& ctx);
 
 /// Host<->device copies ordered on the context stream (setup paths; the
 /// legacy-stream cudaMemcpy would race with the non-blocking context stream).
