@@ -134,6 +134,9 @@ class GpuOps:
     def spmv_add(self, B, r_ext, x_own):
         check(lib.ldgmg_spmv_add(self.ctx.h, B.h, r_ext.data_ptr(), x_own.data_ptr()))
 
+    def spmv(self, A, x_ext, y):
+        check(lib.ldgmg_spmv(self.ctx.h, A.h, x_ext.data_ptr(), y.data_ptr()))
+
     def relax(self, A, F, b, x_src, x_live, x_out, omega):
         check(lib.ldgmg_relax(self.ctx.h, A.h, F.h, b.data_ptr(), x_src.data_ptr(), x_live.data_ptr(),
                               x_out.data_ptr(), float(omega)))
@@ -350,6 +353,21 @@ class DistMultigrid:
             dsum = float(np.add.accumulate(np.concatenate([[0.0], prods]))[-1])
             v_own[off::bs][:n_own] += (-dsum) * kval
 
+    def apply(self, b_own, x_own):
+        """Multigrid::apply on the owned slices (multigrid.hpp:90-101): the
+        V-cycle from zero on the projected right-hand side, then project."""
+        d, bs = self.L[0], self.bs
+        n_own = d["plan"].n_own
+        if self.koffs:
+            bp = b_own.clone()
+            self.project(bp)
+        else:
+            bp = b_own
+        d["x"].zero_()
+        self._vcycle(0, bp)
+        x_own.copy_(d["x"][:n_own * bs])
+        self.project(x_own)
+
     def cycle(self, x_own, b_own):
         """Multigrid::cycle on the owned slices (multigrid.hpp:82-85)."""
         d, bs = self.L[0], self.bs
@@ -384,6 +402,10 @@ class DistMultigrid:
             dof += td
             byts += tb
         return dof, byts
+
+    def symmetric(self):
+        """symmetric_plan (multigrid.hpp:41-43)"""
+        return self.cfg.smoother.kind == L.JACOBI or self.cfg.pre != self.cfg.post
 
     def owned_range(self, level=0):
         p = self.L[level]["plan"]
@@ -579,3 +601,220 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64)
                        coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank)
     dm._problem = prob
     return dm
+
+
+
+# ------------------------------------------------------ distributed Krylov
+_libm = C.CDLL("libm.so.6")
+_libm.hypot.restype = C.c_double
+_libm.hypot.argtypes = [C.c_double, C.c_double]
+
+
+def fit_rate(residuals):
+    """fit_rate (krylov.hpp:54-95) restated: (rho, eta, classification,
+    low_confidence) from a residual history (same libm log/exp)."""
+    import math
+    r = list(residuals)
+    if not r or r[0] <= 0.0:
+        return 0.0, 0.0, 0, True
+    floor = 1e-13 * r[0]
+    K = 0
+    while K + 1 < len(r) and r[K + 1] > floor:
+        K += 1
+    low = True
+    if K >= 2:
+        sx = sy = sxx = sxy = 0.0
+        for k in range(1, K + 1):
+            x, y = float(k), math.log(r[k])
+            sx += x
+            sy += y
+            sxx += x * x
+            sxy += x * y
+        slope = (K * sxy - sx * sy) / (K * sxx - sx * sx)
+        low = K < 3
+    elif len(r) >= 2:
+        slope = math.log(max(r[1], 1e-300)) - math.log(r[0])
+    else:
+        return 0.0, 0.0, 0, True
+    rho = math.exp(slope)
+    if rho >= 1.0:
+        return rho, float("inf"), 2, low
+    eta = math.log(0.1) / math.log(rho)
+    return rho, eta, (0 if eta < 2.0 else 1 if eta < 10.0 else 2), low
+
+
+class DistKrylov:
+    """pcg / gmres_left / estimate_eta (krylov.hpp:117-306) over the ranks of
+    a DistMultigrid: vectors are the owned slices, the operator is the level-0
+    spmv after a ghost exchange, the preconditioner DistMultigrid.apply.
+    Dot products gather the per-entry products and sum them in the global
+    entry order on every rank (the reference's sequential dot, blockla.hpp:60-63),
+    so every scalar -- and the whole residual history -- is independent of the
+    rank count and bit-identical to the single-process reference."""
+
+    def __init__(self, dm):
+        self.dm = dm
+        self.ops, self.bs = dm.ops, dm.bs
+        d = dm.L[0]
+        self.n_own = d["plan"].n_own * self.bs
+        N0, P = dm.N0, dm.P
+        self.sizes = [((q + 1) * N0 // P - q * N0 // P) * self.bs for q in range(P)]
+
+    def dot(self, a, b):
+        parts = self.dm._allgather((a * b).contiguous(), self.sizes)
+        prods = np.concatenate([[0.0]] + [self.ops.to_host(p) for p in parts])
+        return float(np.add.accumulate(prods)[-1])
+
+    def norm2(self, a):
+        return float(np.sqrt(self.dot(a, a)))
+
+    def spmv(self, x_own, y_own):
+        d = self.dm.L[0]
+        x_ext = d["x"]
+        x_ext[:self.n_own] = x_own
+        d["xA"](x_ext)
+        self.ops.spmv(d["A"], x_ext, y_own)
+
+    def apply(self, b_own):
+        x = self.ops.tensor(self.n_own)
+        self.dm.apply(b_own, x)
+        return x
+
+    @staticmethod
+    def _axpy(alpha, x, y):  # y += alpha * x, two roundings (no FMA)
+        y.add_(x * alpha)
+
+    def pcg(self, b_own, tol=1e-12, maxit=60):
+        if not self.dm.symmetric():
+            raise L.InvalidArgument("pcg: preconditioner plan is not symmetric")
+        res, it, conv, brk = [], 0, False, False
+        x = self.ops.tensor(self.n_own)
+        r = b_own.clone()
+        z = self.apply(r)
+        rz = self.dot(r, z)
+        r0 = float(np.sqrt(max(rz, 0.0)))
+        res.append(r0)
+        if r0 == 0.0:
+            return x, self._report(res, 0, True, False)
+        p = z.clone()
+        Ap = self.ops.tensor(self.n_own)
+        for k in range(1, maxit + 1):
+            self.spmv(p, Ap)
+            pAp = self.dot(p, Ap)
+            if pAp <= 0.0:
+                brk = True
+                break
+            alpha = rz / pAp
+            self._axpy(alpha, p, x)
+            self._axpy(-alpha, Ap, r)
+            z = self.apply(r)
+            rz_new = self.dot(r, z)
+            rk = float(np.sqrt(max(rz_new, 0.0)))
+            res.append(rk)
+            it = k
+            if rz_new < 0.0:
+                brk = True
+                break
+            if rk <= tol * r0:
+                conv = True
+                break
+            beta = rz_new / rz
+            rz = rz_new
+            p.mul_(beta).add_(z)
+        return x, self._report(res, it, conv, brk)
+
+    def gmres(self, b_own, tol=1e-12, maxit=60):
+        res, conv, brk = [], False, False
+        x = self.ops.tensor(self.n_own)
+        r0 = self.apply(b_own)
+        g0 = self.norm2(r0)
+        res.append(g0)
+        if g0 == 0.0:
+            return x, self._report(res, 0, True, False)
+        r0.mul_(1.0 / g0)
+        basis = [r0]
+        H = np.zeros((maxit + 1, maxit))
+        gamma = np.zeros(maxit + 1)
+        cs, sn = np.zeros(maxit), np.zeros(maxit)
+        gamma[0] = g0
+        m = 0
+        Av = self.ops.tensor(self.n_own)
+        for j in range(maxit):
+            self.spmv(basis[j], Av)
+            w = self.apply(Av)
+            pre_norm = self.norm2(w)
+            for i in range(j + 1):
+                h = self.dot(w, basis[i])
+                H[i, j] = h
+                self._axpy(-h, basis[i], w)
+            hn = self.norm2(w)
+            H[j + 1, j] = hn
+            happy = hn <= 1e-14 * pre_norm
+            if not happy:
+                w.mul_(1.0 / hn)
+                basis.append(w)
+            for i in range(j):
+                t = float(cs[i]) * float(H[i, j]) + float(sn[i]) * float(H[i + 1, j])
+                H[i + 1, j] = -float(sn[i]) * float(H[i, j]) + float(cs[i]) * float(H[i + 1, j])
+                H[i, j] = t
+            d = _libm.hypot(float(H[j, j]), float(H[j + 1, j]))
+            if d == 0.0:
+                cs[j], sn[j] = 1.0, 0.0
+            else:
+                cs[j], sn[j] = float(H[j, j]) / d, float(H[j + 1, j]) / d
+            H[j, j] = d
+            H[j + 1, j] = 0.0
+            gamma[j + 1] = -float(sn[j]) * float(gamma[j])
+            gamma[j] = float(cs[j]) * float(gamma[j])
+            m = j + 1
+            rk = abs(float(gamma[j + 1]))
+            res.append(rk)
+            if happy:
+                brk = conv = True
+                break
+            if rk <= tol * g0:
+                conv = True
+                break
+        y = np.zeros(m)
+        for i in range(m - 1, -1, -1):
+            s_ = float(gamma[i])
+            for k in range(i + 1, m):
+                s_ -= float(H[i, k]) * float(y[k])
+            y[i] = s_ / float(H[i, i]) if H[i, i] != 0.0 else 0.0
+        for i in range(m):
+            self._axpy(float(y[i]), basis[i], x)
+        return x, self._report(res, m, conv, brk)
+
+    @staticmethod
+    def _report(res, iters, conv, brk):
+        rho, eta, cls, low = fit_rate(res)
+        return {"residuals": np.array(res), "iterations": iters, "converged": conv, "breakdown": brk, "rho": rho,
+                "eta": eta, "classification": ["fast", "slow", "nonconvergent"][cls], "low_confidence": low}
+
+    def estimate_eta(self, kind=L.KRYLOV_GMRES, seed=0, tol=1e-12, maxit=60):
+        """estimate_eta (krylov.hpp:293-306): the seeded random rhs (generated
+        in full on every rank), the kernel projected out in the reference's
+        order, zero guess, then CG or GMRES on the ranks."""
+        from .api import random_rhs
+        N0, bs = self.dm.N0, self.bs
+        b = random_rhs(N0, bs, seed)
+        offs = self.dm.koffs
+        if offs:
+            kv = 1.0 / np.sqrt(float(N0))
+            s_ = float(np.add.accumulate(np.full(N0 + 1, kv * kv) * np.r_[0.0, np.ones(N0)])[-1])
+            nrm = float(np.sqrt(s_))
+            if nrm > 1e-10:
+                kv = kv * (1.0 / nrm)
+            for off in offs:
+                kvec = np.zeros(N0 * bs)
+                kvec[off::bs] = kv
+                dd = float(np.add.accumulate(np.r_[0.0, b * kvec])[-1])
+                b = b + (-dd) * kvec
+        r0_, r1_ = self.dm.owned_range()
+        b_own = self.ops.upload(b[r0_ * bs:r1_ * bs]) if hasattr(self.ops, "upload") else \
+            self.ops.torch.as_tensor(b[r0_ * bs:r1_ * bs].copy())
+        if kind == L.KRYLOV_CG:
+            _, rep = self.pcg(b_own, tol, maxit)
+        else:
+            _, rep = self.gmres(b_own, tol, maxit)
+        return rep

@@ -39,6 +39,13 @@ class CpuOps:
         ptr, col, val, _, _, bs = A
         r.copy_(self.torch.as_tensor(b.numpy() - self.port.spmv(ptr, col, val, bs, bs, x_ext.numpy())))
 
+    def upload(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, np.float64).copy())
+
+    def spmv(self, A, x_ext, y):
+        ptr, col, val, _, _, bs = A
+        y.copy_(self.torch.as_tensor(self.port.spmv(ptr, col, val, bs, bs, x_ext.numpy())))
+
     def spmv_add(self, B, r_ext, x_own):
         ptr, col, val, _, _, bs = B
         x_own.copy_(self.torch.as_tensor(x_own.numpy() + self.port.spmv(ptr, col, val, bs, bs, r_ext.numpy())))
@@ -65,7 +72,7 @@ class CpuOps:
         return t.numpy()
 
 
-def worker(rank, world, port_no, case, outdir, partial=False):
+def worker(rank, world, port_no, case, outdir, partial=False, krylov=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port_no)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -116,6 +123,13 @@ def worker(rank, world, port_no, case, outdir, partial=False):
     else:
         dm = parallel.DistMultigrid(CpuOps(), dist, cfg, levels, transfers, P.K, R.dim, P.bss, P.ncomp, P.koffs,
                                     coarse_factory, min_rows_per_rank=min_rows)
+    if krylov is not None:
+        rep = parallel.DistKrylov(dm).estimate_eta(kind=krylov, seed=3, tol=1e-12, maxit=30)
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), residuals=rep["residuals"], iterations=rep["iterations"],
+                 rho=rep["rho"], eta=rep["eta"], converged=rep["converged"])
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     n, bs = levels[0]["n"], levels[0]["bs"]
     rng = np.random.default_rng(5)
     b = rng.uniform(-1, 1, n * bs)

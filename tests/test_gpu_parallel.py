@@ -75,3 +75,18 @@ def test_distributed_setup_world1_matches_replicated(ctx, dist1, name, spec, cfg
     da, ba = a.cycle_costs()
     db, bb = b.cycle_costs()
     assert da == db and ba == bb
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_distributed_krylov_world1_matches_single_gpu_strict(ctx, dist1, kind):
+    """DistKrylov (P-independent dots) on one rank = the single-GPU strict
+    Krylov (both are the reference's sequential order)."""
+    from paper_2412_12506_b200 import parallel
+    spec, cfg = K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=2)
+    dm = parallel.from_problem(ctx, g.Problem(spec, min_depth=cfg.min_depth), cfg, dist1, min_rows_per_rank=16)
+    full = dm._full
+    full.set_strict_order(True)
+    want = full.estimate_eta(kind=kind, seed=3, tol=1e-12, maxit=30)
+    got = parallel.DistKrylov(dm).estimate_eta(kind=kind, seed=3, tol=1e-12, maxit=30)
+    assert np.array_equal(got["residuals"], want["residuals"])
+    assert got["iterations"] == want["iterations"] and got["eta"] == want["eta"]
