@@ -184,6 +184,11 @@ int ldgmg_factors_upload(ldgmg_ctx* ctx, int n, int bs, const double* V, const d
 int ldgmg_factors_destroy(ldgmg_factors* F);
 int ldgmg_relax(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, const double* b,
                 const double* x_src, const double* x_live, double* x_out, double omega);
+/* the same restricted to the block rows `rows` (device int32, nrows entries):
+ * one colour phase of coloured GS on a rank's rows */
+int ldgmg_relax_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, const double* b,
+                     const double* x_src, const double* x_live, double* x_out, double omega, const int* rows,
+                     int nrows);
 
 /* out[i*bs .. i*bs+bs) = x[idx[i]*bs ..]  (ghost-exchange packing; idx on the device) */
 int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out);

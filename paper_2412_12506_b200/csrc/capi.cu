@@ -379,6 +379,32 @@ int ldgmg_relax(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, cons
     });
 }
 
+int ldgmg_relax_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F, const double* b,
+                     const double* x_src, const double* x_live, double* x_out, double omega, const int* rows,
+                     int nrows) {
+    return guarded([&] {
+        need(ctx, "relax_rows");
+        need(A, "relax_rows");
+        need(F, "relax_rows(factors)");
+        if (F->f.n != A->brows) fail(LDGMG_ERR_INVALID_ARGUMENT, "relax: factor count != block rows");
+        if (nrows < 0 || nrows > A->brows) fail(LDGMG_ERR_INVALID_ARGUMENT, "relax: bad row count");
+        if (nrows == 0) return;
+        need(rows, "relax_rows(rows)");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_RELAX;
+        p.x = x_src;
+        p.b = b;
+        p.xe = x_live;
+        p.y = x_out;
+        p.rows = rows;
+        p.nrows = nrows;
+        p.F = &F->f;
+        p.omega = omega;
+        launch_rowpass(*ctx, p);
+    });
+}
+
 int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out) {
     return guarded([&] {
         need(ctx, "gather_blocks");

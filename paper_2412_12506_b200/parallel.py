@@ -141,6 +141,10 @@ class GpuOps:
         check(lib.ldgmg_relax(self.ctx.h, A.h, F.h, b.data_ptr(), x_src.data_ptr(), x_live.data_ptr(),
                               x_out.data_ptr(), float(omega)))
 
+    def relax_rows(self, A, F, b, x_src, x_live, x_out, omega, rows):
+        check(lib.ldgmg_relax_rows(self.ctx.h, A.h, F.h, b.data_ptr(), x_src.data_ptr(), x_live.data_ptr(),
+                                   x_out.data_ptr(), float(omega), rows.data_ptr(), int(rows.numel())))
+
     def restrict(self, T, rf, rc):
         T.restrict(rf, rc)
 
@@ -242,6 +246,10 @@ class DistMultigrid:
                 V, lam, s = lv["factors"]
                 a, b = pa.r0, pa.r1
                 d["F"] = ops.factors(pa.n_own, bs, V[a * bs * bs:b * bs * bs], lam[a * bs:b * bs], s[a * bs:b * bs])
+            if "colour" in lv:  # coloured GS: own rows per colour, local ids, ascending
+                col_own = np.asarray(lv["colour"])[pa.r0:pa.r1]
+                nc = int(np.max(lv["colour"])) + 1 if len(lv["colour"]) else 0
+                d["crows"] = [ops.itensor(np.nonzero(col_own == c)[0]) for c in range(nc)]
             # transfer to level l+1, rank-local (nested ranges)
             parent, orth = transfers[l]
             nc = levels[l + 1]["n"]
@@ -290,8 +298,18 @@ class DistMultigrid:
             snap = d["snap"]
             snap.copy_(x_ext)
             self.ops.relax(d["A"], d["F"], b, snap, snap[:n_own * bs], x_ext[:n_own * bs], self.cfg.smoother.omega)
+        elif kind == L.COLOURED_GS:
+            # colours ascending (reverse for a reverse sweep), one ghost
+            # exchange per colour phase (smoothers.hpp:417-425), omega = 1
+            crows = d["crows"]
+            order = range(len(crows)) if sweep == L.SWEEP_FORWARD else range(len(crows) - 1, -1, -1)
+            for c in order:
+                d["xA"](x_ext)
+                if crows[c].numel():
+                    self.ops.relax_rows(d["A"], d["F"], b, x_ext, x_ext[:n_own * bs], x_ext[:n_own * bs], 1.0,
+                                        crows[c])
         else:
-            raise ValueError("distributed V-cycle supports the Jacobi and SAI smoothers")
+            raise ValueError("distributed V-cycle supports the Jacobi, coloured GS and SAI smoothers")
 
     # ---------------------------------------------------------------- V-cycle
     def _vcycle(self, l, b):
@@ -428,6 +446,8 @@ def from_problem(ctx, problem, cfg, dist, group=None, min_rows_per_rank=64):
                 lv["B"] = S.sai_matrix()
             else:
                 lv["factors"] = S.diag_factors()
+                if cfg.smoother.kind == L.COLOURED_GS:
+                    lv["colour"] = S.colours()
             transfers.append(problem.level_transfer(l))
         levels.append(lv)
     K = problem.injection()
@@ -456,15 +476,17 @@ def from_problem(ctx, problem, cfg, dist, group=None, min_rows_per_rank=64):
 
 # --------------------------------------------------------- distributed setup
 def sai_halo_hops(spec, smoother) -> int:
-    """Face-graph layers a rank must assemble around its range so that every
-    SAI column its B / B^T rows need is solved exactly: B row i needs the
-    columns c in pattern^l(i), whose least-squares rows reach
-    pattern^(2l+1) of the range; one operator hop is one face layer, two for
-    the stress-form Stokes operator (its G_j^T G_i cross terms couple
-    diagonal neighbours).  Non-SAI smoothers need the rank's rows only."""
-    if smoother.kind != L.SAI:
-        return 0
+    """Face-graph layers a rank must assemble around its range.  SAI: every
+    SAI column its B / B^T rows need must be solved exactly -- B row i needs
+    the columns c in pattern^l(i), whose least-squares rows reach
+    pattern^(2l+1) of the range, so (2l+1) operator hops.  Other smoothers:
+    one operator hop, so that the rank sees its neighbours' rows that
+    reference it (the ghost send lists are derived from them).  One operator
+    hop is one face layer, two for the stress-form Stokes operator (its
+    G_j^T G_i cross terms couple diagonal neighbours)."""
     r_a = 2 if (spec.kind == L.SYSTEM_STOKES and spec.gamma != 0.0) else 1
+    if smoother.kind != L.SAI:
+        return r_a
     return (2 * smoother.level + 1) * r_a
 
 
@@ -520,7 +542,32 @@ def local_sai(ptr, col, val, n, bs, r0, r1, level, build):
     return gptr, H[Bc].astype(np.int32), np.asarray(Bv)
 
 
-def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_fn):
+def distributed_colouring(ptr, col, n, nranks, rank, bcast):
+    """colour_mesh (smoothers.hpp:63-84: greedy, elements ascending, smallest
+    colour unused by the already-coloured neighbours) from the ranks' own rows
+    only.  An element's colour depends on its lower-numbered neighbours, which
+    live on this or lower ranks, so the ranks colour their ranges in rank
+    order; `bcast(q, colours_of_q)` (collective) publishes rank q's range
+    before rank q+1 starts.  Identical to the sequential colouring."""
+    ptr, col = np.asarray(ptr), np.asarray(col)
+    colour = np.full(n, -1, np.int32)
+    for q in range(nranks):
+        r0, r1 = q * n // nranks, (q + 1) * n // nranks
+        mine = np.zeros(r1 - r0, np.int32)
+        if q == rank:
+            for e in range(r0, r1):
+                nb = col[ptr[e]:ptr[e + 1]]
+                used = set(int(colour[j]) for j in nb if j != e and colour[j] >= 0)
+                c = 0
+                while c in used:
+                    c += 1
+                colour[e] = c
+            mine = colour[r0:r1].copy()
+        colour[r0:r1] = bcast(q, mine)
+    return colour
+
+
+def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_fn, bcast=None):
     """Per-level data for DistMultigrid from a Problem.partial: global-shaped
     operators (assembled rows only), transfers, and for the distributed
     levels the rank's SAI matrix (local_sai with `sai_fn`) or diagonal
@@ -546,10 +593,12 @@ def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_f
                     dk = np.array([ptr[e] + int(np.nonzero(col[ptr[e]:ptr[e + 1]] == e)[0][0])
                                    for e in range(r0, r1)], np.int64)
                     D = np.asarray(val).reshape(-1, bs * bs)[dk].reshape(-1)
-                    V, lam, s = factors_fn(r1 - r0, bs, D)
+                    V, lam, s = factors_fn(l, r0, r1, bs, D)
                     Vg, lg, sg = np.zeros(n * bs * bs), np.zeros(n * bs), np.zeros(n * bs)
                     Vg[r0 * bs * bs:r1 * bs * bs], lg[r0 * bs:r1 * bs], sg[r0 * bs:r1 * bs] = V, lam, s
                     lv["factors"] = (Vg, lg, sg)
+                    if cfg.smoother.kind == L.COLOURED_GS:
+                        lv["colour"] = distributed_colouring(ptr, col, n, nranks, rank, bcast)
         levels.append(lv)
     return levels, transfers
 
@@ -574,12 +623,19 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64)
                          cfg.smoother.cache, col_mask=mask)
         return B.download()
 
-    def gpu_factors(n_own, bs, D):
+    def gpu_factors(l, r0, r1, bs, D):
+        n_own = r1 - r0
         Ad = DeviceBsr(ctx, n_own, n_own, bs, bs, np.arange(n_own + 1, dtype=np.int32),
                        np.arange(n_own, dtype=np.int32), D)
         return Smoother(ctx, Ad, SmootherConfig.jacobi(cfg.smoother.omega)).diag_factors()
 
-    levels, transfers = partial_levels(prob, cfg, P, rank, min_rows_per_rank, gpu_sai, gpu_factors)
+    def bcast(q, mine):
+        import torch
+        t = torch.as_tensor(np.ascontiguousarray(mine, np.int32).astype(np.int64)).cuda()
+        dist.broadcast(t, src=dist.get_global_rank(group, q) if group is not None else q, group=group)
+        return t.cpu().numpy().astype(np.int32)
+
+    levels, transfers = partial_levels(prob, cfg, P, rank, min_rows_per_rank, gpu_sai, gpu_factors, bcast)
     K = prob.injection()
 
     def coarse_factory(ld_):

@@ -56,6 +56,13 @@ class CpuOps:
                                    omega)
         x_out.copy_(self.torch.as_tensor(out.reshape(-1)))
 
+    def relax_rows(self, A, F, b, x_src, x_live, x_out, omega, rows):
+        ptr, col, val, n, _, bs = A
+        r = rows.numpy()
+        out = self.port.relax_rows(r, ptr, col, val, bs, b.numpy(), x_src.numpy(), x_live.numpy(), *F, omega)
+        xo = x_out.view(-1, bs)
+        xo[self.torch.as_tensor(r)] = self.torch.as_tensor(out)
+
     def restrict(self, T, rf, rc):
         parent, orth, K, bss, ncomp, nc = T
         rc.copy_(self.torch.as_tensor(self.port.restrict(parent, orth, K, bss, ncomp, nc, rf.numpy())))
@@ -90,6 +97,8 @@ def worker(rank, world, port_no, case, outdir, partial=False, krylov=None):
         "jacobi-scalar2d-periodic": (K.scalar(16, 2, K.P, degree=1), K.cfg("jacobi", omega=0.7, nu=2), 16),
         "sai-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=1), K.cfg("sai", level=1, zeta=0.13, nu=1), 8),
         "sai-scalar3d-periodic": (K.scalar(8, 3, K.P, degree=1), K.cfg("sai", level=1, nu=1), 32),
+        "gs-scalar2d-dirichlet-p2": (K.scalar(16, 2, K.D, degree=2), K.cfg("gs", nu=1), 8),
+        "gs-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=1), K.cfg("gs", nu=1), 8),
     }[case]
     R = ref.RefMultigrid(spec, cfg)
     P = port.from_reference(R, cfg)
@@ -115,7 +124,16 @@ def worker(rank, world, port_no, case, outdir, partial=False, krylov=None):
             (bp, bc, bv), _ = ref.sai_build(kind, prob.dim, prob.n_comp, prob.bs_scalar, nl, lptr, lcol, lval,
                                             cfg.smoother.level, cfg.smoother.zeta)
             return bp, bc, bv
-        plevels, ptransfers = parallel.partial_levels(prob, cfg, world, rank, min_rows, ref_build, None)
+        def ref_factors(l, r0, r1, bs, D):
+            V, lam, s_ = R.diag_factors(l)
+            return V[r0 * bs * bs:r1 * bs * bs], lam[r0 * bs:r1 * bs], s_[r0 * bs:r1 * bs]
+
+        def bcast(q, mine):
+            t = torch.as_tensor(np.ascontiguousarray(mine, np.int64))
+            dist.broadcast(t, src=q)
+            return t.numpy().astype(np.int32)
+        plevels, ptransfers = parallel.partial_levels(prob, cfg, world, rank, min_rows, ref_build, ref_factors,
+                                                      bcast)
         # the agglomerated tail keeps the reference's full data (identical by construction)
         dm = parallel.DistMultigrid(CpuOps(), dist, cfg, plevels, ptransfers, prob.injection(), prob.dim,
                                     prob.bs_scalar, prob.n_comp, P.koffs, coarse_factory,

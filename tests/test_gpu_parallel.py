@@ -57,6 +57,7 @@ def test_partitioned_path_world1_bitwise(ctx, dist1, name, spec, cfg, min_rows):
 @pytest.mark.parametrize("name,spec,cfg,min_rows", [
     ("sai-2d-dirichlet", K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=2), 16),
     ("jacobi-2d", K.scalar(16, 2, K.P, degree=3, beta=9.0), K.cfg("jacobi", omega=0.7, nu=2), 16),
+    ("gs-2d", K.scalar(16, 2, K.D, degree=2), K.cfg("gs", nu=2), 16),
 ])
 def test_distributed_setup_world1_matches_replicated(ctx, dist1, name, spec, cfg, min_rows):
     """from_problem_partial (distributed setup path, GPU SAI / GPU factors on

@@ -26,7 +26,10 @@ def free_port():
     ("sai-scalar2d-periodic", False), ("sai-scalar2d-dirichlet-p2", False), ("jacobi-scalar2d-periodic", False),
     ("sai-stokes2d-stress", False), ("sai-scalar3d-periodic", False),
     # distributed setup (each rank assembles its rows + halo, solves its SAI columns)
-    ("sai-scalar2d-periodic", True), ("sai-scalar2d-dirichlet-p2", True), ("sai-stokes2d-stress", True)])
+    ("sai-scalar2d-periodic", True), ("sai-scalar2d-dirichlet-p2", True), ("sai-stokes2d-stress", True),
+    # coloured GS: one exchange per colour phase; colouring from the ranks' rows
+    ("gs-scalar2d-dirichlet-p2", False), ("gs-scalar2d-dirichlet-p2", True), ("gs-stokes2d-stress", True),
+    ("jacobi-scalar2d-periodic", True)])
 def test_partitioned_vcycle_matches_reference(ref, tmp_path, case, partial, world):
     import torch.multiprocessing as mp
     from oracle import port
@@ -41,6 +44,8 @@ def test_partitioned_vcycle_matches_reference(ref, tmp_path, case, partial, worl
         "jacobi-scalar2d-periodic": (K.scalar(16, 2, K.P, degree=1), K.cfg("jacobi", omega=0.7, nu=2)),
         "sai-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=1), K.cfg("sai", level=1, zeta=0.13, nu=1)),
         "sai-scalar3d-periodic": (K.scalar(8, 3, K.P, degree=1), K.cfg("sai", level=1, nu=1)),
+        "gs-scalar2d-dirichlet-p2": (K.scalar(16, 2, K.D, degree=2), K.cfg("gs", nu=1)),
+        "gs-stokes2d-stress": (K.stokes(8, 2, K.P, gamma=1.0, degree=1), K.cfg("gs", nu=1)),
     }[case]
     R = ref.RefMultigrid(spec, cfg)
     n, bs, _ = R.shape(0)
