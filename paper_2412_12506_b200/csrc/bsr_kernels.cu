@@ -617,8 +617,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
             return;
         }
         const size_t smem = sizeof(double) * (size_t(maxlen) * 32 + 64);
-        if (smem > 48 * 1024)
-            ensure_dyn_smem(rowsplit_kernel, size_t(smem));
+        ensure_dyn_smem(rowsplit_kernel, size_t(smem));
         const int grid = std::min(p.nrows, ctx.num_sms * 16);
         static bool once = (max_carveout(rowsplit_kernel), true);
         (void)once;

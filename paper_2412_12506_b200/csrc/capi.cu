@@ -121,6 +121,7 @@ int ldgmg_ctx_destroy(ldgmg_ctx* ctx) {
         cudaFree(ctx->d_red);
         cudaFreeHost(ctx->h_red);
         ctx_release_staging(*ctx);
+        ctx_release_blas(*ctx);
         delete ctx;
     });
 }

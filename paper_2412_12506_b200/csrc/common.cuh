@@ -85,27 +85,28 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 /// attribute is cached per (kernel, device).
 template <class K>
 inline void ensure_dyn_smem(K* kernel, size_t bytes) {
-    if (bytes <= 48 * 1024) return;
     struct Entry {
         const void* f;
         int dev;
-        size_t bytes;
+        size_t bytes;  // current cudaFuncAttributeMaxDynamicSharedMemorySize
     };
     static std::vector<Entry> set;
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     const void* f = reinterpret_cast<const void*>(kernel);
-    for (auto& e : set)
-        if (e.f == f && e.dev == dev) {
-            if (e.bytes >= bytes) return;
-            cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
-                       "cudaFuncSetAttribute");
-            e.bytes = bytes;
-            return;
-        }
+    Entry* e = nullptr;
+    for (auto& x : set)
+        if (x.f == f && x.dev == dev) e = &x;
+    if (!e) {  // the default limit is 48 KB minus the kernel's static shared memory
+        cudaFuncAttributes fa{};
+        cuda_check(cudaFuncGetAttributes(&fa, f), "cudaFuncGetAttributes");
+        set.push_back({f, dev, size_t(fa.maxDynamicSharedSizeBytes)});
+        e = &set.back();
+    }
+    if (bytes <= e->bytes) return;
     cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
                "cudaFuncSetAttribute");
-    set.push_back({f, dev, bytes});
+    e->bytes = bytes;
 }
 
 /// Pin a kernel's shared-memory carveout to the maximum (once per kernel).

@@ -31,6 +31,7 @@ struct Ctx {
     unsigned char* pin[2] = {nullptr, nullptr};
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     size_t pin_bytes = 0;
+    void* blas = nullptr;  // cuBLAS handle (SAI setup GEMMs), created on first use
 };
 
 /// Large pageable host -> device copy: threaded memcpy into a pinned double
@@ -39,6 +40,7 @@ struct Ctx {
 /// Returns after the copy completed.
 void h2d_staged(Ctx& ctx, void* dst, const void* src, size_t bytes);
 void ctx_release_staging(Ctx& ctx);
+void ctx_release_blas(Ctx& ctx);
 
 /// Host<->device copies ordered on the context stream (setup paths; the
 /// legacy-stream cudaMemcpy would race with the non-blocking context stream).

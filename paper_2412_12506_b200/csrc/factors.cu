@@ -221,8 +221,7 @@ void compute_factors_gpu(Ctx& ctx, const Bsr& A, DiagFactors& F) {
     LDGMG_CUDA(cudaMemsetAsync(d_bad.p, 0, d_bad.bytes, ctx.stream));
     const size_t smem = diag_factor_smem(bs);
     if (smem > 227 * 1024) fail(LDGMG_ERR_INVALID_ARGUMENT, "factor_diagonal: block too large for the GPU factor kernel");
-    if (smem > 48 * 1024)
-        ensure_dyn_smem(diag_factor_kernel, size_t(smem));
+    ensure_dyn_smem(diag_factor_kernel, size_t(smem));
     diag_factor_kernel<<<N, kFactorThreads, smem, ctx.stream>>>(
         A.val.as<double>(), A.blk_stride, d_dk.as<int>(), bs, F.ld, F.vstride, F.V.as<double>(),
         F.lambda.as<double>(), F.scale.as<double>(), F.lmax.as<double>(), d_bad.as<int>());

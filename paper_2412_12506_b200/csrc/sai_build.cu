@@ -17,6 +17,7 @@
 //      minimum-norm fallback by one-sided Jacobi SVD (dgelsd, :298-308)   GPU, one CTA/problem
 //   7. scatter B(J_b, j) = alpha_J X_b alpha_j (:357-364)         GPU
 // Results are independent of caching (the cache only changes the work done).
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -273,7 +274,9 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
                                                       const int* __restrict__ ni, const int* __restrict__ nj, int bs,
                                                       int j0, const double* __restrict__ tolv, double* __restrict__ Vg,
                                                       const int64_t* __restrict__ voff, double* __restrict__ Tg,
-                                                      int* __restrict__ deficient) {
+                                                      int* __restrict__ deficient, double* __restrict__ Vbig = nullptr,
+                                                      int ldbig = 0, int64_t bigstride = 0, int bigcol = 0,
+                                                      double* __restrict__ taus = nullptr, int taustride = 0) {
     extern __shared__ __align__(16) double Vp[];  // mr x NB panel, column-major (row j0 stored at 0)
     __shared__ double red[NT / 32];
     __shared__ double sT[NB * NB], stau[NB], sh_beta;
@@ -357,6 +360,15 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
         V[t] = (c < nb && r >= c) ? Vp[size_t(c) * mr + r] : 0.0;
     }
     for (int t = tid; t < NB * NB; t += NT) Tg[size_t(p) * NB * NB + t] = sT[t];
+    if (Vbig) {  // also into the wide panel: columns bigcol.., rows shifted by bigcol (zeros above)
+        double* VB = Vbig + size_t(p) * bigstride + size_t(bigcol) * ldbig;
+        for (int t = tid; t < ldbig * nb; t += NT) {
+            const int c = t / ldbig, r = t - c * ldbig;
+            const int rr = r - bigcol;  // row within this panel
+            VB[size_t(c) * ldbig + r] = (rr >= c && rr < mr) ? Vp[size_t(c) * mr + rr] : 0.0;
+        }
+        for (int t = tid; t < nb; t += NT) taus[size_t(p) * taustride + bigcol + t] = stau[t];
+    }
     if (def && tid == 0) deficient[p] = 1;
 }
 
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
                                                               const int* __restrict__ ni, const int* __restrict__ nj,
                                                               int bs, int j0, const double* __restrict__ Vg,
                                                               const int64_t* __restrict__ voff,
-                                                              const double* __restrict__ Tg) {
+                                                              const double* __restrict__ Tg, int col_limit = -1) {
     extern __shared__ __align__(16) double sC[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ double sy[8][CPW * NB];
@@ -462,7 +474,7 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
     if (j0 >= n) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nb = min(NB, n - j0), mr = m - j0;
-    const int nm = n - j0 - nb, ncols = nm + bs;
+    const int nm = n - j0 - nb, ncols = col_limit >= 0 ? min(nm + bs, col_limit) : nm + bs;
     const int c0 = blockIdx.x * CPW;
     if (c0 >= ncols) return;
     const int nc = min(CPW, ncols - c0);
@@ -571,6 +583,29 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
                 colp[c][r] = sC[size_t(c) * ld + off[c] + r] - d;
             }
         }
+    }
+}
+
+/// T of the wide compact-WY panel (dlarft, forward / columnwise) from the
+/// Gram matrix G = V^T V of its reflectors and their taus: T(i,i) = tau_i,
+/// T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i).  One CTA per problem, column-major.
+__global__ void qr_wide_t_kernel(const double* __restrict__ G, const double* __restrict__ taus, int taustride,
+                                 double* __restrict__ T, int w, int64_t mstride) {
+    const int p = blockIdx.x;
+    const double* Gp = G + size_t(p) * mstride;  // w x w, ld w, problem stride mstride
+    const double* tp = taus + size_t(p) * taustride;
+    double* Tp = T + size_t(p) * mstride;
+    for (int t = threadIdx.x; t < w * w; t += blockDim.x) Tp[t] = 0.0;
+    __syncthreads();
+    for (int i = 0; i < w; ++i) {
+        const double ti = tp[i];
+        for (int a = threadIdx.x; a < i; a += blockDim.x) {
+            double s = 0.0;
+            for (int b = a; b < i; ++b) s += Tp[size_t(b) * w + a] * Gp[size_t(i) * w + b];
+            Tp[size_t(i) * w + a] = -ti * s;
+        }
+        if (threadIdx.x == 0) Tp[size_t(i) * w + i] = ti;
+        __syncthreads();
     }
 }
 
@@ -805,7 +840,9 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
                                                     d_tol.as<double>(), d_def.as<int>());
     after_launch("qr_init_kernel");
     const size_t smem = sizeof(double) * size_t(max_m) * NB;
-    LDGMG_CUDA(cudaFuncSetAttribute(qr_panel_kernel<256, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ensure_dyn_smem(qr_panel_kernel<256, NB>, size_t(smem));
+    if (getenv("LDGMG_SAI_TIMING") && atoi(getenv("LDGMG_SAI_TIMING")))
+        fprintf(stderr, "[qr_blocked] NB=%d max_m=%d max_n=%d batch=%d smem=%zu\n", NB, max_m, max_n, nb, smem);
     // TMA-staged trailing tiles of tcpw columns (needs the 2-double tail pad
     // on M and W that build_sai_gpu allocates).  Wider tiles re-read the
     // reflectors from L2 fewer times; the widest tile that fits is used.
@@ -836,7 +873,7 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
             const dim3 g(div_up(ncols, tcpw), nb);
             tma_kernel<<<g, 256, tsmem, ctx.stream>>>(
                 d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_ni.as<int>(),
-                d_nj.as<int>(), bs, j0, d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>());
+                d_nj.as<int>(), bs, j0, d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), -1);
         } else {
             const dim3 g(div_up(ncols, 8 * CPW), nb);
             qr_trailing_kernel<NB, CPW><<<g, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
@@ -853,6 +890,128 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
         d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
     after_launch("qr_backsub_kernel");
     (void)d_X;
+}
+
+namespace {
+void blas_check(cublasStatus_t st, const char* what) {
+    if (st != CUBLAS_STATUS_SUCCESS) fail(LDGMG_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(int(st)));
+}
+cublasHandle_t ctx_blas(Ctx& ctx) {
+    if (!ctx.blas) {
+        cublasHandle_t h;
+        blas_check(cublasCreate(&h), "cublasCreate");
+        ctx.blas = h;
+    }
+    cublasHandle_t h = static_cast<cublasHandle_t>(ctx.blas);
+    blas_check(cublasSetStream(h, ctx.stream), "cublasSetStream");
+    return h;
+}
+}  // namespace
+
+void ctx_release_blas(Ctx& ctx) {
+    if (ctx.blas) cublasDestroy(static_cast<cublasHandle_t>(ctx.blas));
+    ctx.blas = nullptr;
+}
+
+/// Blocked Householder QR least squares for a batch of problems of ONE shape
+/// (m x n, k = bs right-hand sides), compact WY with wide panels of WB = 64
+/// columns: each wide panel is factored as 8-column sub-panels
+/// (qr_panel_kernel in shared memory, the rest of the wide panel updated by
+/// qr_trailing_tma_kernel), its T follows from the Gram matrix of its
+/// reflectors (qr_wide_t_kernel), and the trailing matrix and the right-hand
+/// sides get C -= V (T^T (V^T C)) as three strided-batched cuBLAS DGEMMs per
+/// panel.  The trailing update -- all but ~2 % of the flops -- thus runs at
+/// GEMM arithmetic intensity (64 reflectors per pass over C instead of 8).
+template <int NB>
+void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_X, DevBuf& d_xoff,
+                   DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, int bs, int nb, int m, int n) {
+    constexpr int WB = 64, TCPW = 4;
+    const int k = bs;
+    cublasHandle_t h = ctx_blas(ctx);
+    std::vector<int64_t> voff(nb + 1);
+    for (int i = 0; i <= nb; ++i) voff[i] = int64_t(i) * m * NB;
+    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, voff[nb])), d_voff(sizeof(int64_t) * (nb + 1)),
+        d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
+        d_Vb(sizeof(double) * size_t(nb) * m * WB), d_G(sizeof(double) * size_t(nb) * WB * WB),
+        d_Tb(sizeof(double) * size_t(nb) * WB * WB), d_tau(sizeof(double) * size_t(nb) * WB),
+        d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k));
+    h2d(ctx, d_voff.p, voff.data(), d_voff.bytes);
+    qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
+                                                    d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
+                                                    d_tol.as<double>(), d_def.as<int>());
+    after_launch("qr_init_kernel");
+    const size_t psmem = sizeof(double) * size_t(m) * NB;
+    ensure_dyn_smem(qr_panel_kernel<256, NB>, psmem);
+    if (getenv("LDGMG_SAI_TIMING") && atoi(getenv("LDGMG_SAI_TIMING")))
+        fprintf(stderr, "[qr_gemm] NB=%d m=%d n=%d batch=%d\n", NB, m, n, nb);
+    const size_t tsmem = sizeof(double) * size_t(TCPW) * (((m + 1) & ~1) + 2);
+    ensure_dyn_smem(qr_trailing_tma_kernel<NB, TCPW>, tsmem);
+    const double one = 1.0, zero = 0.0, mone = -1.0;
+    double* M = d_M.as<double>();
+    double* W = d_W.as<double>();
+    const long long sM = (long long)m * n, sW = (long long)m * k, sV = (long long)m * WB, sG = WB * WB,
+                    sY = (long long)WB * (n + k);
+    for (int jb = 0; jb < n; jb += WB) {
+        const int w = std::min(WB, n - jb), mrb = m - jb;
+        for (int s0 = 0; s0 < w; s0 += NB) {
+            const int j0 = jb + s0;
+            qr_panel_kernel<256, NB><<<nb, 256, psmem, ctx.stream>>>(
+                M, d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(), d_V.as<double>(),
+                d_voff.as<int64_t>(), d_T.as<double>(), d_def.as<int>(), d_Vb.as<double>(), mrb, sV, s0,
+                d_tau.as<double>(), WB);
+            {
+                const cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) {
+                    cudaFuncAttributes fa{};
+                    cudaFuncGetAttributes(&fa, qr_panel_kernel<256, NB>);
+                    fail(LDGMG_ERR_CUDA, std::string("qr_panel_kernel (wide): ") + cudaGetErrorString(e) +
+                                             " NB=" + std::to_string(NB) + " m=" + std::to_string(m) +
+                                             " smem=" + std::to_string(psmem) +
+                                             " maxdyn=" + std::to_string(fa.maxDynamicSharedSizeBytes) +
+                                             " batch=" + std::to_string(nb));
+                }
+                launch_counter().fetch_add(1, std::memory_order_relaxed);
+            }
+            const int rest = w - s0 - NB;
+            if (rest > 0) {
+                qr_trailing_tma_kernel<NB, TCPW><<<dim3(div_up(rest, TCPW), nb), 256, tsmem, ctx.stream>>>(
+                    M, d_moff.as<int64_t>(), W, d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0,
+                    d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), rest);
+                after_launch("qr_trailing_tma_kernel");
+            }
+        }
+        // T of the wide panel from the Gram matrix of its reflectors
+        blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, w, mrb, &one, d_Vb.as<double>(), mrb, sV,
+                                             d_Vb.as<double>(), mrb, sV, &zero, d_G.as<double>(), w, sG, nb),
+                   "gram");
+        qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(d_G.as<double>(), d_tau.as<double>(), WB, d_Tb.as<double>(), w,
+                                                    sG);
+        after_launch("qr_wide_t_kernel");
+        // C -= V (T^T (V^T C)) on the trailing columns of M and on W
+        struct Part {
+            double* C;
+            long long stride;
+            int cols;
+        };
+        const Part parts[2] = {{M + jb + size_t(jb + w) * m, sM, n - jb - w}, {W + jb, sW, k}};
+        for (const Part& pt : parts) {
+            if (pt.cols <= 0) continue;
+            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, pt.cols, mrb, &one, d_Vb.as<double>(),
+                                                 mrb, sV, pt.C, m, pt.stride, &zero, d_Y.as<double>(), w, sY, nb),
+                       "V^T C");
+            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, pt.cols, w, &one, d_Tb.as<double>(), w,
+                                                 sG, d_Y.as<double>(), w, sY, &zero, d_Z.as<double>(), w, sY, nb),
+                       "T^T Y");
+            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, mrb, pt.cols, w, &mone, d_Vb.as<double>(),
+                                                 mrb, sV, d_Z.as<double>(), w, sY, &one, pt.C, m, pt.stride, nb),
+                       "C -= V Z");
+        }
+    }
+    constexpr int CB = 16;
+    qr_backsub_kernel<CB><<<dim3(div_up(bs, CB), nb), 256, 0, ctx.stream>>>(
+        d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
+        d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, d_def.as<int>());
+    after_launch("qr_backsub_kernel");
 }
 
 SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity, int level, double zeta,
@@ -1140,6 +1299,8 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 const int64_t m = int64_t(probs[bord[p1]].ni) * bs, n = int64_t(probs[bord[p1]].nj) * bs;
                 const size_t add = sizeof(double) * size_t(m * n + m * bs);
                 if (p1 > p0 && (need + add > budget || p1 - p0 >= 4 * ctx.num_sms)) break;
+                if (p1 > p0 && (probs[bord[p1]].ni != probs[bord[p0]].ni || probs[bord[p1]].nj != probs[bord[p0]].nj))
+                    break;  // one shape per batch (strided-batched GEMM path)
                 need += add;
                 mn += size_t(m * n);
                 mk += size_t(m * bs);
@@ -1194,7 +1355,16 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 qr_env = e ? atoi(e) : 0;
             }
             const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
-            if (!qr_env && smem8 <= 200 * 1024)
+            static int gemm_env = -2;
+            if (gemm_env == -2) {
+                const char* e = getenv("LDGMG_QR_GEMM");
+                gemm_env = e ? atoi(e) : 1;
+            }
+            if (!qr_env && gemm_env && smem8 <= 200 * 1024 && max_n >= 128)
+                qr_gemm_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
+            else if (!qr_env && gemm_env && smem4 <= 200 * 1024 && max_n >= 128)
+                qr_gemm_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
+            else if (!qr_env && smem8 <= 200 * 1024)
                 qr_blocked_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
                                     max_n);
             else if (!qr_env && smem4 <= 200 * 1024)

@@ -631,8 +631,7 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         zero_xc = nullptr;
     }
     if (warp_ok) {
-        if (smem_w > 48 * 1024)
-            ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
+        ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(restrict_warp_kernel<8>), true);
         (void)once;
@@ -663,8 +662,7 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
     const int nK = transfer_nK(T);
     const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
     if (T.max_children <= 8 && smem_w <= 200 * 1024) {
-        if (smem_w > 48 * 1024)
-            ensure_dyn_smem(prolong_warp_kernel, size_t(smem_w));
+        ensure_dyn_smem(prolong_warp_kernel, size_t(smem_w));
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(prolong_warp_kernel), true);
         (void)once;

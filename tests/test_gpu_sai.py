@@ -56,6 +56,8 @@ def test_gpu_sai_matches_reference(ctx, ref, name):
         assert np.array_equal(bp, Bref[0]) and np.array_equal(bc, Bref[1])
         err = np.linalg.norm(bv - Bref[2]) / np.linalg.norm(Bref[2])
         assert err <= B_RTOL, (name, level, err)
+        # every block, not only the aggregate (a few wrong columns must not hide)
+        assert np.max(np.abs(bv - Bref[2])) <= 1e-9 * np.max(np.abs(Bref[2])), (name, level)
         gs = S.sai_stats()
         assert (gs.cache_hits, gs.cache_misses) == (st.cache_hits, st.cache_misses)
         assert gs.rank_deficient_columns == st.rank_deficient_columns
