@@ -21,15 +21,15 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case,partial", [
-    ("sai-scalar2d-periodic", False), ("sai-scalar2d-dirichlet-p2", False), ("jacobi-scalar2d-periodic", False),
-    ("sai-stokes2d-stress", False), ("sai-scalar3d-periodic", False),
+@pytest.mark.parametrize("case,partial,world", [
+    ("sai-scalar2d-periodic", False, 2), ("sai-scalar2d-periodic", False, 4),
+    ("sai-scalar2d-dirichlet-p2", False, 2), ("jacobi-scalar2d-periodic", False, 4),
+    ("sai-stokes2d-stress", False, 2), ("sai-scalar3d-periodic", False, 4),
     # distributed setup (each rank assembles its rows + halo, solves its SAI columns)
-    ("sai-scalar2d-periodic", True), ("sai-scalar2d-dirichlet-p2", True), ("sai-stokes2d-stress", True),
+    ("sai-scalar2d-periodic", True, 4), ("sai-scalar2d-dirichlet-p2", True, 2), ("sai-stokes2d-stress", True, 4),
     # coloured GS: one exchange per colour phase; colouring from the ranks' rows
-    ("gs-scalar2d-dirichlet-p2", False), ("gs-scalar2d-dirichlet-p2", True), ("gs-stokes2d-stress", True),
-    ("jacobi-scalar2d-periodic", True)])
+    ("gs-scalar2d-dirichlet-p2", False, 2), ("gs-scalar2d-dirichlet-p2", True, 4), ("gs-stokes2d-stress", True, 2),
+    ("jacobi-scalar2d-periodic", True, 2)])
 def test_partitioned_vcycle_matches_reference(ref, tmp_path, case, partial, world):
     import torch.multiprocessing as mp
     from oracle import port
@@ -85,10 +85,9 @@ def test_partition_plan_invariants():
         partition_level(ptr, col, N, N + 1, 0)
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case,kind", [("sai-scalar2d-periodic", 1), ("sai-scalar2d-dirichlet-p2", 1),
-                                       ("jacobi-scalar2d-periodic", 0), ("sai-stokes2d-stress", 1),
-                                       ("sai-scalar2d-dirichlet-p2", 0)])
+@pytest.mark.parametrize("case,kind,world", [("sai-scalar2d-periodic", 1, 4), ("sai-scalar2d-dirichlet-p2", 1, 2),
+                                             ("jacobi-scalar2d-periodic", 0, 2), ("sai-stokes2d-stress", 1, 2),
+                                             ("sai-scalar2d-dirichlet-p2", 0, 4)])
 def test_distributed_krylov_matches_reference(ref, tmp_path, case, kind, world):
     """estimate_eta (GMRES / PCG with the partitioned V-cycle as
     preconditioner, P-independent dots) reproduces the reference's residual
