@@ -21,6 +21,11 @@
 
 namespace ldgmg_b200 {
 
+/// cudaHostAlloc when a CUDA device is visible and LDGMG_PINNED_SETUP=1
+/// (nullptr otherwise); pinned_free returns false for non-pinned pointers.
+void* pinned_alloc(size_t bytes);
+bool pinned_free(void* p);
+
 /// std::allocator that default-initialises (no zero fill on resize): the
 /// operator values are written exactly once by the (threaded) assembly, so
 /// zeroing gigabytes first only costs a serial memset and the page faults.
@@ -46,6 +51,9 @@ struct DefaultInitAlloc : std::allocator<T> {
     T* allocate(size_t n) {
         const size_t bytes = n * sizeof(T);
         if (bytes < (size_t(64) << 20)) return std::allocator<T>::allocate(n);
+        // page-locked on request (LDGMG_PINNED_SETUP=1: the operator upload is
+        // then a plain DMA); else 2 MiB-aligned, huge-page advised
+        if (void* p = pinned_alloc(bytes)) return static_cast<T*>(p);
         const size_t huge = size_t(2) << 20;
         void* p = std::aligned_alloc(huge, (bytes + huge - 1) / huge * huge);
         if (!p) throw std::bad_alloc();
@@ -55,7 +63,7 @@ struct DefaultInitAlloc : std::allocator<T> {
     void deallocate(T* p, size_t n) {
         if (n * sizeof(T) < (size_t(64) << 20))
             std::allocator<T>::deallocate(p, n);
-        else
+        else if (!pinned_free(p))
             std::free(p);
     }
 };
