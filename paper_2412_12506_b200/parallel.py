@@ -183,16 +183,24 @@ class Exchanger:
         if p.n_ghost == 0 and len(p.send_idx) == 0:
             return
         self.ops.gather(x_ext, self.idx, len(p.send_idx), bs, self.sendbuf)
-        P2P = self.dist.P2POp
-        reqs = []
-        for q in range(len(p.send_count)):
-            if q == self.rank:
-                continue
-            if p.send_count[q]:
-                reqs.append(P2P(self.dist.isend, self.sendbuf[self.so[q] * bs:self.so[q + 1] * bs], q, self.group))
-            if p.recv_count[q]:
-                g0 = (p.n_own + self.ro[q]) * bs
-                reqs.append(P2P(self.dist.irecv, x_ext[g0:g0 + int(p.recv_count[q]) * bs], q, self.group))
+        # the op list only depends on the (fixed) buffers: build it once per target
+        key = x_ext.data_ptr() if hasattr(x_ext, "data_ptr") else id(x_ext)
+        reqs = self._reqs.get(key) if hasattr(self, "_reqs") else None
+        if reqs is None:
+            P2P = self.dist.P2POp
+            reqs = []
+            for q in range(len(p.send_count)):
+                if q == self.rank:
+                    continue
+                if p.send_count[q]:
+                    reqs.append(P2P(self.dist.isend, self.sendbuf[self.so[q] * bs:self.so[q + 1] * bs], q,
+                                    self.group))
+                if p.recv_count[q]:
+                    g0 = (p.n_own + self.ro[q]) * bs
+                    reqs.append(P2P(self.dist.irecv, x_ext[g0:g0 + int(p.recv_count[q]) * bs], q, self.group))
+            if not hasattr(self, "_reqs"):
+                self._reqs = {}
+            self._reqs[key] = reqs
         if reqs:
             for w in self.dist.batch_isend_irecv(reqs):
                 w.wait()
