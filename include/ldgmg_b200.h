@@ -341,6 +341,18 @@ int ldgmg_problem_create_partial(const ldgmg_problem_spec* spec, int min_depth, 
                                  ldgmg_problem** out);
 /* 1 when the level was assembled partially (rank rows + halo) */
 int ldgmg_problem_level_partial(const ldgmg_problem* P, int level);
+/* General form of the two above.  flags: LDGMG_PROBLEM_DEVICE_ASSEMBLY = the
+ * level operators are not built on the host; the product records each
+ * block's accumulation (accumulate_AtDB products, penalty / coupling blocks,
+ * ldg_core.hpp:547-586, ldg_stokes.hpp:149-191) and evaluates it on the GPU,
+ * bit-identical to the host assembly (ldgmg_problem_device_operator,
+ * ldgmg_mg_create_from_problem).  ldgmg_problem_level_matrix then returns the
+ * pattern only (val must be NULL). */
+enum { LDGMG_PROBLEM_DEVICE_ASSEMBLY = 1 };
+int ldgmg_problem_create_ex(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements, int nranks,
+                            int rank, int halo_hops, int min_rows_per_rank, int flags, ldgmg_problem** out);
+/* the level operator as a device BSR (device assembly, or upload of the host one) */
+int ldgmg_problem_device_operator(ldgmg_ctx* ctx, const ldgmg_problem* P, int level, ldgmg_bsr** out);
 int ldgmg_problem_depth(const ldgmg_problem* P);
 int ldgmg_problem_level_shape(const ldgmg_problem* P, int level, int* n_elements, int* bs,
                               int64_t* nnzb);

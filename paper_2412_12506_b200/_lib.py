@@ -181,6 +181,8 @@ _SIGS = {
     "ldgmg_problem_create": ([C.POINTER(ProblemSpec), _I, _I, C.POINTER(_P)], _I),
     "ldgmg_problem_create_partial": ([C.POINTER(ProblemSpec), _I, _I, _I, _I, _I, _I, C.POINTER(_P)], _I),
     "ldgmg_problem_level_partial": ([_P, _I], _I),
+    "ldgmg_problem_create_ex": ([C.POINTER(ProblemSpec), _I, _I, _I, _I, _I, _I, _I, C.POINTER(_P)], _I),
+    "ldgmg_problem_device_operator": ([_P, _P, _I, C.POINTER(_P)], _I),
     "ldgmg_problem_depth": ([_P], _I),
     "ldgmg_problem_level_shape": ([_P, _I, _IP, _IP, C.POINTER(_I64)], _I),
     "ldgmg_problem_level_matrix": ([_P, _I, _P, _P, _P], _I),

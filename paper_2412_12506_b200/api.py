@@ -369,12 +369,20 @@ class ProblemSpec:
 class Problem:
     """Built-in host setup: mesh chain + LDG operators per level."""
 
-    def __init__(self, spec: ProblemSpec, min_depth=2, bottom_max_elements=64):
+    def __init__(self, spec: ProblemSpec, min_depth=2, bottom_max_elements=64, device_assembly=False):
+        """device_assembly: the level operators are assembled on the GPU when a
+        hierarchy / device operator is created (bit-identical to the host
+        assembly; level_matrix then returns no values)."""
         self.spec = spec
         cs = spec.c()
         h = C.c_void_p()
-        check(lib.ldgmg_problem_create(C.byref(cs), int(min_depth), int(bottom_max_elements), C.byref(h)))
+        if device_assembly:
+            check(lib.ldgmg_problem_create_ex(C.byref(cs), int(min_depth), int(bottom_max_elements), 1, 0, 0, 0, 1,
+                                              C.byref(h)))
+        else:
+            check(lib.ldgmg_problem_create(C.byref(cs), int(min_depth), int(bottom_max_elements), C.byref(h)))
         self.h = h
+        self.device_assembly = bool(device_assembly)
         self._init_info()
 
     def _init_info(self):
@@ -389,7 +397,7 @@ class Problem:
 
     @classmethod
     def partial(cls, spec: ProblemSpec, nranks: int, rank: int, halo_hops: int, min_rows_per_rank: int = 64,
-                min_depth=2, bottom_max_elements=64) -> "Problem":
+                min_depth=2, bottom_max_elements=64, device_assembly=False) -> "Problem":
         """Distributed setup (ldgmg_problem_create_partial): levels with >=
         nranks*min_rows_per_rank elements assemble only this rank's rows plus
         `halo_hops` face layers (other rows empty, global numbering kept)."""
@@ -397,11 +405,24 @@ class Problem:
         obj.spec = spec
         cs = spec.c()
         h = C.c_void_p()
-        check(lib.ldgmg_problem_create_partial(C.byref(cs), int(min_depth), int(bottom_max_elements), int(nranks),
-                                               int(rank), int(halo_hops), int(min_rows_per_rank), C.byref(h)))
+        check(lib.ldgmg_problem_create_ex(C.byref(cs), int(min_depth), int(bottom_max_elements), int(nranks),
+                                          int(rank), int(halo_hops), int(min_rows_per_rank),
+                                          1 if device_assembly else 0, C.byref(h)))
         obj.h = h
+        obj.device_assembly = bool(device_assembly)
         obj._init_info()
         return obj
+
+    def device_operator(self, ctx: "Context", l: int) -> "DeviceBsr":
+        """The level operator on the device (device assembly or upload)."""
+        h = C.c_void_p()
+        check(lib.ldgmg_problem_device_operator(ctx.h, self.h, int(l), C.byref(h)))
+        B = DeviceBsr.__new__(DeviceBsr)
+        B.ctx, B.h = ctx, h
+        br, bc, rb, cb, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+        check(lib.ldgmg_bsr_shape(h, C.byref(br), C.byref(bc), C.byref(rb), C.byref(cb), C.byref(nz)))
+        B.brows, B.bcols, B.row_bs, B.col_bs, B.nnzb = br.value, bc.value, rb.value, cb.value, nz.value
+        return B
 
     def level_partial(self, l) -> bool:
         return bool(lib.ldgmg_problem_level_partial(self.h, int(l)))
@@ -418,6 +439,13 @@ class Problem:
         val = np.empty(max(nnzb * bs * bs, 1), np.float64)
         check(lib.ldgmg_problem_level_matrix(self.h, l, ptr.ctypes.data, col.ctypes.data, val.ctypes.data))
         return ptr, col[:nnzb], val[: nnzb * bs * bs]
+
+    def level_pattern(self, l):
+        n, bs, nnzb = self.level_shape(l)
+        ptr = np.empty(n + 1, np.int32)
+        col = np.empty(max(nnzb, 1), np.int32)
+        check(lib.ldgmg_problem_level_matrix(self.h, l, ptr.ctypes.data, col.ctypes.data, None))
+        return ptr, col[:nnzb]
 
     def level_transfer(self, l):
         n, _, _ = self.level_shape(l)

@@ -1025,6 +1025,40 @@ int ldgmg_problem_create_partial(const ldgmg_problem_spec* spec, int min_depth, 
     });
 }
 
+int ldgmg_problem_create_ex(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements, int nranks,
+                            int rank, int halo_hops, int min_rows_per_rank, int flags, ldgmg_problem** out) {
+    return guarded([&] {
+        need(spec, "problem_create_ex");
+        need(out, "problem_create_ex");
+        auto* h = new ldgmg_problem();
+        try {
+            problem_build_partial(*spec, min_depth, bottom_max_elements, nranks, rank, halo_hops, min_rows_per_rank,
+                                  h->p, (flags & LDGMG_PROBLEM_DEVICE_ASSEMBLY) != 0);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+static std::unique_ptr<Bsr> level_operator(Ctx& ctx, const Problem& p, int l) {
+    const auto& L = p.levels[l];
+    if (L.deferred) return assemble_on_device(ctx, L.prog);
+    return bsr_upload(ctx, L.A.brows, L.A.brows, L.A.bs, L.A.bs, L.A.ptr.data(), L.A.col.data(), L.A.val.data());
+}
+
+int ldgmg_problem_device_operator(ldgmg_ctx* ctx, const ldgmg_problem* P, int level, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "problem_device_operator");
+        need(P, "problem_device_operator");
+        need(out, "problem_device_operator(out)");
+        if (level < 0 || level >= int(P->p.levels.size())) fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: bad level");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(level_operator(*ctx, P->p, level)));
+    });
+}
+
 int ldgmg_problem_level_partial(const ldgmg_problem* P, int level) {
     if (!P || level < 0 || level >= int(P->p.levels.size())) return 0;
     return P->p.levels[level].partial ? 1 : 0;
@@ -1067,6 +1101,8 @@ int ldgmg_problem_level_matrix(const ldgmg_problem* P, int level, int* ptr, int*
         need(P, "problem_level_matrix");
         if (level < 0 || level >= int(P->p.levels.size())) fail(LDGMG_ERR_INVALID_ARGUMENT, "problem: bad level");
         const auto& A = P->p.levels[level].A;
+        if (val && P->p.levels[level].deferred)
+            fail(LDGMG_ERR_LOGIC, "problem: operator assembled on the device (use ldgmg_problem_device_operator)");
         if (ptr) std::memcpy(ptr, A.ptr.data(), sizeof(int) * A.ptr.size());
         if (col) std::memcpy(col, A.col.data(), sizeof(int) * A.col.size());
         if (val) std::memcpy(val, A.val.data(), sizeof(double) * A.val.size());
@@ -1128,8 +1164,7 @@ int ldgmg_mg_create_from_problem(ldgmg_ctx* ctx, const ldgmg_problem* P, const l
         m.n_velocity = p.kind == LDGMG_SYSTEM_STOKES ? p.dim * p.bs_scalar : 0;
         SetupTimer tm("mg_create_from_problem", ctx->stream);
         for (int l = 0; l < m.depth; ++l) {
-            const auto& A = p.levels[l].A;
-            m.own_A.push_back(bsr_upload(*ctx, A.brows, A.brows, A.bs, A.bs, A.ptr.data(), A.col.data(), A.val.data()));
+            m.own_A.push_back(level_operator(*ctx, p, l));
             m.A.push_back(m.own_A.back().get());
         }
         tm.stamp("operator upload");

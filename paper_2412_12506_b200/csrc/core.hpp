@@ -42,6 +42,10 @@ void h2d_staged(Ctx& ctx, void* dst, const void* src, size_t bytes);
 void ctx_release_staging(Ctx& ctx);
 void ctx_release_blas(Ctx& ctx);
 
+struct LevelProgram;  // setup.hpp
+/// Evaluate a deferred-assembly program on the device (assembly_gpu.cu).
+std::unique_ptr<struct Bsr> assemble_on_device(Ctx& ctx, const LevelProgram& P);
+
 /// Host<->device copies ordered on the context stream (setup paths; the
 /// legacy-stream cudaMemcpy would race with the non-blocking context stream).
 inline void h2d(Ctx& ctx, void* dst, const void* src, size_t bytes) {

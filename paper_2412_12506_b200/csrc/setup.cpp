@@ -731,6 +731,230 @@ std::vector<char> with_neighbours(const LevelMesh& m, const std::vector<char>& r
     }
     return g;
 }
+
+// ------------------------------------------------ deferred (device) assembly
+/// Stored-block table of the program: the rows of the given Rows objects
+/// concatenated (bsv^2 doubles per block); base[t][r] = first block of row r.
+struct BlockTable {
+    std::vector<std::vector<int64_t>> base;
+    int64_t total = 0;
+    void add(const Rows& R) {
+        std::vector<int64_t> b(R.cols.size() + 1, 0);
+        for (size_t r = 0; r < R.cols.size(); ++r) b[r + 1] = b[r] + int64_t(R.cols[r].size());
+        for (auto& v : b) v += total;
+        total = b.back();
+        base.push_back(std::move(b));
+    }
+    int id(int t, int r, int k) const { return int(base[t][r] + k); }
+};
+
+void fill_blocks(const std::vector<const Rows*>& rows, LevelProgram& P, int bsv) {
+    int64_t total = 0;
+    for (const Rows* R : rows)
+        for (const auto& c : R->cols) total += int64_t(c.size());
+    P.blocks.resize(size_t(total) * bsv * bsv);
+    std::vector<int64_t> off;
+    int64_t o = 0;
+    for (const Rows* R : rows)
+        for (size_t r = 0; r < R->cols.size(); ++r) {
+            off.push_back(o);
+            o += int64_t(R->cols[r].size());
+        }
+    size_t idx = 0;
+    for (const Rows* R : rows) {
+        const size_t base = idx;
+        parallel_for(int(R->cols.size()), [&](int lo, int hi) {
+            for (int r = lo; r < hi; ++r)
+                std::copy(R->vals[r].begin(), R->vals[r].end(), P.blocks.begin() + off[base + r] * bsv * bsv);
+        });
+        idx += R->cols.size();
+    }
+}
+
+/// One recorded inner block: prods (b1, b2, d) in accumulation order, then
+/// an optional stored block added with scale 1.
+struct SymCell {
+    std::vector<int> b1, b2;
+    std::vector<double> d;
+    int add = -1;
+};
+using SymRow = std::map<int, SymCell>;
+
+/// at_d_b_row, recorded: the same source / block visiting order.
+void sym_at_d_b_row(const std::vector<std::pair<int, int>>& sources, const Rows& L, int tL, const Rows& R, int tR,
+                    const BlockTable& T, const std::vector<double>& d, SymRow& dst) {
+    for (const auto& [r, k1] : sources)
+        for (int k2 = 0; k2 < int(R.cols[r].size()); ++k2) {
+            SymCell& cell = dst[R.cols[r][k2]];
+            cell.b1.push_back(T.id(tL, r, k1));
+            cell.b2.push_back(T.id(tR, r, k2));
+            cell.d.push_back(d[r]);
+        }
+}
+
+/// Appends the inner blocks of `rows` (row-major in row, ascending columns)
+/// to the program; returns, per row, the inner ids of its cells.
+std::vector<std::vector<std::pair<int, int>>> emit_inner(std::vector<SymRow>& rows, LevelProgram& P) {
+    std::vector<std::vector<std::pair<int, int>>> ids(rows.size());
+    for (size_t r = 0; r < rows.size(); ++r)
+        for (auto& [j, cell] : rows[r]) {
+            const int id = int(P.inner_ptr.size()) - 1;
+            ids[r].push_back({j, id});
+            P.prod_b1.insert(P.prod_b1.end(), cell.b1.begin(), cell.b1.end());
+            P.prod_b2.insert(P.prod_b2.end(), cell.b2.begin(), cell.b2.end());
+            P.prod_d.insert(P.prod_d.end(), cell.d.begin(), cell.d.end());
+            P.inner_ptr.push_back(int64_t(P.prod_b1.size()));
+            P.inner_add.push_back(cell.add);
+        }
+    return ids;
+}
+
+struct Term {
+    int kind, idx;
+    double scale;
+};
+
+/// program_scalar: assemble_scalar (ldg_scalar.hpp:83-125) recorded.
+void program_scalar(const Ctx& c, LevelProgram& P) {
+    const int N = c.mesh->n_elements(), bs = c.bs;
+    std::array<Rows, 3> G;
+    gradient_rows(c, G);
+    Rows E;
+    penalty_rows(c, false, 0.0, 0.0, E);
+    std::vector<double> dmu(N);
+    for (int e = 0; e < N; ++e) dmu[e] = c.mu[e] * c.msc[e];
+    std::array<std::vector<std::vector<std::pair<int, int>>>, 3> src;
+    for (int k = 0; k < c.dim; ++k) src[k] = column_sources(G[k], N);
+    BlockTable T;
+    std::vector<const Rows*> tabs;
+    for (int k = 0; k < c.dim; ++k) {
+        T.add(G[k]);
+        tabs.push_back(&G[k]);
+    }
+    const int tE = c.dim;
+    T.add(E);
+    tabs.push_back(&E);
+    P.n = N;
+    P.bs = P.bsv = bs;
+    P.ncomp = 1;
+    fill_blocks(tabs, P, bs);
+    std::vector<SymRow> rows(N);
+    parallel_for(N, [&](int lo, int hi) {
+        for (int e = lo; e < hi; ++e) {
+            if (!c.want(e)) continue;
+            for (int k = 0; k < c.dim; ++k) sym_at_d_b_row(src[k][e], G[k], k, G[k], k, T, dmu, rows[e]);
+            for (int kk = 0; kk < int(E.cols[e].size()); ++kk) rows[e][E.cols[e][kk]].add = T.id(tE, e, kk);
+        }
+    });
+    const auto ids = emit_inner(rows, P);
+    P.ptr.assign(N + 1, 0);
+    for (int e = 0; e < N; ++e) {
+        P.ptr[e + 1] = P.ptr[e] + int(ids[e].size());
+        for (const auto& [j, id] : ids[e]) {
+            P.col.push_back(j);
+            P.term_kind.push_back(3);
+            P.term_idx.push_back(id);
+            P.term_scale.push_back(1.0);
+            P.term_ptr.push_back(int64_t(P.term_kind.size()));
+        }
+    }
+}
+
+/// program_stokes: assemble_stokes (ldg_stokes.hpp:102-192) recorded.
+void program_stokes(const Ctx& c, double gamma, double beta_p, double delta, LevelProgram& P) {
+    const int N = c.mesh->n_elements(), bsv = c.bs, dim = c.dim, nc = dim + 1;
+    const bool unsteady = delta > 0;
+    std::array<Rows, 3> G;
+    gradient_rows(c, G);
+    Rows Ev, Ep;
+    penalty_rows(c, false, 0.0, 0.0, Ev);
+    penalty_rows(c, true, beta_p, delta, Ep);
+    std::vector<double> dmu(N);
+    for (int e = 0; e < N; ++e) dmu[e] = c.mu[e] * c.msc[e];
+    std::array<std::vector<std::vector<std::pair<int, int>>>, 3> src;
+    for (int k = 0; k < dim; ++k) src[k] = column_sources(G[k], N);
+    BlockTable T;
+    std::vector<const Rows*> tabs;
+    for (int k = 0; k < dim; ++k) {
+        T.add(G[k]);
+        tabs.push_back(&G[k]);
+    }
+    const int tEv = dim, tEp = dim + 1;
+    T.add(Ev);
+    tabs.push_back(&Ev);
+    T.add(Ep);
+    tabs.push_back(&Ep);
+    P.n = N;
+    P.bsv = bsv;
+    P.ncomp = nc;
+    P.bs = nc * bsv;
+    fill_blocks(tabs, P, bsv);
+    // inner blocks: visc rows, then cross[i][j] rows
+    std::vector<SymRow> visc(N);
+    std::vector<std::vector<SymRow>> cross(gamma != 0.0 ? dim * dim : 0, std::vector<SymRow>(N));
+    parallel_for(N, [&](int lo, int hi) {
+        for (int e = lo; e < hi; ++e) {
+            if (!c.want(e)) continue;
+            for (int k = 0; k < dim; ++k) sym_at_d_b_row(src[k][e], G[k], k, G[k], k, T, dmu, visc[e]);
+            for (int kk = 0; kk < int(Ev.cols[e].size()); ++kk) visc[e][Ev.cols[e][kk]].add = T.id(tEv, e, kk);
+            if (gamma != 0.0)
+                for (int i = 0; i < dim; ++i)
+                    for (int j = 0; j < dim; ++j)
+                        sym_at_d_b_row(src[j][e], G[j], j, G[i], i, T, dmu, cross[i * dim + j][e]);
+        }
+    });
+    const auto vids = emit_inner(visc, P);
+    std::vector<std::vector<std::vector<std::pair<int, int>>>> cids;
+    for (auto& cr : cross) cids.push_back(emit_inner(cr, P));
+    std::array<std::vector<std::vector<std::pair<int, int>>>, 3> gsrc;
+    for (int i = 0; i < dim; ++i) gsrc[i] = column_sources(G[i], N);
+    // final rows: per cell the sub-block term lists in the saddle scatter's order
+    using CellTerms = std::vector<std::vector<Term>>;  // [sub-block] -> terms
+    std::vector<std::map<int, CellTerms>> fin(N);
+    parallel_for(N, [&](int lo, int hi) {
+        for (int r0 = lo; r0 < hi; ++r0) {
+            if (!c.want(r0)) continue;
+            auto& row = fin[r0];
+            auto add = [&](int cell, int ci, int cj, Term t) {
+                auto& ct = row[cell];
+                if (ct.empty()) ct.resize(size_t(nc) * nc);
+                ct[size_t(ci) * nc + cj].push_back(t);
+            };
+            for (const auto& [j, id] : vids[r0])
+                for (int i = 0; i < dim; ++i) add(j, i, i, {0, id, 1.0});
+            if (gamma != 0.0)
+                for (int i = 0; i < dim; ++i)
+                    for (int j = 0; j < dim; ++j)
+                        for (const auto& [cc, id] : cids[size_t(i) * dim + j][r0]) add(cc, i, j, {0, id, gamma});
+            for (int i = 0; i < dim; ++i) {
+                for (const auto& [r, kk] : gsrc[i][r0]) add(r, i, dim, {2, T.id(i, r, kk), -c.msc[r]});
+                for (int k = 0; k < int(G[i].cols[r0].size()); ++k)
+                    add(G[i].cols[r0][k], dim, i, {1, T.id(i, r0, k), -c.msc[r0]});
+            }
+            for (int k = 0; k < int(Ep.cols[r0].size()); ++k) add(Ep.cols[r0][k], dim, dim, {1, T.id(tEp, r0, k), -1.0});
+            if (unsteady) {
+                const double m = c.rho[r0] * c.msc[r0] / delta;
+                for (int i = 0; i < dim; ++i) add(r0, i, i, {4, 0, m});
+            }
+        }
+    });
+    P.ptr.assign(N + 1, 0);
+    for (int r0 = 0; r0 < N; ++r0) {
+        P.ptr[r0 + 1] = P.ptr[r0] + int(fin[r0].size());
+        for (auto& [cell, ct] : fin[r0]) {
+            P.col.push_back(cell);
+            for (const auto& terms : ct) {
+                for (const Term& t : terms) {
+                    P.term_kind.push_back(t.kind);
+                    P.term_idx.push_back(t.idx);
+                    P.term_scale.push_back(t.scale);
+                }
+                P.term_ptr.push_back(int64_t(P.term_kind.size()));
+            }
+        }
+    }
+}
+
 }  // namespace
 
 void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_elements, Problem& P) {
@@ -738,7 +962,7 @@ void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_el
 }
 
 void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int bottom_max_elements, int nranks,
-                           int rank, int halo_hops, int min_rows_per_rank, Problem& P) {
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& P, bool deferred) {
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: bad rank / rank count");
     if (halo_hops < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: negative halo");
     if (s.dim != 2 && s.dim != 3) fail(LDGMG_ERR_INVALID_ARGUMENT, "mesh: dim must be 2 or 3");
@@ -854,12 +1078,25 @@ void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int botto
             c.grows = with_neighbours(m, c.rows);
             L.partial = true;
         }
+        L.deferred = deferred;
         if (s.kind == LDGMG_SYSTEM_SCALAR) {
-            assemble_scalar(c, L.A);
+            if (deferred)
+                program_scalar(c, L.prog);
+            else
+                assemble_scalar(c, L.A);
         } else {
             if (has_kind(m, LDGMG_BC_NEUMANN) && s.gamma == 0.0)
                 fail(LDGMG_ERR_INVALID_ARGUMENT, "stokes: stress boundary conditions require the stress form");
-            assemble_stokes(c, s.gamma, s.beta_p, s.delta, L.A);
+            if (deferred)
+                program_stokes(c, s.gamma, s.beta_p, s.delta, L.prog);
+            else
+                assemble_stokes(c, s.gamma, s.beta_p, s.delta, L.A);
+        }
+        if (deferred) {  // shape of the (device-built) operator for the level queries
+            L.A.brows = L.prog.n;
+            L.A.bs = L.prog.bs;
+            L.A.ptr = L.prog.ptr;
+            L.A.col = L.prog.col;
         }
         if (l + 1 < meshes.size()) {
             const int group = 1 << s.dim;

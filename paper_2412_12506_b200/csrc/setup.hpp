@@ -74,12 +74,37 @@ struct HostCsr {
     std::vector<double, DefaultInitAlloc<double>> val;
 };
 
+/// Device-assembly program of one level operator (problem_build with
+/// deferred assembly): every operator block as the host assembly computes it,
+/// recorded instead of evaluated so the GPU (assembly_gpu.cu) can evaluate it
+/// in the same order, bit for bit.
+///   inner block  v = ((0 + d_1 B1_1^T B2_1) + d_2 B1_2^T B2_2 + ...) [+ 1.0 S]
+///                (the G_k^T D G_k accumulation of accumulate_AtDB plus the
+///                penalty block; bsv x bsv)
+///   final block  per sub-block (ncomp x ncomp of bsv x bsv): acc = 0, then
+///                per term: acc += scale * X, X an inner block, a stored block
+///                or a stored block transposed; kind 3 = the inner block
+///                itself (scalar operators); kind 4 = +scale on the diagonal.
+struct LevelProgram {
+    int n = 0, bs = 0, bsv = 0, ncomp = 1;
+    std::vector<int> ptr, col;                          // final pattern
+    std::vector<double, DefaultInitAlloc<double>> blocks;  // stored bsv^2 blocks (row-major)
+    std::vector<int64_t> inner_ptr{0};                   // prods of inner block i
+    std::vector<int> prod_b1, prod_b2, inner_add;        // block ids; add: -1 none
+    std::vector<double> prod_d;
+    std::vector<int64_t> term_ptr{0};                    // per (cell, sub-block)
+    std::vector<int> term_kind, term_idx;
+    std::vector<double> term_scale;
+};
+
 struct ProblemLevel {
     int n = 0;  // elements per axis
     HostCsr A;
     std::vector<int> phase;
     std::vector<int> parent_of, orthant_of;  // to the next coarser level
     bool partial = false;  // only the rank's rows + halo assembled (others empty)
+    bool deferred = false;  // A not built on the host: `prog` holds the device-assembly program
+    LevelProgram prog;
 };
 
 struct Problem {
@@ -97,7 +122,7 @@ void problem_build(const ldgmg_problem_spec& spec, int min_depth, int bottom_max
 /// [rank*N/P, (rank+1)*N/P) plus `halo_hops` face layers; every assembled
 /// row is bit-identical to problem_build's.  Smaller levels are complete.
 void problem_build_partial(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements, int nranks,
-                           int rank, int halo_hops, int min_rows_per_rank, Problem& out);
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& out, bool deferred = false);
 
 std::vector<double> injection_matrices(int dim, int degree);
 

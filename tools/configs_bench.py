@@ -95,6 +95,7 @@ def main():
     ap.add_argument("names", nargs="*", default=["C1", "C1-512", "C2", "C3-GS", "C3-SAI", "C4", "C5"])
     ap.add_argument("--c5n", type=int, default=16)
     ap.add_argument("--csv", default=None, help="also write reference-format CSV rows (+perf columns)")
+    ap.add_argument("--host-assembly", action="store_true", help="assemble the operators on the host (default: GPU)")
     ap.add_argument("--cycles", type=int, default=20)
     a = ap.parse_args()
     stream = torch.cuda.Stream()
@@ -105,7 +106,8 @@ def main():
     for name in a.names:
         spec, cfg, rk = cfgs[name]
         t0 = time.time()
-        P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+        P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements,
+                      device_assembly=not a.host_assembly)
         t_asm = time.time() - t0
         t0 = time.time()
         mg = g.Multigrid(ctx, cfg, P)
