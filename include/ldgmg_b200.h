@@ -191,6 +191,15 @@ int ldgmg_relax_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F,
                      int nrows);
 
 /* out[i*bs .. i*bs+bs) = x[idx[i]*bs ..]  (ghost-exchange packing; idx on the device) */
+/* Kernel projection of a rank's element slice [r0, r1) of an N-element
+ * vector in the deterministic fast mode (256 fixed global element ranges, one
+ * fixed-tree partial per range; the slice must be a union of ranges, true for
+ * contiguous partitions into P | 256 parts).  partials: 256 * ncomp doubles,
+ * the slice's ranges written; apply needs all 256 * ncomp (gathered). */
+int ldgmg_project_partials(ldgmg_ctx* ctx, const double* v_own, int N, int r0, int r1, int bs, const int* offs,
+                           int ncomp, double kval, double* partials);
+int ldgmg_project_apply(ldgmg_ctx* ctx, double* v_own, int N, int r0, int r1, int bs, const int* offs, int ncomp,
+                        double kval, const double* partials);
 int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out);
 
 /* Partition plan of one level for `nranks` contiguous element ranges

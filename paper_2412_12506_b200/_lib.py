@@ -141,6 +141,8 @@ _SIGS = {
     "ldgmg_factors_destroy": ([_P], _I),
     "ldgmg_relax": ([_P, _P, _P, _P, _P, _P, _P, _D], _I),
     "ldgmg_relax_rows": ([_P, _P, _P, _P, _P, _P, _P, _D, _P, _I], _I),
+    "ldgmg_project_partials": ([_P, _P, _I, _I, _I, _I, _P, _I, _D, _P], _I),
+    "ldgmg_project_apply": ([_P, _P, _I, _I, _I, _I, _P, _I, _D, _P], _I),
     "ldgmg_gather_blocks": ([_P, _P, _P, _I, _I, _P], _I),
     "ldgmg_partition_level": ([_I, _P, _P, _I, _I, _IP, _IP, _IP, _IP, _P, _P, _P, _P, _P], _I),
     "ldgmg_spmv": ([_P, _P, _P, _P], _I),

@@ -406,6 +406,22 @@ int ldgmg_relax_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const ldgmg_factors* F,
     });
 }
 
+int ldgmg_project_partials(ldgmg_ctx* ctx, const double* v_own, int N, int r0, int r1, int bs, const int* offs,
+                           int ncomp, double kval, double* partials) {
+    return guarded([&] {
+        need(ctx, "project_partials");
+        launch_project_partials_slice(*ctx, v_own, N, r0, r1, bs, offs, ncomp, kval, partials);
+    });
+}
+
+int ldgmg_project_apply(ldgmg_ctx* ctx, double* v_own, int N, int r0, int r1, int bs, const int* offs, int ncomp,
+                        double kval, const double* partials) {
+    return guarded([&] {
+        need(ctx, "project_apply");
+        launch_project_apply_slice(*ctx, v_own, N, r0, r1, bs, offs, ncomp, kval, partials);
+    });
+}
+
 int ldgmg_gather_blocks(ldgmg_ctx* ctx, const double* x, const int* idx, int n, int bs, double* out) {
     return guarded([&] {
         need(ctx, "gather_blocks");

@@ -168,6 +168,10 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
 /// `scratch` (>= 256 * ncomp doubles) enables the multi-CTA fast path.
 void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* comp_offsets,
                               int ncomp, double kval, bool strict_order, double* scratch = nullptr);
+void launch_project_partials_slice(Ctx& ctx, const double* v, int N, int r0, int r1, int bs, const int* offs,
+                                   int ncomp, double kval, double* part);
+void launch_project_apply_slice(Ctx& ctx, double* v, int N, int r0, int r1, int bs, const int* offs, int ncomp,
+                                double kval, const double* part);
 void launch_axpy(Ctx& ctx, int64_t n, double alpha, const double* x, double* y);
 /// deterministic fixed-tree dot (partials per CTA, ascending final sum)
 void launch_dot(Ctx& ctx, int64_t n, const double* a, const double* b, double* d_out);

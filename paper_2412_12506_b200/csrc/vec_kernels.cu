@@ -527,14 +527,14 @@ __global__ void axpy_kernel(int64_t n, double alpha, const double* __restrict__ 
 constexpr int kProjParts = 256;
 __global__ void __launch_bounds__(256) project_partial_kernel(const double* __restrict__ v, int N, int bs,
                                                               const int* __restrict__ offs, double kval,
-                                                              double* __restrict__ part) {
+                                                              double* __restrict__ part, int k0 = 0, int ebase = 0) {
     __shared__ double red[8];
     pdl_wait();
     pdl_trigger();
-    const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
+    const int k = k0 + blockIdx.x, c = blockIdx.y, off = offs[c];
     const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
     double s = 0.0;
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) s = madd_rn(s, v[size_t(e) * bs + off], kval);
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) s = madd_rn(s, v[size_t(e - ebase) * bs + off], kval);
     for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -546,12 +546,13 @@ __global__ void __launch_bounds__(256) project_partial_kernel(const double* __re
 }
 __global__ void __launch_bounds__(256) project_apply_kernel(double* __restrict__ v, int N, int bs,
                                                             const int* __restrict__ offs, double kval,
-                                                            const double* __restrict__ part) {
+                                                            const double* __restrict__ part, int k0 = 0,
+                                                            int ebase = 0) {
     __shared__ double red[8];
     __shared__ double md;
     pdl_wait();
     pdl_trigger();
-    const int k = blockIdx.x, c = blockIdx.y, off = offs[c];
+    const int k = k0 + blockIdx.x, c = blockIdx.y, off = offs[c];
     double s = part[c * kProjParts + threadIdx.x];
     for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(256) project_apply_kernel(double* __restrict__
     const double m = md;
     const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        double& xv = v[size_t(e) * bs + off];
+        double& xv = v[size_t(e - ebase) * bs + off];
         xv = __dadd_rn(xv, __dmul_rn(m, kval));
     }
 }
@@ -726,15 +727,50 @@ void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* com
         static bool once = (max_carveout(project_partial_kernel), max_carveout(project_apply_kernel), true);
         (void)once;
         launch_pdl(project_partial_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream,
-                   static_cast<const double*>(v), N, bs, comp_offsets, kval, scratch);
+                   static_cast<const double*>(v), N, bs, comp_offsets, kval, scratch, 0, 0);
         after_launch("project_partial_kernel");
         launch_pdl(project_apply_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream, v, N, bs, comp_offsets,
-                   kval, static_cast<const double*>(scratch));
+                   kval, static_cast<const double*>(scratch), 0, 0);
         after_launch("project_apply_kernel");
     } else {
         project_fast_kernel<<<ncomp, 1024, 0, ctx.stream>>>(v, N, bs, comp_offsets, ncomp, kval);
         after_launch("project_fast_kernel");
     }
+}
+
+/// Fast projection over a rank's element slice [r0, r1): the ranges of the
+/// 256 fixed global ranges that lie inside the slice (the slice must be a
+/// union of ranges); same per-range trees as launch_project_constants.
+static void slice_ranges(int N, int r0, int r1, int& k0, int& nk) {
+    k0 = -1;
+    nk = 0;
+    for (int k = 0; k < kProjParts; ++k) {
+        const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
+        if (e0 >= r0 && e1 <= r1 && e1 > e0) {
+            if (k0 < 0) k0 = k;
+            ++nk;
+        } else if ((e0 < r1 && e1 > r0) && !(e0 >= r0 && e1 <= r1)) {
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "project: rank slice is not a union of the 256 projection ranges");
+        }
+    }
+}
+
+void launch_project_partials_slice(Ctx& ctx, const double* v, int N, int r0, int r1, int bs, const int* offs,
+                                   int ncomp, double kval, double* part) {
+    int k0, nk;
+    slice_ranges(N, r0, r1, k0, nk);
+    if (!nk || !ncomp) return;
+    project_partial_kernel<<<dim3(nk, ncomp), 256, 0, ctx.stream>>>(v, N, bs, offs, kval, part, k0, r0);
+    after_launch("project_partial_kernel");
+}
+
+void launch_project_apply_slice(Ctx& ctx, double* v, int N, int r0, int r1, int bs, const int* offs, int ncomp,
+                                double kval, const double* part) {
+    int k0, nk;
+    slice_ranges(N, r0, r1, k0, nk);
+    if (!nk || !ncomp) return;
+    project_apply_kernel<<<dim3(nk, ncomp), 256, 0, ctx.stream>>>(v, N, bs, offs, kval, part, k0, r0);
+    after_launch("project_apply_kernel");
 }
 
 void launch_gather_blocks(Ctx& ctx, const double* x, const int* idx, int n, int bs, double* out) {

@@ -154,6 +154,14 @@ class GpuOps:
     def gather(self, x, idx, n, bs, out):
         check(lib.ldgmg_gather_blocks(self.ctx.h, x.data_ptr(), idx.data_ptr(), int(n), int(bs), out.data_ptr()))
 
+    def project_partials(self, v_own, N, r0, r1, bs, offs, kval, part):
+        check(lib.ldgmg_project_partials(self.ctx.h, v_own.data_ptr(), int(N), int(r0), int(r1), int(bs),
+                                         offs.data_ptr(), int(offs.numel()), float(kval), part.data_ptr()))
+
+    def project_apply(self, v_own, N, r0, r1, bs, offs, kval, part):
+        check(lib.ldgmg_project_apply(self.ctx.h, v_own.data_ptr(), int(N), int(r0), int(r1), int(bs),
+                                      offs.data_ptr(), int(offs.numel()), float(kval), part.data_ptr()))
+
     def to_host(self, t):
         return t.detach().cpu().numpy()
 
@@ -394,14 +402,97 @@ class DistMultigrid:
         x_own.copy_(d["x"][:n_own * bs])
         self.project(x_own)
 
-    def cycle(self, x_own, b_own):
-        """Multigrid::cycle on the owned slices (multigrid.hpp:82-85)."""
+    def project_fast(self, v_own):
+        """Kernel projection in the deterministic FAST mode, entirely on the
+        device (capturable): the 256 fixed global ranges of the single-GPU
+        fast projection, each summed by the rank that owns it, all-gathered
+        and combined in the same fixed tree -- bit-identical to the single-GPU
+        fast mode and independent of P (P must divide 256)."""
+        if not self.koffs:
+            return
+        torch = self.ops.torch
+        N0, bs = self.N0, self.bs
+        r0, r1 = self.owned_range()
+        if not hasattr(self, "_pf"):
+            nc = len(self.koffs)
+            owner = np.array([next(q for q in range(self.P)
+                                   if q * N0 // self.P <= k * N0 // 256 < (q + 1) * N0 // self.P)
+                              for k in range(256)])
+            idx = torch.as_tensor(np.concatenate([owner * (256 * nc) + c * 256 + np.arange(256)
+                                                  for c in range(nc)])).to(self.ops.tensor(1).device)
+            self._pf = {"offs": self.ops.itensor(np.asarray(self.koffs, np.int32)),
+                        "part": self.ops.tensor(256 * nc), "all": [self.ops.tensor(256 * nc) for _ in range(self.P)],
+                        "idx": idx, "full": self.ops.tensor(256 * nc),
+                        "kval": 1.0 / np.sqrt(float(N0))}
+        pf = self._pf
+        pf["part"].zero_()
+        self.ops.project_partials(v_own, N0, r0, r1, bs, pf["offs"], pf["kval"], pf["part"])
+        self.dist.all_gather(pf["all"], pf["part"], group=self.group)
+        pf["full"].copy_(torch.cat(pf["all"])[pf["idx"]])
+        self.ops.project_apply(v_own, N0, r0, r1, bs, pf["offs"], pf["kval"], pf["full"])
+
+    def _cycle_body(self, x_own, b_own, fast):
         d, bs = self.L[0], self.bs
         n_own = d["plan"].n_own
         d["x"][:n_own * bs] = x_own
         self._vcycle(0, b_own)
         x_own.copy_(d["x"][:n_own * bs])
-        self.project(x_own)
+        if fast:
+            self.project_fast(x_own)
+        else:
+            self.project(x_own)
+
+    def cycle(self, x_own, b_own, fast=False):
+        """Multigrid::cycle on the owned slices (multigrid.hpp:82-85).  fast:
+        device-side deterministic projection (and the captured graph when
+        enable_graph succeeded) instead of the reference-order host sum."""
+        g = getattr(self, "_graph", None)
+        if fast and g is not None:
+            self._gx.copy_(x_own)
+            self._gb.copy_(b_own)
+            g.replay()
+            x_own.copy_(self._gx)
+            return
+        self._cycle_body(x_own, b_own, fast)
+
+    def enable_graph(self, x_probe, b_probe):
+        """Capture one fast-mode cycle (V-cycle kernels, NCCL exchanges and
+        the device projection) as a CUDA graph, then VALIDATE it: a replay
+        from (x_probe, b_probe) must equal an eager fast cycle bit for bit.
+        Any capture error or mismatch leaves the eager path in place.
+        Returns True when the graph is in use."""
+        torch = self.ops.torch
+        self._graph = None
+        ok, g = False, None
+        if torch.cuda.current_stream() == torch.cuda.default_stream():
+            self._graph_error = "graph capture needs the hierarchy on a non-default stream"
+        try:
+            if getattr(self, "_graph_error", None):
+                raise RuntimeError(self._graph_error)
+            x_e = x_probe.clone()
+            self._cycle_body(x_e, b_probe, True)  # eager reference + warm-up
+            self._gx = x_probe.clone()
+            self._gb = b_probe.clone()
+            g = torch.cuda.CUDAGraph()
+            torch.cuda.synchronize()
+            n0 = L.launch_count()
+            with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
+                self._cycle_body(self._gx, self._gb, True)
+            self.graph_kernels = L.launch_count() - n0  # our kernels per replay
+            self._gx.copy_(x_probe)
+            self._gb.copy_(b_probe)
+            g.replay()
+            torch.cuda.synchronize()
+            ok = bool(torch.equal(self._gx, x_e))
+        except Exception as exc:  # capture not supported for some op: stay eager
+            self._graph_error = repr(exc)
+            ok = False
+        # every rank reaches this collective, whatever happened above
+        okt = torch.tensor([1 if ok else 0], dtype=torch.int32, device=x_probe.device)
+        self.dist.all_reduce(okt, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(okt.item()) == 1:
+            self._graph = g
+        return self._graph is not None
 
     def cycle_costs(self):
         """(DOF-updates, algorithmic HBM bytes) of one cycle on THIS rank: its

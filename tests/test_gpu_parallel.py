@@ -91,3 +91,37 @@ def test_distributed_krylov_world1_matches_single_gpu_strict(ctx, dist1, kind):
     got = parallel.DistKrylov(dm).estimate_eta(kind=kind, seed=3, tol=1e-12, maxit=30)
     assert np.array_equal(got["residuals"], want["residuals"])
     assert got["iterations"] == want["iterations"] and got["eta"] == want["eta"]
+
+
+def test_fast_projection_and_graph_world1(dist1):
+    """Fast-mode distributed cycle (device projection over the 256 fixed
+    ranges) = single-GPU fast mode bitwise; the captured whole-cycle graph
+    validates and replays identically."""
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        _fast_projection_and_graph(g.Context(0, stream=stream), dist1)
+
+
+def _fast_projection_and_graph(ctx, dist1):
+    from paper_2412_12506_b200 import parallel
+    spec, cfg = K.scalar(16, 2, K.P, degree=2), K.cfg("sai", level=1, nu=2)
+    dm = parallel.from_problem(ctx, g.Problem(spec, min_depth=cfg.min_depth), cfg, dist1, min_rows_per_rank=16)
+    full = dm._full
+    full.set_strict_order(False)
+    n, bs = full.n, full.bs
+    b = torch.as_tensor(np.random.default_rng(3).uniform(-1, 1, n * bs)).cuda()
+    xs, xd = torch.zeros_like(b), torch.zeros_like(b)
+    for _ in range(2):
+        full.cycle(xs, b)
+        dm.cycle(xd, b, fast=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(xs.cpu().numpy(), xd.cpu().numpy())
+    assert dm.enable_graph(torch.zeros_like(b), b), getattr(dm, "_graph_error", "")
+    assert dm.graph_kernels > 0
+    xg = torch.zeros_like(b)
+    xe = torch.zeros_like(b)
+    for _ in range(2):
+        dm.cycle(xg, b, fast=True)        # graph replay
+        dm._cycle_body(xe, b, True)       # eager
+    torch.cuda.synchronize()
+    assert np.array_equal(xg.cpu().numpy(), xe.cpu().numpy())
