@@ -112,6 +112,7 @@ class RefMultigrid:
         if not h:
             raise RefError(-1, lib().ref_last_error().decode())
         self.h = h
+        self._destroy = lib().ref_mg_destroy  # bound now: module globals are gone at interpreter exit
         self.depth = lib().ref_mg_depth(h)
         dim, nc, bss, kc, kp, nv = (C.c_int() for _ in range(6))
         _chk(lib().ref_system_info(h, *(C.byref(v) for v in (dim, nc, bss, kc, kp, nv))))
@@ -120,7 +121,7 @@ class RefMultigrid:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().ref_mg_destroy(self.h)
+            self._destroy(self.h)
             self.h = None
 
     def shape(self, l):

@@ -1,7 +1,7 @@
 """GPU SAI build (batched least squares) against the reference build_sai
 (smoothers.hpp:259-367): identical pattern / index arrays, identical cache
 statistics and LS shapes (tests/test_smoothers.cpp:398-543,
-tests/test_multigrid.cpp:309-325), B within 1e-11 relative Frobenius norm of
+tests/test_multigrid.cpp:309-325), B within 1e-12 relative Frobenius norm of
 the reference's LAPACK-dgels B, and the stored-block normal equations
 (test_smoothers.cpp:324-348)."""
 import numpy as np
@@ -13,7 +13,7 @@ from tests import cases as K
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-B_RTOL = 1e-11
+B_RTOL = 1e-12  # measured: <= 8.1e-15 on every case below
 
 
 def build_pair(ctx, ref, spec, level, zeta=0.1, cache=True):
@@ -44,6 +44,8 @@ SYSTEMS = {
     "scalar2d-ball-p4-C3": (K.baseline_configs()["C3-SAI"][0], [1], 0.1),
     "stokes2d-stress-p1": (K.stokes(4, 2, K.P, gamma=1.0, degree=1), [0, 1], 0.1),
     "stokes2d-standard-p3-C4": (K.baseline_configs()["C4"][0], [1], 0.0990),
+    # C5 shape (2700x756 least squares, k=108: the wide-panel cuBLAS path)
+    "stokes3d-unsteady-p2-C5": (K.baseline_configs()["C5"][0], [1], 0.107),
 }
 
 
@@ -57,7 +59,7 @@ def test_gpu_sai_matches_reference(ctx, ref, name):
         err = np.linalg.norm(bv - Bref[2]) / np.linalg.norm(Bref[2])
         assert err <= B_RTOL, (name, level, err)
         # every block, not only the aggregate (a few wrong columns must not hide)
-        assert np.max(np.abs(bv - Bref[2])) <= 1e-9 * np.max(np.abs(Bref[2])), (name, level)
+        assert np.max(np.abs(bv - Bref[2])) <= 1e-12 * np.max(np.abs(Bref[2])), (name, level)
         gs = S.sai_stats()
         assert (gs.cache_hits, gs.cache_misses) == (st.cache_hits, st.cache_misses)
         assert gs.rank_deficient_columns == st.rank_deficient_columns
