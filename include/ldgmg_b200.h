@@ -91,7 +91,7 @@ typedef struct ldgmg_sai_stats {
 typedef struct ldgmg_problem_spec {
     int kind;          /* LDGMG_SYSTEM_SCALAR / _STOKES */
     int dim;           /* 2 or 3 */
-    int n;             /* elements per axis (power of two) */
+    int n;             /* elements per axis (power of two; any n >= 2 with LDGMG_PROBLEM_ANY_N) */
     int degree;        /* polynomial degree p */
     int bc[6];         /* per side 2*axis+{0 lower,1 upper}: LDGMG_BC_* */
     double beta;       /* <=0: 4 p^2 (library default, ldg_core.hpp:101) */
@@ -357,7 +357,11 @@ int ldgmg_problem_level_partial(const ldgmg_problem* P, int level);
  * bit-identical to the host assembly (ldgmg_problem_device_operator,
  * ldgmg_mg_create_from_problem).  ldgmg_problem_level_matrix then returns the
  * pattern only (val must be NULL). */
-enum { LDGMG_PROBLEM_DEVICE_ASSEMBLY = 1 };
+/* LDGMG_PROBLEM_ANY_N = extension A1 (the reference
+ * requires a power of two, mesh.hpp:143-149): n may be any count >= 2; the
+ * elements are the in-range cells of the bounding power-of-two grid in its
+ * Morton order, and coarsening halves n while it is even (48 -> ... -> 3). */
+enum { LDGMG_PROBLEM_DEVICE_ASSEMBLY = 1, LDGMG_PROBLEM_ANY_N = 2 };
 int ldgmg_problem_create_ex(const ldgmg_problem_spec* spec, int min_depth, int bottom_max_elements, int nranks,
                             int rank, int halo_hops, int min_rows_per_rank, int flags, ldgmg_problem** out);
 /* the level operator as a device BSR (device assembly, or upload of the host one) */

@@ -94,6 +94,7 @@ class SolveReportC(C.Structure):
 
 
 KRYLOV_CG, KRYLOV_GMRES = 0, 1
+PROBLEM_DEVICE_ASSEMBLY, PROBLEM_ANY_N = 1, 2  # ldgmg_problem_create_ex flags
 
 
 def _load():

@@ -369,15 +369,18 @@ class ProblemSpec:
 class Problem:
     """Built-in host setup: mesh chain + LDG operators per level."""
 
-    def __init__(self, spec: ProblemSpec, min_depth=2, bottom_max_elements=64, device_assembly=False):
+    def __init__(self, spec: ProblemSpec, min_depth=2, bottom_max_elements=64, device_assembly=False, any_n=False):
         """device_assembly: the level operators are assembled on the GPU when a
         hierarchy / device operator is created (bit-identical to the host
-        assembly; level_matrix then returns no values)."""
+        assembly; level_matrix then returns no values).
+        any_n: extension A1 -- spec.n need not be a
+        power of two (Morton order of the bounding grid, restricted)."""
         self.spec = spec
         cs = spec.c()
         h = C.c_void_p()
-        if device_assembly:
-            check(lib.ldgmg_problem_create_ex(C.byref(cs), int(min_depth), int(bottom_max_elements), 1, 0, 0, 0, 1,
+        flags = (L.PROBLEM_DEVICE_ASSEMBLY if device_assembly else 0) | (L.PROBLEM_ANY_N if any_n else 0)
+        if flags:
+            check(lib.ldgmg_problem_create_ex(C.byref(cs), int(min_depth), int(bottom_max_elements), 1, 0, 0, 0, flags,
                                               C.byref(h)))
         else:
             check(lib.ldgmg_problem_create(C.byref(cs), int(min_depth), int(bottom_max_elements), C.byref(h)))
@@ -397,7 +400,7 @@ class Problem:
 
     @classmethod
     def partial(cls, spec: ProblemSpec, nranks: int, rank: int, halo_hops: int, min_rows_per_rank: int = 64,
-                min_depth=2, bottom_max_elements=64, device_assembly=False) -> "Problem":
+                min_depth=2, bottom_max_elements=64, device_assembly=False, any_n=False) -> "Problem":
         """Distributed setup (ldgmg_problem_create_partial): levels with >=
         nranks*min_rows_per_rank elements assemble only this rank's rows plus
         `halo_hops` face layers (other rows empty, global numbering kept)."""
@@ -407,7 +410,8 @@ class Problem:
         h = C.c_void_p()
         check(lib.ldgmg_problem_create_ex(C.byref(cs), int(min_depth), int(bottom_max_elements), int(nranks),
                                           int(rank), int(halo_hops), int(min_rows_per_rank),
-                                          1 if device_assembly else 0, C.byref(h)))
+                                          (L.PROBLEM_DEVICE_ASSEMBLY if device_assembly else 0)
+                                          | (L.PROBLEM_ANY_N if any_n else 0), C.byref(h)))
         obj.h = h
         obj.device_assembly = bool(device_assembly)
         obj._init_info()

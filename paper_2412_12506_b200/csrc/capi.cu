@@ -1049,7 +1049,7 @@ int ldgmg_problem_create_ex(const ldgmg_problem_spec* spec, int min_depth, int b
         auto* h = new ldgmg_problem();
         try {
             problem_build_partial(*spec, min_depth, bottom_max_elements, nranks, rank, halo_hops, min_rows_per_rank,
-                                  h->p, (flags & LDGMG_PROBLEM_DEVICE_ASSEMBLY) != 0);
+                                  h->p, (flags & LDGMG_PROBLEM_DEVICE_ASSEMBLY) != 0, (flags & LDGMG_PROBLEM_ANY_N) != 0);
         } catch (...) {
             delete h;
             throw;

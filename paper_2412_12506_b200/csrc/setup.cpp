@@ -124,6 +124,10 @@ struct LevelMesh {
     double h = 0.5;
     std::vector<std::array<int, 3>> idx;  // Morton order
     std::vector<int> phase;
+    // extension A1: the elements are the in-range cells
+    // of the 2^level grid, in its Morton order; Morton code -> element index
+    // (empty: the identity, n a power of two on the reference's path)
+    std::vector<int> code2elem;
 
     bool periodic(int a) const { return bc[2 * a] == LDGMG_BC_PERIODIC; }
     int n_elements() const { return int(idx.size()); }
@@ -133,7 +137,7 @@ struct LevelMesh {
         int code = 0;
         for (int b = 0; b < level; ++b)
             for (int a = 0; a < dim; ++a) code |= ((ix[a] >> b) & 1) << (b * dim + a);
-        return code;
+        return code2elem.empty() ? code : code2elem[code];
     }
     /// Faces of element e in the reference's canonical local order
     /// (element_face_table, ldg_core.hpp:287-309): axis-major, lower first.
@@ -172,28 +176,43 @@ struct LevelMesh {
     }
 };
 
-LevelMesh uniform_mesh(int n, int dim, const int* bc) {
+/// build_uniform (mesh.hpp:143-183): Morton-ordered uniform mesh.  any_n
+/// (extension A1): n need not be a power of two -- the elements are the cells
+/// of the bounding 2^ceil(log2 n) grid with every index < n, kept in that
+/// grid's Morton order (so 2^d siblings stay contiguous whenever n is even
+/// and the order stays monotone along every axis), h = 1/n.  For a power of
+/// two this is exactly the reference's mesh.
+LevelMesh uniform_mesh(int n, int dim, const int* bc, bool any_n = false) {
     LevelMesh m;
     m.dim = dim;
     m.n = n;
     if (n < 2) throw std::invalid_argument("mesh: need at least 2 elements per axis");
-    if (n & (n - 1)) throw std::invalid_argument("mesh: element count per axis must be a power of two");
+    const bool pow2 = (n & (n - 1)) == 0;
+    if (!pow2 && !any_n) throw std::invalid_argument("mesh: element count per axis must be a power of two");
     m.level = 0;
     while ((1 << m.level) < n) ++m.level;
-    m.h = std::ldexp(1.0, -m.level);
+    m.h = pow2 ? std::ldexp(1.0, -m.level) : 1.0 / n;
     for (int i = 0; i < 6; ++i) m.bc[i] = bc[i];
     for (int a = 0; a < dim; ++a)
         if ((bc[2 * a] == LDGMG_BC_PERIODIC) != (bc[2 * a + 1] == LDGMG_BC_PERIODIC))
             throw std::invalid_argument("mesh: periodic boundaries must pair opposite sides");
-    const int total = dim == 2 ? n * n : n * n * n;
-    m.idx.resize(total);
-    for (int code = 0; code < total; ++code) {
+    const int side = 1 << m.level;
+    const int64_t codes = dim == 2 ? int64_t(side) * side : int64_t(side) * side * side;
+    const int64_t total = dim == 2 ? int64_t(n) * n : int64_t(n) * n * n;
+    if (total > (int64_t(1) << 30)) throw std::invalid_argument("mesh: too many elements");
+    m.idx.reserve(size_t(total));
+    if (any_n) m.code2elem.assign(size_t(codes), -1);
+    for (int64_t code = 0; code < codes; ++code) {
         std::array<int, 3> ix{0, 0, 0};
         for (int b = 0; b < m.level; ++b)
-            for (int a = 0; a < dim; ++a) ix[a] |= ((code >> (b * dim + a)) & 1) << b;
-        m.idx[code] = ix;
+            for (int a = 0; a < dim; ++a) ix[a] |= int((code >> (b * dim + a)) & 1) << b;
+        bool in = true;
+        for (int a = 0; a < dim; ++a) in &= ix[a] < n;
+        if (!in) continue;
+        if (any_n) m.code2elem[size_t(code)] = int(m.idx.size());
+        m.idx.push_back(ix);
     }
-    m.phase.assign(total, 0);
+    m.phase.assign(size_t(total), 0);
     return m;
 }
 
@@ -962,7 +981,7 @@ void problem_build(const ldgmg_problem_spec& s, int min_depth, int bottom_max_el
 }
 
 void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int bottom_max_elements, int nranks,
-                           int rank, int halo_hops, int min_rows_per_rank, Problem& P, bool deferred) {
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& P, bool deferred, bool any_n) {
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: bad rank / rank count");
     if (halo_hops < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "partition: negative halo");
     if (s.dim != 2 && s.dim != 3) fail(LDGMG_ERR_INVALID_ARGUMENT, "mesh: dim must be 2 or 3");
@@ -1005,12 +1024,13 @@ void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int botto
 
     // mesh chain (multigrid.hpp:168-194)
     std::vector<LevelMesh> meshes;
-    meshes.push_back(uniform_mesh(s.n, s.dim, s.bc));
+    meshes.push_back(uniform_mesh(s.n, s.dim, s.bc, any_n));
     if (s.phase_shape == LDGMG_PHASE_BOXES) assign_box_phases(meshes[0], regs);
     for (;;) {
         const LevelMesh& m = meshes.back();
         if (m.n < 4) break;  // coarsen: uniform mesh already at n=2
-        LevelMesh cm = uniform_mesh(m.n / 2, m.dim, m.bc);
+        if (m.n & 1) break;  // A1: an odd count has no sibling groups (48 -> 24 -> 12 -> 6 -> 3)
+        LevelMesh cm = uniform_mesh(m.n / 2, m.dim, m.bc, any_n);
         const int group = 1 << m.dim;
         bool phase_ok = true;
         for (int p = 0; p < cm.n_elements(); ++p) {

@@ -122,7 +122,8 @@ void problem_build(const ldgmg_problem_spec& spec, int min_depth, int bottom_max
 /// [rank*N/P, (rank+1)*N/P) plus `halo_hops` face layers; every assembled
 /// row is bit-identical to problem_build's.  Smaller levels are complete.
 void problem_build_partial(const ldgmg_problem_spec& spec, int min_depth, int bottom_max_elements, int nranks,
-                           int rank, int halo_hops, int min_rows_per_rank, Problem& out, bool deferred = false);
+                           int rank, int halo_hops, int min_rows_per_rank, Problem& out, bool deferred = false,
+                           bool any_n = false);
 
 std::vector<double> injection_matrices(int dim, int degree);
 
