@@ -888,16 +888,23 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
         const double bn = std::sqrt(ctx->h_red[0]);
+        // With an SAI level-0 smoother the residual check of iterate k is the
+        // first kernel of cycle k+1 (r = b - A x, same kernel, same bits):
+        // compute it into the smoother's residual buffer and let the cycle
+        // start from it, one level-0 pass saved per iteration.
+        double* rbuf = m.r0_buffer();
+        const bool reuse = rbuf != nullptr;
+        if (!rbuf) rbuf = r.as<double>();
         auto relres = [&]() {
             RowPass p;
             p.A = m.A[0];
             p.mode = MODE_RESIDUAL;
             p.x = x.as<double>();
             p.b = b.as<double>();
-            p.y = r.as<double>();
+            p.y = rbuf;
             p.nrows = m.A[0]->brows;
             launch_rowpass(*ctx, p);
-            launch_dot(*ctx, n, r.as<double>(), r.as<double>(), ctx->d_red);
+            launch_dot(*ctx, n, rbuf, rbuf, ctx->d_red);
             LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
             LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
             return bn > 0 ? std::sqrt(ctx->h_red[0]) / bn : std::sqrt(ctx->h_red[0]);
@@ -906,7 +913,7 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         if (history) history[0] = rr;
         int it = 0;
         while (rr > tol && it < maxit) {
-            m.cycles(*ctx, x.as<double>(), b.as<double>(), 1);
+            m.cycles(*ctx, x.as<double>(), b.as<double>(), 1, reuse);
             ++it;
             rr = relres();
             if (history) history[it] = rr;

@@ -213,7 +213,7 @@ void Smoother::init_common(Ctx& ctx) {
     (void)ctx;
 }
 
-void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep) const {
+void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready) const {
     switch (cfg.kind) {
         case LDGMG_JACOBI: {
             LDGMG_CUDA(cudaMemcpyAsync(snap.p, x, sizeof(double) * size_t(N) * bs,
@@ -273,14 +273,16 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep) const {
         }
         case LDGMG_SAI: {
             double* r = snap.as<double>();
-            RowPass p;
-            p.A = A;
-            p.mode = MODE_RESIDUAL;
-            p.x = x;
-            p.b = b;
-            p.y = r;
-            p.nrows = N;
-            launch_rowpass(ctx, p);
+            if (!r_ready) {
+                RowPass p;
+                p.A = A;
+                p.mode = MODE_RESIDUAL;
+                p.x = x;
+                p.b = b;
+                p.y = r;
+                p.nrows = N;
+                launch_rowpass(ctx, p);
+            }
             RowPass q;
             q.A = sweep == LDGMG_SWEEP_FORWARD ? B.get() : &bsr_transpose(ctx, *B);
             q.mode = MODE_ADD;
@@ -435,7 +437,7 @@ void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
     h2d(ctx, bottom.lambda.p, lam.data(), sizeof(double) * n);
 }
 
-void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
+void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready) {
     if (l + 1 == depth) {
         launch_pinv_apply(ctx, bottom, cfg.bottom_tol, b, x);
         return;
@@ -445,7 +447,7 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b) {
         return;
     }
     const Smoother& S = *sm[l];
-    for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre);
+    for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre, r0_ready && i == 0);
     RowPass p;
     p.A = A[l];
     p.mode = MODE_RESIDUAL;
@@ -465,8 +467,14 @@ void Mg::project(Ctx& ctx, double* v) {
                              red.as<double>());
 }
 
-void Mg::cycle(Ctx& ctx, double* x, const double* b) {
-    v_cycle(ctx, 0, x, b);
+double* Mg::r0_buffer() const {
+    if (depth < 2 || cfg.nu1 < 1 || sm.empty() || !sm[0] || sm[0]->cfg.kind != LDGMG_SAI) return nullptr;
+    return sm[0]->snap.as<double>();
+}
+
+void Mg::cycle(Ctx& ctx, double* x, const double* b, bool r0_ready) {
+    require(!r0_ready || r0_buffer(), "multigrid: no level-0 residual to start from");
+    v_cycle(ctx, 0, x, b, r0_ready);
     project(ctx, x);
 }
 
@@ -483,10 +491,11 @@ void Mg::apply(Ctx& ctx, const double* b, double* x) {
     project(ctx, x);
 }
 
-void Mg::cycles(Ctx& ctx, double* x, const double* b, int n) {
+void Mg::cycles(Ctx& ctx, double* x, const double* b, int n, bool r0_ready) {
     if (n <= 0) return;
+    require(n == 1 || !r0_ready, "multigrid: a precomputed residual serves one cycle");
     if (!warm) {  // first run un-captured: sets kernel attributes, lazy transposes
-        cycle(ctx, x, b);
+        cycle(ctx, x, b, r0_ready);
         --n;
         warm = true;
         LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -494,9 +503,9 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n) {
     if (n <= 0) return;
     Graph* G = nullptr;
     for (auto& g : graphs)
-        if (g.x == x && g.b == b && g.s == ctx.stream) G = &g;
+        if (g.x == x && g.b == b && g.s == ctx.stream && g.r0 == r0_ready) G = &g;
     if (!G) {
-        Graph ng{x, b, ctx.stream, nullptr, 0};
+        Graph ng{x, b, ctx.stream, nullptr, 0, r0_ready};
         cudaGraph_t graph;
         const int64_t c0 = launch_counter().load();
         // capture on a private non-blocking stream (the context stream may be
@@ -506,7 +515,7 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n) {
         Ctx cctx = ctx;
         cctx.stream = cap_stream;
         LDGMG_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
-        cycle(cctx, x, b);
+        cycle(cctx, x, b, r0_ready);
         LDGMG_CUDA(cudaStreamEndCapture(cap_stream, &graph));
         // captured launches did not run; they are counted per graph launch
         ng.nkernels = launch_counter().load() - c0;

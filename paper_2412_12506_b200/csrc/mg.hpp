@@ -49,7 +49,10 @@ struct Smoother {
     std::vector<int> sched_ptr[2];
 
     void init_common(Ctx& ctx);
-    void apply(Ctx& ctx, const double* b, double* x, int sweep) const;
+    /// `r_ready`: SAI only -- `snap` already holds b - A x for this x (the
+    /// caller's residual check computed it with the same kernel), so the
+    /// sweep's own residual pass is skipped; the bits are unchanged.
+    void apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready = false) const;
     double bytes_per_apply() const;
 };
 
@@ -82,6 +85,7 @@ struct Mg {
         cudaStream_t s;
         cudaGraphExec_t exec;
         int64_t nkernels;
+        bool r0;  // captured with the level-0 residual precomputed (cycle(..., r0_ready))
     };
     std::vector<Graph> graphs;
     cudaStream_t cap_stream = nullptr;
@@ -104,11 +108,14 @@ struct Mg {
 
     void init(Ctx& ctx);
     void set_bottom(Ctx& ctx, const double* V, const double* lambda);
-    void v_cycle(Ctx& ctx, int l, double* x, const double* b);
+    void v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready = false);
     void project(Ctx& ctx, double* v);
-    void cycle(Ctx& ctx, double* x, const double* b);
+    void cycle(Ctx& ctx, double* x, const double* b, bool r0_ready = false);
     void apply(Ctx& ctx, const double* b, double* x);
-    void cycles(Ctx& ctx, double* x, const double* b, int n);
+    void cycles(Ctx& ctx, double* x, const double* b, int n, bool r0_ready = false);
+    /// Level-0 residual buffer the first pre-smoothing sweep can start from
+    /// (SAI smoother with nu1 >= 1), nullptr when the smoother has none.
+    double* r0_buffer() const;
     double dof_updates_per_cycle() const;
     double bytes_per_cycle() const;
     ~Mg();

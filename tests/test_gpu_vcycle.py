@@ -177,3 +177,28 @@ def test_kernel_preserved_and_textbook_contraction(ctx, ref):
     for i in range(5):
         assert hist[i + 1] < 0.4 * hist[i]
     assert hist[5] < 5e-3
+
+
+@pytest.mark.parametrize("name", ["C2", "C1"])
+def test_solve_host_equals_cycle_loop_bitwise(ctx, name):
+    """solve_host reuses its residual check as the first pass of the next SAI
+    sweep: the iterate and the history must be bit-identical to a plain loop of
+    cycle() + residual norm (C1 = Jacobi, where nothing is reused)."""
+    spec, cfg = K.baseline_configs()[name]
+    P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+    mg = g.Multigrid(ctx, cfg, P)
+    b = rand(mg.n * mg.bs, 3)
+    xs, hs, its = mg.solve_host(b, tol=0.0, maxit=4)
+    xs2, hs2, _ = mg.solve_host(b, tol=0.0, maxit=4)  # second call replays the cached graphs
+    assert its == 4 and np.array_equal(xs, xs2) and np.array_equal(hs, hs2)
+    bd = dev(b)
+    xd = torch.zeros_like(bd)
+    A0 = P.device_operator(ctx, 0) if hasattr(P, "device_operator") else None
+    for _ in range(4):
+        mg.cycle(xd, bd)
+    assert np.array_equal(host(xd), xs)
+    if A0 is not None:
+        r = torch.empty_like(bd)
+        g.residual(ctx, A0, bd, xd, r)
+        rn = np.linalg.norm(host(r)) / np.linalg.norm(b)
+        assert abs(rn - hs[-1]) <= 1e-14 * max(rn, 1e-300)
