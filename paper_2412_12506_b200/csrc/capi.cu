@@ -14,6 +14,7 @@
 #include "core.hpp"
 #include "formats.hpp"
 #include "mg.hpp"
+#include "host_eig.hpp"
 #include "krylov.hpp"
 #include "setup.hpp"
 
@@ -874,20 +875,36 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
             m.h_stage = nullptr;
             LDGMG_CUDA(cudaMallocHost(&m.h_stage, sizeof(double) * std::max<int64_t>(1, n)));
         }
-        DevBuf &b = m.solve_b, &x = m.solve_x, &r = m.solve_r;
-        // pageable -> pinned copies in chunks, each chunk's DMA overlapping the next memcpy
-        constexpr int64_t kChunk = 1 << 17;  // doubles (1 MiB)
-        for (int64_t o = 0; o < n; o += kChunk) {
-            const int64_t c = std::min(kChunk, n - o);
-            std::memcpy(m.h_stage + o, b_host + o, sizeof(double) * c);
-            LDGMG_CUDA(cudaMemcpyAsync(b.as<double>() + o, m.h_stage + o, sizeof(double) * c,
-                                       cudaMemcpyHostToDevice, ctx->stream));
+        if (m.solve_xs.bytes < m.solve_x.bytes) {
+            m.solve_xs.alloc(m.solve_x.bytes);
+            if (m.h_stage_x) cudaFreeHost(m.h_stage_x);
+            m.h_stage_x = nullptr;
+            LDGMG_CUDA(cudaMallocHost(&m.h_stage_x, m.solve_x.bytes));
         }
+        if (!m.d2h_stream) {
+            LDGMG_CUDA(cudaStreamCreateWithFlags(&m.d2h_stream, cudaStreamNonBlocking));
+            LDGMG_CUDA(cudaEventCreateWithFlags(&m.ev_snap, cudaEventDisableTiming));
+            LDGMG_CUDA(cudaEventCreateWithFlags(&m.ev_d2h, cudaEventDisableTiming));
+        }
+        DevBuf &b = m.solve_b, &x = m.solve_x, &r = m.solve_r;
+        static const bool timing = getenv("LDGMG_SOLVE_TIMING") && atoi(getenv("LDGMG_SOLVE_TIMING"));
+        auto tnow = [] { return std::chrono::steady_clock::now(); };
+        auto tsec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count() * 1e3; };
+        const auto T0 = tnow();
+        // pageable -> pinned with host threads, then one DMA
+        static const int h2d_mode = getenv("LDGMG_SOLVE_H2D") ? atoi(getenv("LDGMG_SOLVE_H2D")) : 0;
+        if (h2d_mode == 1) parallel_memcpy(m.h_stage, b_host, sizeof(double) * n);
+        const auto T0a = tnow();
+        LDGMG_CUDA(cudaMemcpyAsync(b.p, h2d_mode == 1 ? m.h_stage : b_host, sizeof(double) * n,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+        if (timing) LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        const auto T0b = tnow();
         LDGMG_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, ctx->stream));
         launch_dot(*ctx, n, b.as<double>(), b.as<double>(), ctx->d_red);
         LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
         const double bn = std::sqrt(ctx->h_red[0]);
+        const auto T1 = tnow();
         // With an SAI level-0 smoother the residual check of iterate k is the
         // first kernel of cycle k+1 (r = b - A x, same kernel, same bits):
         // compute it into the smoother's residual buffer and let the cycle
@@ -909,35 +926,41 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
             LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
             return bn > 0 ? std::sqrt(ctx->h_red[0]) / bn : std::sqrt(ctx->h_red[0]);
         };
+        // Every iterate is snapshotted on the device and its copy to the host
+        // runs on a side stream under the next residual check and cycle, so
+        // the converged x is already in pinned memory when the loop exits.
+        bool snapped = false;
+        auto snapshot = [&]() {
+            if (snapped) LDGMG_CUDA(cudaStreamWaitEvent(ctx->stream, m.ev_d2h, 0));  // previous copy done
+            LDGMG_CUDA(cudaMemcpyAsync(m.solve_xs.p, x.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+            LDGMG_CUDA(cudaEventRecord(m.ev_snap, ctx->stream));
+            LDGMG_CUDA(cudaStreamWaitEvent(m.d2h_stream, m.ev_snap, 0));
+            LDGMG_CUDA(cudaMemcpyAsync(m.h_stage_x, m.solve_xs.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                       m.d2h_stream));
+            LDGMG_CUDA(cudaEventRecord(m.ev_d2h, m.d2h_stream));
+            snapped = true;
+        };
         double rr = relres();
         if (history) history[0] = rr;
         int it = 0;
         while (rr > tol && it < maxit) {
             m.cycles(*ctx, x.as<double>(), b.as<double>(), 1, reuse);
             ++it;
+            snapshot();
             rr = relres();
             if (history) history[it] = rr;
         }
         if (iters) *iters = it;
-        // device -> pinned in chunks; the host copy of chunk k overlaps the DMA of chunk k+1
-        std::vector<cudaEvent_t> done;
-        for (int64_t o = 0; o < n; o += kChunk) {
-            const int64_t c = std::min(kChunk, n - o);
-            LDGMG_CUDA(cudaMemcpyAsync(m.h_stage + o, x.as<double>() + o, sizeof(double) * c,
-                                       cudaMemcpyDeviceToHost, ctx->stream));
-            cudaEvent_t ev;
-            LDGMG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            LDGMG_CUDA(cudaEventRecord(ev, ctx->stream));
-            done.push_back(ev);
+        const auto T2 = tnow();
+        if (snapped) {
+            LDGMG_CUDA(cudaEventSynchronize(m.ev_d2h));
+            parallel_memcpy(x_host, m.h_stage_x, sizeof(double) * n);
+        } else {
+            std::memset(x_host, 0, sizeof(double) * n);  // x = 0 exactly (no cycle ran)
         }
-        int64_t o = 0;
-        for (cudaEvent_t ev : done) {
-            LDGMG_CUDA(cudaEventSynchronize(ev));
-            const int64_t c = std::min(kChunk, n - o);
-            std::memcpy(x_host + o, m.h_stage + o, sizeof(double) * c);
-            o += c;
-            cudaEventDestroy(ev);
-        }
+        if (timing)
+            fprintf(stderr, "[solve_host] memcpy %.3f dma %.3f norm %.3f ms, %d cycles+checks %.3f ms, d2h %.3f ms\n",
+                    tsec(T0, T0a), tsec(T0a, T0b), tsec(T0b, T1), it, tsec(T1, T2), tsec(T2, tnow()));
     });
 }
 

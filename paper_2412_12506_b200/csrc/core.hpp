@@ -150,6 +150,8 @@ struct Transfer {
     int n_fine = 0, n_coarse = 0, dim = 2, bss = 0, ncomp = 1, bs = 0;
     int max_children = 0;
     DevBuf parent, orth, child_ptr, child_list, K;
+    DevBuf child_orth;  // orth[child_list[q]] in child-list order (restrict_flat_kernel)
+    DevBuf Kt;          // K_o transposed, (j, i) at j*bss + i (prolong_flat_kernel)
     std::vector<int> hparent, horth;
 };
 /// `zero_xc` (optional): also zero this coarse vector (the V-cycle's x_{l+1}).

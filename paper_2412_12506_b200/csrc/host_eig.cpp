@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <stdexcept>
+#include <cstring>
 #include <thread>
 
 namespace ldgmg_b200 {
@@ -195,6 +196,25 @@ void parallel_for(int n, const std::function<void(int, int)>& body) {
         const int lo = int(int64_t(n) * t / nt), hi = int(int64_t(n) * (t + 1) / nt);
         pool.emplace_back([&, lo, hi] { body(lo, hi); });
     }
+    for (auto& th : pool) th.join();
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPerThread = size_t(1) << 20;
+    unsigned hw = std::thread::hardware_concurrency();
+    const int nt = int(std::min<size_t>(std::min(8u, std::max(1u, hw)), std::max<size_t>(1, bytes / kPerThread)));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) {
+        const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
+        pool.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+        });
+    }
+    std::memcpy(dst, src, bytes / nt);
     for (auto& th : pool) th.join();
 }
 

@@ -342,7 +342,17 @@ std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, co
     h2d(ctx, T->child_ptr.p, cptr.data(), sizeof(int) * cptr.size());
     h2d(ctx, T->child_list.p, clist.data(), sizeof(int) * n_fine);
     h2d(ctx, T->K.p, K, T->K.bytes);
-    (void)ctx;
+    std::vector<int> corth(n_fine);
+    for (int q = 0; q < n_fine; ++q) corth[q] = orthant_of[clist[q]];
+    T->child_orth.alloc(sizeof(int) * std::max(1, n_fine));
+    h2d(ctx, T->child_orth.p, corth.data(), sizeof(int) * n_fine);
+    std::vector<double> Kt(nk * bss * bss);
+    for (size_t o = 0; o < nk; ++o)
+        for (int i = 0; i < bss; ++i)
+            for (int j = 0; j < bss; ++j)
+                Kt[o * bss * bss + size_t(j) * bss + i] = K[o * bss * bss + size_t(i) * bss + j];
+    T->Kt.alloc(sizeof(double) * Kt.size());
+    h2d(ctx, T->Kt.p, Kt.data(), T->Kt.bytes);
     return T;
 }
 
@@ -554,6 +564,10 @@ Mg::~Mg() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (h_red) cudaFreeHost(h_red);
     if (h_stage) cudaFreeHost(h_stage);
+    if (h_stage_x) cudaFreeHost(h_stage_x);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    if (ev_snap) cudaEventDestroy(ev_snap);
+    if (ev_d2h) cudaEventDestroy(ev_d2h);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (sai_cache) sai_cache_free(sai_cache);
 }

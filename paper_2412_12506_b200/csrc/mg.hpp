@@ -103,8 +103,11 @@ struct Mg {
     void launch_coarse_program(Ctx& ctx);
     SaiCache* sai_cache = nullptr;  // shared across levels (multigrid.hpp:60)
     // ldgmg_mg_solve_host scratch (cached so the graph of (x, b) is reused)
-    DevBuf solve_b, solve_x, solve_r;
-    double* h_stage = nullptr;  // pinned staging for host <-> device
+    DevBuf solve_b, solve_x, solve_r, solve_xs;
+    double* h_stage = nullptr;    // pinned staging for host -> device
+    double* h_stage_x = nullptr;  // pinned landing buffer of the iterate snapshots
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t ev_snap = nullptr, ev_d2h = nullptr;
 
     void init(Ctx& ctx);
     void set_bottom(Ctx& ctx, const double* V, const double* lambda);

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "core.hpp"
 
@@ -146,6 +148,120 @@ __global__ void prolong_cta_kernel(const int* __restrict__ child_ptr, const int*
         }
         __syncthreads();
     }
+}
+
+/// Restriction, one THREAD per (parent p, child q, output o = (c, j)): the
+/// per-child sum s_q = 0 + K_o[0,j] src_q[c,0] + K_o[1,j] src_q[c,1] + ... is
+/// one BSS-long chain whose 2*BSS operands are all loaded up front (BSS
+/// compile-time, fully unrolled), so a parent costs ~3 memory round trips
+/// (child_ptr -> child ids -> K / residual blocks) + one chain; the s_q meet
+/// in shared memory and thread o sums them in child order,
+/// acc = 0 + s_1 + s_2 + ... (restrict_kernel's bits).  `ppc` parents per CTA.
+template <int BSS>
+__global__ void __launch_bounds__(256) restrict_item_kernel(const int* __restrict__ child_ptr,
+                                                            const int* __restrict__ child,
+                                                            const int* __restrict__ corth,
+                                                            const double* __restrict__ K,
+                                                            const double* __restrict__ rf, double* __restrict__ rc,
+                                                            int n_coarse, int bss_rt, int ncomp, int maxch, int ppc,
+                                                            double* __restrict__ zero_xc) {
+    extern __shared__ double ssum[];  // ppc x maxch x BS
+    const int bss = BSS > 0 ? BSS : bss_rt;
+    const int BS = bss * ncomp, bb = bss * bss, per = maxch * BS;
+    pdl_wait();
+    pdl_trigger();
+    for (int p0 = blockIdx.x * ppc; p0 < n_coarse; p0 += gridDim.x * ppc) {
+        for (int t = threadIdx.x; t < ppc * per; t += blockDim.x) {
+            const int lp = t / per, r = t - lp * per, q = r / BS, o = r - q * BS;
+            const int p = p0 + lp;
+            if (p >= n_coarse) continue;
+            const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
+            if (q >= nch) continue;
+            const int f = __ldg(child + q0 + q), ot = __ldg(corth + q0 + q);
+            const double* src = rf + size_t(f) * BS;
+            double sq;
+            if (ot < 0) {
+                sq = src[o];
+            } else {
+                const int c = o / bss, j = o - c * bss;
+                const double* Ko = K + size_t(ot) * bb + j;
+                const double* sc = src + c * bss;
+                sq = 0.0;
+                if constexpr (BSS > 0) {
+                    double kv[BSS], xv[BSS];
+#pragma unroll
+                    for (int i = 0; i < BSS; ++i) {
+                        kv[i] = __ldg(Ko + i * BSS);
+                        xv[i] = sc[i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < BSS; ++i) sq = madd_rn(sq, kv[i], xv[i]);
+                } else {
+#pragma unroll 9
+                    for (int i = 0; i < bss; ++i) sq = madd_rn(sq, __ldg(Ko + size_t(i) * bss), sc[i]);
+                }
+            }
+            ssum[t] = sq;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < ppc * BS; t += blockDim.x) {
+            const int lp = t / BS, o = t - lp * BS, p = p0 + lp;
+            if (p >= n_coarse) continue;
+            const int nch = __ldg(child_ptr + p + 1) - __ldg(child_ptr + p);
+            const double* ss = ssum + size_t(lp) * per + o;
+            double acc = 0.0;
+            for (int q = 0; q < nch; ++q) acc = __dadd_rn(acc, ss[q * BS]);
+            rc[size_t(p) * BS + o] = acc;
+            if (zero_xc) zero_xc[size_t(p) * BS + o] = 0.0;  // the coarse iterate starts at 0
+        }
+        __syncthreads();
+    }
+}
+
+/// Prolongation, one THREAD per fine entry (f, ii = (c, i)):
+/// xf[ii] += 0 + K_o[i,0] xc_p[c,0] + K_o[i,1] xc_p[c,1] + ...  (prolong_kernel's
+/// bits).  K is read transposed (Kt[j,i]) so the threads of one child
+/// (consecutive i) load consecutive words; xc loads broadcast.
+template <int BSS>
+__global__ void __launch_bounds__(256) prolong_flat_kernel(const int* __restrict__ parent,
+                                                           const int* __restrict__ orth,
+                                                           const double* __restrict__ Kt,
+                                                           const double* __restrict__ xc,
+                                                           double* __restrict__ xf, int n_fine, int bss_rt,
+                                                           int ncomp) {
+    const int bss = BSS > 0 ? BSS : bss_rt;
+    const int BS = bss * ncomp, bb = bss * bss;
+    const int64_t total = int64_t(n_fine) * BS;
+    const int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const bool live = o < total;
+    const int f = live ? int(o / BS) : 0;
+    const int ii = int(o - int64_t(f) * BS), c = ii / bss, i = ii - c * bss;
+    const int p = __ldg(parent + f), ot = __ldg(orth + f);
+    pdl_wait();
+    pdl_trigger();
+    if (!live) return;
+    const double* src = xc + size_t(p) * BS + c * bss;
+    const double old = xf[o];
+    if (ot < 0) {
+        xf[o] = __dadd_rn(old, xc[size_t(p) * BS + ii]);
+        return;
+    }
+    const double* Kc = Kt + size_t(ot) * bb + i;
+    double s = 0.0;
+    if constexpr (BSS > 0) {
+        double kv[BSS], xv[BSS];
+#pragma unroll
+        for (int jj = 0; jj < BSS; ++jj) {
+            kv[jj] = __ldg(Kc + jj * BSS);
+            xv[jj] = src[jj];
+        }
+#pragma unroll
+        for (int jj = 0; jj < BSS; ++jj) s = madd_rn(s, kv[jj], xv[jj]);
+    } else {
+#pragma unroll 9
+        for (int jj = 0; jj < bss; ++jj) s = madd_rn(s, __ldg(Kc + size_t(jj) * bss), src[jj]);
+    }
+    xf[o] = __dadd_rn(old, s);
 }
 
 /// Copies the 2^d injection matrices (nK doubles, nK even) into shared
@@ -619,6 +735,16 @@ int grid1(int64_t n, int threads, const Ctx& ctx) {
 
 namespace {
 int transfer_nK(const Transfer& T) { return (1 << T.dim) * T.bss * T.bss; }
+/// thread-per-entry transfer kernels (default); LDGMG_TRANSFER=warp selects
+/// the warp-per-parent kernels with shared-memory staged K
+bool transfer_flat() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LDGMG_TRANSFER");
+        v = (e && std::string(e) == "warp") ? 0 : 1;
+    }
+    return v == 1;
+}
 }  // namespace
 
 void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, double* zero_xc) {
@@ -630,6 +756,26 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
     if (zero_xc && !warp_ok) {  // the fallback kernels do not zero
         LDGMG_CUDA(cudaMemsetAsync(zero_xc, 0, sizeof(double) * size_t(total), ctx.stream));
         zero_xc = nullptr;
+    }
+    const int per = std::max(1, T.max_children) * T.bs;
+    if (transfer_flat() && size_t(per) * 8 <= 48 * 1024) {
+        const int ppc = std::max(1, 256 / per);
+        const int threads = std::min(256, ((ppc * per + 31) / 32) * 32);
+        const int grid = std::max(1, std::min(div_up(T.n_coarse, ppc), ctx.num_sms * 32));
+        const size_t smem = sizeof(double) * size_t(ppc) * per;
+        auto launch = [&](auto kern) {
+            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.child_ptr.as<int>(),
+                       T.child_list.as<int>(), T.child_orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse, T.bss,
+                       T.ncomp, std::max(1, T.max_children), ppc, zero_xc);
+        };
+        switch (T.bss) {
+            case 16: launch(restrict_item_kernel<16>); break;
+            case 25: launch(restrict_item_kernel<25>); break;
+            case 27: launch(restrict_item_kernel<27>); break;
+            default: launch(restrict_item_kernel<0>); break;
+        }
+        after_launch("restrict_item_kernel");
+        return;
     }
     if (warp_ok) {
         ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
@@ -662,6 +808,21 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
     if (!total) return;
     const int nK = transfer_nK(T);
     const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
+    if (transfer_flat()) {
+        const int grid = div_up(total, 256);
+        auto launch = [&](auto kern) {
+            launch_pdl(kern, dim3(grid), dim3(256), 0, ctx.stream, T.parent.as<int>(), T.orth.as<int>(),
+                       T.Kt.as<double>(), xc, xf, T.n_fine, T.bss, T.ncomp);
+        };
+        switch (T.bss) {
+            case 16: launch(prolong_flat_kernel<16>); break;
+            case 25: launch(prolong_flat_kernel<25>); break;
+            case 27: launch(prolong_flat_kernel<27>); break;
+            default: launch(prolong_flat_kernel<0>); break;
+        }
+        after_launch("prolong_flat_kernel");
+        return;
+    }
     if (T.max_children <= 8 && smem_w <= 200 * 1024) {
         ensure_dyn_smem(prolong_warp_kernel, size_t(smem_w));
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));

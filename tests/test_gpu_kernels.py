@@ -231,3 +231,54 @@ def test_transfers_bitwise(ctx, ref, name):
     xfd = dev(xf)
     T.interpolate_add(dev(xc), xfd)
     assert bits_equal(host(xfd), R.interpolate_add(0, xc, xf))
+
+
+IRREGULAR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2412_12506_b200 as g
+from oracle import port
+ctx = g.Context(0)
+for dim, bss, ncomp, seed in [(2, 4, 1, 0), (2, 16, 3, 1), (3, 27, 1, 2), (3, 9, 4, 3), (2, 25, 1, 4)]:
+    rng = np.random.default_rng(seed)
+    nc = 37
+    cnt = rng.integers(1, 9, nc)
+    cnt[5] = 11  # more children than one chain batch
+    parent = np.repeat(np.arange(nc), cnt)
+    rng.shuffle(parent)
+    parent = parent.astype(np.int32)
+    nf = len(parent)
+    orth = rng.integers(-1, 1 << dim, nf).astype(np.int32)
+    K = rng.uniform(-1, 1, (1 << dim) * bss * bss)
+    BS = bss * ncomp
+    T = g.Transfer(ctx, nf, nc, parent, orth, dim, bss, ncomp, K)
+    rf = rng.uniform(-1, 1, nf * BS)
+    rc = torch.full((nc * BS,), 7.0, dtype=torch.float64, device="cuda")
+    T.restrict(torch.as_tensor(rf).cuda(), rc)
+    want = port.restrict(parent, orth, K, bss, ncomp, nc, rf)
+    got = rc.cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64)), (dim, bss, ncomp, np.abs(got - want).max())
+    xc, xf = rng.uniform(-1, 1, nc * BS), rng.uniform(-1, 1, nf * BS)
+    xfd = torch.as_tensor(xf).cuda()
+    T.interpolate_add(torch.as_tensor(xc).cuda(), xfd)
+    want = port.interpolate_add(parent, orth, K, bss, ncomp, xc, xf)
+    got = xfd.cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64)), (dim, bss, ncomp, np.abs(got - want).max())
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("family", ["flat", "warp"])
+def test_transfers_irregular_bitwise(family):
+    """Restriction / prolongation on irregular parent maps (1..11 children per
+    parent in shuffled fine order, orthant -1 copies, Stokes-like ncomp) are
+    bit-identical to the oracle port (multigrid.hpp:104-149 order) for both
+    kernel families (LDGMG_TRANSFER selects them once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LDGMG_TRANSFER=family)
+    out = subprocess.run([sys.executable, "-c", IRREGULAR_SCRIPT % root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
