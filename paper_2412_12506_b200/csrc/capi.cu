@@ -802,8 +802,7 @@ static void ensure_smoothers(ldgmg_ctx* ctx, Mg& m) {
         if (env >= 0) m.coarse_rows = env;
         m.build_coarse_program(*ctx);
         m.coarse_dirty = false;
-        for (auto& gr : m.graphs) cudaGraphExecDestroy(gr.exec);
-        m.graphs.clear();
+        m.invalidate_graphs();
     }
 }
 
@@ -855,6 +854,159 @@ int ldgmg_mg_cycles(ldgmg_ctx* ctx, ldgmg_mg* mg, double* x, const double* b, in
     });
 }
 
+namespace {
+
+/// Device state of the graph-resident solve loop: bn, tol, it, maxit, then
+/// the relative-residual history (hist[it] after `it` cycles).
+struct SolveState {
+    double bn, tol;
+    int it, maxit;
+    int pad[4];
+};
+constexpr int kSolveHist = int(sizeof(SolveState) / sizeof(double));
+
+/// LDGMG_SOLVE_SNAP=1: copy every iterate to the host inside the loop body
+/// (overlapped with the check); default 0: one copy of the final x after it
+bool solve_snap_in_loop() {
+    static const int v = getenv("LDGMG_SOLVE_SNAP") ? atoi(getenv("LDGMG_SOLVE_SNAP")) : 0;
+    return v != 0;
+}
+
+/// The loop test of ldgmg_mg_solve_host on the device: rr = ||r|| / ||b||
+/// (IEEE sqrt and division, the host loop's bits), history entry, and the
+/// WHILE node's condition rr > tol && it < maxit.
+__global__ void solve_check_kernel(const double* __restrict__ red_b, const double* __restrict__ red_r,
+                                   double* st_raw, int first, cudaGraphConditionalHandle h) {
+    SolveState* st = reinterpret_cast<SolveState*>(st_raw);
+    if (first) {
+        st->bn = sqrt(red_b[0]);
+        st->it = 0;
+    } else {
+        st->it += 1;
+    }
+    const double rn = sqrt(red_r[0]);
+    const double rr = st->bn > 0 ? rn / st->bn : rn;
+    st_raw[kSolveHist + st->it] = rr;
+    cudaGraphSetConditional(h, (rr > st->tol && st->it < st->maxit) ? 1u : 0u);
+}
+
+/// Capture the whole stationary solve as ONE graph: prologue (x = 0, ||b||,
+/// first residual check) and a conditional WHILE node whose body is one
+/// V-cycle, the iterate's device snapshot + copy to pinned host memory (a
+/// side branch under the residual check) and the check itself.  No host
+/// round trip per iteration.  Returns false (and leaves the host loop in
+/// charge) if the driver rejects any piece.
+bool build_solve_graph(Ctx& ctx, Mg& m, double* x, const double* b, double* rbuf, bool reuse, int64_t n,
+                       int cap, int64_t& n_pro, int64_t& n_body) {
+    auto ok = [](cudaError_t e) {
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    };
+    if (m.solve_exec) {
+        cudaGraphExecDestroy(m.solve_exec);
+        m.solve_exec = nullptr;
+    }
+    if (!m.cap_stream) ok(cudaStreamCreateWithFlags(&m.cap_stream, cudaStreamNonBlocking));
+    if (!m.cap_side) ok(cudaStreamCreateWithFlags(&m.cap_side, cudaStreamNonBlocking));
+    for (auto& e : m.cap_ev)
+        if (!e) ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (m.solve_red.bytes < sizeof(double) * 1024) m.solve_red.alloc(sizeof(double) * 1024);
+    m.solve_state.alloc(sizeof(double) * (kSolveHist + cap));
+    double* red_b = m.solve_red.as<double>();
+    double* red_r = red_b + 512;
+    double* st = m.solve_state.as<double>();
+    if (!m.warm) {  // kernel attributes and lazy transposes outside capture
+        m.cycle(ctx, m.solve_xs.as<double>(), b, false);
+        ok(cudaStreamSynchronize(ctx.stream));
+        m.warm = true;
+    }
+    ok(cudaStreamSynchronize(ctx.stream));
+    Ctx cctx = ctx;
+    cctx.stream = m.cap_stream;
+    auto check_pass = [&](int first) {
+        RowPass p;
+        p.A = m.A[0];
+        p.mode = MODE_RESIDUAL;
+        p.x = x;
+        p.b = b;
+        p.y = rbuf;
+        p.nrows = m.A[0]->brows;
+        launch_rowpass(cctx, p);
+        launch_dot(cctx, n, rbuf, rbuf, red_r);
+        (void)first;
+    };
+    cudaGraph_t g = nullptr;
+    bool capturing = false;
+    const int64_t c0 = launch_counter().load();
+    try {
+        ok(cudaStreamBeginCapture(m.cap_stream, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        ok(cudaMemsetAsync(x, 0, sizeof(double) * n, m.cap_stream));
+        launch_dot(cctx, n, b, b, red_b);
+        check_pass(1);
+        cudaStreamCaptureStatus status;
+        cudaGraph_t cg = nullptr;
+        ok(cudaStreamGetCaptureInfo(m.cap_stream, &status, nullptr, &cg, nullptr, nullptr));
+        cudaGraphConditionalHandle h;
+        ok(cudaGraphConditionalHandleCreate(&h, cg, 0, 0));
+        solve_check_kernel<<<1, 1, 0, m.cap_stream>>>(red_b, red_r, st, 1, h);
+        ok(cudaGetLastError());
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        ok(cudaStreamGetCaptureInfo(m.cap_stream, &status, nullptr, &cg, &deps, &ndeps));
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        ok(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        ok(cudaStreamUpdateCaptureDependencies(m.cap_stream, &node, 1, cudaStreamSetCaptureDependencies));
+        ok(cudaStreamEndCapture(m.cap_stream, &g));
+        capturing = false;
+        n_pro = launch_counter().load() - c0 + 1;
+        const int64_t c1 = launch_counter().load();
+        ok(cudaStreamBeginCaptureToGraph(m.cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        m.cycle(cctx, x, b, reuse);
+        if (solve_snap_in_loop()) {
+            ok(cudaMemcpyAsync(m.solve_xs.p, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, m.cap_stream));
+            ok(cudaEventRecord(m.cap_ev[0], m.cap_stream));
+            ok(cudaStreamWaitEvent(m.cap_side, m.cap_ev[0], 0));
+            ok(cudaMemcpyAsync(m.h_stage_x, m.solve_xs.p, sizeof(double) * n, cudaMemcpyDeviceToHost, m.cap_side));
+            ok(cudaEventRecord(m.cap_ev[1], m.cap_side));
+        }
+        check_pass(0);
+        solve_check_kernel<<<1, 1, 0, m.cap_stream>>>(red_b, red_r, st, 0, h);
+        ok(cudaGetLastError());
+        if (solve_snap_in_loop()) ok(cudaStreamWaitEvent(m.cap_stream, m.cap_ev[1], 0));
+        cudaGraph_t bout = nullptr;
+        ok(cudaStreamEndCapture(m.cap_stream, &bout));
+        capturing = false;
+        n_body = launch_counter().load() - c1 + 1;
+        ok(cudaGraphInstantiate(&m.solve_exec, g, 0));
+        ok(cudaGraphDestroy(g));
+        g = nullptr;
+    } catch (const std::exception& e) {
+        if (capturing) {
+            cudaGraph_t junk = nullptr;
+            cudaStreamEndCapture(m.cap_stream, &junk);
+            if (junk) cudaGraphDestroy(junk);
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        if (getenv("LDGMG_SOLVE_TIMING")) fprintf(stderr, "[solve_host] device loop unavailable: %s\n", e.what());
+        launch_counter().store(c0);
+        m.solve_exec = nullptr;
+        return false;
+    }
+    launch_counter().store(c0);  // captured launches run (and are counted) per graph launch
+    m.solve_cap = cap;
+    return true;
+}
+
+}  // namespace
+
 int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, double* x_host, double tol,
                         int maxit, double* history, int* iters) {
     return guarded([&] {
@@ -899,12 +1051,6 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
                                    cudaMemcpyHostToDevice, ctx->stream));
         if (timing) LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
         const auto T0b = tnow();
-        LDGMG_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, ctx->stream));
-        launch_dot(*ctx, n, b.as<double>(), b.as<double>(), ctx->d_red);
-        LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
-        const double bn = std::sqrt(ctx->h_red[0]);
-        const auto T1 = tnow();
         // With an SAI level-0 smoother the residual check of iterate k is the
         // first kernel of cycle k+1 (r = b - A x, same kernel, same bits):
         // compute it into the smoother's residual buffer and let the cycle
@@ -912,6 +1058,48 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         double* rbuf = m.r0_buffer();
         const bool reuse = rbuf != nullptr;
         if (!rbuf) rbuf = r.as<double>();
+        static const int dev_loop = getenv("LDGMG_SOLVE_GRAPH") ? atoi(getenv("LDGMG_SOLVE_GRAPH")) : 1;
+        if (dev_loop && !m.solve_graph_bad) {
+            int64_t& n_pro = m.solve_npro;
+            int64_t& n_body = m.solve_nbody;
+            const int cap = std::max(maxit + 1, 128);
+            if (!m.solve_exec || m.solve_cap < maxit + 1)
+                if (!build_solve_graph(*ctx, m, x.as<double>(), b.as<double>(), rbuf, reuse, n, cap, n_pro, n_body))
+                    m.solve_graph_bad = true;
+            if (m.solve_exec) {
+                std::vector<double> hs(kSolveHist + size_t(maxit) + 1, 0.0);
+                SolveState* S = reinterpret_cast<SolveState*>(hs.data());
+                S->tol = tol;
+                S->maxit = maxit;
+                LDGMG_CUDA(cudaMemcpyAsync(m.solve_state.p, hs.data(), sizeof(SolveState), cudaMemcpyHostToDevice,
+                                           ctx->stream));
+                LDGMG_CUDA(cudaGraphLaunch(m.solve_exec, ctx->stream));
+                if (!solve_snap_in_loop())
+                    LDGMG_CUDA(cudaMemcpyAsync(m.h_stage_x, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                               ctx->stream));
+                LDGMG_CUDA(cudaMemcpyAsync(hs.data(), m.solve_state.p, sizeof(double) * hs.size(),
+                                           cudaMemcpyDeviceToHost, ctx->stream));
+                LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+                const int it = S->it;
+                launch_counter().fetch_add(n_pro + int64_t(it) * n_body, std::memory_order_relaxed);
+                if (history) std::memcpy(history, hs.data() + kSolveHist, sizeof(double) * (it + 1));
+                if (iters) *iters = it;
+                const auto T2 = tnow();
+                if (it > 0) parallel_memcpy(x_host, m.h_stage_x, sizeof(double) * n);
+                else std::memset(x_host, 0, sizeof(double) * n);  // x = 0 exactly (no cycle ran)
+                if (timing)
+                    fprintf(stderr, "[solve_host] device loop: h2d %.3f ms, %d cycles %.3f ms, d2h %.3f ms\n",
+                            tsec(T0, T0b), it, tsec(T0b, T2), tsec(T2, tnow()));
+                return;
+            }
+        }
+        // host-driven loop (device loop disabled or rejected by the driver)
+        LDGMG_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * n, ctx->stream));
+        launch_dot(*ctx, n, b.as<double>(), b.as<double>(), ctx->d_red);
+        LDGMG_CUDA(cudaMemcpyAsync(ctx->h_red, ctx->d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
+        const double bn = std::sqrt(ctx->h_red[0]);
+        const auto T1 = tnow();
         auto relres = [&]() {
             RowPass p;
             p.A = m.A[0];
@@ -968,8 +1156,7 @@ int ldgmg_mg_set_strict_order(ldgmg_mg* mg, int strict) {
     return guarded([&] {
         need(mg, "mg_set_strict_order");
         mg->m.strict_order = strict != 0;
-        for (auto& gr : mg->m.graphs) cudaGraphExecDestroy(gr.exec);
-        mg->m.graphs.clear();
+        mg->m.invalidate_graphs();
     });
 }
 

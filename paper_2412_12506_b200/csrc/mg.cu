@@ -541,6 +541,13 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n, bool r0_ready) {
     }
 }
 
+void Mg::invalidate_graphs() {
+    for (auto& gr : graphs) cudaGraphExecDestroy(gr.exec);
+    graphs.clear();
+    if (solve_exec) cudaGraphExecDestroy(solve_exec);
+    solve_exec = nullptr;
+}
+
 double Mg::dof_updates_per_cycle() const {
     double s = 0.0;
     for (int l = 0; l + 1 < depth; ++l) s += double(cfg.nu1 + cfg.nu2) * A[l]->brows * bs;
@@ -568,6 +575,10 @@ Mg::~Mg() {
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (ev_snap) cudaEventDestroy(ev_snap);
     if (ev_d2h) cudaEventDestroy(ev_d2h);
+    if (solve_exec) cudaGraphExecDestroy(solve_exec);
+    if (cap_side) cudaStreamDestroy(cap_side);
+    for (auto e : cap_ev)
+        if (e) cudaEventDestroy(e);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (sai_cache) sai_cache_free(sai_cache);
 }

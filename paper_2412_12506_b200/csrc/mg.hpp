@@ -108,6 +108,17 @@ struct Mg {
     double* h_stage_x = nullptr;  // pinned landing buffer of the iterate snapshots
     cudaStream_t d2h_stream = nullptr;
     cudaEvent_t ev_snap = nullptr, ev_d2h = nullptr;
+    // device-resident solve loop (capi.cu build_solve_graph): prologue + a
+    // conditional WHILE node whose body is cycle -> snapshot -> check
+    cudaGraphExec_t solve_exec = nullptr;
+    int solve_cap = 0;          // history capacity the graph was built for
+    int64_t solve_npro = 0, solve_nbody = 0;  // kernels per prologue / per loop body
+    /// drop every captured graph (after a change the captures baked in)
+    void invalidate_graphs();
+    bool solve_graph_bad = false;
+    DevBuf solve_red, solve_state;
+    cudaStream_t cap_side = nullptr;
+    cudaEvent_t cap_ev[2] = {nullptr, nullptr};
 
     void init(Ctx& ctx);
     void set_bottom(Ctx& ctx, const double* V, const double* lambda);
