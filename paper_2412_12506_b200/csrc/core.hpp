@@ -152,6 +152,7 @@ struct Transfer {
     DevBuf parent, orth, child_ptr, child_list, K;
     DevBuf child_orth;  // orth[child_list[q]] in child-list order (restrict_flat_kernel)
     DevBuf Kt;          // K_o transposed, (j, i) at j*bss + i (prolong_flat_kernel)
+    bool regular = false;  // every parent p has 2^dim children 2^dim p + o in orthant order o
     std::vector<int> hparent, horth;
 };
 /// `zero_xc` (optional): also zero this coarse vector (the V-cycle's x_{l+1}).

@@ -342,6 +342,12 @@ std::unique_ptr<Transfer> transfer_create(Ctx& ctx, int n_fine, int n_coarse, co
     h2d(ctx, T->child_ptr.p, cptr.data(), sizeof(int) * cptr.size());
     h2d(ctx, T->child_list.p, clist.data(), sizeof(int) * n_fine);
     h2d(ctx, T->K.p, K, T->K.bytes);
+    {
+        const int nc = 1 << dim;
+        bool reg = n_fine == n_coarse * nc;
+        for (int f = 0; reg && f < n_fine; ++f) reg = parent_of[f] == f / nc && orthant_of[f] == f % nc;
+        T->regular = reg;
+    }
     std::vector<int> corth(n_fine);
     for (int q = 0; q < n_fine; ++q) corth[q] = orthant_of[clist[q]];
     T->child_orth.alloc(sizeof(int) * std::max(1, n_fine));

@@ -264,6 +264,84 @@ __global__ void __launch_bounds__(256) prolong_flat_kernel(const int* __restrict
     xf[o] = __dadd_rn(old, s);
 }
 
+/// Transfers of a REGULAR hierarchy (children of p are NCH p + o, o the
+/// orthant): "K-stationary" kernels.  Thread (o, j) keeps column j of K_o
+/// (restriction) or row i of K_o (prolongation) in registers for the whole
+/// kernel and streams PB parents at a time through shared memory, so every
+/// multiply-add needs one broadcast shared-memory operand and nothing else;
+/// the arithmetic (and the bits) are restrict_kernel's / prolong_kernel's.
+template <int BSS, int NCH, int PB>
+__global__ void __launch_bounds__(NCH * BSS) restrict_ks_kernel(const double* __restrict__ K,
+                                                               const double* __restrict__ rf, double* __restrict__ rc,
+                                                               int n_coarse, int ncomp, double* __restrict__ zero_xc) {
+    extern __shared__ double sm[];  // sx: PB x NCH x BS, ss: PB x NCH x BS
+    const int BS = BSS * ncomp;
+    double* sx = sm;
+    double* ss = sm + size_t(PB) * NCH * BS;
+    const int t = threadIdx.x, o = t / BSS, j = t - o * BSS;
+    double kc[BSS];
+#pragma unroll
+    for (int i = 0; i < BSS; ++i) kc[i] = __ldg(K + size_t(o) * BSS * BSS + i * BSS + j);
+    pdl_wait();
+    pdl_trigger();
+    for (int p0 = blockIdx.x * PB; p0 < n_coarse; p0 += gridDim.x * PB) {
+        const int np = min(PB, n_coarse - p0);
+        // children of p0..p0+np-1 are one contiguous run of fine blocks
+        const double* src = rf + size_t(p0) * NCH * BS;
+        for (int e = t; e < np * NCH * BS; e += NCH * BSS) sx[e] = src[e];
+        __syncthreads();
+        for (int lp = 0; lp < np; ++lp)
+            for (int c = 0; c < ncomp; ++c) {
+                const double* xv = sx + (size_t(lp) * NCH + o) * BS + c * BSS;
+                double s = 0.0;
+#pragma unroll
+                for (int i = 0; i < BSS; ++i) s = madd_rn(s, kc[i], xv[i]);
+                ss[(size_t(lp) * NCH + o) * BS + c * BSS + j] = s;
+            }
+        __syncthreads();
+        for (int e = t; e < np * BS; e += NCH * BSS) {
+            const int lp = e / BS, oo = e - lp * BS;
+            const double* sp = ss + size_t(lp) * NCH * BS + oo;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) acc = __dadd_rn(acc, sp[q * BS]);
+            rc[size_t(p0) * BS + e] = acc;
+            if (zero_xc) zero_xc[size_t(p0) * BS + e] = 0.0;  // the coarse iterate starts at 0
+        }
+        __syncthreads();
+    }
+}
+
+template <int BSS, int NCH, int PB>
+__global__ void __launch_bounds__(NCH * BSS) prolong_ks_kernel(const double* __restrict__ K,
+                                                              const double* __restrict__ xc, double* __restrict__ xf,
+                                                              int n_coarse, int ncomp) {
+    extern __shared__ double sm[];  // PB x BS coarse blocks
+    const int BS = BSS * ncomp;
+    const int t = threadIdx.x, o = t / BSS, i = t - o * BSS;
+    double kr[BSS];
+#pragma unroll
+    for (int jj = 0; jj < BSS; ++jj) kr[jj] = __ldg(K + size_t(o) * BSS * BSS + i * BSS + jj);
+    pdl_wait();
+    pdl_trigger();
+    for (int p0 = blockIdx.x * PB; p0 < n_coarse; p0 += gridDim.x * PB) {
+        const int np = min(PB, n_coarse - p0);
+        for (int e = t; e < np * BS; e += NCH * BSS) sm[e] = xc[size_t(p0) * BS + e];
+        __syncthreads();
+        for (int lp = 0; lp < np; ++lp)
+            for (int c = 0; c < ncomp; ++c) {
+                const double* xv = sm + size_t(lp) * BS + c * BSS;
+                double* dst = xf + (size_t(p0 + lp) * NCH + o) * BS + c * BSS + i;
+                const double old = *dst;
+                double s = 0.0;
+#pragma unroll
+                for (int jj = 0; jj < BSS; ++jj) s = madd_rn(s, kr[jj], xv[jj]);
+                *dst = __dadd_rn(old, s);
+            }
+        __syncthreads();
+    }
+}
+
 /// Copies the 2^d injection matrices (nK doubles, nK even) into shared
 /// memory with one TMA bulk copy: a single memory round trip per CTA.
 __device__ __forceinline__ void stage_K_bulk(double* sK, const double* K, int nK, uint64_t* bar) {
@@ -757,6 +835,27 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         LDGMG_CUDA(cudaMemsetAsync(zero_xc, 0, sizeof(double) * size_t(total), ctx.stream));
         zero_xc = nullptr;
     }
+    if (transfer_flat() && T.regular) {
+        constexpr int PB = 4;
+        const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
+        const size_t smem = sizeof(double) * 2 * PB * (size_t(1) << T.dim) * T.bs;
+        bool done = true;
+        auto launch = [&](auto kern, int threads) {
+            ensure_dyn_smem(kern, smem);
+            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), rf, rc, T.n_coarse,
+                       T.ncomp, zero_xc);
+        };
+        if (T.dim == 3 && T.bss == 27) launch(restrict_ks_kernel<27, 8, PB>, 216);
+        else if (T.dim == 3 && T.bss == 8) launch(restrict_ks_kernel<8, 8, PB>, 64);
+        else if (T.dim == 2 && T.bss == 16) launch(restrict_ks_kernel<16, 4, PB>, 64);
+        else if (T.dim == 2 && T.bss == 25) launch(restrict_ks_kernel<25, 4, PB>, 100);
+        else if (T.dim == 2 && T.bss == 9) launch(restrict_ks_kernel<9, 4, PB>, 36);
+        else done = false;
+        if (done) {
+            after_launch("restrict_ks_kernel");
+            return;
+        }
+    }
     const int per = std::max(1, T.max_children) * T.bs;
     if (transfer_flat() && size_t(per) * 8 <= 48 * 1024) {
         const int ppc = std::max(1, 256 / per);
@@ -808,6 +907,27 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
     if (!total) return;
     const int nK = transfer_nK(T);
     const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
+    if (transfer_flat() && T.regular) {
+        constexpr int PB = 4;
+        const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
+        const size_t smem = sizeof(double) * PB * T.bs;
+        bool done = true;
+        auto launch = [&](auto kern, int threads) {
+            ensure_dyn_smem(kern, smem);
+            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), xc, xf, T.n_coarse,
+                       T.ncomp);
+        };
+        if (T.dim == 3 && T.bss == 27) launch(prolong_ks_kernel<27, 8, PB>, 216);
+        else if (T.dim == 3 && T.bss == 8) launch(prolong_ks_kernel<8, 8, PB>, 64);
+        else if (T.dim == 2 && T.bss == 16) launch(prolong_ks_kernel<16, 4, PB>, 64);
+        else if (T.dim == 2 && T.bss == 25) launch(prolong_ks_kernel<25, 4, PB>, 100);
+        else if (T.dim == 2 && T.bss == 9) launch(prolong_ks_kernel<9, 4, PB>, 36);
+        else done = false;
+        if (done) {
+            after_launch("prolong_ks_kernel");
+            return;
+        }
+    }
     if (transfer_flat()) {
         const int grid = div_up(total, 256);
         auto launch = [&](auto kern) {
