@@ -1287,44 +1287,60 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         std::vector<int> bord(np);
         for (int i = 0; i < np; ++i) bord[i] = i;
         std::stable_sort(bord.begin(), bord.end(), [&](int a, int b) {
-            return probs[a].ni != probs[b].ni ? probs[a].ni < probs[b].ni : probs[a].nj < probs[b].nj;
+            return probs[a].nj != probs[b].nj ? probs[a].nj < probs[b].nj : probs[a].ni < probs[b].ni;
         });
         const size_t budget = size_t(4) << 30;
+        // One shape per batch (strided-batched GEMM path).  Problems with the
+        // same column count whose row counts differ by at most `pad` are
+        // batched together with their M (and right-hand side) padded by zero
+        // rows at the end: the least-squares minimiser and ||M||_F are
+        // unchanged, and a few large batches replace many latency-bound small
+        // ones.  LDGMG_SAI_PAD=1 keeps exact shapes.
+        static const double pad = getenv("LDGMG_SAI_PAD") ? atof(getenv("LDGMG_SAI_PAD")) : 1.25;
         std::vector<std::pair<int, int>> batches;
+        std::vector<int> batch_ni;
         size_t max_mn = 0, max_mk = 0;
         for (int p0 = 0; p0 < np;) {
-            int p1 = p0;
-            size_t need = 0, mn = 0, mk = 0;
+            int p1 = p0, ni_pad = probs[bord[p0]].ni;
+            const int64_t n = int64_t(probs[bord[p0]].nj) * bs;
             while (p1 < np) {
-                const int64_t m = int64_t(probs[bord[p1]].ni) * bs, n = int64_t(probs[bord[p1]].nj) * bs;
-                const size_t add = sizeof(double) * size_t(m * n + m * bs);
-                if (p1 > p0 && (need + add > budget || p1 - p0 >= 4 * ctx.num_sms)) break;
-                if (p1 > p0 && (probs[bord[p1]].ni != probs[bord[p0]].ni || probs[bord[p1]].nj != probs[bord[p0]].nj))
-                    break;  // one shape per batch (strided-batched GEMM path)
-                need += add;
-                mn += size_t(m * n);
-                mk += size_t(m * bs);
+                if (p1 > p0 && probs[bord[p1]].nj != probs[bord[p0]].nj) break;
+                const int ni1 = std::max(ni_pad, probs[bord[p1]].ni);
+                if (p1 > p0 && double(ni1) > pad * double(probs[bord[p0]].ni)) break;
+                const int64_t m = int64_t(ni1) * bs;
+                const size_t need = sizeof(double) * size_t(p1 - p0 + 1) * size_t(m * n + m * bs);
+                if (p1 > p0 && (need > budget || p1 - p0 >= 4 * ctx.num_sms)) break;
+                ni_pad = ni1;
                 ++p1;
             }
+            const int64_t m = int64_t(ni_pad) * bs;
             batches.push_back({p0, p1});
-            max_mn = std::max(max_mn, mn);
-            max_mk = std::max(max_mk, mk);
+            batch_ni.push_back(ni_pad);
+            max_mn = std::max(max_mn, size_t(p1 - p0) * size_t(m * n));
+            max_mk = std::max(max_mk, size_t(p1 - p0) * size_t(m * bs));
             p0 = p1;
         }
         DevBuf d_M(sizeof(double) * (max_mn + 2)), d_W(sizeof(double) * (max_mk + 2));
-        for (auto [p0, p1] : batches) {
+        for (size_t bi = 0; bi < batches.size(); ++bi) {
+            const auto [p0, p1] = batches[bi];
+            const int ni_pad = batch_ni[bi];
             std::vector<int64_t> moff(1, 0), woff(1, 0), boff(1, 0), xo;
             std::vector<int> hni, hnj, hblk;
             for (int q = p0; q < p1; ++q) {
                 const int pid = bord[q];
-                const int64_t m = int64_t(probs[pid].ni) * bs, n = int64_t(probs[pid].nj) * bs;
-                hni.push_back(probs[pid].ni);
+                const int ni = probs[pid].ni;
+                const int64_t m = int64_t(ni_pad) * bs, n = int64_t(probs[pid].nj) * bs;
+                hni.push_back(ni_pad);
                 hnj.push_back(probs[pid].nj);
                 const ColumnPlan& P = plan[probs[pid].column];
-                hblk.insert(hblk.end(), P.blk.begin(), P.blk.end());
+                // block list, column block b at b * ni_pad; rows past ni are zero (-1)
+                for (int b = 0; b < probs[pid].nj; ++b) {
+                    hblk.insert(hblk.end(), P.blk.begin() + size_t(b) * ni, P.blk.begin() + size_t(b + 1) * ni);
+                    hblk.insert(hblk.end(), size_t(ni_pad - ni), -1);
+                }
                 moff.push_back(moff.back() + m * n);
                 woff.push_back(woff.back() + m * bs);
-                boff.push_back(boff.back() + int64_t(P.blk.size()));
+                boff.push_back(boff.back() + int64_t(probs[pid].nj) * ni_pad);
                 xo.push_back(xoff[pid]);
             }
             const int nb = p1 - p0;
