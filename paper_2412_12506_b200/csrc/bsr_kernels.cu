@@ -100,7 +100,8 @@ __device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int i
         const double* src;
         uint32_t bytes;
         if (kind == 0) {
-            src = a.val + size_t(idx) * a.blk_stride;
+            const int64_t blk = a.perm ? int64_t(__ldg(a.perm + idx)) : int64_t(idx);
+            src = a.val + size_t(blk) * a.blk_stride;
             bytes = uint32_t(a.blk_stride) * 8u;
         } else {
             src = a.V + size_t(idx) * a.vstride;
@@ -147,6 +148,65 @@ __device__ __forceinline__ void bdot2(const double* __restrict__ B1, const doubl
         for (int c = 0; c < cbs; ++c) {
             u = madd_rn(u, B1[size_t(c) * rbs], X1[c]);
             v = madd_rn(v, B2[size_t(c) * rbs], X2[c]);
+        }
+    }
+    s1 = u;
+    s2 = v;
+}
+
+/// Transposed-view dot products: lane t reads ROW t of the transposed block,
+/// i.e. the stored column t of the base block, consecutive words Bt[0..cbs)
+/// (Bt = stage + t*cbs).  Odd cbs: 8-byte loads, lane stride odd ->
+/// conflict-free.  Even cbs: 16-byte loads (pairs), conflict-free when cbs/2
+/// is odd, 2-way for cbs = 108.  Sum order c = 0, 1, ... as bdot.
+template <int BS>
+__device__ __forceinline__ double bdot_t(const double* __restrict__ Bt, const double* __restrict__ X, int cbs) {
+    double s = 0.0;
+    if constexpr (BS > 0 && (BS % 2) == 0) {
+        const double2* B2 = reinterpret_cast<const double2*>(Bt);
+#pragma unroll
+        for (int c = 0; c < BS / 2; ++c) {
+            const double2 v = B2[c];
+            s = madd_rn(s, v.x, X[2 * c]);
+            s = madd_rn(s, v.y, X[2 * c + 1]);
+        }
+    } else if constexpr (BS > 0) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) s = madd_rn(s, Bt[c], X[c]);
+    } else {
+#pragma unroll 8
+        for (int c = 0; c < cbs; ++c) s = madd_rn(s, Bt[c], X[c]);
+    }
+    return s;
+}
+
+template <int BS>
+__device__ __forceinline__ void bdot2_t(const double* __restrict__ B1, const double* __restrict__ X1,
+                                        const double* __restrict__ B2, const double* __restrict__ X2, int cbs,
+                                        double& s1, double& s2) {
+    double u = 0.0, v = 0.0;
+    if constexpr (BS > 0 && (BS % 2) == 0) {
+        const double2* P1 = reinterpret_cast<const double2*>(B1);
+        const double2* P2 = reinterpret_cast<const double2*>(B2);
+#pragma unroll
+        for (int c = 0; c < BS / 2; ++c) {
+            const double2 a1 = P1[c], a2 = P2[c];
+            u = madd_rn(u, a1.x, X1[2 * c]);
+            v = madd_rn(v, a2.x, X2[2 * c]);
+            u = madd_rn(u, a1.y, X1[2 * c + 1]);
+            v = madd_rn(v, a2.y, X2[2 * c + 1]);
+        }
+    } else if constexpr (BS > 0) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) {
+            u = madd_rn(u, B1[c], X1[c]);
+            v = madd_rn(v, B2[c], X2[c]);
+        }
+    } else {
+#pragma unroll 4
+        for (int c = 0; c < cbs; ++c) {
+            u = madd_rn(u, B1[c], X1[c]);
+            v = madd_rn(v, B2[c], X2[c]);
         }
     }
     s1 = u;
@@ -231,8 +291,12 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                 mbar_wait(bars + st2, ((q + 1) / uint32_t(NS)) & 1u);
                 if (act) {
                     double s1, s2;
-                    bdot2<BS>(S + t, X, stages + size_t(st2) * a.stage_doubles + t,
-                              xslots + size_t(st2) * a.xslot_doubles, cbs, rbs, s1, s2);
+                    if (a.tview)
+                        bdot2_t<BS>(S + size_t(t) * cbs, X, stages + size_t(st2) * a.stage_doubles + size_t(t) * cbs,
+                                    xslots + size_t(st2) * a.xslot_doubles, cbs, s1, s2);
+                    else
+                        bdot2<BS>(S + t, X, stages + size_t(st2) * a.stage_doubles + t,
+                                  xslots + size_t(st2) * a.xslot_doubles, cbs, rbs, s1, s2);
                     acc = relax ? __dsub_rn(acc, s1) : __dadd_rn(acc, s1);
                     acc = relax ? __dsub_rn(acc, s2) : __dadd_rn(acc, s2);
                 }
@@ -240,7 +304,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                 used = 2;
             } else if (nblk == 1) {
                 if (act) {
-                    const double s = bdot<BS>(S + t, X, cbs, rbs);
+                    const double s = a.tview ? bdot_t<BS>(S + size_t(t) * cbs, X, cbs) : bdot<BS>(S + t, X, cbs, rbs);
                     acc = relax ? __dsub_rn(acc, s) : __dadd_rn(acc, s);
                 }
                 k = k + 1;
@@ -565,6 +629,77 @@ const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A) {
 }
 
 namespace {
+int split_threshold_rows(const Ctx& ctx);
+}  // namespace
+
+const Bsr& bsr_transpose_view(Ctx& ctx, const Bsr& A) {
+    if (A.TV) return *A.TV;
+    require(!A.tbase, "bsr_transpose_view: already a view");
+    auto T = std::make_unique<Bsr>();
+    T->brows = A.bcols;
+    T->bcols = A.brows;
+    T->rbs = A.cbs;
+    T->cbs = A.rbs;
+    T->nnzb = A.nnzb;
+    T->blk_stride = A.blk_stride;
+    T->tbase = &A;
+    T->hptr.assign(A.bcols + 1, 0);
+    for (int64_t k = 0; k < A.nnzb; ++k) ++T->hptr[A.hcol[k] + 1];
+    for (int j = 0; j < A.bcols; ++j) T->hptr[j + 1] += T->hptr[j];
+    T->hcol.resize(A.nnzb);
+    std::vector<int> perm(std::max<int64_t>(1, A.nnzb)), fill(T->hptr.begin(), T->hptr.end() - 1);
+    for (int i = 0; i < A.brows; ++i)
+        for (int k = A.hptr[i]; k < A.hptr[i + 1]; ++k) {
+            const int q = fill[A.hcol[k]]++;
+            T->hcol[q] = i;
+            perm[q] = k;
+        }
+    set_max_row(*T);
+    T->ptr.alloc(sizeof(int) * (T->brows + 1));
+    T->col.alloc(sizeof(int) * std::max<int64_t>(1, T->nnzb));
+    T->tperm.alloc(sizeof(int) * perm.size());
+    h2d(ctx, T->ptr.p, T->hptr.data(), sizeof(int) * T->hptr.size());
+    if (T->nnzb) h2d(ctx, T->col.p, T->hcol.data(), sizeof(int) * T->nnzb);
+    h2d(ctx, T->tperm.p, perm.data(), sizeof(int) * perm.size());
+    const_cast<Bsr&>(A).TV = std::move(T);
+    return *A.TV;
+}
+
+const Bsr& bsr_transpose_for_sweep(Ctx& ctx, const Bsr& A) {
+    if (A.T) return *A.T;
+    if (A.TV) return *A.TV;
+    // LDGMG_TVIEW=1 always views, 0 always copies; default: copy while the
+    // copy fits with a margin (measured 0.4 % (bs 27) to 5 % (bs 108) faster
+    // than the view), view when it does not (C5 at 48^3 on one GPU)
+    static int env = -2;
+    if (env == -2) {
+        const char* e = getenv("LDGMG_TVIEW");
+        env = e ? atoi(e) : -1;
+    }
+    if (env < 0) {
+        size_t free_b = 0, total_b = 0;
+        LDGMG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t need = size_t(A.val.bytes) + std::max<size_t>(size_t(4) << 30, total_b / 20);
+        if (free_b >= need) return bsr_transpose(ctx, A);
+    }
+    // transposed reads are conflict-free for odd sizes, and for even sizes
+    // whose half is odd (pairs); 108 = 2*54 costs a 2-way conflict, still
+    // well under the block's HBM time; 16/48 (8-way) keep the explicit copy
+    const int s = A.rbs;
+    int g = 1;
+    if (s % 2 == 0) {
+        int h = s / 2;
+        g = 1;
+        while (h % 2 == 0 && g < 8) {
+            h /= 2;
+            g *= 2;
+        }
+    }
+    const bool ok = env != 0 && A.rbs == A.cbs && A.brows == A.bcols && g <= 2 && A.brows > split_threshold_rows(ctx);
+    return ok ? bsr_transpose_view(ctx, A) : bsr_transpose(ctx, A);
+}
+
+namespace {
 
 /// Split-row variant for SMALL levels (few rows per SM): one CTA per block
 /// row, its blocks spread over the warps (each warp computes whole s_k dot
@@ -611,6 +746,16 @@ int split_threshold_rows(const Ctx& ctx) {
 void launch_rowpass(Ctx& ctx, const RowPass& p) {
     const Bsr& A = *p.A;
     if (p.nrows == 0) return;
+    if (A.tbase) {
+        require(p.mode != MODE_RELAX, "rowpass: a transpose view cannot be relaxed");
+        // small levels: the split-row kernels read blocks in stored layout
+        if (A.rbs <= 32 && A.cbs <= 32 && p.nrows <= split_threshold_rows(ctx)) {
+            RowPass q = p;
+            q.A = &bsr_transpose(ctx, *A.tbase);
+            launch_rowpass(ctx, q);
+            return;
+        }
+    }
     if (A.rbs <= 32 && A.cbs <= 32 && p.nrows <= split_threshold_rows(ctx)) {
         RowPassArgs a{};
         a.ptr = A.ptr.as<int>();
@@ -670,7 +815,9 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
     RowPassArgs a{};
     a.ptr = A.ptr.as<int>();
     a.col = A.col.as<int>();
-    a.val = A.val.as<double>();
+    a.val = A.tbase ? A.tbase->val.as<double>() : A.val.as<double>();
+    a.perm = A.tbase ? A.tperm.as<int>() : nullptr;
+    a.tview = A.tbase ? 1 : 0;
     a.blk_stride = A.blk_stride;
     a.rbs = A.rbs;
     a.cbs = A.cbs;

@@ -99,6 +99,10 @@ struct Bsr {
     DevBuf ptr, col, val;
     std::vector<int> hptr, hcol;
     std::unique_ptr<Bsr> T;  // lazily built transpose (spmv_transpose, B^T sweeps)
+    std::unique_ptr<Bsr> TV; // lazily built transpose VIEW (no value copy)
+    // set on a transpose view: values live in tbase->val, block q = tbase block tperm[q]
+    const Bsr* tbase = nullptr;
+    DevBuf tperm;
     int64_t device_bytes() const { return int64_t(ptr.bytes + col.bytes + val.bytes); }
 };
 
@@ -117,6 +121,14 @@ void launch_gather_blocks(Ctx& ctx, const double* x, const int* idx, int n, int 
 /// Device copy of A with the layout of A^T (used for B^T r, bitwise equal to
 /// the reference's scatter order, blockla.hpp:163-175).
 const Bsr& bsr_transpose(Ctx& ctx, const Bsr& A);
+/// A^T as a VIEW of A's values (CSC index + block permutation, no copy): the
+/// streaming row pass reads each stored block transposed.  Same bits as
+/// bsr_transpose.  Halves the SAI smoother's memory (B^T sweeps at C5 48^3
+/// would otherwise need another 72 GB).
+const Bsr& bsr_transpose_view(Ctx& ctx, const Bsr& A);
+/// The operator a B^T sweep should use: the view when the streaming kernel
+/// reads it conflict-free (LDGMG_TVIEW=0 forces the explicit copy).
+const Bsr& bsr_transpose_for_sweep(Ctx& ctx, const Bsr& A);
 void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val);
 
 /// Per-element factors of the block-diagonal solve (smoothers.hpp:464-494).

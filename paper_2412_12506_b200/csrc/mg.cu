@@ -284,7 +284,7 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_rea
                 launch_rowpass(ctx, p);
             }
             RowPass q;
-            q.A = sweep == LDGMG_SWEEP_FORWARD ? B.get() : &bsr_transpose(ctx, *B);
+            q.A = sweep == LDGMG_SWEEP_FORWARD ? B.get() : &bsr_transpose_for_sweep(ctx, *B);
             q.mode = MODE_ADD;
             q.x = r;
             q.xe = x;

@@ -29,6 +29,11 @@ struct RowPassArgs {
     int ld, vstride;
     double omega, kernel_tol;
     int nstages, stage_doubles, xslot_doubles;
+    // transpose view (bsr_transpose_view): block q of this operator is block
+    // perm[q] of the base matrix, read transposed (lane r sums along a stored
+    // column of the base block)
+    const int* perm;
+    int tview;
     // processor-block GS (smoothers.hpp:426-436): neighbour j of row e is read
     // from x when part[j] == part[e], else from x_alt (the sweep's snapshot)
     const int* part;

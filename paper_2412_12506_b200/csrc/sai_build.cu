@@ -64,21 +64,6 @@ __global__ void balance_kernel(const double* __restrict__ val, const int* __rest
     for (int i = 0; i < bs; ++i) alpha[size_t(e) * bs + i] = i < nv ? av : ap;
 }
 
-__global__ void scale_kernel(const double* __restrict__ val, double* __restrict__ out,
-                             const int* __restrict__ rowof, const int* __restrict__ col,
-                             const double* __restrict__ alpha, int64_t nnzb, int bs, int stride) {
-    const int64_t total = nnzb * int64_t(bs) * bs;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t k = t / (int64_t(bs) * bs);
-        const int e = int(t - k * int64_t(bs) * bs);
-        const int j = e / bs, i = e % bs;  // column-major position (i, j)
-        const size_t o = size_t(k) * stride + e;
-        const double a = alpha[size_t(rowof[k]) * bs + i] * alpha[size_t(col[k]) * bs + j];
-        out[o] = val[o] * a;
-    }
-}
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -86,16 +71,32 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+/// The balanced operator At = diag(alpha) A diag(alpha) read on the fly
+/// (element (i, j) of block k = val * (alpha_row(i) * alpha_col(j)), the
+/// reference's scaling order): no materialised copy of A, which at the
+/// C5 48^3 size (72 GB) would not fit next to A and B on one GPU.
+struct ScaledView {
+    const double* val;
+    const int* rowof;
+    const int* col;
+    const double* alpha;
+    int bs, stride;
+    __device__ __forceinline__ double operator()(int64_t k, int i, int j) const {
+        const double a = alpha[size_t(__ldg(rowof + k)) * bs + i] * alpha[size_t(__ldg(col + k)) * bs + j];
+        return val[size_t(k) * stride + size_t(j) * bs + i] * a;
+    }
+};
+
 /// Two-lane multiply-xor hash over the block's words in row-major order.
-__global__ void block_hash_kernel(const double* __restrict__ val, int64_t nnzb, int bs, int stride,
+__global__ void block_hash_kernel(const ScaledView At, int64_t nnzb, int bs, int stride,
                                   unsigned long long* __restrict__ out) {
     const int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (k >= nnzb) return;
-    const double* B = val + size_t(k) * stride;
+    (void)stride;
     uint64_t h1 = 0xcbf29ce484222325ull, h2 = 0x84222325cbf29ce4ull;
     for (int i = 0; i < bs; ++i)
         for (int j = 0; j < bs; ++j) {
-            const uint64_t w = __double_as_longlong(B[size_t(j) * bs + i]);
+            const uint64_t w = __double_as_longlong(At(k, i, j));
             h1 = (h1 ^ w) * 0x00000100000001b3ull;
             h2 = (h2 ^ w) * 0x9e3779b97f4a7c15ull;
         }
@@ -104,21 +105,22 @@ __global__ void block_hash_kernel(const double* __restrict__ val, int64_t nnzb, 
 }
 
 /// Row-major copies of selected blocks (for the host memcmp ranking).
-__global__ void gather_rowmajor_kernel(const double* __restrict__ val, const int* __restrict__ idx, int n,
+__global__ void gather_rowmajor_kernel(const ScaledView At, const int* __restrict__ idx, int n,
                                        int bs, int stride, double* __restrict__ out) {
     const int64_t total = int64_t(n) * bs * bs;
+    (void)stride;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
          t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t q = t / (int64_t(bs) * bs);
         const int e = int(t - q * int64_t(bs) * bs);
         const int i = e / bs, j = e % bs;
-        out[t] = val[size_t(idx[q]) * stride + size_t(j) * bs + i];
+        out[t] = At(idx[q], i, j);
     }
 }
 
 /// Dense local matrix M (m x n, column-major) of problem p from At blocks:
 /// M(a*bs+i, b*bs+c) = At[blk(a,b)](i,c), zero when the block is absent.
-__global__ void assemble_m_kernel(const double* __restrict__ At, int stride, int bs,
+__global__ void assemble_m_kernel(const ScaledView At, int stride, int bs,
                                   const int* __restrict__ blk, const int64_t* __restrict__ blk_off,
                                   const int* __restrict__ ni, const int* __restrict__ nj,
                                   const int64_t* __restrict__ moff, double* __restrict__ M) {
@@ -133,7 +135,7 @@ __global__ void assemble_m_kernel(const double* __restrict__ At, int stride, int
         const int b = colidx / bs, c = colidx - b * bs;
         const int a = row / bs, i = row - a * bs;
         const int k = bl[size_t(b) * ni[p] + a];
-        Mp[t] = k < 0 ? 0.0 : At[size_t(k) * stride + size_t(c) * bs + i];
+        Mp[t] = k < 0 ? 0.0 : At(k, i, c);
     }
 }
 
@@ -1061,17 +1063,10 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     }
 
     // ---- 2./3. scaled operator and block hashes
-    DevBuf d_At(sizeof(double) * std::max<int64_t>(1, nnzb * stride));
-    LDGMG_CUDA(cudaMemsetAsync(d_At.p, 0, d_At.bytes, ctx.stream));
-    const int64_t tot = nnzb * int64_t(bs) * bs;
-    if (tot)
-        scale_kernel<<<int(std::min<int64_t>((tot + 255) / 256, int64_t(ctx.num_sms) * 32)), 256, 0, ctx.stream>>>(
-            A.val.as<double>(), d_At.as<double>(), d_rowof.as<int>(), A.col.as<int>(), d_alpha.as<double>(), nnzb,
-            bs, stride);
-    after_launch("scale_kernel");
+    const ScaledView d_At{A.val.as<double>(), d_rowof.as<int>(), A.col.as<int>(), d_alpha.as<double>(), bs, stride};
     DevBuf d_hash(sizeof(unsigned long long) * 2 * std::max<int64_t>(1, nnzb));
     block_hash_kernel<<<div_up(std::max<int64_t>(1, nnzb), 128), 128, 0, ctx.stream>>>(
-        d_At.as<double>(), nnzb, bs, stride, d_hash.as<unsigned long long>());
+        d_At, nnzb, bs, stride, d_hash.as<unsigned long long>());
     after_launch("block_hash_kernel");
     std::vector<uint64_t> hash(2 * std::max<int64_t>(1, nnzb));
     d2h(ctx, hash.data(), d_hash.p, sizeof(uint64_t) * 2 * nnzb);
@@ -1098,7 +1093,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         DevBuf d_reps(sizeof(int) * ndist), d_rm(sizeof(double) * size_t(ndist) * bs * bs);
         h2d(ctx, d_reps.p, reps.data(), sizeof(int) * ndist);
         gather_rowmajor_kernel<<<div_up(int64_t(ndist) * bs * bs, 256), 256, 0, ctx.stream>>>(
-            d_At.as<double>(), d_reps.as<int>(), ndist, bs, stride, d_rm.as<double>());
+            d_At, d_reps.as<int>(), ndist, bs, stride, d_rm.as<double>());
         after_launch("gather_rowmajor_kernel");
         std::vector<double> rm(size_t(ndist) * bs * bs);
         d2h(ctx, rm.data(), d_rm.p, sizeof(double) * rm.size());
@@ -1355,7 +1350,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             h2d(ctx, d_nj.p, hnj.data(), sizeof(int) * nb);
             h2d(ctx, d_xoff.p, xo.data(), sizeof(int64_t) * nb);
             const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
-            assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At.as<double>(), stride, bs, d_blk.as<int>(),
+            assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
                                                          d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                          d_moff.as<int64_t>(), d_M.as<double>());
             after_launch("assemble_m_kernel");
@@ -1401,7 +1396,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             for (int i = 0; i < nb; ++i)
                 if (def[i]) defl.push_back(i);
             if (!defl.empty()) {
-                assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At.as<double>(), stride, bs, d_blk.as<int>(),
+                assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
                                                              d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                              d_moff.as<int64_t>(), d_M.as<double>());
                 after_launch("assemble_m_kernel");

@@ -282,3 +282,59 @@ def test_transfers_irregular_bitwise(family):
     out = subprocess.run([sys.executable, "-c", IRREGULAR_SCRIPT % root], env=env, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+TVIEW_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2412_12506_b200 as g
+from tests import cases as K
+case = %r
+ctx = g.Context(0)
+if case == "scalar3d-p2-16":
+    spec, kind, zeta = K.scalar(16, 3, K.P, degree=2, beta=4.0), g.SYSTEM_SCALAR, 0.1
+elif case == "scalar2d-p4-64":
+    spec, kind, zeta = K.scalar(64, 2, K.D, degree=4, beta=16.0), g.SYSTEM_SCALAR, 0.1
+else:
+    spec = K.stokes(12, 3, K.P, gamma=0.0, degree=2, beta=4.0, beta_p=1 / 16, delta=0.01)
+    kind, zeta = g.SYSTEM_STOKES, 0.107
+P = g.Problem(spec, any_n=True)
+n, bs, _ = P.level_shape(0)
+assert n > 8 * 148
+A = P.device_operator(ctx, 0)
+S = g.Smoother(ctx, A, g.SmootherConfig.sai(1, zeta), system_kind=kind, n_velocity=P.n_velocity)
+Bd = g.DeviceBsr(ctx, n, n, bs, bs, *S.sai_matrix())
+rng = np.random.default_rng(7)
+b = torch.as_tensor(rng.uniform(-1, 1, n * bs)).cuda()
+x = torch.as_tensor(rng.uniform(-1, 1, n * bs)).cuda()
+r = torch.empty_like(b)
+g.residual(ctx, A, b, x, r)
+for sweep, op in ((g.SWEEP_REVERSE, g.spmv_transpose), (g.SWEEP_FORWARD, g.spmv)):
+    y = torch.empty_like(b)
+    op(ctx, Bd, r, y)
+    want = x.cpu().numpy() + y.cpu().numpy()
+    got = x.clone()
+    S.apply(b, got, sweep)
+    got = got.cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64)), (case, sweep, np.abs(got - want).max())
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("case", ["scalar3d-p2-16", "scalar2d-p4-64", "stokes3d-p2-12"])
+def test_sai_transpose_view_sweeps_bitwise(case):
+    """Reverse SAI sweeps read B^T as a VIEW of B's blocks (CSC index +
+    permutation, transposed reads in the row pass; forced by LDGMG_TVIEW=1,
+    by default only when the explicit copy does not fit): bit-identical to
+    x + spmv_transpose(B, b - A x) through the explicit transposed copy
+    (blockla.hpp:157-176 order).  Sizes exceed the split-row threshold so the
+    streaming kernel runs: bs 27 (odd, 8-byte reads), 25, and 108 (paired
+    16-byte reads)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LDGMG_TVIEW="1")
+    out = subprocess.run([sys.executable, "-c", TVIEW_SCRIPT % (root, case)], env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
