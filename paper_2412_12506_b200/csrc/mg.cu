@@ -16,6 +16,9 @@
 #include "host_eig.hpp"
 #include "mg.hpp"
 
+#include <cusolverDn.h>
+#include <string>
+
 namespace ldgmg_b200 {
 
 // ------------------------------------------------------------- colouring
@@ -409,6 +412,38 @@ void Mg::init(Ctx& ctx) {
     (void)ctx;
 }
 
+/// Dense symmetric eigensolve of a LARGE bottom operator at setup time
+/// (cuSOLVER dsyevd on the device; the host tred2/tql2 takes ~19 s at
+/// n = 2916).  Same contract as sym_eig_host: eigenvalues ascending,
+/// eigenvectors as the columns of V (column-major).  Setup only.
+void sym_eig_device(Ctx& ctx, int n, const double* A, double* lambda, double* V) {
+    cusolverDnHandle_t h = nullptr;
+    auto ck = [](cusolverStatus_t st, const char* what) {
+        if (st != CUSOLVER_STATUS_SUCCESS) fail(LDGMG_ERR_RUNTIME, std::string("sym_eig: ") + what + " failed");
+    };
+    ck(cusolverDnCreate(&h), "cusolverDnCreate");
+    struct Guard {
+        cusolverDnHandle_t h;
+        ~Guard() { cusolverDnDestroy(h); }
+    } guard{h};
+    ck(cusolverDnSetStream(h, ctx.stream), "cusolverDnSetStream");
+    DevBuf dA(sizeof(double) * size_t(n) * n), dW(sizeof(double) * n), dinfo(sizeof(int));
+    h2d(ctx, dA.p, A, dA.bytes);
+    int lwork = 0;
+    ck(cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA.as<double>(), n,
+                                   dW.as<double>(), &lwork),
+       "dsyevd_bufferSize");
+    DevBuf work(sizeof(double) * std::max(1, lwork));
+    ck(cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, dA.as<double>(), n, dW.as<double>(),
+                        work.as<double>(), lwork, dinfo.as<int>()),
+       "dsyevd");
+    int info = 0;
+    d2h(ctx, &info, dinfo.p, sizeof(int));
+    if (info != 0) fail(LDGMG_ERR_RUNTIME, "sym_eig: eigensolver failed");
+    d2h(ctx, lambda, dW.p, sizeof(double) * n);
+    d2h(ctx, V, dA.p, dA.bytes);
+}
+
 void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
     const Bsr& Ab = *A.back();
     const int n = Ab.brows * bs;
@@ -435,7 +470,11 @@ void Mg::set_bottom(Ctx& ctx, const double* V, const double* lambda) {
             }
         if (std::sqrt(asym) > 1e-13 * std::max(1e-300, std::sqrt(nrm)))
             fail(LDGMG_ERR_INVALID_ARGUMENT, "sym_eig: matrix is not symmetric");
-        sym_eig_host(n, D.data(), lam.data(), Vc.data());
+        static const int gpu_min = getenv("LDGMG_GPU_EIG_MIN") ? atoi(getenv("LDGMG_GPU_EIG_MIN")) : 1024;
+        if (n >= gpu_min && gpu_min >= 0)
+            sym_eig_device(ctx, n, D.data(), lam.data(), Vc.data());  // large bottoms (C5 48^3: n = 2916)
+        else
+            sym_eig_host(n, D.data(), lam.data(), Vc.data());
     }
     std::vector<double> Vr(size_t(n) * n);
     for (int i = 0; i < n; ++i)

@@ -97,6 +97,7 @@ def main():
     ap.add_argument("--csv", default=None, help="also write reference-format CSV rows (+perf columns)")
     ap.add_argument("--host-assembly", action="store_true", help="assemble the operators on the host (default: GPU)")
     ap.add_argument("--cycles", type=int, default=20)
+    ap.add_argument("--no-solve", action="store_true", help="V-cycle timing only (no stationary / GMRES solve)")
     a = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -106,8 +107,9 @@ def main():
     for name in a.names:
         spec, cfg, rk = cfgs[name]
         t0 = time.time()
+        pow2 = spec.n & (spec.n - 1) == 0
         P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements,
-                      device_assembly=not a.host_assembly)
+                      device_assembly=not a.host_assembly, any_n=not pow2)
         t_asm = time.time() - t0
         t0 = time.time()
         mg = g.Multigrid(ctx, cfg, P)
@@ -128,11 +130,16 @@ def main():
         rec = {"config": name, "N": P.level_shape(0)[0], "bs": P.bs, "fine_dof": P.level_shape(0)[0] * P.bs,
                "levels": P.depth, "setup_s": {"assembly": round(t_asm, 2), "gpu_hierarchy": round(t_mg, 2)},
                "vcycle_ms": tc * 1e3, "dof_updates_per_s": dof / tc, "alg_GBps": byts / tc / 1e9,
-               "alg_bytes_per_cycle": byts}
+               "alg_bytes_per_cycle": byts, "device_mem_used_GB": round((lambda f, t: (t - f) / 1e9)(
+                   *torch.cuda.mem_get_info()), 1)}
         if cfg.smoother.kind == g.SAI:
             st = mg.smoother(0).sai_stats()
             rec["sai_level0"] = {"cache_misses": st.cache_misses, "cache_hits": st.cache_hits,
                                  "ls_shapes": {f"{k[0]}x{k[1]}": v for k, v in st.ls_dims().items()}}
+        if a.no_solve:
+            print(json.dumps(rec), flush=True)
+            del mg, P
+            continue
         t0 = time.perf_counter()
         xs, hist, its = mg.solve_host(bh, tol=1e-10, maxit=40)
         ts = time.perf_counter() - t0
