@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
 }
 
 template <int GT, int BS>
-void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
+int rowpass_occupancy(Ctx& ctx, size_t smem) {
     static int attr_set_device = -1;
     if (attr_set_device != ctx.device) {
         LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -366,15 +366,41 @@ void configure_and_launch(Ctx& ctx, const RowPassArgs& a, size_t smem) {
         attr_set_device = ctx.device;
     }
     static std::vector<std::pair<size_t, int>> occ_cache;
-    int occ = -1;
     for (const auto& e : occ_cache)
-        if (e.first == smem) occ = e.second;
-    if (occ < 0) {
-        LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<GT, BS>, GT, smem));
-        occ_cache.push_back({smem, occ});
+        if (e.first == smem) return e.second;
+    int occ = 0;
+    LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rowpass_kernel<GT, BS>, GT, smem));
+    occ_cache.push_back({smem, occ});
+    return occ;
+}
+
+/// Ring depth and grid for one pass.  Large passes: 3 stages (block pairs in
+/// compute + one in flight).  Passes with only a few rows per resident CTA
+/// (C2 level 1: 4096 rows over 1628 CTAs): 2 stages -> more resident CTAs,
+/// and the grid sized so every CTA gets the same number of rows (the pass
+/// ends with the CTA holding the most rows).  Measured on B200, C2 level 1:
+/// 33.5 us (3 stages, 1628 CTAs) -> 30.9 us (2 stages).  LDGMG_NS overrides.
+template <int GT, int BS>
+void configure_and_launch(Ctx& ctx, RowPassArgs a, size_t stage_bytes, int ns_env) {
+    auto smem_for = [&](int ns) {
+        return size_t(ns) * stage_bytes + size_t(ns) * a.xslot_doubles * 8 + 2 * size_t(a.xslot_doubles) * 8 +
+               size_t(ns) * 8;
+    };
+    int ns = ns_env > 1 ? ns_env : 3;
+    while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
+    if (ns_env <= 1 && ns == 3) {
+        const int occ3 = rowpass_occupancy<GT, BS>(ctx, smem_for(3));
+        if (occ3 >= 1 && a.nrows < 4 * occ3 * ctx.num_sms) ns = 2;
     }
+    const size_t smem = smem_for(ns);
+    if (smem > ctx.smem_optin) fail(LDGMG_ERR_INVALID_ARGUMENT, "rowpass: block too large for shared memory");
+    a.nstages = ns;
+    const int occ = rowpass_occupancy<GT, BS>(ctx, smem);
     if (occ < 1) fail(LDGMG_ERR_CUDA, "rowpass: block does not fit on an SM");
-    const int grid = std::max(1, std::min(a.nrows, occ * ctx.num_sms));
+    const int slots = occ * ctx.num_sms;
+    int grid = std::max(1, std::min(a.nrows, slots));
+    const int per = (a.nrows + slots - 1) / slots;  // rows of the busiest CTA
+    if (per <= 8) grid = std::max(1, (a.nrows + per - 1) / per);
     launch_pdl(rowpass_kernel<GT, BS>, dim3(grid), dim3(GT), smem, ctx.stream, a);
     after_launch("rowpass_kernel");
 }
@@ -854,25 +880,17 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         const char* e = getenv("LDGMG_NS");
         ns_env = e ? atoi(e) : -1;
     }
-    // 3 stages: pairs of blocks in compute + one in flight per CTA, 12 CTAs/SM
-    // for 27x27 blocks (measured best on B200: 6.7 TB/s on the C2 residual)
-    int ns = ns_env > 1 ? ns_env : 3;
-    while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
-    a.nstages = ns;
-    const size_t smem = size_t(ns) * stage_bytes + size_t(ns) * a.xslot_doubles * 8 +
-                        2 * size_t(a.xslot_doubles) * 8 + size_t(ns) * 8;
-    if (smem > ctx.smem_optin) fail(LDGMG_ERR_INVALID_ARGUMENT, "rowpass: block too large for shared memory");
     const bool sq = A.rbs == A.cbs;
-    if (sq && A.rbs == 16) configure_and_launch<32, 16>(ctx, a, smem);
-    else if (sq && A.rbs == 25) configure_and_launch<32, 25>(ctx, a, smem);
-    else if (sq && A.rbs == 27) configure_and_launch<32, 27>(ctx, a, smem);
-    else if (sq && A.rbs == 48) configure_and_launch<64, 48>(ctx, a, smem);
-    else if (sq && A.rbs == 108) configure_and_launch<128, 108>(ctx, a, smem);
+    if (sq && A.rbs == 16) configure_and_launch<32, 16>(ctx, a, stage_bytes, ns_env);
+    else if (sq && A.rbs == 25) configure_and_launch<32, 25>(ctx, a, stage_bytes, ns_env);
+    else if (sq && A.rbs == 27) configure_and_launch<32, 27>(ctx, a, stage_bytes, ns_env);
+    else if (sq && A.rbs == 48) configure_and_launch<64, 48>(ctx, a, stage_bytes, ns_env);
+    else if (sq && A.rbs == 108) configure_and_launch<128, 108>(ctx, a, stage_bytes, ns_env);
     else switch (GT) {
-        case 32: configure_and_launch<32, 0>(ctx, a, smem); break;
-        case 64: configure_and_launch<64, 0>(ctx, a, smem); break;
-        case 128: configure_and_launch<128, 0>(ctx, a, smem); break;
-        default: configure_and_launch<256, 0>(ctx, a, smem); break;
+        case 32: configure_and_launch<32, 0>(ctx, a, stage_bytes, ns_env); break;
+        case 64: configure_and_launch<64, 0>(ctx, a, stage_bytes, ns_env); break;
+        case 128: configure_and_launch<128, 0>(ctx, a, stage_bytes, ns_env); break;
+        default: configure_and_launch<256, 0>(ctx, a, stage_bytes, ns_env); break;
     }
 }
 
