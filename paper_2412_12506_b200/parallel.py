@@ -479,13 +479,25 @@ class DistMultigrid:
             with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
                 self._cycle_body(self._gx, self._gb, True)
             self.graph_kernels = L.launch_count() - n0  # our kernels per replay
-            self._gx.copy_(x_probe)
-            self._gb.copy_(b_probe)
-            g.replay()
-            torch.cuda.synchronize()
-            ok = bool(torch.equal(self._gx, x_e))
+            ok = True
         except Exception as exc:  # capture not supported for some op: stay eager
             self._graph_error = repr(exc)
+            ok = False
+        # a replay posts NCCL exchanges: replay only if EVERY rank captured
+        # (a lone replay would wait forever on its peers)
+        capt = torch.tensor([1 if ok else 0], dtype=torch.int32, device=x_probe.device)
+        self.dist.all_reduce(capt, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(capt.item()) == 1:
+            try:
+                self._gx.copy_(x_probe)
+                self._gb.copy_(b_probe)
+                g.replay()
+                torch.cuda.synchronize()
+                ok = bool(torch.equal(self._gx, x_e))
+            except Exception as exc:
+                self._graph_error = repr(exc)
+                ok = False
+        else:
             ok = False
         # every rank reaches this collective, whatever happened above
         okt = torch.tensor([1 if ok else 0], dtype=torch.int32, device=x_probe.device)
