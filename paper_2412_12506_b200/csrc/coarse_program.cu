@@ -106,6 +106,281 @@ __global__ void __launch_bounds__(256) coarse_program_kernel(const CoarseOp* __r
     }
 }
 
+// ------------------------------------------------------------------------
+// Cluster tail: the same program run by ONE thread-block cluster (up to 16
+// CTAs on 16 SMs of one GPC) with hardware cluster barriers between ops
+// instead of grid-wide ones.  Used for the tail of the hierarchy whose level
+// operators are only a few MB (C2 from 4^3, C1 from 16^2), where every
+// graph-launched pass costs ~4-7 us of launch and dependency latency for
+// ~1 us of work.  Every op keeps the reference order of the standalone
+// kernels (bit-identical).  Data written inside the kernel (iterates,
+// residuals, right-hand sides) is read with ld.global.cg (L2, never a stale
+// L1 line) after the release/acquire cluster barrier; immutable operands
+// (blocks, factors, K, bottom V) use TMA bulk copies / the read-only path.
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+constexpr int kTailThreads = 256;
+constexpr int kTailMaxRows = 64;  // rows per wave
+
+/// One row op over the cluster: CTA `cta` of `ncta` takes rows cta, cta+ncta,
+/// ... in waves that fit shared memory.  Per wave: the rows' contiguous
+/// blocks (and relax factors V) arrive by TMA bulk copies, the x blocks and
+/// epilogue operands by L2 loads, warps compute s_k per (row, block), one
+/// warp per row combines them in CSR order and runs the epilogue
+/// (split_row_task_tma's arithmetic).  rbs, cbs <= 32.
+__device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, size_t sm_doubles, uint64_t* bar,
+                          uint32_t& phase, int* srow, int* sk0, int* snk, int* soff) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
+    const bool relax = a.mode == MODE_RELAX;
+    const int xs = (a.cbs + 1) & ~1;
+    const int nmine = cta < a.nrows ? (a.nrows - cta + ncta - 1) / ncta : 0;
+    for (int k = 0; k < nmine;) {
+        // plan the wave (all threads compute the same plan)
+        int nr = 0, nb = 0;
+        size_t need = 0;
+        while (k + nr < nmine && nr < kTailMaxRows) {
+            const int row = row_at(a, cta + (k + nr) * ncta);
+            const int k0 = __ldg(a.ptr + row), len = __ldg(a.ptr + row + 1) - k0;
+            const size_t add = size_t(len) * (a.blk_stride + xs + 32) + (relax ? size_t(a.vstride) : 0) + 4 * 32;
+            if (nr > 0 && need + add > sm_doubles) break;
+            if (tid == 0) {
+                srow[nr] = row;
+                sk0[nr] = k0;
+                snk[nr] = len;
+                soff[nr] = nb;
+            }
+            need += add;
+            nb += len;
+            ++nr;
+        }
+        __syncthreads();
+        double* sB = sm;                                       // nb blocks
+        double* sV = sB + size_t(nb) * a.blk_stride;           // nr factors
+        double* sX = sV + (relax ? size_t(nr) * a.vstride : 0);  // nb x-blocks
+        double* ss = sX + size_t(nb) * xs;                     // nb x 32 partial sums
+        double* ep = ss + size_t(nb) * 32;                     // nr x (b, xe, scal, lam) x 32
+        if (tid == 0) {
+            fence_proxy_async();  // earlier generic reads of these stages precede the async writes
+            uint32_t bytes = uint32_t(nb) * uint32_t(a.blk_stride) * 8u + (relax ? uint32_t(nr * a.vstride) * 8u : 0u);
+            mbar_arrive_expect_tx(bar, bytes);
+            for (int i = 0; i < nr; ++i) {
+                bulk_g2s(sB + size_t(soff[i]) * a.blk_stride, a.val + size_t(sk0[i]) * a.blk_stride,
+                         uint32_t(snk[i]) * uint32_t(a.blk_stride) * 8u, bar);
+                if (relax) bulk_g2s(sV + size_t(i) * a.vstride, a.V + size_t(srow[i]) * a.vstride,
+                                    uint32_t(a.vstride) * 8u, bar);
+            }
+        }
+        // x blocks of every (row, block) and the epilogue operands
+        for (int i = 0; i < nr; ++i) {
+            for (int t = tid; t < snk[i] * a.cbs; t += blockDim.x) {
+                const int q = t / a.cbs, c = t - q * a.cbs;
+                const int j = __ldg(a.col + sk0[i] + q);
+                sX[size_t(soff[i] + q) * xs + c] = __ldcg(a.x + size_t(j) * a.cbs + c);
+            }
+            if (tid < a.rbs) {
+                const size_t o = size_t(srow[i]) * a.rbs + tid;
+                double* e = ep + size_t(i) * 128;
+                if (a.mode == MODE_RESIDUAL || relax) e[tid] = __ldcg(a.b + o);
+                if (relax || a.mode == MODE_ADD) e[32 + tid] = __ldcg(a.xe + o);
+                if (relax) {
+                    e[64 + tid] = __ldg(a.scal + o);
+                    e[96 + tid] = __ldg(a.lam + o);
+                }
+            }
+        }
+        __syncthreads();
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        // s_k per (row, block), one warp per item
+        for (int i = 0; i < nr; ++i)
+            for (int q = warp; q < snk[i]; q += W) {
+                if (relax && __ldg(a.col + sk0[i] + q) == srow[i]) continue;
+                if (lane < a.rbs) {
+                    const double* Bc = sB + size_t(soff[i] + q) * a.blk_stride + lane;
+                    const double* xq = sX + size_t(soff[i] + q) * xs;
+                    double s = 0.0;
+#pragma unroll 9
+                    for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, Bc[size_t(c) * a.rbs], xq[c]);
+                    ss[size_t(soff[i] + q) * 32 + lane] = s;
+                }
+            }
+        __syncthreads();
+        // epilogue, one warp per row
+        for (int i = warp; i < nr; i += W) {
+            const bool act = lane < a.rbs;
+            const int row = srow[i];
+            const double* e = ep + size_t(i) * 128;
+            double acc = 0.0;
+            if (act) {
+                if (relax) {
+                    acc = e[lane];
+                    for (int q = 0; q < snk[i]; ++q)
+                        if (__ldg(a.col + sk0[i] + q) != row) acc = __dsub_rn(acc, ss[size_t(soff[i] + q) * 32 + lane]);
+                } else {
+                    for (int q = 0; q < snk[i]; ++q) acc = __dadd_rn(acc, ss[size_t(soff[i] + q) * 32 + lane]);
+                }
+            }
+            if (relax) {
+                // reuse this row's x-block slots as the u / t scratch (consumed above)
+                double* ubuf = sX + size_t(soff[i]) * xs;
+                double* tbuf = ss + size_t(soff[i]) * 32;
+                const int bs = a.rbs, ld = a.ld;
+                const double* Vr = sV + size_t(i) * a.vstride;
+                const double sc = act ? e[64 + lane] : 0.0;
+                const double lam = act ? e[96 + lane] : 0.0;
+                const double xe = act ? e[32 + lane] : 0.0;
+                __syncwarp();
+                if (act) ubuf[lane] = __dmul_rn(sc, acc);
+                __syncwarp();
+                double tv = 0.0;
+                if (act) {
+                    double tt = 0.0;
+                    const double* Vcol = Vr + size_t(lane) * ld;
+                    for (int kk = 0; kk < bs; ++kk) tt = madd_rn(tt, Vcol[kk], ubuf[kk]);
+                    const double cut = a.kernel_tol * __ldg(a.lmax + row);
+                    tv = fabs(lam) <= cut ? 0.0 : tt / lam;
+                }
+                __syncwarp();
+                if (act) tbuf[lane] = tv;
+                __syncwarp();
+                if (act) {
+                    double w = 0.0;
+                    for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, Vr[size_t(kk) * ld + lane], tbuf[kk]);
+                    const double yv = __dmul_rn(sc, w);
+                    acc = __dadd_rn(__dmul_rn(1.0 - a.omega, xe), __dmul_rn(a.omega, yv));
+                }
+            }
+            if (act) {
+                double out;
+                switch (a.mode) {
+                    case MODE_RESIDUAL: out = __dsub_rn(e[lane], acc); break;
+                    case MODE_ADD: out = __dadd_rn(e[32 + lane], acc); break;
+                    default: out = acc; break;
+                }
+                a.y[size_t(row) * a.rbs + lane] = out;
+            }
+        }
+        __syncthreads();
+        k += nr;
+    }
+}
+
+__global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const CoarseOp* __restrict__ ops, int nops,
+                                                                      int sm_doubles) {
+    extern __shared__ __align__(128) double tsm[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int srow[kTailMaxRows], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows];
+    __shared__ CoarseOp sop;
+    const int cta = blockIdx.x, ncta = gridDim.x, tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    const int64_t gt = int64_t(cta) * blockDim.x + tid, nth = int64_t(ncta) * blockDim.x;
+    for (int i = 0; i < nops; ++i) {
+        {
+            const int nw = int(sizeof(CoarseOp) / sizeof(int));
+            const int* src = reinterpret_cast<const int*>(ops + i);
+            int* dst = reinterpret_cast<int*>(&sop);
+            for (int w = tid; w < nw; w += blockDim.x) dst[w] = src[w];
+            __syncthreads();
+        }
+        const CoarseOp& op = sop;
+        switch (op.type) {
+            case OP_ROWS:
+                tail_rows(op.rows, cta, ncta, tsm, size_t(sm_doubles), &bar, phase, srow, sk0, snk, soff);
+                break;
+            case OP_COPY:
+                for (int64_t t = gt; t < op.count; t += nth) op.dst[t] = __ldcg(op.src + t);
+                break;
+            case OP_ZERO:
+                for (int64_t t = gt; t < op.count; t += nth) op.dst[t] = 0.0;
+                break;
+            case OP_RESTRICT: {
+                // thread (child q, entry o) of parent p: s_q in shared memory, then
+                // thread o sums them in child order (restrict_parent_task's bits)
+                const int BS = op.bss * op.ncomp, bb = op.bss * op.bss;
+                double* ssum = tsm;
+                for (int p = cta; p < op.n_parents; p += ncta) {
+                    const int q0 = __ldg(op.child_ptr + p), nch = __ldg(op.child_ptr + p + 1) - q0;
+                    for (int t = tid; t < nch * BS; t += blockDim.x) {
+                        const int q = t / BS, o = t - q * BS;
+                        const int f = __ldg(op.child + q0 + q), ot = __ldg(op.orth + f);
+                        const double* src = op.src + size_t(f) * BS;
+                        double sq;
+                        if (ot < 0) {
+                            sq = __ldcg(src + o);
+                        } else {
+                            const int c = o / op.bss, j = o - c * op.bss;
+                            const double* Ko = op.K + size_t(ot) * bb + j;
+                            sq = 0.0;
+#pragma unroll 9
+                            for (int ii = 0; ii < op.bss; ++ii)
+                                sq = madd_rn(sq, __ldg(Ko + size_t(ii) * op.bss), __ldcg(src + c * op.bss + ii));
+                        }
+                        ssum[t] = sq;
+                    }
+                    __syncthreads();
+                    for (int o = tid; o < BS; o += blockDim.x) {
+                        double acc = 0.0;
+                        for (int q = 0; q < nch; ++q) acc = __dadd_rn(acc, ssum[q * BS + o]);
+                        op.dst[size_t(p) * BS + o] = acc;
+                    }
+                    __syncthreads();
+                }
+                break;
+            }
+            case OP_PROLONG: {
+                const int BS = op.bss * op.ncomp, bb = op.bss * op.bss;
+                for (int p = cta; p < op.n_parents; p += ncta) {
+                    const int q0 = __ldg(op.child_ptr + p), nch = __ldg(op.child_ptr + p + 1) - q0;
+                    const double* xc = op.src + size_t(p) * BS;
+                    for (int t = tid; t < nch * BS; t += blockDim.x) {
+                        const int q = t / BS, ii = t - q * BS;
+                        const int f = __ldg(op.child + q0 + q), ot = __ldg(op.orth + f);
+                        double* dst = op.dst + size_t(f) * BS + ii;
+                        const double old = __ldcg(dst);
+                        if (ot < 0) {
+                            *dst = __dadd_rn(old, __ldcg(xc + ii));
+                            continue;
+                        }
+                        const int c = ii / op.bss, i2 = ii - c * op.bss;
+                        const double* Ko = op.K + size_t(ot) * bb + size_t(i2) * op.bss;
+                        double s = 0.0;
+#pragma unroll 9
+                        for (int j = 0; j < op.bss; ++j) s = madd_rn(s, __ldg(Ko + j), __ldcg(xc + c * op.bss + j));
+                        *dst = __dadd_rn(old, s);
+                    }
+                }
+                break;
+            }
+            case OP_PINV_T:
+                for (int64_t t = gt; t < op.n; t += nth) {
+                    double s = 0.0;
+#pragma unroll 8
+                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), __ldcg(op.src + k));
+                    const double l = __ldg(op.lam + t);
+                    op.dst[t] = fabs(l) <= op.cut ? 0.0 : s / l;
+                }
+                break;
+            case OP_PINV_X:
+                for (int64_t t = gt; t < op.n; t += nth) {
+                    double s = 0.0;
+#pragma unroll 8
+                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), __ldcg(op.src + k));
+                    op.dst[t] = s;
+                }
+                break;
+        }
+        cluster_sync_all();  // op results visible cluster-wide; descriptor reloaded after
+    }
+}
+
 CoarseOp rows_op(const Bsr& A, int mode, const double* x, const double* b, const double* xe, double* y,
                  const int* rows, int nrows, const DiagFactors* F, double omega) {
     CoarseOp op{};
@@ -142,15 +417,43 @@ CoarseOp rows_op(const Bsr& A, int mode, const double* x, const double* b, const
 /// Record the V-cycle of levels >= lc (Mg::v_cycle order) as a program.
 void Mg::build_coarse_program(Ctx& ctx) {
     coarse_level = -1;
+    coarse_cluster = 0;
     int lc = -1;
-    for (int l = 1; l + 1 < depth && coarse_rows > 0; ++l)
-        if (A[l]->brows <= coarse_rows) {
-            lc = l;
-            break;
-        }
+    // LDGMG_COARSE_ROWS=n (> 0): grid-wide cooperative program for levels with
+    // <= n elements.  LDGMG_TAIL=1: the cluster tail for the levels whose
+    // operators are at most LDGMG_TAIL_BYTES (default 4 MB: ~256 KB per CTA
+    // of a 16-CTA cluster).  Both are bit-identical to the graph-launched
+    // passes and both measured slower on B200 (C2: 3.25 -> 3.62 ms grid-wide,
+    // 3.20 -> 3.49 ms cluster: 18 dependent ops on one cluster take 350 us,
+    // mostly cluster-barrier waits behind the busiest CTA's load round trips,
+    // against ~85 us of graph nodes), so both are off by default.
+    static int tail_env = -2;
+    static long long tail_bytes = 0;
+    if (tail_env == -2) {
+        const char* e = getenv("LDGMG_TAIL");
+        tail_env = e ? atoi(e) : 0;
+        const char* tb = getenv("LDGMG_TAIL_BYTES");
+        tail_bytes = tb ? atoll(tb) : (4ll << 20);
+    }
+    bool cluster = false;
+    if (coarse_rows > 0) {
+        for (int l = 1; l + 1 < depth; ++l)
+            if (A[l]->brows <= coarse_rows) {
+                lc = l;
+                break;
+            }
+    } else if (tail_env) {
+        for (int l = 1; l + 1 < depth; ++l)
+            if (int64_t(A[l]->nnzb) * A[l]->blk_stride * 8 <= tail_bytes) {
+                lc = l;
+                break;
+            }
+        cluster = true;
+    }
     if (lc < 0) return;
     int coop = 0;
     LDGMG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx.device));
+    if (cluster) LDGMG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrClusterLaunch, ctx.device));
     if (!coop || bottom.n > 4096) return;
     int maxlen = 1;
     for (int l = lc; l < depth; ++l) {
@@ -241,6 +544,39 @@ void Mg::build_coarse_program(Ctx& ctx) {
         maxbs = std::max(maxbs, A[l]->rbs);
         if (l + 1 < depth) maxch = std::max(maxch, T[l]->max_children);
     }
+    if (cluster) {
+        // one cluster of up to 16 CTAs (non-portable size), ~200 KB of shared memory each
+        const size_t sm_doubles = 200 * 1024 / 8;
+        if (sm_doubles < size_t(maxch) * maxbs) return;
+        int csize = 16;
+        if (const char* e = getenv("LDGMG_TAIL_CTAS")) csize = std::max(1, std::min(16, atoi(e)));
+        LDGMG_CUDA(cudaFuncSetAttribute(coarse_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LDGMG_CUDA(cudaFuncSetAttribute(coarse_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(sm_doubles * 8)));
+        for (; csize >= 1; csize /= 2) {
+            cudaLaunchConfig_t lc_cfg{};
+            lc_cfg.gridDim = dim3(csize);
+            lc_cfg.blockDim = dim3(kTailThreads);
+            lc_cfg.dynamicSmemBytes = sm_doubles * 8;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = csize;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc_cfg.attrs = at;
+            lc_cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, coarse_cluster_kernel, &lc_cfg) == cudaSuccess &&
+                nclusters >= 1)
+                break;
+            cudaGetLastError();
+        }
+        if (csize < 1) return;
+        coarse_cluster = csize;
+        coarse_smem = sm_doubles * 8;
+        coarse_level = lc;
+        return;
+    }
     coarse_smem = sizeof(double) * std::max<size_t>(size_t(maxlen) * 32 + 64, size_t(maxch) * maxbs);
     int occ = 0;
     LDGMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, coarse_program_kernel, 256, coarse_smem));
@@ -257,6 +593,24 @@ void Mg::build_coarse_program(Ctx& ctx) {
 void Mg::launch_coarse_program(Ctx& ctx) {
     const CoarseOp* ops = coarse_prog.as<CoarseOp>();
     int nops = coarse_nops, maxlen = coarse_maxlen;
+    if (coarse_cluster) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(coarse_cluster);
+        cfg.blockDim = dim3(kTailThreads);
+        cfg.dynamicSmemBytes = coarse_smem;
+        cfg.stream = ctx.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = coarse_cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const int smd = int(coarse_smem / 8);
+        cuda_check(cudaLaunchKernelEx(&cfg, coarse_cluster_kernel, ops, nops, smd), "coarse_cluster_kernel");
+        after_launch("coarse_cluster_kernel");
+        return;
+    }
     void* args[] = {&ops, &nops, &maxlen};
     LDGMG_CUDA(cudaLaunchCooperativeKernel((const void*)coarse_program_kernel, dim3(coarse_grid), dim3(256), args,
                                            coarse_smem, ctx.stream));

@@ -95,6 +95,7 @@ struct Mg {
     // LDGMG_COARSE_ROWS=n enables it for levels with <= n elements.
     int coarse_rows = 0;
     int coarse_level = -1;   // first level run by the program (-1: none)
+    int coarse_cluster = 0;  // > 0: run by one thread-block cluster of this many CTAs
     bool coarse_dirty = true;
     DevBuf coarse_prog;
     int coarse_nops = 0, coarse_maxlen = 1, coarse_grid = 0;

@@ -36,14 +36,18 @@ np.save(sys.argv[1], np.concatenate(out))
 """
 
 
-def run(env_rows, path):
-    env = dict(os.environ, LDGMG_COARSE_ROWS=str(env_rows))
+def run(env_rows, path, tail="0"):
+    env = dict(os.environ, LDGMG_COARSE_ROWS=str(env_rows), LDGMG_TAIL=tail)
     subprocess.run([sys.executable, "-c", SCRIPT % ROOT, path], env=env, check=True, timeout=600)
 
 
 def test_coarse_program_bitwise(ctx, tmp_path):
+    """grid-wide cooperative program, cluster tail and the default
+    launch-per-pass V-cycle give the same bits"""
     import numpy as np
-    a, b = str(tmp_path / "on.npy"), str(tmp_path / "off.npy")
+    a, b, c = str(tmp_path / "coop.npy"), str(tmp_path / "tail.npy"), str(tmp_path / "off.npy")
     run(4096, a)
-    run(0, b)
-    assert np.array_equal(np.load(a), np.load(b))
+    run(0, b, tail="1")
+    run(0, c)
+    assert np.array_equal(np.load(a), np.load(c))
+    assert np.array_equal(np.load(b), np.load(c))
