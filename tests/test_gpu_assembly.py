@@ -22,14 +22,21 @@ SPECS = {
     "stokes2d-stress-p1": K.stokes(8, 2, K.P, gamma=1.0, degree=1),
     "stokes2d-stress-neumann": K.stokes(4, 2, (K.N, K.N, K.P, K.P, K.P, K.P), gamma=1.0, degree=2),
     "stokes3d-unsteady-p2-C5": K.baseline_configs()["C5"][0],
+    # extension A1 (the C5 48^3 mesh shape at test scale): non-power-of-two
+    # restricted-Morton mesh, 6^3 -> 3^3
+    "stokes3d-unsteady-p2-C5-6cubed-any-n": K.stokes(6, 3, K.P, gamma=0.0, degree=2, beta=4.0, beta_p=1 / 16,
+                                                     delta=0.01, phase_shape=g.PHASE_BALL, center=(0.5, 0.5, 0.5),
+                                                     radii=(0.25, 0.25, 0.25), mu_in=1e2, mu_out=1.0),
 }
+ANY_N = {"stokes3d-unsteady-p2-C5-6cubed-any-n"}
 
 
 @pytest.mark.parametrize("name", sorted(SPECS))
 def test_device_assembly_bit_identical(ctx, name):
     spec = SPECS[name]
-    host = g.Problem(spec, min_depth=1)
-    dev = g.Problem(spec, min_depth=1, device_assembly=True)
+    an = name in ANY_N
+    host = g.Problem(spec, min_depth=1, any_n=an)
+    dev = g.Problem(spec, min_depth=1, device_assembly=True, any_n=an)
     assert dev.depth == host.depth
     for l in range(host.depth):
         hp, hc, hv = host.level_matrix(l)
