@@ -289,7 +289,23 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
             if (nblk == 2) {
                 const int st2 = int((q + 1) % uint32_t(NS));
                 mbar_wait(bars + st2, ((q + 1) / uint32_t(NS)) & 1u);
-                if (act) {
+                if constexpr (BS > 0 && 2 * BS <= 32) {
+                    // small blocks: the pair's second block on the upper lanes
+                    // (one chain per lane instead of two), s2 shuffled down to
+                    // lane r; the row sum still adds s1 then s2
+                    const bool hi = t >= BS;
+                    const int r = hi ? t - BS : t;
+                    const double* Sx = hi ? stages + size_t(st2) * a.stage_doubles : S;
+                    const double* Xx = hi ? xslots + size_t(st2) * a.xslot_doubles : X;
+                    double s = 0.0;
+                    if (t < 2 * BS)
+                        s = a.tview ? bdot_t<BS>(Sx + size_t(r) * cbs, Xx, cbs) : bdot<BS>(Sx + r, Xx, cbs, rbs);
+                    const double s2 = __shfl_down_sync(0xffffffffu, s, BS);
+                    if (act) {
+                        acc = relax ? __dsub_rn(acc, s) : __dadd_rn(acc, s);
+                        acc = relax ? __dsub_rn(acc, s2) : __dadd_rn(acc, s2);
+                    }
+                } else if (act) {
                     double s1, s2;
                     if (a.tview)
                         bdot2_t<BS>(S + size_t(t) * cbs, X, stages + size_t(st2) * a.stage_doubles + size_t(t) * cbs,
