@@ -751,8 +751,8 @@ namespace {
 /// Requires rbs, cbs <= 32.
 __global__ void __launch_bounds__(256) rowsplit_kernel(const RowPassArgs a, int maxlen) {
     extern __shared__ __align__(16) double ss[];  // maxlen x 32 partial sums, then u, t
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) split_row_task(a, row_at(a, slot), maxlen, ss);
 }
 
@@ -765,11 +765,17 @@ __global__ void __launch_bounds__(256) rowsplit_tma_kernel(const RowPassArgs a, 
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_launch_dependents();
+    // immutable prologue: the first row's blocks (and factor) are requested
+    // before waiting on the predecessor
+    if (blockIdx.x < a.nrows) split_row_issue(a, row_at(a, blockIdx.x), maxlen, sm, &bar);
     pdl_wait();
-    pdl_trigger();
     uint32_t phase = 0;
-    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x)
-        split_row_task_tma(a, row_at(a, slot), maxlen, sm, &bar, phase);
+    bool issued = true;
+    for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) {
+        split_row_task_tma(a, row_at(a, slot), maxlen, sm, &bar, phase, issued);
+        issued = false;
+    }
 }
 
 int split_threshold_rows(const Ctx& ctx) {
@@ -841,7 +847,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
             static bool once = (max_carveout(rowsplit_tma_kernel), true);
             (void)once;
             const int threads = std::max(warps * 32, std::min(256, ((maxlen * A.cbs + 31) / 32) * 32));
-            launch_pdl(rowsplit_tma_kernel, dim3(grid), dim3(threads), smem_tma, ctx.stream, a, maxlen);
+            launch_pdl_small(rowsplit_tma_kernel, dim3(grid), dim3(threads), smem_tma, ctx.stream, a, maxlen);
             after_launch("rowsplit_tma_kernel");
             return;
         }
@@ -850,7 +856,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         const int grid = std::min(p.nrows, ctx.num_sms * 16);
         static bool once = (max_carveout(rowsplit_kernel), true);
         (void)once;
-        launch_pdl(rowsplit_kernel, dim3(grid), dim3(warps * 32), smem, ctx.stream, a, maxlen);
+        launch_pdl_small(rowsplit_kernel, dim3(grid), dim3(warps * 32), smem, ctx.stream, a, maxlen);
         after_launch("rowsplit_kernel");
         return;
     }

@@ -63,6 +63,40 @@ inline bool pdl_enabled() {
     return env != 0;
 }
 
+/// PDL for the SMALL kernels only (split-row passes of the coarse levels,
+/// transfers, bottom, projection; LDGMG_PDL_SMALL=0 disables): they trigger
+/// their dependents at entry and issue their immutable prologue (barrier
+/// init, TMA of the first row's blocks / injection matrices) before
+/// griddepcontrol.wait, so a chain of latency-bound small passes overlaps
+/// launch and prologue with its predecessor.  The big streaming passes are
+/// launched without the attribute (an early trigger there parked dependent
+/// CTAs on the SMs, see pdl_enabled), which also keeps any small kernel from
+/// starting before a big pass ends.
+inline bool pdl_small_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = std::getenv("LDGMG_PDL_SMALL");
+        env = e ? std::atoi(e) : 1;
+    }
+    return env != 0;
+}
+
+template <class... KArgs, class... Args>
+inline void launch_pdl_small(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                             Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl_enabled() || pdl_small_enabled()) ? 1 : 0;
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 template <class... KArgs, class... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args&&... args) {
@@ -174,6 +208,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 /// the previous kernel's completion and memory (no-ops without PDL).
 __device__ __forceinline__ void pdl_trigger() {}  // implicit at grid end (see pdl_enabled)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+/// early trigger of the small kernels (no-op when no dependent was launched
+/// with programmatic serialization)
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 /// Named barrier over `nthreads` threads (row groups wider than one warp).
 __device__ __forceinline__ void group_sync(int id, int nthreads) {

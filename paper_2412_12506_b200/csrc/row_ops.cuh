@@ -130,8 +130,26 @@ __device__ __forceinline__ void split_row_task(const RowPassArgs& a, int row, in
 /// arithmetic (and so the bits) is split_row_task's.
 /// smem layout (doubles): blocks maxlen*blk_stride | V vstride | x maxlen*xs |
 /// partial sums maxlen*32 | u 32 | t 32 | epilogue 4*32.  All threads call it.
+/// The TMA part of split_row_task_tma: the row's blocks (and relax factor)
+/// requested on `bar`.  Immutable data only, so it may run before the PDL
+/// wait.  Thread 0 issues; all threads may call.
+__device__ __forceinline__ void split_row_issue(const RowPassArgs& a, int row, int maxlen, double* sm,
+                                                uint64_t* bar) {
+    if (threadIdx.x != 0) return;
+    const bool relax = a.mode == MODE_RELAX;
+    double* sB = sm;
+    double* sV = sB + size_t(maxlen) * a.blk_stride;
+    const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1), nk = k1 - k0;
+    fence_proxy_async();  // the previous row's generic reads of sB/sV precede these async writes
+    const uint32_t bb = uint32_t(nk) * uint32_t(a.blk_stride) * 8u;
+    const uint32_t vb = relax ? uint32_t(a.vstride) * 8u : 0u;
+    mbar_arrive_expect_tx(bar, bb + vb);
+    if (bb) bulk_g2s(sB, a.val + size_t(k0) * a.blk_stride, bb, bar);
+    if (vb) bulk_g2s(sV, a.V + size_t(row) * a.vstride, vb, bar);
+}
+
 __device__ __forceinline__ void split_row_task_tma(const RowPassArgs& a, int row, int maxlen, double* sm,
-                                                   uint64_t* bar, uint32_t& phase) {
+                                                   uint64_t* bar, uint32_t& phase, bool issued = false) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
     const bool relax = a.mode == MODE_RELAX;
     const int xs = (a.cbs + 1) & ~1;
@@ -143,14 +161,7 @@ __device__ __forceinline__ void split_row_task_tma(const RowPassArgs& a, int row
     double* tbuf = ubuf + 32;
     double* ep = tbuf + 32;  // b, xe, scal, lam
     const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1), nk = k1 - k0;
-    if (tid == 0) {
-        fence_proxy_async();  // the previous row's generic reads of sB/sV precede these async writes
-        const uint32_t bb = uint32_t(nk) * uint32_t(a.blk_stride) * 8u;
-        const uint32_t vb = relax ? uint32_t(a.vstride) * 8u : 0u;
-        mbar_arrive_expect_tx(bar, bb + vb);
-        if (bb) bulk_g2s(sB, a.val + size_t(k0) * a.blk_stride, bb, bar);
-        if (vb) bulk_g2s(sV, a.V + size_t(row) * a.vstride, vb, bar);
-    }
+    if (!issued) split_row_issue(a, row, maxlen, sm, bar);
     // x-blocks: thread t -> (block q, entry c), every load issued before use
     for (int t = tid; t < nk * a.cbs; t += blockDim.x) {
         const int q = t / a.cbs, c = t - q * a.cbs;

@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(256) restrict_item_kernel(const int* __restric
     extern __shared__ double ssum[];  // ppc x maxch x BS
     const int bss = BSS > 0 ? BSS : bss_rt;
     const int BS = bss * ncomp, bb = bss * bss, per = maxch * BS;
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int p0 = blockIdx.x * ppc; p0 < n_coarse; p0 += gridDim.x * ppc) {
         for (int t = threadIdx.x; t < ppc * per; t += blockDim.x) {
             const int lp = t / per, r = t - lp * per, q = r / BS, o = r - q * BS;
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(256) prolong_flat_kernel(const int* __restrict
     const int f = live ? int(o / BS) : 0;
     const int ii = int(o - int64_t(f) * BS), c = ii / bss, i = ii - c * bss;
     const int p = __ldg(parent + f), ot = __ldg(orth + f);
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     if (!live) return;
     const double* src = xc + size_t(p) * BS + c * bss;
     const double old = xf[o];
@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(NCH * BSS) restrict_ks_kernel(const double* __
     double kc[BSS];
 #pragma unroll
     for (int i = 0; i < BSS; ++i) kc[i] = __ldg(K + size_t(o) * BSS * BSS + i * BSS + j);
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int p0 = blockIdx.x * PB; p0 < n_coarse; p0 += gridDim.x * PB) {
         const int np = min(PB, n_coarse - p0);
         // children of p0..p0+np-1 are one contiguous run of fine blocks
@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(NCH * BSS) prolong_ks_kernel(const double* __r
     double kr[BSS];
 #pragma unroll
     for (int jj = 0; jj < BSS; ++jj) kr[jj] = __ldg(K + size_t(o) * BSS * BSS + i * BSS + jj);
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int p0 = blockIdx.x * PB; p0 < n_coarse; p0 += gridDim.x * PB) {
         const int np = min(PB, n_coarse - p0);
         for (int e = t; e < np * BS; e += NCH * BSS) sm[e] = xc[size_t(p0) * BS + e];
@@ -380,8 +380,8 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restric
     double* sK = sm;
     double* src = sm + nK + size_t(warp) * MAXCH * BS;
     stage_K_bulk(sK, K, nK, &bar);  // immutable: overlaps the previous kernel
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
         const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
         int f = 0;
@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(256) prolong_warp_kernel(const int* __restrict
         sKt[size_t(o) * bb + size_t(j) * bss + i] = sK[t];
     }
     __syncthreads();
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
         const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
         int f = 0;
@@ -560,8 +560,8 @@ __global__ void __launch_bounds__(1024) pinv_stream_kernel(const double* __restr
         mbar_init(bars + 1, 1);
         fence_mbar_init();
     }
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     for (int i = tid; i < n; i += NT) sb[i] = b[i];
     __syncthreads();
     uint32_t phases = 0u;  // bit s: parity to wait for on bars[s]
@@ -723,8 +723,8 @@ __global__ void __launch_bounds__(256) project_partial_kernel(const double* __re
                                                               const int* __restrict__ offs, double kval,
                                                               double* __restrict__ part, int k0 = 0, int ebase = 0) {
     __shared__ double red[8];
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     const int k = k0 + blockIdx.x, c = blockIdx.y, off = offs[c];
     const int e0 = int(int64_t(k) * N / kProjParts), e1 = int(int64_t(k + 1) * N / kProjParts);
     double s = 0.0;
@@ -744,8 +744,8 @@ __global__ void __launch_bounds__(256) project_apply_kernel(double* __restrict__
                                                             int ebase = 0) {
     __shared__ double red[8];
     __shared__ double md;
+    pdl_launch_dependents();
     pdl_wait();
-    pdl_trigger();
     const int k = k0 + blockIdx.x, c = blockIdx.y, off = offs[c];
     double s = part[c * kProjParts + threadIdx.x];
     for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
@@ -842,7 +842,7 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         bool done = true;
         auto launch = [&](auto kern, int threads) {
             ensure_dyn_smem(kern, smem);
-            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), rf, rc, T.n_coarse,
+            launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), rf, rc, T.n_coarse,
                        T.ncomp, zero_xc);
         };
         if (T.dim == 3 && T.bss == 27) launch(restrict_ks_kernel<27, 8, PB>, 216);
@@ -863,7 +863,7 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         const int grid = std::max(1, std::min(div_up(T.n_coarse, ppc), ctx.num_sms * 32));
         const size_t smem = sizeof(double) * size_t(ppc) * per;
         auto launch = [&](auto kern) {
-            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.child_ptr.as<int>(),
+            launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.child_ptr.as<int>(),
                        T.child_list.as<int>(), T.child_orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse, T.bss,
                        T.ncomp, std::max(1, T.max_children), ppc, zero_xc);
         };
@@ -881,7 +881,7 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(restrict_warp_kernel<8>), true);
         (void)once;
-        launch_pdl(restrict_warp_kernel<8>, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
+        launch_pdl_small(restrict_warp_kernel<8>, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
                    T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse, T.bss, T.ncomp,
                    nK, zero_xc);
         after_launch("restrict_warp_kernel");
@@ -914,7 +914,7 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
         bool done = true;
         auto launch = [&](auto kern, int threads) {
             ensure_dyn_smem(kern, smem);
-            launch_pdl(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), xc, xf, T.n_coarse,
+            launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), xc, xf, T.n_coarse,
                        T.ncomp);
         };
         if (T.dim == 3 && T.bss == 27) launch(prolong_ks_kernel<27, 8, PB>, 216);
@@ -931,7 +931,7 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
     if (transfer_flat()) {
         const int grid = div_up(total, 256);
         auto launch = [&](auto kern) {
-            launch_pdl(kern, dim3(grid), dim3(256), 0, ctx.stream, T.parent.as<int>(), T.orth.as<int>(),
+            launch_pdl_small(kern, dim3(grid), dim3(256), 0, ctx.stream, T.parent.as<int>(), T.orth.as<int>(),
                        T.Kt.as<double>(), xc, xf, T.n_fine, T.bss, T.ncomp);
         };
         switch (T.bss) {
@@ -948,7 +948,7 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
         const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
         static bool once = (max_carveout(prolong_warp_kernel), true);
         (void)once;
-        launch_pdl(prolong_warp_kernel, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
+        launch_pdl_small(prolong_warp_kernel, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
                    T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), xc, xf, T.n_coarse, T.bss, T.ncomp,
                    nK);
         after_launch("prolong_warp_kernel");
@@ -981,7 +981,7 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
             ensure_dyn_smem(pinv_stream_kernel, size_t(smem));
             static bool once = (max_carveout(pinv_stream_kernel), true);
             (void)once;
-            launch_pdl(pinv_stream_kernel, dim3(1), dim3(1024), smem, ctx.stream, E.Vr.as<double>(),
+            launch_pdl_small(pinv_stream_kernel, dim3(1), dim3(1024), smem, ctx.stream, E.Vr.as<double>(),
                        E.Vc.as<double>(), E.lambda.as<double>(), b, x, n, cut, KC);
             after_launch("pinv_stream_kernel");
             return;
@@ -1007,10 +1007,10 @@ void launch_project_constants(Ctx& ctx, double* v, int N, int bs, const int* com
     } else if (scratch && N >= kProjParts) {
         static bool once = (max_carveout(project_partial_kernel), max_carveout(project_apply_kernel), true);
         (void)once;
-        launch_pdl(project_partial_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream,
+        launch_pdl_small(project_partial_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream,
                    static_cast<const double*>(v), N, bs, comp_offsets, kval, scratch, 0, 0);
         after_launch("project_partial_kernel");
-        launch_pdl(project_apply_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream, v, N, bs, comp_offsets,
+        launch_pdl_small(project_apply_kernel, dim3(kProjParts, ncomp), dim3(256), 0, ctx.stream, v, N, bs, comp_offsets,
                    kval, static_cast<const double*>(scratch), 0, 0);
         after_launch("project_apply_kernel");
     } else {
