@@ -401,7 +401,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "level-0 SAI sweep: residual + B r row passes (rowpass_kernel)",
                          "achieved": alg / tk / 1e9, "peak": peak, "unit": "GB/s", "frac": alg / tk / 1e9 / peak,
                          "traffic": traffic, "alg_bytes_per_launch_pair": alg, "ms": tk * 1e3,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy; a read-mostly stream can exceed it)",
+                         "peak_theoretical": 8000.0, "frac_theoretical": alg / tk / 1e9 / 8000.0},
             "vcycle_hbm_GBps": bytes_cycle * args.steps / t / 1e9,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * n * bs),

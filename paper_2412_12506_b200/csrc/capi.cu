@@ -942,7 +942,10 @@ bool build_solve_graph(Ctx& ctx, Mg& m, double* x, const double* b, double* rbuf
         capturing = true;
         ok(cudaMemsetAsync(x, 0, sizeof(double) * n, m.cap_stream));
         launch_dot(cctx, n, b, b, red_b);
-        check_pass(1);
+        // x = 0: the first residual b - A 0 is b bit for bit (every block
+        // product is +0, b - (+0) = b), so it is copied instead of computed
+        ok(cudaMemcpyAsync(rbuf, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, m.cap_stream));
+        launch_dot(cctx, n, rbuf, rbuf, red_r);
         cudaStreamCaptureStatus status;
         cudaGraph_t cg = nullptr;
         ok(cudaStreamGetCaptureInfo(m.cap_stream, &status, nullptr, &cg, nullptr, nullptr));
