@@ -36,57 +36,112 @@ namespace ldgmg_b200 {
 
 namespace {
 
-struct ItemIt {
-    int m;     // row slot
-    int row;   // current row, -1 when exhausted
-    int k, kend;
-    int vdone;
+/// Row descriptors of a CTA's grid-strided row sequence, pipelined so that
+/// the dependent index loads (row list -> row pointers / diagonal position)
+/// of row m+1 and m+2 are in flight while row m is processed: no warp ever
+/// waits on an index load at a row boundary.
+struct RowPipe {
+    int m;
+    int row, k0, k1, dk;          // row m (row = -1: exhausted)
+    int n_row, n_k0, n_k1, n_dk;  // row m+1
+    int nn_row;                   // row m+2
 };
 
-__device__ __forceinline__ void it_load(const RowPassArgs& a, ItemIt& it, int g, int ng) {
-    const int slot = g + it.m * ng;
-    if (slot >= a.nrows) {
-        it.row = -1;
-        return;
-    }
-    it.row = row_at(a, slot);
-    it.k = __ldg(a.ptr + it.row);
-    it.kend = __ldg(a.ptr + it.row + 1);
-    it.vdone = 0;
+__device__ __forceinline__ int rp_row(const RowPassArgs& a, int m, int g, int ng) {
+    const int slot = g + m * ng;
+    return slot < a.nrows ? row_at(a, slot) : -1;
 }
 
-/// Next item of the group's stream: kind 0 = matrix block `idx`, kind 1 =
-/// diagonal factor V of element `idx`.  Identical on every thread.
-__device__ __forceinline__ bool it_next(const RowPassArgs& a, ItemIt& it, int g, int ng,
-                                        int& kind, int& idx) {
+__device__ __forceinline__ void rp_fetch(const RowPassArgs& a, int row, int& k0, int& k1, int& dk) {
+    if (row < 0) return;
+    k0 = __ldg(a.ptr + row);
+    k1 = __ldg(a.ptr + row + 1);
+    dk = a.dpos ? __ldg(a.dpos + row) : -1;
+}
+
+__device__ __forceinline__ void rp_init(const RowPassArgs& a, RowPipe& p, int g, int ng) {
+    p.m = 0;
+    p.row = rp_row(a, 0, g, ng);
+    p.n_row = rp_row(a, 1, g, ng);
+    p.nn_row = rp_row(a, 2, g, ng);
+    p.k0 = p.k1 = p.n_k0 = p.n_k1 = 0;
+    p.dk = p.n_dk = -1;
+    rp_fetch(a, p.row, p.k0, p.k1, p.dk);
+    rp_fetch(a, p.n_row, p.n_k0, p.n_k1, p.n_dk);
+}
+
+__device__ __forceinline__ void rp_advance(const RowPassArgs& a, RowPipe& p, int g, int ng) {
+    ++p.m;
+    p.row = p.n_row;
+    p.k0 = p.n_k0;
+    p.k1 = p.n_k1;
+    p.dk = p.n_dk;
+    p.n_row = p.nn_row;
+    rp_fetch(a, p.n_row, p.n_k0, p.n_k1, p.n_dk);
+    p.nn_row = rp_row(a, p.m + 2, g, ng);
+}
+
+/// Producer iterator over the items of the CTA's rows (identical on every
+/// thread).  The column index of the next block is loaded one item ahead,
+/// so issuing an item never waits on it.
+struct ItemIt {
+    RowPipe rp;
+    int k;      // next block of the current row
+    int vdone;
+    int jk, jv;  // prefetched column index: col[jk] = jv
+};
+
+__device__ __forceinline__ void it_prefetch_col(const RowPassArgs& a, ItemIt& it) {
+    int k = it.k;
+    if (k == it.rp.dk) ++k;  // relax skips the diagonal block (dk = -1 otherwise)
+    it.jk = k;
+    if (k < it.rp.k1) it.jv = __ldg(a.col + k);
+}
+
+__device__ __forceinline__ void it_start(const RowPassArgs& a, ItemIt& it, int g, int ng) {
+    rp_init(a, it.rp, g, ng);
+    it.k = it.rp.k0;
+    it.vdone = 0;
+    it.jk = -1;
+    if (it.rp.row >= 0) it_prefetch_col(a, it);
+}
+
+/// Next item of the group's stream: kind 0 = matrix block `idx` (column
+/// `j`), kind 1 = diagonal factor V of element `idx`.
+__device__ __forceinline__ bool it_next(const RowPassArgs& a, ItemIt& it, int g, int ng, int& kind, int& idx,
+                                        int& j) {
     for (;;) {
-        if (it.row < 0) return false;
-        if (a.mode == MODE_RELAX)
-            while (it.k < it.kend && __ldg(a.col + it.k) == it.row) ++it.k;
-        if (it.k < it.kend) {
+        if (it.rp.row < 0) return false;
+        if (it.k == it.rp.dk) ++it.k;
+        if (it.k < it.rp.k1) {
             kind = 0;
-            idx = it.k++;
+            idx = it.k;
+            j = it.jk == idx ? it.jv : __ldg(a.col + idx);
+            ++it.k;
+            it_prefetch_col(a, it);
             return true;
         }
         if (a.mode == MODE_RELAX && !it.vdone) {
             it.vdone = 1;
             kind = 1;
-            idx = it.row;
+            idx = it.rp.row;
+            j = -1;
             return true;
         }
-        ++it.m;
-        it_load(a, it, g, ng);
+        rp_advance(a, it.rp, g, ng);
+        it.k = it.rp.k0;
+        it.vdone = 0;
+        if (it.rp.row >= 0) it_prefetch_col(a, it);
     }
 }
 
 template <int GT>
-__device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int row, int st,
+__device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int j, int row, int st,
                                            double* stages, double* xslots, uint64_t* bars) {
     const int t = threadIdx.x;
     double* xs = xslots + size_t(st) * a.xslot_doubles;
     if (t < a.cbs) {
         if (kind == 0) {
-            const int j = __ldg(a.col + idx);
             const double* src = x_source(a, row, j) + size_t(j) * a.cbs + t;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(xs + t)),
                          "l"(src)
@@ -235,24 +290,25 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
 
     // producer iterator: runs NS items ahead of the consumer (row lists and
     // row pointers are immutable: read before the PDL wait)
-    ItemIt pit{0, -1, 0, 0, 0};
-    it_load(a, pit, g, ng);
+    ItemIt pit;
+    it_start(a, pit, g, ng);
+    RowPipe crp;  // the consumer's own row pipeline (same row sequence)
+    rp_init(a, crp, g, ng);
     pdl_wait();
     pdl_trigger();
-    int kind, idx;
+    int kind, idx, jcol;
     for (int s = 0; s < NS; ++s) {
-        if (!it_next(a, pit, g, ng, kind, idx)) break;
-        issue_item<GT>(a, kind, idx, pit.row, s, stages, xslots, bars);
+        if (!it_next(a, pit, g, ng, kind, idx, jcol)) break;
+        issue_item<GT>(a, kind, idx, jcol, pit.rp.row, s, stages, xslots, bars);
     }
 
     uint32_t q = 0;  // items consumed
     const bool relax = a.mode == MODE_RELAX;
     const bool pairs = NS >= 3;
-    for (int m = 0;; ++m) {
-        const int slot = g + m * ng;
-        if (slot >= a.nrows) break;
-        const int row = row_at(a, slot);
-        const int k0 = __ldg(a.ptr + row), k1 = __ldg(a.ptr + row + 1);
+    for (;; rp_advance(a, crp, g, ng)) {
+        const int row = crp.row;
+        if (row < 0) break;
+        const int k0 = crp.k0, k1 = crp.k1, dk = crp.dk;
         const bool act = t < rbs;
         // epilogue operands fetched early; their latency hides under the blocks
         double pre_b = 0.0, pre_x = 0.0, pre_s = 0.0, pre_l = 0.0;
@@ -269,14 +325,12 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
         int k = k0;
         bool vdone = !relax;
         for (;;) {
-            if (relax)
-                while (k < k1 && __ldg(a.col + k) == row) ++k;
+            if (k == dk) ++k;  // relax skips the diagonal block (dk = -1 otherwise)
             int nblk = 0, k2 = k;
             if (k < k1) {
                 nblk = 1;
                 k2 = k + 1;
-                if (relax)
-                    while (k2 < k1 && __ldg(a.col + k2) == row) ++k2;
+                if (k2 == dk) ++k2;
                 if (pairs && k2 < k1) nblk = 2;
             } else if (vdone) {
                 break;
@@ -344,7 +398,9 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                     for (int kk = 0; kk < bs; ++kk) w = madd_rn(w, S[size_t(kk) * ld + t], tbuf[kk]);
                     const double yv = __dmul_rn(pre_s, w);
                     const double om = a.omega;
-                    acc = __dadd_rn(__dmul_rn(1.0 - om, pre_x), __dmul_rn(om, yv));
+                    double px = pre_x;
+                    asm volatile("" : "+d"(px));  // keep (1 - w) x here, not at the row-start load
+                    acc = __dadd_rn(__dmul_rn(1.0 - om, px), __dmul_rn(om, yv));
                 }
                 vdone = true;
             }
@@ -352,9 +408,9 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
             for (int u = 0; u < used; ++u) {
                 const int su = int(q % uint32_t(NS));
                 ++q;
-                if (it_next(a, pit, g, ng, kind, idx)) {
+                if (it_next(a, pit, g, ng, kind, idx, jcol)) {
                     if (t == 0) fence_proxy_async();
-                    issue_item<GT>(a, kind, idx, pit.row, su, stages, xslots, bars);
+                    issue_item<GT>(a, kind, idx, jcol, pit.rp.row, su, stages, xslots, bars);
                 }
             }
         }
@@ -890,6 +946,16 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         a.ld = p.F->ld;
         a.vstride = p.F->vstride;
         stage = std::max(stage, p.F->vstride);
+        if (!A.dpos.p) {  // diagonal positions, once per operator
+            std::vector<int> d(std::max(1, A.brows), -1);
+            for (int i = 0; i < A.brows; ++i)
+                for (int k = A.hptr[i]; k < A.hptr[i + 1]; ++k)
+                    if (A.hcol[k] == i) d[i] = k;
+            Bsr& Am = const_cast<Bsr&>(A);
+            Am.dpos.alloc(sizeof(int) * d.size());
+            h2d(ctx, Am.dpos.p, d.data(), sizeof(int) * d.size());
+        }
+        a.dpos = A.dpos.as<int>();
     }
     a.stage_doubles = even_up(stage);
     a.xslot_doubles = even_up(std::max(A.cbs, A.rbs));

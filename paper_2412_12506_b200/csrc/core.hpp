@@ -103,6 +103,7 @@ struct Bsr {
     // set on a transpose view: values live in tbase->val, block q = tbase block tperm[q]
     const Bsr* tbase = nullptr;
     DevBuf tperm;
+    DevBuf dpos;  // lazily built: CSR position of each row's diagonal block (-1: none)
     int64_t device_bytes() const { return int64_t(ptr.bytes + col.bytes + val.bytes); }
 };
 

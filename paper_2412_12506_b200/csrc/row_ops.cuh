@@ -34,6 +34,9 @@ struct RowPassArgs {
     // column of the base block)
     const int* perm;
     int tview;
+    // relax: CSR position of each row's diagonal block (-1 if none); the
+    // streaming kernel skips it without reading col
+    const int* dpos;
     // processor-block GS (smoothers.hpp:426-436): neighbour j of row e is read
     // from x when part[j] == part[e], else from x_alt (the sweep's snapshot)
     const int* part;
