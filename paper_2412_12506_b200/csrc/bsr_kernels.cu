@@ -137,9 +137,34 @@ __device__ __forceinline__ bool it_next(const RowPassArgs& a, ItemIt& it, int g,
 
 template <int GT>
 __device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int idx, int j, int row, int st,
-                                           double* stages, double* xslots, uint64_t* bars) {
+                                           double* stages, double* xslots, uint64_t* bars, int* xoffs) {
     const int t = threadIdx.x;
     double* xs = xslots + size_t(st) * a.xslot_doubles;
+    if (a.xtma) {
+        if (t == 0) {
+            const double* src;
+            uint32_t bytes;
+            if (kind == 0) {
+                const int64_t blk = a.perm ? int64_t(__ldg(a.perm + idx)) : int64_t(idx);
+                src = a.val + size_t(blk) * a.blk_stride;
+                bytes = uint32_t(a.blk_stride) * 8u;
+                const double* xsrc = x_source(a, row, j) + size_t(j) * a.cbs;
+                const uintptr_t xa = reinterpret_cast<uintptr_t>(xsrc) & ~uintptr_t(15);
+                const int off = int((reinterpret_cast<uintptr_t>(xsrc) - xa) >> 3);
+                const uint32_t xbytes = (uint32_t((off + a.cbs) * 8) + 15u) & ~15u;
+                xoffs[st] = off;
+                mbar_arrive_expect_tx(bars + st, bytes + xbytes);
+                bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
+                bulk_g2s(xs, reinterpret_cast<const void*>(xa), xbytes, bars + st);
+            } else {
+                src = a.V + size_t(idx) * a.vstride;
+                bytes = uint32_t(a.vstride) * 8u;
+                mbar_arrive_expect_tx(bars + st, bytes);
+                bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
+            }
+        }
+        return;
+    }
     if (t < a.cbs) {
         if (kind == 0) {
             const double* src = x_source(a, row, j) + size_t(j) * a.cbs + t;
@@ -276,6 +301,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     double* ubuf = xslots + size_t(a.nstages) * a.xslot_doubles;
     double* tbuf = ubuf + a.xslot_doubles;
     uint64_t* bars = reinterpret_cast<uint64_t*>(tbuf + a.xslot_doubles);
+    int* xoffs = reinterpret_cast<int*>(bars + a.nstages);  // x-TMA: start of x_j within each stage's slot
 
     const int t = threadIdx.x;
     const int g = blockIdx.x, ng = gridDim.x;
@@ -283,7 +309,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     const int rbs = BS > 0 ? BS : a.rbs, cbs = BS > 0 ? BS : a.cbs;
 
     if (t == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1u + uint32_t(a.cbs));
+        for (int s = 0; s < NS; ++s) mbar_init(bars + s, a.xtma ? 1u : 1u + uint32_t(a.cbs));
         fence_mbar_init();
     }
     __syncthreads();
@@ -299,7 +325,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     int kind, idx, jcol;
     for (int s = 0; s < NS; ++s) {
         if (!it_next(a, pit, g, ng, kind, idx, jcol)) break;
-        issue_item<GT>(a, kind, idx, jcol, pit.rp.row, s, stages, xslots, bars);
+        issue_item<GT>(a, kind, idx, jcol, pit.rp.row, s, stages, xslots, bars, xoffs);
     }
 
     uint32_t q = 0;  // items consumed
@@ -338,7 +364,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
             const int st = int(q % uint32_t(NS));
             mbar_wait(bars + st, (q / uint32_t(NS)) & 1u);
             const double* S = stages + size_t(st) * a.stage_doubles;
-            const double* X = xslots + size_t(st) * a.xslot_doubles;
+            const double* X = xslots + size_t(st) * a.xslot_doubles + (a.xtma ? xoffs[st] : 0);
             int used = 1;
             if (nblk == 2) {
                 const int st2 = int((q + 1) % uint32_t(NS));
@@ -350,7 +376,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                     const bool hi = t >= BS;
                     const int r = hi ? t - BS : t;
                     const double* Sx = hi ? stages + size_t(st2) * a.stage_doubles : S;
-                    const double* Xx = hi ? xslots + size_t(st2) * a.xslot_doubles : X;
+                    const double* Xx = hi ? xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0) : X;
                     double s = 0.0;
                     if (t < 2 * BS)
                         s = a.tview ? bdot_t<BS>(Sx + size_t(r) * cbs, Xx, cbs) : bdot<BS>(Sx + r, Xx, cbs, rbs);
@@ -363,10 +389,11 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                     double s1, s2;
                     if (a.tview)
                         bdot2_t<BS>(S + size_t(t) * cbs, X, stages + size_t(st2) * a.stage_doubles + size_t(t) * cbs,
-                                    xslots + size_t(st2) * a.xslot_doubles, cbs, s1, s2);
+                                    xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0), cbs, s1, s2);
                     else
                         bdot2<BS>(S + t, X, stages + size_t(st2) * a.stage_doubles + t,
-                                  xslots + size_t(st2) * a.xslot_doubles, cbs, rbs, s1, s2);
+                                  xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0), cbs, rbs, s1,
+                                  s2);
                     acc = relax ? __dsub_rn(acc, s1) : __dadd_rn(acc, s1);
                     acc = relax ? __dsub_rn(acc, s2) : __dadd_rn(acc, s2);
                 }
@@ -410,7 +437,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                 ++q;
                 if (it_next(a, pit, g, ng, kind, idx, jcol)) {
                     if (t == 0) fence_proxy_async();
-                    issue_item<GT>(a, kind, idx, jcol, pit.rp.row, su, stages, xslots, bars);
+                    issue_item<GT>(a, kind, idx, jcol, pit.rp.row, su, stages, xslots, bars, xoffs);
                 }
             }
         }
@@ -456,7 +483,7 @@ template <int GT, int BS>
 void configure_and_launch(Ctx& ctx, RowPassArgs a, size_t stage_bytes, int ns_env) {
     auto smem_for = [&](int ns) {
         return size_t(ns) * stage_bytes + size_t(ns) * a.xslot_doubles * 8 + 2 * size_t(a.xslot_doubles) * 8 +
-               size_t(ns) * 8;
+               size_t(ns) * 8 + size_t(ns) * 8;
     };
     int ns = ns_env > 1 ? ns_env : 3;
     while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
@@ -958,7 +985,15 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         a.dpos = A.dpos.as<int>();
     }
     a.stage_doubles = even_up(stage);
-    a.xslot_doubles = even_up(std::max(A.cbs, A.rbs));
+    static int xtma_env = -1;
+    if (xtma_env < 0) {
+        const char* e = getenv("LDGMG_XTMA");
+        xtma_env = e ? atoi(e) : 1;
+    }
+    a.xtma = xtma_env;
+    // x-TMA slots hold a 16-byte aligned window around x_j (up to one extra
+    // double in front and the tail rounded up to 16 bytes)
+    a.xslot_doubles = even_up(std::max(A.cbs, A.rbs)) + (a.xtma ? 2 : 0);
     const int wide = std::max(A.rbs, A.cbs);
     const int GT = wide <= 32 ? 32 : wide <= 64 ? 64 : wide <= 128 ? 128 : 256;
     // ring depth: keep >= ~3 blocks in flight per group within a 200 KB budget
