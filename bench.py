@@ -233,6 +233,38 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
     te_t = torch.tensor([te], device="cuda", dtype=torch.float64)
     dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
     e2e_value = dof_cycle * ne / float(te_t.item())
+    # roofline: this rank's level-0 SAI sweep pair (residual + B r row passes on
+    # its rows, no exchange) timed alone with CUDA events; max time over ranks
+    roof = None
+    d0 = dm.L[0]
+    if "B" in d0 and "nnzB" in d0:
+        n_own = d0["plan"].n_own
+        x_ext, rext = d0["x"], d0["rext"]
+
+        def pair():
+            dm.ops.residual(d0["A"], b_own, x_ext, rext[:n_own * bs])
+            dm.ops.spmv_add(d0["B"], rext, x_ext[:n_own * bs])
+
+        for _ in range(3):
+            pair()
+        torch.cuda.synchronize()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        k0.record(stream)
+        for _ in range(reps):
+            pair()
+        k1.record(stream)
+        torch.cuda.synchronize()
+        tk_t = torch.tensor([k0.elapsed_time(k1) * 1e-3 / reps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tk_t, op=dist.ReduceOp.MAX)
+        tk = float(tk_t.item())
+        alg = 8.0 * (bs * bs * (d0["nnzA"] + d0["nnzB"]) + 6 * bs * n_own)
+        peak = peaks().get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "kernel": "level-0 SAI sweep pair on each rank's rows (rowpass_kernel)",
+                "achieved": alg / tk / 1e9, "peak": peak, "unit": "GB/s", "frac": alg / tk / 1e9 / peak,
+                "traffic": None, "alg_bytes_per_launch_pair": alg, "ms": tk * 1e3,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy), per GPU; time = max over ranks",
+                "peak_theoretical": 8000.0, "frac_theoretical": alg / tk / 1e9 / 8000.0}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -252,6 +284,7 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
                                    "note": ("replicated per rank" if args.replicated_setup else
                                             "each rank assembles its rows + SAI halo and solves its SAI columns")}},
             "vcycle_hbm_GBps_total": bytes_cycle * args.steps / t / 1e9,
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * (r1 - r0) * bs),
                     "d2h_bytes_per_step": int(8 * (r1 - r0) * bs),
                     "step": "pinned H2D of the owned b slice + one partitioned V-cycle + D2H of the owned x slice"},
