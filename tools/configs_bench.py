@@ -98,6 +98,9 @@ def main():
     ap.add_argument("--host-assembly", action="store_true", help="assemble the operators on the host (default: GPU)")
     ap.add_argument("--cycles", type=int, default=20)
     ap.add_argument("--no-solve", action="store_true", help="V-cycle timing only (no stationary / GMRES solve)")
+    ap.add_argument("--props", action="store_true",
+                    help="also check size-independent V-cycle properties at this size: apply(2b) == 2 apply(b) "
+                         "bit for bit, graph replay == direct launches")
     a = ap.parse_args()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -136,6 +139,18 @@ def main():
             st = mg.smoother(0).sai_stats()
             rec["sai_level0"] = {"cache_misses": st.cache_misses, "cache_hits": st.cache_hits,
                                  "ls_shapes": {f"{k[0]}x{k[1]}": v for k, v in st.ls_dims().items()}}
+        if a.props:
+            y1, y2 = torch.empty_like(b), torch.empty_like(b)
+            mg.apply(b, y1)
+            mg.apply(2.0 * b, y2)
+            xa, xg = torch.zeros_like(b), torch.zeros_like(b)
+            mg.cycle(xa, b)
+            mg.cycle(xa, b)
+            mg.cycles(xg, b, 2)
+            torch.cuda.synchronize()
+            rec["properties"] = {"apply_homogeneous_bitwise": bool(torch.equal(y2, 2.0 * y1)),
+                                 "graph_equals_direct_bitwise": bool(torch.equal(xa, xg))}
+            del y1, y2, xa, xg
         if a.no_solve:
             print(json.dumps(rec), flush=True)
             del mg, P
