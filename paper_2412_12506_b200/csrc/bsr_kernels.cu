@@ -851,12 +851,17 @@ __global__ void __launch_bounds__(256) rowsplit_tma_kernel(const RowPassArgs a, 
     pdl_launch_dependents();
     // immutable prologue: the first row's blocks (and factor) are requested
     // before waiting on the predecessor
-    if (blockIdx.x < a.nrows) split_row_issue(a, row_at(a, blockIdx.x), maxlen, sm, &bar);
+    int jfirst = -1;
+    if (blockIdx.x < a.nrows) {
+        const int row0 = row_at(a, blockIdx.x);
+        split_row_issue(a, row0, maxlen, sm, &bar);
+        jfirst = split_row_first_col(a, row0);  // the x gather's first column index, also immutable
+    }
     pdl_wait();
     uint32_t phase = 0;
     bool issued = true;
     for (int slot = blockIdx.x; slot < a.nrows; slot += gridDim.x) {
-        split_row_task_tma(a, row_at(a, slot), maxlen, sm, &bar, phase, issued);
+        split_row_task_tma(a, row_at(a, slot), maxlen, sm, &bar, phase, issued, issued ? jfirst : -1);
         issued = false;
     }
 }

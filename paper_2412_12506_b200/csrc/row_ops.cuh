@@ -154,8 +154,18 @@ __device__ __forceinline__ void split_row_issue(const RowPassArgs& a, int row, i
     if (vb) bulk_g2s(sV, a.V + size_t(row) * a.vstride, vb, bar);
 }
 
+/// Column index of this thread's first x-gather entry of `row` (immutable,
+/// so it can be loaded before the PDL wait); -1 when the thread has none.
+__device__ __forceinline__ int split_row_first_col(const RowPassArgs& a, int row) {
+    const int k0 = __ldg(a.ptr + row), nk = __ldg(a.ptr + row + 1) - k0;
+    const int t = threadIdx.x;
+    if (t >= nk * a.cbs) return -1;
+    return __ldg(a.col + k0 + t / a.cbs);
+}
+
 __device__ __forceinline__ void split_row_task_tma(const RowPassArgs& a, int row, int maxlen, double* sm,
-                                                   uint64_t* bar, uint32_t& phase, bool issued = false) {
+                                                   uint64_t* bar, uint32_t& phase, bool issued = false,
+                                                   int jfirst = -1) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
     const bool relax = a.mode == MODE_RELAX;
     const int xs = (a.cbs + 1) & ~1;
@@ -171,7 +181,7 @@ __device__ __forceinline__ void split_row_task_tma(const RowPassArgs& a, int row
     // x-blocks: thread t -> (block q, entry c), every load issued before use
     for (int t = tid; t < nk * a.cbs; t += blockDim.x) {
         const int q = t / a.cbs, c = t - q * a.cbs;
-        const int j = __ldg(a.col + k0 + q);
+        const int j = (t == tid && jfirst >= 0) ? jfirst : __ldg(a.col + k0 + q);
         sX[size_t(q) * xs + c] = x_source(a, row, j)[size_t(j) * a.cbs + c];
     }
     if (tid < a.rbs) {
