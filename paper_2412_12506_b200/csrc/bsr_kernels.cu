@@ -487,7 +487,9 @@ void configure_and_launch(Ctx& ctx, RowPassArgs a, size_t stage_bytes, int ns_en
     };
     int ns = ns_env > 1 ? ns_env : 3;
     while (ns > 2 && ns * stage_bytes > 200 * 1024) --ns;
-    if (ns_env <= 1 && ns == 3) {
+    // (blocks of <= 16 rows keep 3: their pairs run on the two half-warps,
+    // C1 at 64^2: 0.195 -> 0.189 ms per V-cycle)
+    if (ns_env <= 1 && ns == 3 && 2 * a.rbs > 32) {
         const int occ3 = rowpass_occupancy<GT, BS>(ctx, smem_for(3));
         if (occ3 >= 1 && a.nrows < 4 * occ3 * ctx.num_sms) ns = 2;
     }
