@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "core.hpp"
 
@@ -815,6 +816,15 @@ namespace {
 int transfer_nK(const Transfer& T) { return (1 << T.dim) * T.bss * T.bss; }
 /// thread-per-entry transfer kernels (default); LDGMG_TRANSFER=warp selects
 /// the warp-per-parent kernels with shared-memory staged K
+/// parents per K-stationary step (LDGMG_TRANSFER_PB = 4, 8 or 16)
+int transfer_pb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("LDGMG_TRANSFER_PB");
+        v = e ? atoi(e) : 8;
+    }
+    return v;
+}
 bool transfer_flat() {
     static int v = -1;
     if (v < 0) {
@@ -836,21 +846,27 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         zero_xc = nullptr;
     }
     if (transfer_flat() && T.regular) {
-        constexpr int PB = 4;
-        const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
-        const size_t smem = sizeof(double) * 2 * PB * (size_t(1) << T.dim) * T.bs;
         bool done = true;
-        auto launch = [&](auto kern, int threads) {
-            ensure_dyn_smem(kern, smem);
-            launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), rf, rc, T.n_coarse,
-                       T.ncomp, zero_xc);
+        auto go = [&](auto pbc) {
+            constexpr int PB = decltype(pbc)::value;
+            const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
+            const size_t smem = sizeof(double) * 2 * PB * (size_t(1) << T.dim) * T.bs;
+            auto launch = [&](auto kern, int threads) {
+                ensure_dyn_smem(kern, smem);
+                launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), rf, rc,
+                                 T.n_coarse, T.ncomp, zero_xc);
+            };
+            if (T.dim == 3 && T.bss == 27) launch(restrict_ks_kernel<27, 8, PB>, 216);
+            else if (T.dim == 3 && T.bss == 8) launch(restrict_ks_kernel<8, 8, PB>, 64);
+            else if (T.dim == 2 && T.bss == 16) launch(restrict_ks_kernel<16, 4, PB>, 64);
+            else if (T.dim == 2 && T.bss == 25) launch(restrict_ks_kernel<25, 4, PB>, 100);
+            else if (T.dim == 2 && T.bss == 9) launch(restrict_ks_kernel<9, 4, PB>, 36);
+            else done = false;
         };
-        if (T.dim == 3 && T.bss == 27) launch(restrict_ks_kernel<27, 8, PB>, 216);
-        else if (T.dim == 3 && T.bss == 8) launch(restrict_ks_kernel<8, 8, PB>, 64);
-        else if (T.dim == 2 && T.bss == 16) launch(restrict_ks_kernel<16, 4, PB>, 64);
-        else if (T.dim == 2 && T.bss == 25) launch(restrict_ks_kernel<25, 4, PB>, 100);
-        else if (T.dim == 2 && T.bss == 9) launch(restrict_ks_kernel<9, 4, PB>, 36);
-        else done = false;
+        const int pb = transfer_pb();
+        if (pb == 16) go(std::integral_constant<int, 16>{});
+        else if (pb == 4) go(std::integral_constant<int, 4>{});
+        else go(std::integral_constant<int, 8>{});
         if (done) {
             after_launch("restrict_ks_kernel");
             return;
@@ -908,21 +924,27 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
     const int nK = transfer_nK(T);
     const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
     if (transfer_flat() && T.regular) {
-        constexpr int PB = 4;
-        const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
-        const size_t smem = sizeof(double) * PB * T.bs;
         bool done = true;
-        auto launch = [&](auto kern, int threads) {
-            ensure_dyn_smem(kern, smem);
-            launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), xc, xf, T.n_coarse,
-                       T.ncomp);
+        auto go = [&](auto pbc) {
+            constexpr int PB = decltype(pbc)::value;
+            const int grid = std::max(1, std::min(div_up(T.n_coarse, PB), ctx.num_sms * 8));
+            const size_t smem = sizeof(double) * PB * T.bs;
+            auto launch = [&](auto kern, int threads) {
+                ensure_dyn_smem(kern, smem);
+                launch_pdl_small(kern, dim3(grid), dim3(threads), smem, ctx.stream, T.K.as<double>(), xc, xf,
+                                 T.n_coarse, T.ncomp);
+            };
+            if (T.dim == 3 && T.bss == 27) launch(prolong_ks_kernel<27, 8, PB>, 216);
+            else if (T.dim == 3 && T.bss == 8) launch(prolong_ks_kernel<8, 8, PB>, 64);
+            else if (T.dim == 2 && T.bss == 16) launch(prolong_ks_kernel<16, 4, PB>, 64);
+            else if (T.dim == 2 && T.bss == 25) launch(prolong_ks_kernel<25, 4, PB>, 100);
+            else if (T.dim == 2 && T.bss == 9) launch(prolong_ks_kernel<9, 4, PB>, 36);
+            else done = false;
         };
-        if (T.dim == 3 && T.bss == 27) launch(prolong_ks_kernel<27, 8, PB>, 216);
-        else if (T.dim == 3 && T.bss == 8) launch(prolong_ks_kernel<8, 8, PB>, 64);
-        else if (T.dim == 2 && T.bss == 16) launch(prolong_ks_kernel<16, 4, PB>, 64);
-        else if (T.dim == 2 && T.bss == 25) launch(prolong_ks_kernel<25, 4, PB>, 100);
-        else if (T.dim == 2 && T.bss == 9) launch(prolong_ks_kernel<9, 4, PB>, 36);
-        else done = false;
+        const int pb = transfer_pb();
+        if (pb == 16) go(std::integral_constant<int, 16>{});
+        else if (pb == 4) go(std::integral_constant<int, 4>{});
+        else go(std::integral_constant<int, 8>{});
         if (done) {
             after_launch("prolong_ks_kernel");
             return;
