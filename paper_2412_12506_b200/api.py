@@ -533,10 +533,17 @@ class Multigrid:
     def cycles(self, x, b, n: int) -> None:
         check(lib.ldgmg_mg_cycles(self.ctx.h, self.h, _ptr(x), _ptr(b), int(n)))
 
-    def solve_host(self, b: np.ndarray, tol=1e-10, maxit=100):
-        """Stationary V-cycle solve from host buffers (H2D, cycles, D2H)."""
+    def solve_host(self, b: np.ndarray, tol=1e-10, maxit=100, out: np.ndarray | None = None):
+        """Stationary V-cycle solve from host buffers (H2D, cycles, D2H).
+        `out` (optional): the host array receiving x; page-locked buffers
+        (e.g. a pinned torch tensor's .numpy()) are written by DMA directly."""
         b = _np(b, np.float64)
-        x = np.empty_like(b)
+        if out is not None:
+            if out.dtype != np.float64 or out.shape != b.shape or not out.flags["C_CONTIGUOUS"]:
+                raise L.InvalidArgument("solve_host: out must be a contiguous float64 array shaped like b")
+            x = out
+        else:
+            x = np.empty_like(b)
         hist = np.empty(maxit + 1)
         it = C.c_int()
         check(lib.ldgmg_mg_solve_host(self.ctx.h, self.h, b.ctypes.data, x.ctypes.data, float(tol), int(maxit),

@@ -1077,9 +1077,14 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
                 LDGMG_CUDA(cudaMemcpyAsync(m.solve_state.p, hs.data(), sizeof(SolveState), cudaMemcpyHostToDevice,
                                            ctx->stream));
                 LDGMG_CUDA(cudaGraphLaunch(m.solve_exec, ctx->stream));
+                // a page-locked destination takes the iterate by DMA directly
+                cudaPointerAttributes xat{};
+                const bool x_pinned = cudaPointerGetAttributes(&xat, x_host) == cudaSuccess &&
+                                      xat.type == cudaMemoryTypeHost;
+                cudaGetLastError();
                 if (!solve_snap_in_loop())
-                    LDGMG_CUDA(cudaMemcpyAsync(m.h_stage_x, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                                               ctx->stream));
+                    LDGMG_CUDA(cudaMemcpyAsync(x_pinned ? static_cast<void*>(x_host) : m.h_stage_x, x.p,
+                                               sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
                 LDGMG_CUDA(cudaMemcpyAsync(hs.data(), m.solve_state.p, sizeof(double) * hs.size(),
                                            cudaMemcpyDeviceToHost, ctx->stream));
                 LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1088,8 +1093,8 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
                 if (history) std::memcpy(history, hs.data() + kSolveHist, sizeof(double) * (it + 1));
                 if (iters) *iters = it;
                 const auto T2 = tnow();
-                if (it > 0) parallel_memcpy(x_host, m.h_stage_x, sizeof(double) * n);
-                else std::memset(x_host, 0, sizeof(double) * n);  // x = 0 exactly (no cycle ran)
+                if (it == 0) std::memset(x_host, 0, sizeof(double) * n);  // x = 0 exactly (no cycle ran)
+                else if (!(x_pinned && !solve_snap_in_loop())) parallel_memcpy(x_host, m.h_stage_x, sizeof(double) * n);
                 if (timing)
                     fprintf(stderr, "[solve_host] device loop: h2d %.3f ms, %d cycles %.3f ms, d2h %.3f ms\n",
                             tsec(T0, T0b), it, tsec(T0b, T2), tsec(T2, tnow()));

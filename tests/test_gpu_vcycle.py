@@ -235,3 +235,18 @@ def test_device_bottom_eigensolver_matches_host():
         assert out.returncode == 0, out.stderr[-3000:]
         runs.append(np.array(json.loads(out.stdout.strip().splitlines()[-1])))
     assert np.max(np.abs(runs[0] - runs[1]) / np.maximum(runs[1], 1e-300)) <= 1e-9, runs
+
+
+def test_solve_host_pinned_buffers(ctx):
+    """solve_host into a page-locked `out` (DMA straight into it) equals the
+    pageable call bit for bit; a shape mismatch is rejected."""
+    spec, cfg = K.baseline_configs()["C2"]
+    mg = g.Multigrid(ctx, cfg, g.Problem(spec, min_depth=cfg.min_depth))
+    b = rand(mg.n * mg.bs, 4)
+    x1, h1, i1 = mg.solve_host(b, tol=1e-10, maxit=30)
+    bp = torch.from_numpy(b.copy()).pin_memory()
+    xp = torch.empty_like(bp).pin_memory()
+    x2, h2, i2 = mg.solve_host(bp.numpy(), tol=1e-10, maxit=30, out=xp.numpy())
+    assert i1 == i2 and np.array_equal(h1, h2) and np.array_equal(x1, xp.numpy()) and x2 is not None
+    with pytest.raises(g.InvalidArgument):
+        mg.solve_host(b, out=np.empty(3))
