@@ -250,3 +250,20 @@ def test_solve_host_pinned_buffers(ctx):
     assert i1 == i2 and np.array_equal(h1, h2) and np.array_equal(x1, xp.numpy()) and x2 is not None
     with pytest.raises(g.InvalidArgument):
         mg.solve_host(b, out=np.empty(3))
+
+
+def test_solve_host_device_loop_edge_cases(ctx):
+    """The graph-resident solve loop: tol already met (0 cycles, x = 0),
+    maxit = 0, and a maxit beyond the captured history capacity (rebuild)
+    agree with the host-driven semantics of ldgmg_mg_solve_host."""
+    spec, cfg = K.baseline_configs()["C1"]
+    mg = g.Multigrid(ctx, cfg, g.Problem(spec, min_depth=cfg.min_depth))
+    b = rand(mg.n * mg.bs, 8)
+    x, h, it = mg.solve_host(b, tol=10.0, maxit=5)
+    assert it == 0 and len(h) == 1 and h[0] == 1.0 and not np.any(x)
+    x, h, it = mg.solve_host(b, tol=0.0, maxit=0)
+    assert it == 0 and not np.any(x)
+    x, h, it = mg.solve_host(b, tol=0.0, maxit=200)
+    assert it == 200 and len(h) == 201 and np.all(np.diff(h[:20]) < 0)
+    x5, h5, _ = mg.solve_host(b, tol=0.0, maxit=5)
+    assert np.array_equal(h5, h[:6])
