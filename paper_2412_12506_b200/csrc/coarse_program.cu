@@ -123,90 +123,102 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 constexpr int kTailThreads = 256;
-constexpr int kTailMaxRows = 64;  // rows per wave
+constexpr int kTailMaxRows = 64;     // rows per wave
+constexpr int kTailMaxBlocks = 512;  // blocks per wave
 
 /// One row op over the cluster: CTA `cta` of `ncta` takes rows cta, cta+ncta,
-/// ... in waves that fit shared memory.  Per wave: the rows' contiguous
-/// blocks (and relax factors V) arrive by TMA bulk copies, the x blocks and
-/// epilogue operands by L2 loads, warps compute s_k per (row, block), one
-/// warp per row combines them in CSR order and runs the epilogue
-/// (split_row_task_tma's arithmetic).  rbs, cbs <= 32.
+/// ... in waves that fit shared memory.  Per wave every step is flat over
+/// the wave's blocks, not per row: the rows' contiguous blocks (and relax
+/// factors V) arrive by TMA bulk copies, all x blocks and epilogue operands
+/// are gathered in one pass (two dependent L2 round trips per wave), warps
+/// compute s_k over all (row, block) items, then one warp per row combines
+/// them in CSR order and runs the epilogue (split_row_task_tma's
+/// arithmetic).  rbs, cbs <= 32.
 __device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, size_t sm_doubles, uint64_t* bar,
-                          uint32_t& phase, int* srow, int* sk0, int* snk, int* soff) {
+                          uint32_t& phase, int* srow, int* sk0, int* snk, int* soff, int* bk, int* bi) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
     const bool relax = a.mode == MODE_RELAX;
     const int xs = (a.cbs + 1) & ~1;
     const int nmine = cta < a.nrows ? (a.nrows - cta + ncta - 1) / ncta : 0;
     for (int k = 0; k < nmine;) {
-        // plan the wave (all threads compute the same plan)
-        int nr = 0, nb = 0;
-        size_t need = 0;
-        while (k + nr < nmine && nr < kTailMaxRows) {
-            const int row = row_at(a, cta + (k + nr) * ncta);
-            const int k0 = __ldg(a.ptr + row), len = __ldg(a.ptr + row + 1) - k0;
-            const size_t add = size_t(len) * (a.blk_stride + xs + 32) + (relax ? size_t(a.vstride) : 0) + 4 * 32;
-            if (nr > 0 && need + add > sm_doubles) break;
-            if (tid == 0) {
+        // plan the wave on thread 0 (row descriptors + per-block row / CSR index)
+        if (tid == 0) {
+            int nr = 0, nb = 0;
+            size_t need = 0;
+            while (k + nr < nmine && nr < kTailMaxRows) {
+                const int row = row_at(a, cta + (k + nr) * ncta);
+                const int k0 = __ldg(a.ptr + row), len = __ldg(a.ptr + row + 1) - k0;
+                const size_t add =
+                    size_t(len) * (a.blk_stride + xs + 32) + (relax ? size_t(a.vstride) : 0) + 4 * 32;
+                if ((nr > 0 && need + add > sm_doubles) || nb + len > kTailMaxBlocks) break;
                 srow[nr] = row;
                 sk0[nr] = k0;
                 snk[nr] = len;
                 soff[nr] = nb;
+                for (int q = 0; q < len; ++q) {
+                    bk[nb + q] = k0 + q;
+                    bi[nb + q] = nr;
+                }
+                need += add;
+                nb += len;
+                ++nr;
             }
-            need += add;
-            nb += len;
-            ++nr;
+            srow[kTailMaxRows] = nr;
+            soff[kTailMaxRows] = nb;
         }
         __syncthreads();
-        double* sB = sm;                                       // nb blocks
-        double* sV = sB + size_t(nb) * a.blk_stride;           // nr factors
+        const int nr = srow[kTailMaxRows], nb = soff[kTailMaxRows];
+        double* sB = sm;                                         // nb blocks
+        double* sV = sB + size_t(nb) * a.blk_stride;             // nr factors
         double* sX = sV + (relax ? size_t(nr) * a.vstride : 0);  // nb x-blocks
-        double* ss = sX + size_t(nb) * xs;                     // nb x 32 partial sums
-        double* ep = ss + size_t(nb) * 32;                     // nr x (b, xe, scal, lam) x 32
+        double* ss = sX + size_t(nb) * xs;                       // nb x 32 partial sums
+        double* ep = ss + size_t(nb) * 32;                       // nr x (b, xe, scal, lam) x 32
         if (tid == 0) {
             fence_proxy_async();  // earlier generic reads of these stages precede the async writes
-            uint32_t bytes = uint32_t(nb) * uint32_t(a.blk_stride) * 8u + (relax ? uint32_t(nr * a.vstride) * 8u : 0u);
+            const uint32_t bytes =
+                uint32_t(nb) * uint32_t(a.blk_stride) * 8u + (relax ? uint32_t(nr * a.vstride) * 8u : 0u);
             mbar_arrive_expect_tx(bar, bytes);
             for (int i = 0; i < nr; ++i) {
                 bulk_g2s(sB + size_t(soff[i]) * a.blk_stride, a.val + size_t(sk0[i]) * a.blk_stride,
                          uint32_t(snk[i]) * uint32_t(a.blk_stride) * 8u, bar);
-                if (relax) bulk_g2s(sV + size_t(i) * a.vstride, a.V + size_t(srow[i]) * a.vstride,
-                                    uint32_t(a.vstride) * 8u, bar);
+                if (relax)
+                    bulk_g2s(sV + size_t(i) * a.vstride, a.V + size_t(srow[i]) * a.vstride, uint32_t(a.vstride) * 8u,
+                             bar);
             }
         }
-        // x blocks of every (row, block) and the epilogue operands
-        for (int i = 0; i < nr; ++i) {
-            for (int t = tid; t < snk[i] * a.cbs; t += blockDim.x) {
-                const int q = t / a.cbs, c = t - q * a.cbs;
-                const int j = __ldg(a.col + sk0[i] + q);
-                sX[size_t(soff[i] + q) * xs + c] = __ldcg(a.x + size_t(j) * a.cbs + c);
-            }
-            if (tid < a.rbs) {
-                const size_t o = size_t(srow[i]) * a.rbs + tid;
-                double* e = ep + size_t(i) * 128;
-                if (a.mode == MODE_RESIDUAL || relax) e[tid] = __ldcg(a.b + o);
-                if (relax || a.mode == MODE_ADD) e[32 + tid] = __ldcg(a.xe + o);
-                if (relax) {
-                    e[64 + tid] = __ldg(a.scal + o);
-                    e[96 + tid] = __ldg(a.lam + o);
-                }
+        // every x block of the wave in one pass, then the epilogue operands
+        for (int t = tid; t < nb * a.cbs; t += blockDim.x) {
+            const int q = t / a.cbs, c = t - q * a.cbs;
+            const int j = __ldg(a.col + bk[q]);
+            sX[size_t(q) * xs + c] = __ldcg(a.x + size_t(j) * a.cbs + c);
+        }
+        for (int t = tid; t < nr * 32; t += blockDim.x) {
+            const int i = t >> 5, r = t & 31;
+            if (r >= a.rbs) continue;
+            const size_t o = size_t(srow[i]) * a.rbs + r;
+            double* e = ep + size_t(i) * 128;
+            if (a.mode == MODE_RESIDUAL || relax) e[r] = __ldcg(a.b + o);
+            if (relax || a.mode == MODE_ADD) e[32 + r] = __ldcg(a.xe + o);
+            if (relax) {
+                e[64 + r] = __ldg(a.scal + o);
+                e[96 + r] = __ldg(a.lam + o);
             }
         }
         __syncthreads();
         mbar_wait(bar, phase);
         phase ^= 1u;
-        // s_k per (row, block), one warp per item
-        for (int i = 0; i < nr; ++i)
-            for (int q = warp; q < snk[i]; q += W) {
-                if (relax && __ldg(a.col + sk0[i] + q) == srow[i]) continue;
-                if (lane < a.rbs) {
-                    const double* Bc = sB + size_t(soff[i] + q) * a.blk_stride + lane;
-                    const double* xq = sX + size_t(soff[i] + q) * xs;
-                    double s = 0.0;
+        // s_k over all (row, block) items, one warp per item
+        for (int q = warp; q < nb; q += W) {
+            if (relax && __ldg(a.col + bk[q]) == srow[bi[q]]) continue;
+            if (lane < a.rbs) {
+                const double* Bc = sB + size_t(q) * a.blk_stride + lane;
+                const double* xq = sX + size_t(q) * xs;
+                double s = 0.0;
 #pragma unroll 9
-                    for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, Bc[size_t(c) * a.rbs], xq[c]);
-                    ss[size_t(soff[i] + q) * 32 + lane] = s;
-                }
+                for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, Bc[size_t(c) * a.rbs], xq[c]);
+                ss[size_t(q) * 32 + lane] = s;
             }
+        }
         __syncthreads();
         // epilogue, one warp per row
         for (int i = warp; i < nr; i += W) {
@@ -272,7 +284,8 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
                                                                       int sm_doubles) {
     extern __shared__ __align__(128) double tsm[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ int srow[kTailMaxRows], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows];
+    __shared__ int srow[kTailMaxRows + 1], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows + 1];
+    __shared__ int bk[kTailMaxBlocks], bi[kTailMaxBlocks];
     __shared__ CoarseOp sop;
     const int cta = blockIdx.x, ncta = gridDim.x, tid = threadIdx.x;
     if (tid == 0) {
@@ -293,7 +306,7 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
         const CoarseOp& op = sop;
         switch (op.type) {
             case OP_ROWS:
-                tail_rows(op.rows, cta, ncta, tsm, size_t(sm_doubles), &bar, phase, srow, sk0, snk, soff);
+                tail_rows(op.rows, cta, ncta, tsm, size_t(sm_doubles), &bar, phase, srow, sk0, snk, soff, bk, bi);
                 break;
             case OP_COPY:
                 for (int64_t t = gt; t < op.count; t += nth) op.dst[t] = __ldcg(op.src + t);
@@ -360,22 +373,28 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
                 break;
             }
             case OP_PINV_T:
-                for (int64_t t = gt; t < op.n; t += nth) {
+            case OP_PINV_X: {
+                // src staged in every CTA's shared memory; CTA c owns a
+                // contiguous chunk of outputs (coalesced V reads), every
+                // output one k-ascending chain (pinv_apply order)
+                double* sv = tsm;
+                for (int k = tid; k < op.n; k += blockDim.x) sv[k] = __ldcg(op.src + k);
+                __syncthreads();
+                const int chunk = (op.n + ncta - 1) / ncta;
+                const int t0 = cta * chunk, t1 = min(op.n, t0 + chunk);
+                for (int t = t0 + tid; t < t1; t += blockDim.x) {
                     double s = 0.0;
-#pragma unroll 8
-                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), __ldcg(op.src + k));
-                    const double l = __ldg(op.lam + t);
-                    op.dst[t] = fabs(l) <= op.cut ? 0.0 : s / l;
+#pragma unroll 24
+                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), sv[k]);
+                    if (op.type == OP_PINV_T) {
+                        const double l = __ldg(op.lam + t);
+                        op.dst[t] = fabs(l) <= op.cut ? 0.0 : s / l;
+                    } else {
+                        op.dst[t] = s;
+                    }
                 }
                 break;
-            case OP_PINV_X:
-                for (int64_t t = gt; t < op.n; t += nth) {
-                    double s = 0.0;
-#pragma unroll 8
-                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), __ldcg(op.src + k));
-                    op.dst[t] = s;
-                }
-                break;
+            }
         }
         cluster_sync_all();  // op results visible cluster-wide; descriptor reloaded after
     }
