@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <functional>
 #include <vector>
 
@@ -281,7 +282,7 @@ __device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, s
 }
 
 __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const CoarseOp* __restrict__ ops, int nops,
-                                                                      int sm_doubles) {
+                                                                      int sm_doubles, long long* prof) {
     extern __shared__ __align__(128) double tsm[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ int srow[kTailMaxRows + 1], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows + 1];
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
     uint32_t phase = 0;
     const int64_t gt = int64_t(cta) * blockDim.x + tid, nth = int64_t(ncta) * blockDim.x;
     for (int i = 0; i < nops; ++i) {
+        if (prof && tid == 0) prof[size_t(cta) * (nops + 1) + i] = clock64();
         {
             const int nw = int(sizeof(CoarseOp) / sizeof(int));
             const int* src = reinterpret_cast<const int*>(ops + i);
@@ -398,6 +400,7 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
         }
         cluster_sync_all();  // op results visible cluster-wide; descriptor reloaded after
     }
+    if (prof && tid == 0) prof[size_t(cta) * (nops + 1) + nops] = clock64();
 }
 
 CoarseOp rows_op(const Bsr& A, int mode, const double* x, const double* b, const double* xe, double* y,
@@ -626,8 +629,30 @@ void Mg::launch_coarse_program(Ctx& ctx) {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         const int smd = int(coarse_smem / 8);
-        cuda_check(cudaLaunchKernelEx(&cfg, coarse_cluster_kernel, ops, nops, smd), "coarse_cluster_kernel");
+        // LDGMG_TAIL_PROFILE=1: per-op clock64 stamps of every CTA, printed once
+        static const bool tprof = getenv("LDGMG_TAIL_PROFILE") && atoi(getenv("LDGMG_TAIL_PROFILE"));
+        static int printed = 0;
+        long long* prof = nullptr;
+        if (tprof && printed < 2) LDGMG_CUDA(cudaMallocManaged(&prof, sizeof(long long) * coarse_cluster * (nops + 1)));
+        cuda_check(cudaLaunchKernelEx(&cfg, coarse_cluster_kernel, ops, nops, smd, prof), "coarse_cluster_kernel");
         after_launch("coarse_cluster_kernel");
+        if (prof) {
+            LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+            std::vector<CoarseOp> h(nops);
+            LDGMG_CUDA(cudaMemcpy(h.data(), ops, sizeof(CoarseOp) * nops, cudaMemcpyDeviceToHost));
+            fprintf(stderr, "[tail] %d ops, cluster %d:", nops, coarse_cluster);
+            for (int i = 0; i < nops; ++i) {
+                long long mx = 0;
+                for (int c = 0; c < coarse_cluster; ++c) {
+                    const long long* pc = prof + size_t(c) * (nops + 1);
+                    mx = std::max(mx, pc[i + 1] - pc[i]);
+                }
+                fprintf(stderr, " %d:%lld", h[i].type, mx);
+            }
+            fprintf(stderr, "\n");
+            cudaFree(prof);
+            ++printed;
+        }
         return;
     }
     void* args[] = {&ops, &nops, &maxlen};
