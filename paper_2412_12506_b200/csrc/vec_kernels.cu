@@ -644,24 +644,56 @@ __global__ void __launch_bounds__(1024) pinv_cta_kernel(const double* __restrict
 }
 
 /// t_i = cut(sum_k V(k,i) b_k) / lambda_i ; Vr row-major: V(k,i) at k*n+i.
-__global__ void pinv_t_kernel(const double* __restrict__ Vr, const double* __restrict__ lam,
-                              const double* __restrict__ b, double* __restrict__ t, int n,
-                              double cut) {
+/// Large bottoms (n >= 1536, C5 48^3: n = 2916): one thread per output, the
+/// k-ascending chain fed by batches of 32 independent V loads (coalesced
+/// across the warp), so each thread keeps 32 loads in flight instead of
+/// one: the GEMV is latency-bound by construction (the sum order is fixed).
+constexpr int kPinvBatch = 32;
+/// read-only load kept in program order (asm volatile), so a batch of them
+/// is issued before the chain consumes the first
+__device__ __forceinline__ double ldg_ordered(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__global__ void __launch_bounds__(64) pinv_t_kernel(const double* __restrict__ Vr, const double* __restrict__ lam,
+                                                    const double* __restrict__ b, double* __restrict__ t, int n,
+                                                    double cut) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_launch_dependents();
+    pdl_wait();
     if (i >= n) return;
     double s = 0.0;
-    for (int k = 0; k < n; ++k) s = madd_rn(s, Vr[size_t(k) * n + i], b[k]);
+    int k = 0;
+    for (; k + kPinvBatch <= n; k += kPinvBatch) {
+        double v[kPinvBatch];
+#pragma unroll
+        for (int u = 0; u < kPinvBatch; ++u) v[u] = ldg_ordered(Vr + size_t(k + u) * n + i);
+#pragma unroll
+        for (int u = 0; u < kPinvBatch; ++u) s = madd_rn(s, v[u], __ldg(b + k + u));
+    }
+    for (; k < n; ++k) s = madd_rn(s, __ldg(Vr + size_t(k) * n + i), __ldg(b + k));
     const double l = lam[i];
     t[i] = fabs(l) <= cut ? 0.0 : s / l;
 }
 
 /// x_i = sum_k V(i,k) t_k ; Vc column-major: V(i,k) at k*n+i.
-__global__ void pinv_x_kernel(const double* __restrict__ Vc, const double* __restrict__ t,
-                              double* __restrict__ x, int n) {
+__global__ void __launch_bounds__(64) pinv_x_kernel(const double* __restrict__ Vc, const double* __restrict__ t,
+                                                    double* __restrict__ x, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_launch_dependents();
+    pdl_wait();
     if (i >= n) return;
     double s = 0.0;
-    for (int k = 0; k < n; ++k) s = madd_rn(s, Vc[size_t(k) * n + i], t[k]);
+    int k = 0;
+    for (; k + kPinvBatch <= n; k += kPinvBatch) {
+        double v[kPinvBatch];
+#pragma unroll
+        for (int u = 0; u < kPinvBatch; ++u) v[u] = ldg_ordered(Vc + size_t(k + u) * n + i);
+#pragma unroll
+        for (int u = 0; u < kPinvBatch; ++u) s = madd_rn(s, v[u], __ldg(t + k + u));
+    }
+    for (; k < n; ++k) s = madd_rn(s, __ldg(Vc + size_t(k) * n + i), __ldg(t + k));
     x[i] = s;
 }
 
@@ -993,7 +1025,8 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
     const int n = E.n;
     if (!n) return;
     const double cut = tol * E.lmax;
-    if (n <= 3072) {
+    static const int big = getenv("LDGMG_PINV_BIG") ? atoi(getenv("LDGMG_PINV_BIG")) : 1536;
+    if (n < big && n <= 3072) {
         // KC rows of V per stage, two stages, within ~200 KB of shared memory
         const size_t vec = size_t((n + 1) & ~1) * 2;
         int KC = int(std::min<size_t>(size_t(n), ((200 * 1024 / 8 - vec - 2) / (2 * size_t(n)))));
@@ -1013,10 +1046,11 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
         after_launch("pinv_cta_kernel");
         return;
     }
-    pinv_t_kernel<<<div_up(n, 128), 128, 0, ctx.stream>>>(E.Vr.as<double>(), E.lambda.as<double>(),
-                                                         b, E.t.as<double>(), n, cut);
+    launch_pdl_small(pinv_t_kernel, dim3(div_up(n, 64)), dim3(64), 0, ctx.stream, E.Vr.as<double>(),
+                     E.lambda.as<double>(), b, E.t.as<double>(), n, cut);
     after_launch("pinv_t_kernel");
-    pinv_x_kernel<<<div_up(n, 128), 128, 0, ctx.stream>>>(E.Vc.as<double>(), E.t.as<double>(), x, n);
+    launch_pdl_small(pinv_x_kernel, dim3(div_up(n, 64)), dim3(64), 0, ctx.stream, E.Vc.as<double>(),
+                     E.t.as<double>(), x, n);
     after_launch("pinv_x_kernel");
 }
 
