@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <functional>
+#include <map>
 #include <vector>
 
 #include "core.hpp"
@@ -43,6 +44,10 @@ struct CoarseOp {
     const double* lam;
     double cut;
     int n;
+    // cluster tail, row ops: per-CTA wave plans precomputed on the host
+    // (plan[cta] = offset of that CTA's plan within plan_base)
+    const int* plan;
+    const int* plan_base;
 };
 
 namespace {
@@ -123,7 +128,23 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-constexpr int kTailThreads = 256;
+constexpr int kTailThreads = 512;
+
+/// dst[t] = f(t) for t < n over the CTA, 4 loads in flight per thread (the
+/// plain strided loop waits one memory latency per iteration)
+template <class F>
+__device__ __forceinline__ void tail_gather(double* dst, int n, F f) {
+    const int B = blockDim.x;
+    for (int t0 = threadIdx.x; t0 < n; t0 += 4 * B) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (t0 + u * B < n) ? f(t0 + u * B) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (t0 + u * B < n) dst[t0 + u * B] = v[u];
+    }
+}
+
 constexpr int kTailMaxRows = 64;     // rows per wave
 constexpr int kTailMaxBlocks = 512;  // blocks per wave
 
@@ -135,40 +156,40 @@ constexpr int kTailMaxBlocks = 512;  // blocks per wave
 /// compute s_k over all (row, block) items, then one warp per row combines
 /// them in CSR order and runs the epilogue (split_row_task_tma's
 /// arithmetic).  rbs, cbs <= 32.
-__device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, size_t sm_doubles, uint64_t* bar,
-                          uint32_t& phase, int* srow, int* sk0, int* snk, int* soff, int* bk, int* bi) {
+__device__ void tail_rows(const RowPassArgs& a, const int* plan, int cta, double* sm, uint64_t* bar,
+                          uint32_t& phase, int* srow, int* sk0, int* snk, int* soff, int* bk, int* bi,
+                          long long* tprof) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, tid = threadIdx.x;
     const bool relax = a.mode == MODE_RELAX;
     const int xs = (a.cbs + 1) & ~1;
-    const int nmine = cta < a.nrows ? (a.nrows - cta + ncta - 1) / ncta : 0;
-    for (int k = 0; k < nmine;) {
-        // plan the wave on thread 0 (row descriptors + per-block row / CSR index)
-        if (tid == 0) {
-            int nr = 0, nb = 0;
-            size_t need = 0;
-            while (k + nr < nmine && nr < kTailMaxRows) {
-                const int row = row_at(a, cta + (k + nr) * ncta);
-                const int k0 = __ldg(a.ptr + row), len = __ldg(a.ptr + row + 1) - k0;
-                const size_t add =
-                    size_t(len) * (a.blk_stride + xs + 32) + (relax ? size_t(a.vstride) : 0) + 4 * 32;
-                if ((nr > 0 && need + add > sm_doubles) || nb + len > kTailMaxBlocks) break;
-                srow[nr] = row;
-                sk0[nr] = k0;
-                snk[nr] = len;
-                soff[nr] = nb;
-                for (int q = 0; q < len; ++q) {
-                    bk[nb + q] = k0 + q;
-                    bi[nb + q] = nr;
-                }
-                need += add;
-                nb += len;
-                ++nr;
+    const int nwaves = __ldg(plan);
+    const int* wp = plan + 1;
+    (void)cta;
+    for (int wv = 0; wv < nwaves; ++wv) {
+        if (tprof && tid == 0 && cta == 0) tprof[0] = clock64();
+        // the wave's plan (rows, row pointers, per-block column / local row),
+        // precomputed on the host: one coalesced copy
+        const int nr = wp[0], nb = wp[1];
+        {
+            const int* rowv = wp + 2;
+            const int* k0v = rowv + nr;
+            const int* nkv = k0v + nr;
+            const int* sov = nkv + nr;
+            const int* bjv = sov + nr;
+            const int* biv = bjv + nb;
+            for (int t = tid; t < nr; t += blockDim.x) {
+                srow[t] = __ldg(rowv + t);
+                sk0[t] = __ldg(k0v + t);
+                snk[t] = __ldg(nkv + t);
+                soff[t] = __ldg(sov + t);
             }
-            srow[kTailMaxRows] = nr;
-            soff[kTailMaxRows] = nb;
+            for (int t = tid; t < nb; t += blockDim.x) {
+                bk[t] = __ldg(bjv + t);
+                bi[t] = __ldg(biv + t);
+            }
+            wp = biv + nb;
         }
         __syncthreads();
-        const int nr = srow[kTailMaxRows], nb = soff[kTailMaxRows];
         double* sB = sm;                                         // nb blocks
         double* sV = sB + size_t(nb) * a.blk_stride;             // nr factors
         double* sX = sV + (relax ? size_t(nr) * a.vstride : 0);  // nb x-blocks
@@ -188,10 +209,27 @@ __device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, s
             }
         }
         // every x block of the wave in one pass, then the epilogue operands
-        for (int t = tid; t < nb * a.cbs; t += blockDim.x) {
-            const int q = t / a.cbs, c = t - q * a.cbs;
-            const int j = __ldg(a.col + bk[q]);
-            sX[size_t(q) * xs + c] = __ldcg(a.x + size_t(j) * a.cbs + c);
+        {
+            const int cbs = a.cbs;
+            for (int t0 = tid; t0 < nb * cbs; t0 += 4 * int(blockDim.x)) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int t = t0 + u * int(blockDim.x);
+                    if (t < nb * cbs) {
+                        const int q = t / cbs, c = t - q * cbs;
+                        v[u] = __ldcg(a.x + size_t(bk[q]) * cbs + c);  // bk = column index
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int t = t0 + u * int(blockDim.x);
+                    if (t < nb * cbs) {
+                        const int q = t / cbs, c = t - q * cbs;
+                        sX[size_t(q) * xs + c] = v[u];
+                    }
+                }
+            }
         }
         for (int t = tid; t < nr * 32; t += blockDim.x) {
             const int i = t >> 5, r = t & 31;
@@ -205,22 +243,34 @@ __device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, s
                 e[96 + r] = __ldg(a.lam + o);
             }
         }
+        if (tprof && tid == 0 && cta == 0) tprof[1] = clock64();
         __syncthreads();
         mbar_wait(bar, phase);
         phase ^= 1u;
+        if (tprof && tid == 0 && cta == 0) tprof[2] = clock64();
         // s_k over all (row, block) items, one warp per item
-        for (int q = warp; q < nb; q += W) {
-            if (relax && __ldg(a.col + bk[q]) == srow[bi[q]]) continue;
+        for (int q = warp; q < nb; q += 2 * W) {
+            // two blocks per warp step, chains interleaved (each keeps its order)
+            const int q2 = q + W;
+            const bool d1 = !(relax && bk[q] == srow[bi[q]]);
+            const bool d2 = q2 < nb && !(relax && bk[q2] == srow[bi[q2]]);
             if (lane < a.rbs) {
-                const double* Bc = sB + size_t(q) * a.blk_stride + lane;
-                const double* xq = sX + size_t(q) * xs;
-                double s = 0.0;
+                const double* B1 = sB + size_t(q) * a.blk_stride + lane;
+                const double* X1 = sX + size_t(q) * xs;
+                const double* B2 = sB + size_t(q2 < nb ? q2 : q) * a.blk_stride + lane;
+                const double* X2 = sX + size_t(q2 < nb ? q2 : q) * xs;
+                double u = 0.0, v = 0.0;
 #pragma unroll 9
-                for (int c = 0; c < a.cbs; ++c) s = madd_rn(s, Bc[size_t(c) * a.rbs], xq[c]);
-                ss[size_t(q) * 32 + lane] = s;
+                for (int c = 0; c < a.cbs; ++c) {
+                    u = madd_rn(u, B1[size_t(c) * a.rbs], X1[c]);
+                    v = madd_rn(v, B2[size_t(c) * a.rbs], X2[c]);
+                }
+                if (d1) ss[size_t(q) * 32 + lane] = u;
+                if (d2) ss[size_t(q2) * 32 + lane] = v;
             }
         }
         __syncthreads();
+        if (tprof && tid == 0 && cta == 0) tprof[3] = clock64();
         // epilogue, one warp per row
         for (int i = warp; i < nr; i += W) {
             const bool act = lane < a.rbs;
@@ -277,7 +327,6 @@ __device__ void tail_rows(const RowPassArgs& a, int cta, int ncta, double* sm, s
             }
         }
         __syncthreads();
-        k += nr;
     }
 }
 
@@ -285,7 +334,7 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
                                                                       int sm_doubles, long long* prof) {
     extern __shared__ __align__(128) double tsm[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ int srow[kTailMaxRows + 1], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows + 1];
+    __shared__ int srow[kTailMaxRows], sk0[kTailMaxRows], snk[kTailMaxRows], soff[kTailMaxRows];
     __shared__ int bk[kTailMaxBlocks], bi[kTailMaxBlocks];
     __shared__ CoarseOp sop;
     const int cta = blockIdx.x, ncta = gridDim.x, tid = threadIdx.x;
@@ -308,7 +357,8 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
         const CoarseOp& op = sop;
         switch (op.type) {
             case OP_ROWS:
-                tail_rows(op.rows, cta, ncta, tsm, size_t(sm_doubles), &bar, phase, srow, sk0, snk, soff, bk, bi);
+                tail_rows(op.rows, op.plan_base + __ldg(op.plan + cta), cta, tsm, &bar, phase, srow, sk0, snk, soff,
+                          bk, bi, prof ? prof + size_t(ncta) * (nops + 1) + size_t(i) * 4 : nullptr);
                 break;
             case OP_COPY:
                 for (int64_t t = gt; t < op.count; t += nth) op.dst[t] = __ldcg(op.src + t);
@@ -316,60 +366,66 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
             case OP_ZERO:
                 for (int64_t t = gt; t < op.count; t += nth) op.dst[t] = 0.0;
                 break;
-            case OP_RESTRICT: {
-                // thread (child q, entry o) of parent p: s_q in shared memory, then
-                // thread o sums them in child order (restrict_parent_task's bits)
+            case OP_RESTRICT:
+            case OP_PROLONG: {
+                // operands staged first (K, the parents' child blocks / coarse
+                // blocks), then every chain runs from shared memory; restriction
+                // sums s_q in child order (restrict_parent_task's bits),
+                // prolongation adds per entry (prolong_parent_task's bits)
                 const int BS = op.bss * op.ncomp, bb = op.bss * op.bss;
-                double* ssum = tsm;
+                const int nK = (op.child_ptr ? 0 : 0) + 8 * bb;  // up to 2^3 injection matrices
+                double* sK = tsm;
+                double* sx = sK + nK;       // child blocks (restrict) or the coarse block (prolong)
+                double* ssum = sx + 64 * BS;
+                tail_gather(sK, nK, [&](int t) { return __ldg(op.K + t); });
                 for (int p = cta; p < op.n_parents; p += ncta) {
                     const int q0 = __ldg(op.child_ptr + p), nch = __ldg(op.child_ptr + p + 1) - q0;
+                    if (op.type == OP_RESTRICT) {
+                        tail_gather(sx, nch * BS, [&](int t) {
+                            const int q = t / BS, e = t - q * BS;
+                            return __ldcg(op.src + size_t(__ldg(op.child + q0 + q)) * BS + e);
+                        });
+                    } else {
+                        for (int t = tid; t < BS; t += blockDim.x) sx[t] = __ldcg(op.src + size_t(p) * BS + t);
+                    }
+                    __syncthreads();
                     for (int t = tid; t < nch * BS; t += blockDim.x) {
                         const int q = t / BS, o = t - q * BS;
                         const int f = __ldg(op.child + q0 + q), ot = __ldg(op.orth + f);
-                        const double* src = op.src + size_t(f) * BS;
-                        double sq;
-                        if (ot < 0) {
-                            sq = __ldcg(src + o);
+                        const int c = o / op.bss, jj = o - c * op.bss;
+                        if (op.type == OP_RESTRICT) {
+                            const double* src = sx + q * BS;
+                            double sq;
+                            if (ot < 0) {
+                                sq = src[o];
+                            } else {
+                                const double* Ko = sK + size_t(ot) * bb + jj;
+                                sq = 0.0;
+                                for (int ii = 0; ii < op.bss; ++ii)
+                                    sq = madd_rn(sq, Ko[size_t(ii) * op.bss], src[c * op.bss + ii]);
+                            }
+                            ssum[t] = sq;
                         } else {
-                            const int c = o / op.bss, j = o - c * op.bss;
-                            const double* Ko = op.K + size_t(ot) * bb + j;
-                            sq = 0.0;
-#pragma unroll 9
-                            for (int ii = 0; ii < op.bss; ++ii)
-                                sq = madd_rn(sq, __ldg(Ko + size_t(ii) * op.bss), __ldcg(src + c * op.bss + ii));
+                            double* dst = op.dst + size_t(f) * BS + o;
+                            const double old = __ldcg(dst);
+                            if (ot < 0) {
+                                *dst = __dadd_rn(old, sx[o]);
+                            } else {
+                                const double* Ko = sK + size_t(ot) * bb + size_t(jj) * op.bss;
+                                double s = 0.0;
+                                for (int j = 0; j < op.bss; ++j) s = madd_rn(s, Ko[j], sx[c * op.bss + j]);
+                                *dst = __dadd_rn(old, s);
+                            }
                         }
-                        ssum[t] = sq;
                     }
                     __syncthreads();
-                    for (int o = tid; o < BS; o += blockDim.x) {
-                        double acc = 0.0;
-                        for (int q = 0; q < nch; ++q) acc = __dadd_rn(acc, ssum[q * BS + o]);
-                        op.dst[size_t(p) * BS + o] = acc;
-                    }
-                    __syncthreads();
-                }
-                break;
-            }
-            case OP_PROLONG: {
-                const int BS = op.bss * op.ncomp, bb = op.bss * op.bss;
-                for (int p = cta; p < op.n_parents; p += ncta) {
-                    const int q0 = __ldg(op.child_ptr + p), nch = __ldg(op.child_ptr + p + 1) - q0;
-                    const double* xc = op.src + size_t(p) * BS;
-                    for (int t = tid; t < nch * BS; t += blockDim.x) {
-                        const int q = t / BS, ii = t - q * BS;
-                        const int f = __ldg(op.child + q0 + q), ot = __ldg(op.orth + f);
-                        double* dst = op.dst + size_t(f) * BS + ii;
-                        const double old = __ldcg(dst);
-                        if (ot < 0) {
-                            *dst = __dadd_rn(old, __ldcg(xc + ii));
-                            continue;
+                    if (op.type == OP_RESTRICT) {
+                        for (int o = tid; o < BS; o += blockDim.x) {
+                            double acc = 0.0;
+                            for (int q = 0; q < nch; ++q) acc = __dadd_rn(acc, ssum[q * BS + o]);
+                            op.dst[size_t(p) * BS + o] = acc;
                         }
-                        const int c = ii / op.bss, i2 = ii - c * op.bss;
-                        const double* Ko = op.K + size_t(ot) * bb + size_t(i2) * op.bss;
-                        double s = 0.0;
-#pragma unroll 9
-                        for (int j = 0; j < op.bss; ++j) s = madd_rn(s, __ldg(Ko + j), __ldcg(xc + c * op.bss + j));
-                        *dst = __dadd_rn(old, s);
+                        __syncthreads();
                     }
                 }
                 break;
@@ -381,13 +437,23 @@ __global__ void __launch_bounds__(kTailThreads) coarse_cluster_kernel(const Coar
                 // output one k-ascending chain (pinv_apply order)
                 double* sv = tsm;
                 for (int k = tid; k < op.n; k += blockDim.x) sv[k] = __ldcg(op.src + k);
-                __syncthreads();
                 const int chunk = (op.n + ncta - 1) / ncta;
-                const int t0 = cta * chunk, t1 = min(op.n, t0 + chunk);
-                for (int t = t0 + tid; t < t1; t += blockDim.x) {
+                const int t0 = cta * chunk, t1 = min(op.n, t0 + chunk), w = t1 - t0;
+                double* sVc = sv + ((op.n + 1) & ~1);  // this CTA's columns, [k][w]
+                const bool staged = size_t(op.n) * w + size_t((op.n + 1) & ~1) <= size_t(sm_doubles);
+                if (staged)
+                    tail_gather(sVc, op.n * w, [&](int e) {
+                        const int k = e / w, c = e - k * w;
+                        return __ldg(op.Vm + size_t(k) * op.n + t0 + c);
+                    });
+                __syncthreads();
+                for (int c = tid; c < w; c += blockDim.x) {
                     double s = 0.0;
-#pragma unroll 24
-                    for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t), sv[k]);
+                    if (staged)
+                        for (int k = 0; k < op.n; ++k) s = madd_rn(s, sVc[size_t(k) * w + c], sv[k]);
+                    else
+                        for (int k = 0; k < op.n; ++k) s = madd_rn(s, __ldg(op.Vm + size_t(k) * op.n + t0 + c), sv[k]);
+                    const int t = t0 + c;
                     if (op.type == OP_PINV_T) {
                         const double l = __ldg(op.lam + t);
                         op.dst[t] = fabs(l) <= op.cut ? 0.0 : s / l;
@@ -594,6 +660,82 @@ void Mg::build_coarse_program(Ctx& ctx) {
             cudaGetLastError();
         }
         if (csize < 1) return;
+        // per-CTA wave plans of every row op, precomputed here (the device
+        // only copies them): rows, row pointers, shared-memory offsets, and
+        // each block's column index and local row
+        std::map<const int*, const Bsr*> byptr;
+        for (int l = lc; l < depth; ++l) {
+            byptr[A[l]->ptr.as<int>()] = A[l];
+            if (l + 1 < depth && sm[l]->B) {
+                const Bsr* Bm = sm[l]->B.get();
+                byptr[Bm->ptr.as<int>()] = Bm;
+                if (Bm->T) byptr[Bm->T->ptr.as<int>()] = Bm->T.get();
+            }
+        }
+        std::vector<int> plan;
+        std::vector<std::pair<size_t, size_t>> op_plan(prog.size(), {0, 0});  // (offsets index, -)
+        for (size_t oi = 0; oi < prog.size(); ++oi) {
+            CoarseOp& op = prog[oi];
+            if (op.type != OP_ROWS) continue;
+            const RowPassArgs& ra = op.rows;
+            auto it = byptr.find(ra.ptr);
+            if (it == byptr.end()) return;  // unknown operator: no cluster tail
+            const Bsr& M = *it->second;
+            std::vector<int> rows(ra.nrows);
+            if (ra.rows) {
+                d2h(ctx, rows.data(), ra.rows, sizeof(int) * ra.nrows);
+            } else {
+                for (int i = 0; i < ra.nrows; ++i) rows[i] = i;
+            }
+            const bool relax = ra.mode == MODE_RELAX;
+            const size_t xs = size_t((ra.cbs + 1) & ~1);
+            const size_t offs_at = plan.size();
+            plan.resize(plan.size() + csize, 0);
+            for (int c = 0; c < csize; ++c) {
+                plan[offs_at + c] = int(plan.size());  // this CTA's plan: index within plan_base
+                const size_t nw_at = plan.size();
+                plan.push_back(0);
+                std::vector<int> mine;
+                for (int sl = c; sl < ra.nrows; sl += csize) mine.push_back(rows[sl]);
+                for (size_t k = 0; k < mine.size();) {
+                    std::vector<int> wr, wk0, wnk, wso, wbj, wbi;
+                    size_t need = 0;
+                    int nb = 0;
+                    while (k < mine.size() && int(wr.size()) < kTailMaxRows) {
+                        const int row = mine[k];
+                        const int k0 = M.hptr[row], len = M.hptr[row + 1] - k0;
+                        const size_t add = size_t(len) * (size_t(ra.blk_stride) + xs + 32) +
+                                           (relax ? size_t(ra.vstride) : 0) + 128;
+                        if (!wr.empty() && (need + add > sm_doubles || nb + len > kTailMaxBlocks)) break;
+                        if (len > kTailMaxBlocks || add > sm_doubles) return;  // row does not fit a wave
+                        wr.push_back(row);
+                        wk0.push_back(k0);
+                        wnk.push_back(len);
+                        wso.push_back(nb);
+                        for (int q = 0; q < len; ++q) {
+                            wbj.push_back(M.hcol[k0 + q]);
+                            wbi.push_back(int(wr.size()) - 1);
+                        }
+                        need += add;
+                        nb += len;
+                        ++k;
+                    }
+                    plan.push_back(int(wr.size()));
+                    plan.push_back(nb);
+                    for (auto* v : {&wr, &wk0, &wnk, &wso, &wbj, &wbi}) plan.insert(plan.end(), v->begin(), v->end());
+                    ++plan[nw_at];
+                }
+            }
+            op_plan[oi] = {offs_at, 0};
+        }
+        coarse_plan.alloc(sizeof(int) * std::max<size_t>(1, plan.size()));
+        if (!plan.empty()) h2d(ctx, coarse_plan.p, plan.data(), sizeof(int) * plan.size());
+        for (size_t oi = 0; oi < prog.size(); ++oi) {
+            if (prog[oi].type != OP_ROWS) continue;
+            prog[oi].plan = coarse_plan.as<int>() + op_plan[oi].first;  // [csize] offsets into plan_base
+            prog[oi].plan_base = coarse_plan.as<int>();
+        }
+        h2d(ctx, coarse_prog.p, prog.data(), sizeof(CoarseOp) * prog.size());
         coarse_cluster = csize;
         coarse_smem = sm_doubles * 8;
         coarse_level = lc;
@@ -633,7 +775,8 @@ void Mg::launch_coarse_program(Ctx& ctx) {
         static const bool tprof = getenv("LDGMG_TAIL_PROFILE") && atoi(getenv("LDGMG_TAIL_PROFILE"));
         static int printed = 0;
         long long* prof = nullptr;
-        if (tprof && printed < 2) LDGMG_CUDA(cudaMallocManaged(&prof, sizeof(long long) * coarse_cluster * (nops + 1)));
+        if (tprof && printed < 2)
+            LDGMG_CUDA(cudaMallocManaged(&prof, sizeof(long long) * (coarse_cluster * (nops + 1) + 4 * nops)));
         cuda_check(cudaLaunchKernelEx(&cfg, coarse_cluster_kernel, ops, nops, smd, prof), "coarse_cluster_kernel");
         after_launch("coarse_cluster_kernel");
         if (prof) {
@@ -649,6 +792,12 @@ void Mg::launch_coarse_program(Ctx& ctx) {
                 }
                 fprintf(stderr, " %d:%lld", h[i].type, mx);
             }
+            fprintf(stderr, "\n[tail] CTA0 row-op phases (plan->issued, issued->data, data->computed):");
+            for (int i = 0; i < nops; ++i)
+                if (h[i].type == 0) {
+                    const long long* q = prof + size_t(coarse_cluster) * (nops + 1) + size_t(i) * 4;
+                    fprintf(stderr, " [%lld %lld %lld]", q[1] - q[0], q[2] - q[1], q[3] - q[2]);
+                }
             fprintf(stderr, "\n");
             cudaFree(prof);
             ++printed;

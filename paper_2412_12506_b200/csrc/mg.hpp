@@ -97,7 +97,7 @@ struct Mg {
     int coarse_level = -1;   // first level run by the program (-1: none)
     int coarse_cluster = 0;  // > 0: run by one thread-block cluster of this many CTAs
     bool coarse_dirty = true;
-    DevBuf coarse_prog;
+    DevBuf coarse_prog, coarse_plan;
     int coarse_nops = 0, coarse_maxlen = 1, coarse_grid = 0;
     size_t coarse_smem = 0;
     void build_coarse_program(Ctx& ctx);
