@@ -215,6 +215,11 @@ class DeviceMultigrid {
         h_.reset(m);
     }
     int depth() const { return ldgmg_mg_depth(h_.get()); }
+    /// Sequential (reference-order) kernel projection and Krylov reductions:
+    /// bit-identical to the reference on singular systems (periodic scalar,
+    /// Stokes pressure).  Off: fixed-tree device reductions (deterministic,
+    /// within 1e-13 of the reference, faster).
+    void set_strict_order(bool strict) const { check(ldgmg_mg_set_strict_order(h_.get(), strict ? 1 : 0)); }
     void cycle(DeviceVec& x, const DeviceVec& b) const { check(ldgmg_mg_cycle(ctx_->get(), h_.get(), x.data(), b.data())); }
     void apply(const DeviceVec& b, DeviceVec& x) const { check(ldgmg_mg_apply(ctx_->get(), h_.get(), b.data(), x.data())); }
     void cycles(DeviceVec& x, const DeviceVec& b, int n) const {
@@ -331,6 +336,9 @@ class Multigrid {
                                                  S0.kind == SystemKind::Stokes ? LDGMG_SYSTEM_STOKES : LDGMG_SYSTEM_SCALAR,
                                                  S0.dim, S0.n_comp, S0.bs_scalar, S0.kernel_constants,
                                                  S0.kernel_pressure, to_c(cfg));
+        // the drop-in promises the reference's bits: strict-order reductions
+        // by default (set_strict_order(false) selects the fast tree)
+        dev_->set_strict_order(true);
     }
     Multigrid(const Multigrid&) = delete;
     Multigrid& operator=(const Multigrid&) = delete;
@@ -370,6 +378,7 @@ class Multigrid {
         return {std::move(x), r};
     }
     const DeviceMultigrid& device() const { return *dev_; }
+    void set_strict_order(bool strict) const { dev_->set_strict_order(strict); }
 
   private:
     static const Context& default_ctx() {

@@ -10,15 +10,94 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import sys
 
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_LIB = os.path.join(HERE, "_ref", "libldgmg_ref.so")
-sys.path.insert(0, os.path.dirname(HERE))
 
-from paper_2412_12506_b200 import _lib as L  # noqa: E402  (struct layouts shared with the C ABI)
+# Constants and struct layouts of include/ldgmg_b200.h, the plain-C header
+# ref_capi.cpp is compiled against.  Restated here so the oracle never loads
+# the product library (bench.py's reference arm and the tests' checker stay
+# independent of libldgmg_b200.so).
+SWEEP_FORWARD, SWEEP_REVERSE = 0, 1
+JACOBI, COLOURED_GS, PROC_BLOCK_GS, SAI = 0, 1, 2, 3
+SYSTEM_SCALAR, SYSTEM_STOKES = 0, 1
+BC_PERIODIC, BC_DIRICHLET, BC_NEUMANN = 0, 1, 2
+PHASE_SINGLE, PHASE_BOXES, PHASE_BALL, PHASE_ELLIPSE = 0, 1, 2, 3
+
+
+class _SmootherC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("omega", C.c_double), ("partitions", C.c_int),
+                ("level", C.c_int), ("zeta", C.c_double), ("cache", C.c_int)]
+
+
+class _MgConfigC(C.Structure):
+    _fields_ = [("smoother", _SmootherC), ("pre", C.c_int), ("post", C.c_int),
+                ("nu1", C.c_int), ("nu2", C.c_int), ("bottom_max_elements", C.c_int),
+                ("bottom_tol", C.c_double), ("min_depth", C.c_int)]
+
+
+class SaiStats(C.Structure):
+    _fields_ = [("rank_deficient_columns", C.c_int), ("cache_hits", C.c_int64),
+                ("cache_misses", C.c_int64), ("n_shapes", C.c_int),
+                ("shape_rows", C.c_int * 8), ("shape_cols", C.c_int * 8),
+                ("shape_count", C.c_int * 8)]
+
+    def ls_dims(self):
+        return {(self.shape_rows[i], self.shape_cols[i]): self.shape_count[i]
+                for i in range(min(self.n_shapes, 8))}
+
+
+class _ProblemSpecC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("dim", C.c_int), ("n", C.c_int), ("degree", C.c_int),
+                ("bc", C.c_int * 6), ("beta", C.c_double), ("beta_p", C.c_double),
+                ("gamma", C.c_double), ("delta", C.c_double), ("phase_shape", C.c_int),
+                ("center", C.c_double * 3), ("radii", C.c_double * 3),
+                ("mu_in", C.c_double), ("mu_out", C.c_double), ("rho_in", C.c_double),
+                ("rho_out", C.c_double)]
+
+
+def _spec_c(spec) -> _ProblemSpecC:
+    """Any object with the ProblemSpec attributes (the product's dataclass or
+    a types.SimpleNamespace) -> the C struct."""
+    s = _ProblemSpecC()
+    s.kind, s.dim, s.n, s.degree = spec.kind, spec.dim, spec.n, spec.degree
+    for i in range(6):
+        s.bc[i] = spec.bc[i]
+    s.beta, s.beta_p, s.gamma, s.delta = spec.beta, spec.beta_p, spec.gamma, spec.delta
+    s.phase_shape = spec.phase_shape
+    for i in range(3):
+        s.center[i] = spec.center[i]
+        s.radii[i] = spec.radii[i]
+    s.mu_in, s.mu_out, s.rho_in, s.rho_out = spec.mu_in, spec.mu_out, spec.rho_in, spec.rho_out
+    return s
+
+
+def _cfg_c(cfg) -> _MgConfigC:
+    sm = cfg.smoother
+    return _MgConfigC(_SmootherC(sm.kind, sm.omega, sm.partitions, sm.level, sm.zeta, int(sm.cache)), cfg.pre,
+                      cfg.post, cfg.nu1, cfg.nu2, cfg.bottom_max_elements, cfg.bottom_tol, cfg.min_depth)
+
+
+def problem_spec(**kw):
+    """A ProblemSpec with the product API's defaults (harness.hpp:30-40)."""
+    from types import SimpleNamespace
+    d = dict(kind=SYSTEM_SCALAR, dim=2, n=8, degree=1, bc=(BC_PERIODIC,) * 6, beta=-1.0, beta_p=1.0, gamma=0.0,
+             delta=0.0, phase_shape=PHASE_SINGLE, center=(0.5, 0.5, 0.5), radii=(0.25, 0.25, 0.25), mu_in=1.0,
+             mu_out=1.0, rho_in=1.0, rho_out=1.0)
+    d.update(kw)
+    return SimpleNamespace(**d)
+
+
+def mg_config(smoother_kind=SAI, omega=1.0, partitions=1, level=1, zeta=0.1, cache=True, **kw):
+    """A MultigridConfig with the reference defaults (multigrid.hpp:26-36)."""
+    from types import SimpleNamespace
+    sm = SimpleNamespace(kind=smoother_kind, omega=omega, partitions=partitions, level=level, zeta=zeta, cache=cache)
+    d = dict(smoother=sm, pre=SWEEP_FORWARD, post=SWEEP_REVERSE, nu1=3, nu2=3, bottom_max_elements=64,
+             bottom_tol=1e-10, min_depth=2)
+    d.update(kw)
+    return SimpleNamespace(**d)
 
 
 def available() -> bool:
@@ -38,7 +117,7 @@ def lib():
         IP, LLP = C.POINTER(C.c_int), C.POINTER(C.c_longlong)
         sigs = {
             "ref_last_error": ([], C.c_char_p),
-            "ref_mg_create": ([C.POINTER(L.ProblemSpec), C.POINTER(L.MgConfig)], P),
+            "ref_mg_create": ([C.POINTER(_ProblemSpecC), C.POINTER(_MgConfigC)], P),
             "ref_mg_destroy": ([P], None),
             "ref_mg_depth": ([P], I),
             "ref_level_shape": ([P, I, IP, IP, LLP], I),
@@ -51,7 +130,7 @@ def lib():
             "ref_colours": ([P, I, P, IP], I),
             "ref_sai_nnzb": ([P, I, LLP], I),
             "ref_sai_matrix": ([P, I, P, P, P], I),
-            "ref_sai_stats": ([P, I, C.POINTER(L.SaiStats)], I),
+            "ref_sai_stats": ([P, I, C.POINTER(SaiStats)], I),
             "ref_bottom_size": ([P], I),
             "ref_bottom": ([P, P, P], I),
             "ref_kernel": ([P, IP, P], I),
@@ -63,6 +142,11 @@ def lib():
             "ref_apply": ([P, P, P], I),
             "ref_solve": ([P, P, P, D, I, P, IP], I),
             "ref_cycles_parallel": ([P, P, I, I, C.POINTER(D)], I),
+            "ref_cache_new": ([], P),
+            "ref_cache_free": ([P], None),
+            "ref_cache_entries": ([P], LL),
+            "ref_mg_create_shared": ([C.POINTER(_ProblemSpecC), C.POINTER(_MgConfigC), P], P),
+            "ref_cycles_multi": ([C.POINTER(P), I, P, I, C.POINTER(D)], I),
             "ref_random_rhs": ([I, I, C.c_ulonglong, P], I),
             "ref_eta": ([P, I, C.c_ulonglong, D, I, P, IP, IP, IP, C.POINTER(D), C.POINTER(D)], I),
             "ref_bsr_spmv": ([I, I, I, I, P, P, P, P, P, I, C.POINTER(C.c_ulonglong)], I),
@@ -74,7 +158,7 @@ def lib():
             "ref_sai_build": ([I, I, I, I, I, P, P, P, I, D, I], P),
             "ref_sai_raw_nnzb": ([P], LL),
             "ref_sai_raw_matrix": ([P, P, P, P], None),
-            "ref_sai_raw_stats": ([P, C.POINTER(L.SaiStats)], None),
+            "ref_sai_raw_stats": ([P, C.POINTER(SaiStats)], None),
             "ref_sai_raw_free": ([P], None),
             "ref_balance_vector": ([I, I, I, I, I, P, P, P, D, P], I),
             "ref_colour_mesh": ([I, P, P, P], I),
@@ -105,10 +189,15 @@ def _p(a):
 class RefMultigrid:
     """The reference Multigrid (multigrid.hpp:45-274) on a catalogue problem."""
 
-    def __init__(self, spec, cfg):
-        self.spec, self.cfg = spec, cfg
-        cs, cc = spec.c(), cfg.c()
-        h = lib().ref_mg_create(C.byref(cs), C.byref(cc))
+    def __init__(self, spec, cfg, cache=None):
+        """`cache`: an optional SaiCache shared with other hierarchies
+        (MultigridConfig::cache, multigrid.hpp:35)."""
+        self.spec, self.cfg, self.cache = spec, cfg, cache
+        cs, cc = _spec_c(spec), _cfg_c(cfg)
+        if cache is None:
+            h = lib().ref_mg_create(C.byref(cs), C.byref(cc))
+        else:
+            h = lib().ref_mg_create_shared(C.byref(cs), C.byref(cc), cache.h)
         if not h:
             raise RefError(-1, lib().ref_last_error().decode())
         self.h = h
@@ -173,7 +262,7 @@ class RefMultigrid:
         return ptr, col, val
 
     def sai_stats(self, l):
-        st = L.SaiStats()
+        st = SaiStats()
         _chk(lib().ref_sai_stats(self.h, l, C.byref(st)))
         return st
 
@@ -252,6 +341,32 @@ class RefMultigrid:
                     rho=rho.value, eta=eta.value)
 
 
+class SaiCache:
+    """The reference's SaiCache (smoothers.hpp:242-250), shareable across hierarchies."""
+
+    def __init__(self):
+        self.h = lib().ref_cache_new()
+        self._free = lib().ref_cache_free
+
+    def entries(self):
+        return int(lib().ref_cache_entries(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._free(self.h)
+            self.h = None
+
+
+def cycles_multi(hierarchies, b, ncycles):
+    """`ncycles` V-cycles on each hierarchy, one thread per hierarchy, all
+    started together; wall seconds (ref_cycles_multi)."""
+    b = np.ascontiguousarray(b, np.float64)
+    arr = (C.c_void_p * len(hierarchies))(*[m.h for m in hierarchies])
+    sec = C.c_double()
+    _chk(lib().ref_cycles_multi(arr, len(hierarchies), _p(b), int(ncycles), C.byref(sec)))
+    return sec.value
+
+
 def random_rhs(nblocks, bs, seed=0):
     out = np.empty(nblocks * bs)
     _chk(lib().ref_random_rhs(nblocks, bs, seed, _p(out)))
@@ -292,7 +407,7 @@ def sai_build(kind, dim, ncomp, bs_scalar, N, ptr, col, val, level, zeta, cache=
         bc = np.empty(nnzb, np.int32)
         bv = np.empty(nnzb * bs * bs)
         lib().ref_sai_raw_matrix(h, _p(bp), _p(bc), _p(bv))
-        st = L.SaiStats()
+        st = SaiStats()
         lib().ref_sai_raw_stats(h, C.byref(st))
         return (bp, bc, bv), st
     finally:

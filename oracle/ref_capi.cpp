@@ -26,6 +26,7 @@
 #include <fstream>
 #include <memory>
 #include <string>
+#include <atomic>
 #include <thread>
 
 using namespace ldgmg;
@@ -205,6 +206,63 @@ void* ref_mg_create(const ldgmg_problem_spec* spec, const ldgmg_mg_config* cfg) 
 }
 
 void ref_mg_destroy(void* h) { delete static_cast<RefMg*>(h); }
+
+/// A least-squares cache shared across hierarchies (MultigridConfig::cache,
+/// multigrid.hpp:35): the reference's own way of building several
+/// hierarchies of one problem without repeating the SAI solves.
+void* ref_cache_new(void) { return new SaiCache(); }
+void ref_cache_free(void* c) { delete static_cast<SaiCache*>(c); }
+long long ref_cache_entries(void* c) { return (long long)static_cast<SaiCache*>(c)->entries(); }
+
+void* ref_mg_create_shared(const ldgmg_problem_spec* spec, const ldgmg_mg_config* cfg, void* cache) {
+    RefMg* h = nullptr;
+    const int rc = guard([&] {
+        auto r = std::make_unique<RefMg>();
+        r->spec = *spec;
+        r->built = build(*spec);
+        MultigridConfig mc = mg_of(*cfg);
+        mc.cache = static_cast<SaiCache*>(cache);
+        r->mg = std::make_unique<Multigrid>(r->built.mesh, r->built.assemble, mc);
+        h = r.release();
+    });
+    return rc == 0 ? h : nullptr;
+}
+
+/// `ncycles` Multigrid::cycle calls on each of `nh` INDEPENDENT hierarchies,
+/// hierarchy i on its own thread with its own x (the reference's run_cells
+/// parallelism, harness.hpp:305-327: each cell owns its hierarchy).  Wall
+/// seconds from the common start to the last thread's end.
+int ref_cycles_multi(void* const* hs, int nh, const double* b, int ncycles, double* seconds) {
+    return guard([&] {
+        if (nh < 1) throw std::invalid_argument("ref_cycles_multi: no hierarchies");
+        const System& S = static_cast<RefMg*>(hs[0])->mg->system(0);
+        const BlockVec bv = vec_in(b, S.n_elements(), S.block_size());
+        std::atomic<int> ready{0};
+        std::atomic<bool> go{false};
+        std::chrono::steady_clock::time_point t0;
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(nh);
+        for (int t = 0; t < nh; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    const Multigrid& mg = *static_cast<RefMg*>(hs[t])->mg;
+                    BlockVec x(S.n_elements(), S.block_size());
+                    ready.fetch_add(1);
+                    while (!go.load()) std::this_thread::yield();
+                    for (int c = 0; c < ncycles; ++c) mg.cycle(x, bv);
+                } catch (const std::exception& e) {
+                    errs[t] = e.what();
+                }
+            });
+        while (ready.load() < nh) std::this_thread::yield();
+        t0 = std::chrono::steady_clock::now();
+        go.store(true);
+        for (auto& th : pool) th.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+    });
+}
 
 int ref_mg_depth(void* h) { return static_cast<RefMg*>(h)->mg->depth(); }
 

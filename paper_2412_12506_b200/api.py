@@ -538,6 +538,10 @@ class Multigrid:
         `out` (optional): the host array receiving x; page-locked buffers
         (e.g. a pinned torch tensor's .numpy()) are written by DMA directly."""
         b = _np(b, np.float64)
+        if b.ndim != 1 or b.size != self.n * self.bs:
+            raise L.InvalidArgument("solve_host: b must hold n * bs entries")
+        if int(maxit) < 0:
+            raise L.InvalidArgument("mg_solve_host: maxit must be nonnegative")
         if out is not None:
             if out.dtype != np.float64 or out.shape != b.shape or not out.flags["C_CONTIGUOUS"]:
                 raise L.InvalidArgument("solve_host: out must be a contiguous float64 array shaped like b")

@@ -140,42 +140,8 @@ __device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int i
                                            double* stages, double* xslots, uint64_t* bars, int* xoffs) {
     const int t = threadIdx.x;
     double* xs = xslots + size_t(st) * a.xslot_doubles;
-    if (a.xtma) {
-        if (t == 0) {
-            const double* src;
-            uint32_t bytes;
-            if (kind == 0) {
-                const int64_t blk = a.perm ? int64_t(__ldg(a.perm + idx)) : int64_t(idx);
-                src = a.val + size_t(blk) * a.blk_stride;
-                bytes = uint32_t(a.blk_stride) * 8u;
-                const double* xsrc = x_source(a, row, j) + size_t(j) * a.cbs;
-                const uintptr_t xa = reinterpret_cast<uintptr_t>(xsrc) & ~uintptr_t(15);
-                const int off = int((reinterpret_cast<uintptr_t>(xsrc) - xa) >> 3);
-                const uint32_t xbytes = (uint32_t((off + a.cbs) * 8) + 15u) & ~15u;
-                xoffs[st] = off;
-                mbar_arrive_expect_tx(bars + st, bytes + xbytes);
-                bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
-                bulk_g2s(xs, reinterpret_cast<const void*>(xa), xbytes, bars + st);
-            } else {
-                src = a.V + size_t(idx) * a.vstride;
-                bytes = uint32_t(a.vstride) * 8u;
-                mbar_arrive_expect_tx(bars + st, bytes);
-                bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
-            }
-        }
-        return;
-    }
-    if (t < a.cbs) {
-        if (kind == 0) {
-            const double* src = x_source(a, row, j) + size_t(j) * a.cbs + t;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(xs + t)),
-                         "l"(src)
-                         : "memory");
-        }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
-                         smem_addr(bars + st))
-                     : "memory");
-    }
+    // one elected thread issues the block and (kind 0) the 16-byte aligned
+    // window around x_j as two bulk copies on the stage's mbarrier
     if (t == 0) {
         const double* src;
         uint32_t bytes;
@@ -183,12 +149,20 @@ __device__ __forceinline__ void issue_item(const RowPassArgs& a, int kind, int i
             const int64_t blk = a.perm ? int64_t(__ldg(a.perm + idx)) : int64_t(idx);
             src = a.val + size_t(blk) * a.blk_stride;
             bytes = uint32_t(a.blk_stride) * 8u;
+            const double* xsrc = x_source(a, row, j) + size_t(j) * a.cbs;
+            const uintptr_t xa = reinterpret_cast<uintptr_t>(xsrc) & ~uintptr_t(15);
+            const int off = int((reinterpret_cast<uintptr_t>(xsrc) - xa) >> 3);
+            const uint32_t xbytes = (uint32_t((off + a.cbs) * 8) + 15u) & ~15u;
+            xoffs[st] = off;
+            mbar_arrive_expect_tx(bars + st, bytes + xbytes);
+            bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
+            bulk_g2s(xs, reinterpret_cast<const void*>(xa), xbytes, bars + st);
         } else {
             src = a.V + size_t(idx) * a.vstride;
             bytes = uint32_t(a.vstride) * 8u;
+            mbar_arrive_expect_tx(bars + st, bytes);
+            bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
         }
-        mbar_arrive_expect_tx(bars + st, bytes);
-        bulk_g2s(stages + size_t(st) * a.stage_doubles, src, bytes, bars + st);
     }
 }
 
@@ -309,7 +283,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
     const int rbs = BS > 0 ? BS : a.rbs, cbs = BS > 0 ? BS : a.cbs;
 
     if (t == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(bars + s, a.xtma ? 1u : 1u + uint32_t(a.cbs));
+        for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1u);
         fence_mbar_init();
     }
     __syncthreads();
@@ -364,7 +338,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
             const int st = int(q % uint32_t(NS));
             mbar_wait(bars + st, (q / uint32_t(NS)) & 1u);
             const double* S = stages + size_t(st) * a.stage_doubles;
-            const double* X = xslots + size_t(st) * a.xslot_doubles + (a.xtma ? xoffs[st] : 0);
+            const double* X = xslots + size_t(st) * a.xslot_doubles + xoffs[st];
             int used = 1;
             if (nblk == 2) {
                 const int st2 = int((q + 1) % uint32_t(NS));
@@ -376,7 +350,7 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                     const bool hi = t >= BS;
                     const int r = hi ? t - BS : t;
                     const double* Sx = hi ? stages + size_t(st2) * a.stage_doubles : S;
-                    const double* Xx = hi ? xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0) : X;
+                    const double* Xx = hi ? xslots + size_t(st2) * a.xslot_doubles + xoffs[st2] : X;
                     double s = 0.0;
                     if (t < 2 * BS)
                         s = a.tview ? bdot_t<BS>(Sx + size_t(r) * cbs, Xx, cbs) : bdot<BS>(Sx + r, Xx, cbs, rbs);
@@ -389,10 +363,10 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
                     double s1, s2;
                     if (a.tview)
                         bdot2_t<BS>(S + size_t(t) * cbs, X, stages + size_t(st2) * a.stage_doubles + size_t(t) * cbs,
-                                    xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0), cbs, s1, s2);
+                                    xslots + size_t(st2) * a.xslot_doubles + xoffs[st2], cbs, s1, s2);
                     else
                         bdot2<BS>(S + t, X, stages + size_t(st2) * a.stage_doubles + t,
-                                  xslots + size_t(st2) * a.xslot_doubles + (a.xtma ? xoffs[st2] : 0), cbs, rbs, s1,
+                                  xslots + size_t(st2) * a.xslot_doubles + xoffs[st2], cbs, rbs, s1,
                                   s2);
                     acc = relax ? __dsub_rn(acc, s1) : __dadd_rn(acc, s1);
                     acc = relax ? __dsub_rn(acc, s2) : __dadd_rn(acc, s2);
@@ -924,14 +898,9 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         }
         const int maxlen = std::max(1, A.max_row);
         const int warps = std::min(8, maxlen);
-        static int tma_env = -1;
-        if (tma_env < 0) {
-            const char* e = getenv("LDGMG_SPLIT_TMA");
-            tma_env = e ? atoi(e) : 1;
-        }
         const size_t smem_tma =
             sizeof(double) * split_row_tma_doubles(maxlen, A.blk_stride, p.mode == MODE_RELAX ? p.F->vstride : 0, A.cbs);
-        if (tma_env && smem_tma <= 120 * 1024) {
+        if (smem_tma <= 120 * 1024) {  // else: long rows, plain-load kernel
             ensure_dyn_smem(rowsplit_tma_kernel, smem_tma);
             const int grid = std::min(p.nrows, ctx.num_sms * 16);
             static bool once = (max_carveout(rowsplit_tma_kernel), true);
@@ -992,15 +961,9 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         a.dpos = A.dpos.as<int>();
     }
     a.stage_doubles = even_up(stage);
-    static int xtma_env = -1;
-    if (xtma_env < 0) {
-        const char* e = getenv("LDGMG_XTMA");
-        xtma_env = e ? atoi(e) : 1;
-    }
-    a.xtma = xtma_env;
-    // x-TMA slots hold a 16-byte aligned window around x_j (up to one extra
+    // x slots hold a 16-byte aligned window around x_j (up to one extra
     // double in front and the tail rounded up to 16 bytes)
-    a.xslot_doubles = even_up(std::max(A.cbs, A.rbs)) + (a.xtma ? 2 : 0);
+    a.xslot_doubles = even_up(std::max(A.cbs, A.rbs)) + 2;
     const int wide = std::max(A.rbs, A.cbs);
     const int GT = wide <= 32 ? 32 : wide <= 64 ? 64 : wide <= 128 ? 128 : 256;
     // ring depth: keep >= ~3 blocks in flight per group within a 200 KB budget

@@ -780,7 +780,7 @@ int ldgmg_mg_set_smoother(ldgmg_mg* mg, int level, ldgmg_smoother* S) {
         if (level < 0 || level + 1 >= mg->m.depth) fail(LDGMG_ERR_LOGIC, "multigrid: the bottom level has no smoother");
         if (S->s.A != mg->m.A[level]) fail(LDGMG_ERR_INVALID_ARGUMENT, "mg_set_smoother: smoother bound to another operator");
         mg->m.sm[level] = &S->s;
-        mg->m.coarse_dirty = true;
+        mg->m.invalidate_graphs();
     });
 }
 
@@ -792,17 +792,6 @@ static void ensure_smoothers(ldgmg_ctx* ctx, Mg& m) {
         mg_default_smoothers(ctx, m);
         for (int l = 0; l + 1 < m.depth; ++l)
             if (keep[l]) m.sm[l] = keep[l];
-    }
-    if (m.coarse_dirty) {
-        static int env = -2;
-        if (env == -2) {
-            const char* s = getenv("LDGMG_COARSE_ROWS");
-            env = s ? atoi(s) : -1;
-        }
-        if (env >= 0) m.coarse_rows = env;
-        m.build_coarse_program(*ctx);
-        m.coarse_dirty = false;
-        m.invalidate_graphs();
     }
 }
 
@@ -1017,6 +1006,7 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         need(mg, "mg_solve_host");
         need(b_host, "mg_solve_host(b)");
         need(x_host, "mg_solve_host(x)");
+        if (maxit < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "mg_solve_host: maxit must be nonnegative");
         Mg& m = mg->m;
         ensure_smoothers(ctx, m);
         const int64_t n = int64_t(m.A[0]->brows) * m.bs;

@@ -184,11 +184,16 @@ void Smoother::init_common(Ctx& ctx) {
         // precede it in the sweep; relaxing the wavefronts of that DAG one
         // launch at a time reproduces the sequential result bit for bit.
         for (int d = 0; d < 2; ++d) {
-            std::vector<int> lev(N, 0);
+            // need[j]: write-after-read edge -- an element e preceding j in
+            // the sweep that reads x_j (A[e][j] != 0) must see the OLD x_j,
+            // so j goes to a later wavefront than e.  Implied by the
+            // read-after-write edge on symmetric patterns, explicit here so
+            // the schedule is exact for any pattern.
+            std::vector<int> lev(N, 0), need(N, 0);
             int nlev = N ? 1 : 0;
             for (int i = 0; i < N; ++i) {
                 const int e = d == 0 ? i : N - 1 - i;
-                int l = 0;
+                int l = need[e];
                 for (int k = A->hptr[e]; k < A->hptr[e + 1]; ++k) {
                     const int j = A->hcol[k];
                     if (j == e || part_of[j] != part_of[e]) continue;
@@ -196,6 +201,11 @@ void Smoother::init_common(Ctx& ctx) {
                 }
                 lev[e] = l;
                 nlev = std::max(nlev, l + 1);
+                for (int k = A->hptr[e]; k < A->hptr[e + 1]; ++k) {
+                    const int j = A->hcol[k];
+                    if (j != e && part_of[j] == part_of[e] && (d == 0 ? j > e : j < e))
+                        need[j] = std::max(need[j], l + 1);
+                }
             }
             std::vector<int> rows;
             rows.reserve(N);
@@ -377,6 +387,16 @@ void Mg::init(Ctx& ctx) {
     for (int l = 0; l < depth; ++l) {
         if (A[l]->rbs != bs || A[l]->cbs != bs || A[l]->brows != A[l]->bcols)
             fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: level assembler changed the discretization");
+        // check_level (multigrid.hpp:201-204): every stored (i, j) has a stored (j, i)
+        const Bsr& L = *A[l];
+        for (int i = 0; i < L.brows; ++i)
+            for (int k = L.hptr[i]; k < L.hptr[i + 1]; ++k) {
+                const int j = L.hcol[k];
+                const int* b0 = L.hcol.data() + L.hptr[j];
+                const int* b1 = L.hcol.data() + L.hptr[j + 1];
+                if (std::find(b0, b1, i) == b1)
+                    fail(LDGMG_ERR_INVALID_ARGUMENT, "multigrid: level operator pattern not symmetric");
+            }
         if (l + 1 < depth) {
             require(T[l] != nullptr, "multigrid: missing transfer");
             require(T[l]->n_fine == A[l]->brows && T[l]->n_coarse == A[l + 1]->brows && T[l]->bs == bs,
@@ -497,10 +517,6 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready) {
         launch_pinv_apply(ctx, bottom, cfg.bottom_tol, b, x);
         return;
     }
-    if (l > 0 && l == coarse_level && x == xl[l].as<double>() && b == bl[l].as<double>()) {
-        launch_coarse_program(ctx);  // the rest of the V-cycle in one cooperative kernel
-        return;
-    }
     const Smoother& S = *sm[l];
     for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre, r0_ready && i == 0);
     RowPass p;
@@ -570,7 +586,17 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n, bool r0_ready) {
         Ctx cctx = ctx;
         cctx.stream = cap_stream;
         LDGMG_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
-        cycle(cctx, x, b, r0_ready);
+        try {
+            cycle(cctx, x, b, r0_ready);
+        } catch (...) {
+            // leave the capture stream usable: end (and drop) the partial capture
+            cudaGraph_t partial = nullptr;
+            cudaStreamEndCapture(cap_stream, &partial);
+            if (partial) cudaGraphDestroy(partial);
+            cudaGetLastError();
+            launch_counter().fetch_sub(launch_counter().load() - c0);
+            throw;
+        }
         LDGMG_CUDA(cudaStreamEndCapture(cap_stream, &graph));
         // captured launches did not run; they are counted per graph launch
         ng.nkernels = launch_counter().load() - c0;
@@ -587,6 +613,9 @@ void Mg::cycles(Ctx& ctx, double* x, const double* b, int n, bool r0_ready) {
 }
 
 void Mg::invalidate_graphs() {
+    // the next cycles() runs un-captured once more: a new smoother may need
+    // lazy setup (B^T views, kernel attributes) that cannot run under capture
+    warm = false;
     for (auto& gr : graphs) cudaGraphExecDestroy(gr.exec);
     graphs.clear();
     if (solve_exec) cudaGraphExecDestroy(solve_exec);

@@ -89,19 +89,6 @@ struct Mg {
     };
     std::vector<Graph> graphs;
     cudaStream_t cap_stream = nullptr;
-    // persistent cooperative program for the small levels (coarse_program.cu)
-    // Off by default: measured slower than graph-launched passes on B200 (C2
-    // 3.46 -> 3.89 ms, grid-wide barriers cost more than graph node launches);
-    // LDGMG_COARSE_ROWS=n enables it for levels with <= n elements.
-    int coarse_rows = 0;
-    int coarse_level = -1;   // first level run by the program (-1: none)
-    int coarse_cluster = 0;  // > 0: run by one thread-block cluster of this many CTAs
-    bool coarse_dirty = true;
-    DevBuf coarse_prog, coarse_plan;
-    int coarse_nops = 0, coarse_maxlen = 1, coarse_grid = 0;
-    size_t coarse_smem = 0;
-    void build_coarse_program(Ctx& ctx);
-    void launch_coarse_program(Ctx& ctx);
     SaiCache* sai_cache = nullptr;  // shared across levels (multigrid.hpp:60)
     // ldgmg_mg_solve_host scratch (cached so the graph of (x, b) is reused)
     DevBuf solve_b, solve_x, solve_r, solve_xs;

@@ -37,9 +37,6 @@ struct RowPassArgs {
     // relax: CSR position of each row's diagonal block (-1 if none); the
     // streaming kernel skips it without reading col
     const int* dpos;
-    // x blocks by one TMA bulk copy per block (16-byte aligned window, the
-    // block's start offset kept per stage) instead of per-lane cp.async
-    int xtma;
     // processor-block GS (smoothers.hpp:426-436): neighbour j of row e is read
     // from x when part[j] == part[e], else from x_alt (the sweep's snapshot)
     const int* part;

@@ -1228,6 +1228,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     std::vector<int> col_problem(N, -1);           // -1: served by a cache entry
     std::vector<const SaiCacheEntry*> col_entry(N, nullptr);
     std::vector<std::pair<int, Key>> inserts;  // (problem id, key) to insert after solving
+    std::unordered_map<Key, int, KeyHash> pending;  // keys in `inserts` (O(1) hit test)
     size_t pending_bytes = cache ? cache->bytes : 0;
     for (int j = 0; j < N; ++j) {
         if (colmask && !(*colmask)[j]) continue;
@@ -1236,9 +1237,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         if (cache) {
             auto it = cache->map.find(P.key);
             bool hit = it != cache->map.end();
-            if (!hit)
-                for (auto& ins : inserts)
-                    if (ins.second == P.key) hit = true;
+            if (!hit) hit = pending.count(P.key) != 0;
             if (hit) {
                 ++res.stats.cache_hits;
                 if (it != cache->map.end())
@@ -1264,6 +1263,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             if (pending_bytes + bytes <= kCacheBudget) {
                 pending_bytes += bytes;
                 inserts.push_back({pid, P.key});
+                pending.emplace(P.key, pid);
             }
         }
     }

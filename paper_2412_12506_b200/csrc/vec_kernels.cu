@@ -51,29 +51,6 @@ __global__ void restrict_kernel(const int* __restrict__ child_ptr, const int* __
     }
 }
 
-__global__ void prolong_kernel(const int* __restrict__ parent, const int* __restrict__ orth,
-                               const double* __restrict__ K, const double* __restrict__ xc,
-                               double* __restrict__ xf, int n_fine, int bss, int ncomp) {
-    const int BS = bss * ncomp;
-    const int64_t total = int64_t(n_fine) * BS;
-    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
-         o += int64_t(gridDim.x) * blockDim.x) {
-        const int f = int(o / BS);
-        const int ii = int(o - int64_t(f) * BS);
-        const int p = parent[f], ot = orth[f];
-        const double* src = xc + size_t(p) * BS;
-        if (ot < 0) {
-            xf[o] = __dadd_rn(xf[o], src[ii]);
-            continue;
-        }
-        const int c = ii / bss, i = ii - c * bss;
-        const double* Ko = K + size_t(ot) * bss * bss + size_t(i) * bss;
-        double s = 0.0;
-        for (int j = 0; j < bss; ++j) s = madd_rn(s, __ldg(Ko + j), src[c * bss + j]);
-        xf[o] = __dadd_rn(xf[o], s);
-    }
-}
-
 /// Restriction, one CTA per coarse element p: the children's residual
 /// blocks are staged in shared memory, thread (c, j) runs the reference's
 /// sequential sums (children ascending, i ascending) with K read through the
@@ -118,37 +95,6 @@ __global__ void restrict_cta_kernel(const int* __restrict__ child_ptr, const int
         __syncthreads();
     }
     (void)maxch;
-}
-
-/// Prolongation, one CTA per coarse element p: xc_p staged in shared memory,
-/// every child f of p updated by thread (f, c, i) (reference order, j ascending).
-__global__ void prolong_cta_kernel(const int* __restrict__ child_ptr, const int* __restrict__ child,
-                                   const int* __restrict__ orth, const double* __restrict__ K,
-                                   const double* __restrict__ xc, double* __restrict__ xf, int n_coarse,
-                                   int bss, int ncomp) {
-    extern __shared__ double sx[];  // BS
-    const int BS = bss * ncomp;
-    for (int p = blockIdx.x; p < n_coarse; p += gridDim.x) {
-        for (int t = threadIdx.x; t < BS; t += blockDim.x) sx[t] = xc[size_t(p) * BS + t];
-        __syncthreads();
-        const int q0 = child_ptr[p], nch = child_ptr[p + 1] - q0;
-        for (int t = threadIdx.x; t < nch * BS; t += blockDim.x) {
-            const int q = t / BS, ii = t - q * BS;
-            const int f = child[q0 + q], ot = orth[f];
-            double* dst = xf + size_t(f) * BS + ii;
-            if (ot < 0) {
-                *dst = __dadd_rn(*dst, sx[ii]);
-                continue;
-            }
-            const int c = ii / bss, i = ii - c * bss;
-            const double* Ko = K + size_t(ot) * bss * bss + size_t(i) * bss;
-            double s = 0.0;
-#pragma unroll 9
-            for (int j = 0; j < bss; ++j) s = madd_rn(s, __ldg(Ko + j), sx[c * bss + j]);
-            *dst = __dadd_rn(*dst, s);
-        }
-        __syncthreads();
-    }
 }
 
 /// Restriction, one THREAD per (parent p, child q, output o = (c, j)): the
@@ -343,201 +289,6 @@ __global__ void __launch_bounds__(NCH * BSS) prolong_ks_kernel(const double* __r
     }
 }
 
-/// Copies the 2^d injection matrices (nK doubles, nK even) into shared
-/// memory with one TMA bulk copy: a single memory round trip per CTA.
-__device__ __forceinline__ void stage_K_bulk(double* sK, const double* K, int nK, uint64_t* bar) {
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(bar, uint32_t(nK) * 8u);
-        bulk_g2s(sK, K, uint32_t(nK) * 8u, bar);
-    }
-    mbar_wait(bar, 0);
-}
-
-/// Restriction, one WARP per coarse element p with the injection matrices in
-/// shared memory.  Every global access of a parent is issued in batches
-/// (children ids, orthants, then all child residual blocks) so a parent costs
-/// ~3 memory round trips; lane (c, j) then computes the per-child sums s_f
-/// as independent chains (ILP across children) and accumulates them in the
-/// reference order acc = 0 + s_f1 + s_f2 + ... (copies for orthant -1).
-/// Same bits as restrict_kernel.
-template <int MAXCH>
-__global__ void __launch_bounds__(256) restrict_warp_kernel(const int* __restrict__ child_ptr,
-                                                            const int* __restrict__ child,
-                                                            const int* __restrict__ orth,
-                                                            const double* __restrict__ K,
-                                                            const double* __restrict__ rf, double* __restrict__ rc,
-                                                            int n_coarse, int bss, int ncomp, int nK,
-                                                            double* __restrict__ zero_xc) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ int sch[8][MAXCH], sor[8][MAXCH];
-    __shared__ __align__(8) uint64_t bar;
-    const int BS = bss * ncomp, bb = bss * bss;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
-    double* sK = sm;
-    double* src = sm + nK + size_t(warp) * MAXCH * BS;
-    stage_K_bulk(sK, K, nK, &bar);  // immutable: overlaps the previous kernel
-    pdl_launch_dependents();
-    pdl_wait();
-    for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
-        const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
-        int f = 0;
-        if (lane < nch) f = __ldg(child + q0 + lane);
-        if (lane < nch) {
-            sch[warp][lane] = f;
-            sor[warp][lane] = __ldg(orth + f);
-        }
-        __syncwarp();
-        const int total = nch * BS;
-        for (int t0 = lane; t0 < total; t0 += 32 * 8) {
-            double tmp[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = t0 + u * 32;
-                tmp[u] = 0.0;
-                if (t < total) {
-                    const int q = t / BS, e = t - q * BS;
-                    tmp[u] = rf[size_t(sch[warp][q]) * BS + e];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (t0 + u * 32 < total) src[t0 + u * 32] = tmp[u];
-        }
-        __syncwarp();
-        for (int o = lane; o < BS; o += 32) {
-            const int c = o / bss, j = o - c * bss;
-            // every chain runs unconditionally on valid addresses (inactive
-            // ones read K_0 / child 0 and are discarded): no branches in the
-            // loop, so the 2*MAXCH shared loads of a step issue back to back
-            double sq[MAXCH];
-            int ko[MAXCH], so[MAXCH];
-#pragma unroll
-            for (int q = 0; q < MAXCH; ++q) {
-                sq[q] = 0.0;
-                const bool act = q < nch && sor[warp][q] >= 0;
-                ko[q] = (act ? sor[warp][q] * bb : 0) + j;
-                so[q] = (q < nch ? q * BS : 0) + c * bss;
-            }
-            for (int i = 0; i < bss; ++i) {
-                double kv[MAXCH], xv[MAXCH];
-#pragma unroll
-                for (int q = 0; q < MAXCH; ++q) {
-                    kv[q] = sK[ko[q] + i * bss];
-                    xv[q] = src[so[q] + i];
-                }
-#pragma unroll
-                for (int q = 0; q < MAXCH; ++q) sq[q] = madd_rn(sq[q], kv[q], xv[q]);
-            }
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < MAXCH; ++q)
-                if (q < nch) acc = __dadd_rn(acc, sor[warp][q] < 0 ? src[q * BS + o] : sq[q]);
-            rc[size_t(p) * BS + o] = acc;
-            if (zero_xc) zero_xc[size_t(p) * BS + o] = 0.0;  // the coarse iterate starts at 0
-        }
-        __syncwarp();
-    }
-}
-
-/// Prolongation, one WARP per coarse element with the injection matrices
-/// staged (bulk copy, then transposed in shared memory so lanes = consecutive
-/// fine rows i read consecutive words).  Per parent: children/orthants and
-/// xc_p in two batched round trips, then RU outputs per lane in flight with
-/// their xf read-modify-writes issued together.  Same bits as prolong_kernel.
-__global__ void __launch_bounds__(256) prolong_warp_kernel(const int* __restrict__ child_ptr,
-                                                           const int* __restrict__ child,
-                                                           const int* __restrict__ orth,
-                                                           const double* __restrict__ K,
-                                                           const double* __restrict__ xc, double* __restrict__ xf,
-                                                           int n_coarse, int bss, int ncomp, int nK) {
-    extern __shared__ __align__(16) double sm[];
-    __shared__ int sch[8][8], sor[8][8];
-    __shared__ __align__(8) uint64_t bar;
-    constexpr int RU = 8;
-    const int BS = bss * ncomp, bb = bss * bss;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
-    double* sKt = sm;        // [o][j][i]
-    double* sK = sm + nK;    // bulk-copied K, [o][i][j]
-    double* sx = sm + 2 * size_t(nK) + size_t(warp) * BS;
-    stage_K_bulk(sK, K, nK, &bar);  // immutable: overlaps the previous kernel
-    for (int t = threadIdx.x; t < nK; t += blockDim.x) {
-        const int o = t / bb, r = t - o * bb, i = r / bss, j = r - i * bss;
-        sKt[size_t(o) * bb + size_t(j) * bss + i] = sK[t];
-    }
-    __syncthreads();
-    pdl_launch_dependents();
-    pdl_wait();
-    for (int p = blockIdx.x * W + warp; p < n_coarse; p += gridDim.x * W) {
-        const int q0 = __ldg(child_ptr + p), nch = __ldg(child_ptr + p + 1) - q0;
-        int f = 0;
-        if (lane < nch) f = __ldg(child + q0 + lane);
-        for (int t = lane; t < BS; t += 32) sx[t] = xc[size_t(p) * BS + t];
-        if (lane < nch) {
-            sch[warp][lane] = f;
-            sor[warp][lane] = __ldg(orth + f);
-        }
-        __syncwarp();
-        const int total = nch * BS;
-        for (int t0 = lane; t0 < total; t0 += 32 * RU) {
-            double sv[RU], old[RU];
-            int kb[RU], xb[RU];
-            double* dst[RU];
-#pragma unroll
-            for (int u = 0; u < RU; ++u) {
-                const int t = t0 + u * 32;
-                sv[u] = 0.0;
-                old[u] = 0.0;
-                kb[u] = -2;  // inactive
-                dst[u] = xf;
-                xb[u] = 0;
-                if (t < total) {
-                    const int q = t / BS, ii = t - q * BS;
-                    const int ot = sor[warp][q];
-                    dst[u] = xf + size_t(sch[warp][q]) * BS + ii;
-                    old[u] = *dst[u];
-                    if (ot < 0) {
-                        kb[u] = -1;
-                        xb[u] = ii;
-                    } else {
-                        const int c = ii / bss, i = ii - c * bss;
-                        kb[u] = ot * bb + i;
-                        xb[u] = c * bss;
-                    }
-                }
-            }
-            // branch-free chains (inactive ones read K_0 and are discarded)
-            int kk[RU], xx[RU];
-#pragma unroll
-            for (int u = 0; u < RU; ++u) {
-                kk[u] = kb[u] >= 0 ? kb[u] : 0;
-                xx[u] = kb[u] >= 0 ? xb[u] : 0;
-            }
-            for (int j = 0; j < bss; ++j) {
-                double kv[RU], xv[RU];
-#pragma unroll
-                for (int u = 0; u < RU; ++u) {
-                    kv[u] = sKt[kk[u] + j * bss];
-                    xv[u] = sx[xx[u] + j];
-                }
-#pragma unroll
-                for (int u = 0; u < RU; ++u) sv[u] = madd_rn(sv[u], kv[u], xv[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < RU; ++u) {
-                if (kb[u] == -2) continue;
-                const double add = kb[u] == -1 ? sx[xb[u]] : sv[u];
-                *dst[u] = __dadd_rn(old[u], add);
-            }
-        }
-        __syncwarp();
-    }
-}
-
 /// Bottom pseudoinverse streaming V through shared memory: KC rows of the
 /// row-major Vr (then of Vc) per TMA bulk copy, double buffered; thread i
 /// keeps its sequential k-ascending chain (reference order) for up to 3
@@ -616,30 +367,6 @@ __global__ void __launch_bounds__(1024) pinv_stream_kernel(const double* __restr
             }
         }
         __syncthreads();
-    }
-}
-
-/// Bottom pseudoinverse in one CTA (n <= 4096): b and t in shared memory.
-__global__ void __launch_bounds__(1024) pinv_cta_kernel(const double* __restrict__ Vr, const double* __restrict__ Vc,
-                                                        const double* __restrict__ lam, const double* __restrict__ b,
-                                                        double* __restrict__ x, int n, double cut) {
-    extern __shared__ double sb[];  // b (n) then t (n)
-    double* st = sb + n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = b[i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < n; ++k) s = madd_rn(s, __ldg(Vr + size_t(k) * n + i), sb[k]);
-        const double l = lam[i];
-        st[i] = fabs(l) <= cut ? 0.0 : s / l;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double s = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < n; ++k) s = madd_rn(s, __ldg(Vc + size_t(k) * n + i), st[k]);
-        x[i] = s;
     }
 }
 
@@ -845,39 +572,14 @@ int grid1(int64_t n, int threads, const Ctx& ctx) {
 }  // namespace
 
 namespace {
-int transfer_nK(const Transfer& T) { return (1 << T.dim) * T.bss * T.bss; }
-/// thread-per-entry transfer kernels (default); LDGMG_TRANSFER=warp selects
-/// the warp-per-parent kernels with shared-memory staged K
-/// parents per K-stationary step (LDGMG_TRANSFER_PB = 4, 8 or 16)
-int transfer_pb() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("LDGMG_TRANSFER_PB");
-        v = e ? atoi(e) : 8;
-    }
-    return v;
-}
-bool transfer_flat() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("LDGMG_TRANSFER");
-        v = (e && std::string(e) == "warp") ? 0 : 1;
-    }
-    return v == 1;
-}
+/// parents per K-stationary step of the regular-hierarchy transfer kernels
+constexpr int kTransferPB = 8;
 }  // namespace
 
 void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, double* zero_xc) {
     const int64_t total = int64_t(T.n_coarse) * T.bs;
     if (!total) return;
-    const int nK = transfer_nK(T);
-    const size_t smem_w = sizeof(double) * (size_t(nK) + size_t(8) * 8 * T.bs);
-    const bool warp_ok = T.max_children <= 8 && smem_w <= 200 * 1024;
-    if (zero_xc && !warp_ok) {  // the fallback kernels do not zero
-        LDGMG_CUDA(cudaMemsetAsync(zero_xc, 0, sizeof(double) * size_t(total), ctx.stream));
-        zero_xc = nullptr;
-    }
-    if (transfer_flat() && T.regular) {
+    if (T.regular) {
         bool done = true;
         auto go = [&](auto pbc) {
             constexpr int PB = decltype(pbc)::value;
@@ -895,17 +597,14 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
             else if (T.dim == 2 && T.bss == 9) launch(restrict_ks_kernel<9, 4, PB>, 36);
             else done = false;
         };
-        const int pb = transfer_pb();
-        if (pb == 16) go(std::integral_constant<int, 16>{});
-        else if (pb == 4) go(std::integral_constant<int, 4>{});
-        else go(std::integral_constant<int, 8>{});
+        go(std::integral_constant<int, kTransferPB>{});
         if (done) {
             after_launch("restrict_ks_kernel");
             return;
         }
     }
     const int per = std::max(1, T.max_children) * T.bs;
-    if (transfer_flat() && size_t(per) * 8 <= 48 * 1024) {
+    if (size_t(per) * 8 <= 48 * 1024) {
         const int ppc = std::max(1, 256 / per);
         const int threads = std::min(256, ((ppc * per + 31) / 32) * 32);
         const int grid = std::max(1, std::min(div_up(T.n_coarse, ppc), ctx.num_sms * 32));
@@ -924,17 +623,8 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
         after_launch("restrict_item_kernel");
         return;
     }
-    if (warp_ok) {
-        ensure_dyn_smem(restrict_warp_kernel<8>, size_t(smem_w));
-        const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
-        static bool once = (max_carveout(restrict_warp_kernel<8>), true);
-        (void)once;
-        launch_pdl_small(restrict_warp_kernel<8>, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
-                   T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), rf, rc, T.n_coarse, T.bss, T.ncomp,
-                   nK, zero_xc);
-        after_launch("restrict_warp_kernel");
-        return;
-    }
+    if (zero_xc)  // the fallback kernels below do not zero
+        LDGMG_CUDA(cudaMemsetAsync(zero_xc, 0, sizeof(double) * size_t(total), ctx.stream));
     if (T.max_children <= 64 && size_t(T.max_children) * T.bs * 8 <= 48 * 1024) {
         const int threads = T.bs <= 32 ? 32 : T.bs <= 64 ? 64 : T.bs <= 128 ? 128 : 256;
         restrict_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads,
@@ -953,9 +643,7 @@ void launch_restrict(Ctx& ctx, const Transfer& T, const double* rf, double* rc, 
 void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* xf) {
     const int64_t total = int64_t(T.n_fine) * T.bs;
     if (!total) return;
-    const int nK = transfer_nK(T);
-    const size_t smem_w = sizeof(double) * (size_t(2) * nK + size_t(8) * T.bs);
-    if (transfer_flat() && T.regular) {
+    if (T.regular) {
         bool done = true;
         auto go = [&](auto pbc) {
             constexpr int PB = decltype(pbc)::value;
@@ -973,16 +661,13 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
             else if (T.dim == 2 && T.bss == 9) launch(prolong_ks_kernel<9, 4, PB>, 36);
             else done = false;
         };
-        const int pb = transfer_pb();
-        if (pb == 16) go(std::integral_constant<int, 16>{});
-        else if (pb == 4) go(std::integral_constant<int, 4>{});
-        else go(std::integral_constant<int, 8>{});
+        go(std::integral_constant<int, kTransferPB>{});
         if (done) {
             after_launch("prolong_ks_kernel");
             return;
         }
     }
-    if (transfer_flat()) {
+    {
         const int grid = div_up(total, 256);
         auto launch = [&](auto kern) {
             launch_pdl_small(kern, dim3(grid), dim3(256), 0, ctx.stream, T.parent.as<int>(), T.orth.as<int>(),
@@ -995,38 +680,15 @@ void launch_prolong_add(Ctx& ctx, const Transfer& T, const double* xc, double* x
             default: launch(prolong_flat_kernel<0>); break;
         }
         after_launch("prolong_flat_kernel");
-        return;
     }
-    if (T.max_children <= 8 && smem_w <= 200 * 1024) {
-        ensure_dyn_smem(prolong_warp_kernel, size_t(smem_w));
-        const int grid = std::max(1, std::min(div_up(T.n_coarse, 8), ctx.num_sms * 2));
-        static bool once = (max_carveout(prolong_warp_kernel), true);
-        (void)once;
-        launch_pdl_small(prolong_warp_kernel, dim3(grid), dim3(256), smem_w, ctx.stream, T.child_ptr.as<int>(),
-                   T.child_list.as<int>(), T.orth.as<int>(), T.K.as<double>(), xc, xf, T.n_coarse, T.bss, T.ncomp,
-                   nK);
-        after_launch("prolong_warp_kernel");
-        return;
-    }
-    if (T.bs * 8 <= 48 * 1024) {
-        const int threads = std::min(256, std::max(32, ((T.max_children * T.bs + 31) / 32) * 32));
-        prolong_cta_kernel<<<std::max(1, std::min(T.n_coarse, ctx.num_sms * 16)), threads, size_t(T.bs) * 8,
-                             ctx.stream>>>(T.child_ptr.as<int>(), T.child_list.as<int>(), T.orth.as<int>(),
-                                           T.K.as<double>(), xc, xf, T.n_coarse, T.bss, T.ncomp);
-        after_launch("prolong_cta_kernel");
-        return;
-    }
-    prolong_kernel<<<grid1(total, 256, ctx), 256, 0, ctx.stream>>>(
-        T.parent.as<int>(), T.orth.as<int>(), T.K.as<double>(), xc, xf, T.n_fine, T.bss, T.ncomp);
-    after_launch("prolong_kernel");
 }
 
 void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b, double* x) {
     const int n = E.n;
     if (!n) return;
     const double cut = tol * E.lmax;
-    static const int big = getenv("LDGMG_PINV_BIG") ? atoi(getenv("LDGMG_PINV_BIG")) : 1536;
-    if (n < big && n <= 3072) {
+    constexpr int big = 1536;  // above: one thread per output, batched V loads
+    if (n < big) {
         // KC rows of V per stage, two stages, within ~200 KB of shared memory
         const size_t vec = size_t((n + 1) & ~1) * 2;
         int KC = int(std::min<size_t>(size_t(n), ((200 * 1024 / 8 - vec - 2) / (2 * size_t(n)))));
@@ -1041,10 +703,6 @@ void launch_pinv_apply(Ctx& ctx, const DenseEig& E, double tol, const double* b,
             after_launch("pinv_stream_kernel");
             return;
         }
-        pinv_cta_kernel<<<1, 1024, sizeof(double) * 2 * n, ctx.stream>>>(E.Vr.as<double>(), E.Vc.as<double>(),
-                                                                        E.lambda.as<double>(), b, x, n, cut);
-        after_launch("pinv_cta_kernel");
-        return;
     }
     launch_pdl_small(pinv_t_kernel, dim3(div_up(n, 64)), dim3(64), 0, ctx.stream, E.Vr.as<double>(),
                      E.lambda.as<double>(), b, E.t.as<double>(), n, cut);

@@ -239,11 +239,15 @@ sys.path.insert(0, %r)
 import paper_2412_12506_b200 as g
 from oracle import port
 ctx = g.Context(0)
-for dim, bss, ncomp, seed in [(2, 4, 1, 0), (2, 16, 3, 1), (3, 27, 1, 2), (3, 9, 4, 3), (2, 25, 1, 4)]:
+# big: one parent with 60 / 80 children of 108-entry blocks -- above the
+# per-thread kernel's 48 KB staging, so the per-CTA (<= 64 children) and the
+# plain per-entry fallback kernels run
+for dim, bss, ncomp, seed, big in [(2, 4, 1, 0, 0), (2, 16, 3, 1, 0), (3, 27, 1, 2, 0), (3, 9, 4, 3, 0),
+                                   (2, 25, 1, 4, 0), (3, 27, 4, 5, 60), (3, 27, 4, 6, 80)]:
     rng = np.random.default_rng(seed)
     nc = 37
     cnt = rng.integers(1, 9, nc)
-    cnt[5] = 11  # more children than one chain batch
+    cnt[5] = big or 11  # more children than one chain batch
     parent = np.repeat(np.arange(nc), cnt)
     rng.shuffle(parent)
     parent = parent.astype(np.int32)
@@ -268,18 +272,16 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("family", ["flat", "warp"])
-def test_transfers_irregular_bitwise(family):
+def test_transfers_irregular_bitwise():
     """Restriction / prolongation on irregular parent maps (1..11 children per
-    parent in shuffled fine order, orthant -1 copies, Stokes-like ncomp) are
-    bit-identical to the oracle port (multigrid.hpp:104-149 order) for both
-    kernel families (LDGMG_TRANSFER selects them once per process)."""
+    parent in shuffled fine order, orthant -1 copies, Stokes-like ncomp, and
+    60 / 80 children of 108-entry blocks for the large-shape fallbacks) are
+    bit-identical to the oracle port (multigrid.hpp:104-149 order)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LDGMG_TRANSFER=family)
-    out = subprocess.run([sys.executable, "-c", IRREGULAR_SCRIPT % root], env=env, capture_output=True, text=True,
+    out = subprocess.run([sys.executable, "-c", IRREGULAR_SCRIPT % root], capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
