@@ -163,6 +163,26 @@ int ldgmg_bsr_upload_ex(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int co
                         const int* ptr, const int* col, const double* val, int flags,
                         ldgmg_bsr** out);
 
+/* Values of blocks [first_block, first_block + nblocks) in the reference's
+ * layout (row-major blocks, BlockCsr::val order); a matrix uploaded with
+ * val == NULL starts from zero blocks.  Streams a BlockBuilder::freeze'd
+ * operator (blockla.hpp:113-132) in pieces: the distributed setup fills a
+ * rank's rows from several host slices without concatenating them. */
+int ldgmg_bsr_set_values(ldgmg_ctx* ctx, ldgmg_bsr* A, int64_t first_block, int64_t nblocks,
+                         const double* val);
+/* The first nrows block rows of `base` as a matrix of their own (values
+ * shared, not copied; `base` must outlive the view).  Distributed B: the
+ * forward sweep's rank rows of a matrix that also stores the ghost rows the
+ * transposed sweep needs. */
+int ldgmg_bsr_row_prefix_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int nrows, ldgmg_bsr** out);
+/* A transposed VIEW with its own pattern: block q of the result is block
+ * perm[q] of `base` read transposed (no copy).  spmv_transpose's scatter
+ * order (blockla.hpp:157-176, source rows ascending) is the caller's choice
+ * of (ptr, col, perm).  The distributed B^T: a rank's B^T rows (its columns
+ * of B) read from the B rows it stores. */
+int ldgmg_bsr_transposed_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int brows, int bcols, const int* ptr,
+                              const int* col, const int* perm, ldgmg_bsr** out);
+
 /* replaces spmv(const BlockCsr&, const BlockVec&, BlockVec&)  blockla.hpp:136-154 */
 int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
 /* replaces spmv_transpose(...)                                 blockla.hpp:157-176 */
@@ -172,6 +192,19 @@ int ldgmg_residual(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const do
                    double* r);
 /* y += A x  (the SAI update x += B r, smoothers.hpp:441-446, as one pass) */
 int ldgmg_spmv_add(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
+/* residual / spmv_add restricted to the block rows `rows` (device int32):
+ * the interior / boundary halves of a distributed pass (the interior runs
+ * while the ghost layer is in flight); per-row arithmetic is unchanged */
+int ldgmg_residual_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const double* x, double* r,
+                        const int* rows, int nrows);
+int ldgmg_spmv_add_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y, const int* rows,
+                        int nrows);
+/* Processor-block GS on one rank (smoothers.hpp:426-436 with partitions =
+ * ranks): wavefront schedule of the sequential sweep over the rank's n_own
+ * rows (local CSR; columns >= n_own are frozen ghosts).  rows (n_own) and
+ * level_ptr (nlevels + 1) may be NULL to query nlevels. */
+int ldgmg_pgs_schedule(int n_own, const int* ptr, const int* col, int reverse, int* rows, int* level_ptr,
+                       int* nlevels);
 
 /* Block-diagonal relaxation of every row of a (possibly rank-local,
  * rectangular) operator with caller-held factors: x_out[e] = (1-w) x_live[e]

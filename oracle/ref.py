@@ -367,6 +367,16 @@ def cycles_multi(hierarchies, b, ncycles):
     return sec.value
 
 
+def sym_eig(A):
+    """sym_eig (blockla.hpp:318-326) of a dense symmetric matrix: (lambda
+    ascending, V column-major flattened)."""
+    A = np.asfortranarray(A, np.float64)
+    n = A.shape[0]
+    lam, V = np.empty(n), np.empty(n * n)
+    _chk(lib().ref_sym_eig(n, _p(A.reshape(-1, order="F").copy()), _p(lam), _p(V)))
+    return lam, V
+
+
 def random_rhs(nblocks, bs, seed=0):
     out = np.empty(nblocks * bs)
     _chk(lib().ref_random_rhs(nblocks, bs, seed, _p(out)))

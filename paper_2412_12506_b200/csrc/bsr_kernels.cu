@@ -655,32 +655,125 @@ std::unique_ptr<Bsr> bsr_upload(Ctx& ctx, int brows, int bcols, int rbs, int cbs
     if (A->nnzb) {
         LDGMG_CUDA(cudaMemcpyAsync(A->col.p, col, sizeof(int) * A->nnzb, cudaMemcpyHostToDevice, ctx.stream));
         LDGMG_CUDA(cudaMemsetAsync(A->val.p, 0, A->val.bytes, ctx.stream));
-        // stage through a device buffer in chunks to bound the temporary
-        const int64_t per_blk = int64_t(rbs) * cbs;
-        const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(256) << 20) / (per_blk * 8));
-        DevBuf tmp(sizeof(double) * std::min(A->nnzb, chunk_blocks) * per_blk);
-        for (int64_t k0 = 0; k0 < A->nnzb; k0 += chunk_blocks) {
-            const int64_t nb = std::min(chunk_blocks, A->nnzb - k0);
-            h2d_staged(ctx, tmp.p, val + k0 * per_blk, sizeof(double) * nb * per_blk);
-            upload_permute_kernel<<<grid_for(nb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
-                tmp.as<double>(), A->val.as<double>() + k0 * A->blk_stride, nb, rbs, cbs,
-                A->blk_stride);
-            after_launch("upload_permute_kernel");
-            LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
-        }
+        if (val) bsr_set_values(ctx, *A, 0, A->nnzb, val);  // null: zero blocks, filled later
     }
     LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
     return A;
 }
 
+void bsr_set_values(Ctx& ctx, Bsr& A, int64_t k0, int64_t nb, const double* val) {
+    require(!A.tbase && !A.vbase, "bsr_set_values: a view has no values of its own");
+    require(k0 >= 0 && nb >= 0 && k0 + nb <= A.nnzb, "bsr_set_values: block range out of bounds");
+    if (!nb) return;
+    require(val != nullptr, "bsr_set_values: null values");
+    // stage through a device buffer in chunks to bound the temporary
+    const int64_t per_blk = int64_t(A.rbs) * A.cbs;
+    const int64_t chunk_blocks = std::max<int64_t>(1, (int64_t(256) << 20) / (per_blk * 8));
+    DevBuf tmp(sizeof(double) * std::min(nb, chunk_blocks) * per_blk);
+    for (int64_t q0 = 0; q0 < nb; q0 += chunk_blocks) {
+        const int64_t n = std::min(chunk_blocks, nb - q0);
+        h2d_staged(ctx, tmp.p, val + q0 * per_blk, sizeof(double) * n * per_blk);
+        upload_permute_kernel<<<grid_for(n * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
+            tmp.as<double>(), A.val.as<double>() + (k0 + q0) * A.blk_stride, n, A.rbs, A.cbs, A.blk_stride);
+        after_launch("upload_permute_kernel");
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+}
+
+std::unique_ptr<Bsr> bsr_row_prefix_view(Ctx& ctx, const Bsr& base, int nrows) {
+    require(!base.tbase && !base.vbase, "bsr_row_prefix_view: base is a view");
+    require(nrows >= 0 && nrows <= base.brows, "bsr_row_prefix_view: row count out of range");
+    auto V = std::make_unique<Bsr>();
+    V->brows = nrows;
+    V->bcols = base.bcols;
+    V->rbs = base.rbs;
+    V->cbs = base.cbs;
+    V->blk_stride = base.blk_stride;
+    V->vbase = &base;
+    V->hptr.assign(base.hptr.begin(), base.hptr.begin() + nrows + 1);
+    V->nnzb = V->hptr[nrows];
+    V->hcol.assign(base.hcol.begin(), base.hcol.begin() + V->nnzb);
+    set_max_row(*V);
+    V->ptr.alloc(sizeof(int) * (nrows + 1));
+    V->col.alloc(sizeof(int) * std::max<int64_t>(1, V->nnzb));
+    h2d(ctx, V->ptr.p, V->hptr.data(), sizeof(int) * V->hptr.size());
+    if (V->nnzb) h2d(ctx, V->col.p, V->hcol.data(), sizeof(int) * V->nnzb);
+    return V;
+}
+
+const Bsr& bsr_materialize(Ctx& ctx, const Bsr& view) {
+    if (!view.tbase) return view;  // stored layout already (own or prefix-view values)
+    if (view.mat) return *view.mat;
+    auto M = std::make_unique<Bsr>();
+    M->brows = view.brows;
+    M->bcols = view.bcols;
+    M->rbs = view.rbs;
+    M->cbs = view.cbs;
+    M->nnzb = view.nnzb;
+    M->blk_stride = view.blk_stride;
+    M->hptr = view.hptr;
+    M->hcol = view.hcol;
+    M->max_row = view.max_row;
+    M->ptr.alloc(sizeof(int) * (M->brows + 1));
+    M->col.alloc(sizeof(int) * std::max<int64_t>(1, M->nnzb));
+    M->val.alloc(sizeof(double) * std::max<int64_t>(1, M->nnzb * M->blk_stride));
+    h2d(ctx, M->ptr.p, M->hptr.data(), sizeof(int) * M->hptr.size());
+    if (M->nnzb) {
+        h2d(ctx, M->col.p, M->hcol.data(), sizeof(int) * M->nnzb);
+        LDGMG_CUDA(cudaMemsetAsync(M->val.p, 0, M->val.bytes, ctx.stream));
+        const Bsr& B = *view.tbase;
+        transpose_blocks_kernel<<<grid_for(M->nnzb * int64_t(B.rbs) * B.cbs, 256, ctx), 256, 0, ctx.stream>>>(
+            B.val.as<double>(), M->val.as<double>(), view.tperm.as<int>(), M->nnzb, B.rbs, B.cbs, B.blk_stride);
+        after_launch("transpose_blocks_kernel");
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    const_cast<Bsr&>(view).mat = std::move(M);
+    return *view.mat;
+}
+
+std::unique_ptr<Bsr> bsr_transposed_view(Ctx& ctx, const Bsr& base, int brows, int bcols, const int* ptr,
+                                         const int* col, const int* perm) {
+    require(!base.tbase && !base.vbase, "bsr_transposed_view: base is a view");
+    require(brows >= 0 && bcols >= 0 && ptr && ptr[0] == 0, "bsr_transposed_view: bad shape");
+    auto T = std::make_unique<Bsr>();
+    T->brows = brows;
+    T->bcols = bcols;
+    T->rbs = base.cbs;
+    T->cbs = base.rbs;
+    T->blk_stride = base.blk_stride;
+    T->tbase = &base;
+    T->hptr.assign(ptr, ptr + brows + 1);
+    for (int i = 0; i < brows; ++i) require(T->hptr[i + 1] >= T->hptr[i], "bsr_transposed_view: ptr must be nondecreasing");
+    T->nnzb = T->hptr[brows];
+    T->hcol.assign(col, col + T->nnzb);
+    for (int64_t q = 0; q < T->nnzb; ++q) {
+        require(T->hcol[q] >= 0 && T->hcol[q] < bcols, "bsr_transposed_view: column out of range");
+        require(perm[q] >= 0 && perm[q] < base.nnzb, "bsr_transposed_view: block index out of range");
+    }
+    set_max_row(*T);
+    T->ptr.alloc(sizeof(int) * (brows + 1));
+    T->col.alloc(sizeof(int) * std::max<int64_t>(1, T->nnzb));
+    T->tperm.alloc(sizeof(int) * std::max<int64_t>(1, T->nnzb));
+    h2d(ctx, T->ptr.p, T->hptr.data(), sizeof(int) * T->hptr.size());
+    if (T->nnzb) {
+        h2d(ctx, T->col.p, T->hcol.data(), sizeof(int) * T->nnzb);
+        h2d(ctx, T->tperm.p, perm, sizeof(int) * T->nnzb);
+    }
+    return T;
+}
+
 void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val) {
+    if (A.tbase && val) {
+        bsr_download(ctx, bsr_materialize(ctx, A), ptr, col, val);
+        return;
+    }
     if (ptr) std::memcpy(ptr, A.hptr.data(), sizeof(int) * A.hptr.size());
     if (col) std::memcpy(col, A.hcol.data(), sizeof(int) * A.hcol.size());
     if (val && A.nnzb) {
         const int64_t per_blk = int64_t(A.rbs) * A.cbs;
         DevBuf tmp(sizeof(double) * A.nnzb * per_blk);
         download_permute_kernel<<<grid_for(A.nnzb * per_blk, 256, ctx), 256, 0, ctx.stream>>>(
-            A.val.as<double>(), tmp.as<double>(), A.nnzb, A.rbs, A.cbs, A.blk_stride);
+            bsr_values(A), tmp.as<double>(), A.nnzb, A.rbs, A.cbs, A.blk_stride);
         after_launch("download_permute_kernel");
         LDGMG_CUDA(cudaMemcpyAsync(val, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, ctx.stream));
         LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -863,7 +956,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         // small levels: the split-row kernels read blocks in stored layout
         if (A.rbs <= 32 && A.cbs <= 32 && p.nrows <= split_threshold_rows(ctx)) {
             RowPass q = p;
-            q.A = &bsr_transpose(ctx, *A.tbase);
+            q.A = &bsr_materialize(ctx, A);
             launch_rowpass(ctx, q);
             return;
         }
@@ -872,7 +965,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
         RowPassArgs a{};
         a.ptr = A.ptr.as<int>();
         a.col = A.col.as<int>();
-        a.val = A.val.as<double>();
+        a.val = bsr_values(A);
         a.blk_stride = A.blk_stride;
         a.rbs = A.rbs;
         a.cbs = A.cbs;
@@ -922,7 +1015,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
     RowPassArgs a{};
     a.ptr = A.ptr.as<int>();
     a.col = A.col.as<int>();
-    a.val = A.tbase ? A.tbase->val.as<double>() : A.val.as<double>();
+    a.val = bsr_values(A);
     a.perm = A.tbase ? A.tperm.as<int>() : nullptr;
     a.tview = A.tbase ? 1 : 0;
     a.blk_stride = A.blk_stride;

@@ -338,6 +338,94 @@ int ldgmg_spmv_add(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* 
     });
 }
 
+int ldgmg_bsr_set_values(ldgmg_ctx* ctx, ldgmg_bsr* A, int64_t first_block, int64_t nblocks, const double* val) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_set_values");
+        need(A, "ldgmg_bsr_set_values");
+        bind(*ctx);
+        bsr_set_values(*ctx, *A, first_block, nblocks, val);
+    });
+}
+
+int ldgmg_bsr_row_prefix_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int nrows, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_row_prefix_view");
+        need(base, "ldgmg_bsr_row_prefix_view");
+        need(out, "ldgmg_bsr_row_prefix_view(out)");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(bsr_row_prefix_view(*ctx, *base, nrows)));
+    });
+}
+
+int ldgmg_bsr_transposed_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int brows, int bcols, const int* ptr,
+                              const int* col, const int* perm, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_transposed_view");
+        need(base, "ldgmg_bsr_transposed_view");
+        need(ptr, "ldgmg_bsr_transposed_view(ptr)");
+        need(out, "ldgmg_bsr_transposed_view(out)");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(bsr_transposed_view(*ctx, *base, brows, bcols, ptr, col, perm)));
+    });
+}
+
+int ldgmg_residual_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* b, const double* x, double* r,
+                        const int* rows, int nrows) {
+    return guarded([&] {
+        need(ctx, "residual_rows");
+        need(A, "residual_rows");
+        if (A->rbs != A->cbs) fail(LDGMG_ERR_INVALID_ARGUMENT, "residual: operator must have square blocks");
+        if (nrows < 0 || nrows > A->brows) fail(LDGMG_ERR_INVALID_ARGUMENT, "residual_rows: bad row count");
+        if (nrows == 0) return;
+        need(rows, "residual_rows(rows)");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_RESIDUAL;
+        p.x = x;
+        p.b = b;
+        p.y = r;
+        p.rows = rows;
+        p.nrows = nrows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_spmv_add_rows(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y, const int* rows,
+                        int nrows) {
+    return guarded([&] {
+        need(ctx, "spmv_add_rows");
+        need(A, "spmv_add_rows");
+        if (nrows < 0 || nrows > A->brows) fail(LDGMG_ERR_INVALID_ARGUMENT, "spmv_add_rows: bad row count");
+        if (nrows == 0) return;
+        need(rows, "spmv_add_rows(rows)");
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_ADD;
+        p.x = x;
+        p.xe = y;
+        p.y = y;
+        p.rows = rows;
+        p.nrows = nrows;
+        launch_rowpass(*ctx, p);
+    });
+}
+
+int ldgmg_pgs_schedule(int n_own, const int* ptr, const int* col, int reverse, int* rows, int* level_ptr,
+                       int* nlevels) {
+    return guarded([&] {
+        need(ptr, "pgs_schedule(ptr)");
+        need(nlevels, "pgs_schedule(nlevels)");
+        if (n_own < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "pgs_schedule: negative row count");
+        std::vector<int> part(static_cast<size_t>(n_own), 0);
+        std::vector<int> hp(ptr, ptr + n_own + 1), hc(col, col + (n_own ? ptr[n_own] : 0));
+        std::vector<int> r, lp;
+        pgs_wavefronts(n_own, hp.data(), hc.data(), part.data(), n_own, reverse != 0, r, lp);
+        *nlevels = int(lp.size()) - 1;
+        if (rows) std::copy(r.begin(), r.end(), rows);
+        if (level_ptr) std::copy(lp.begin(), lp.end(), level_ptr);
+    });
+}
+
 struct ldgmg_factors {
     DiagFactors f;
 };

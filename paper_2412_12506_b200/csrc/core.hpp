@@ -103,6 +103,10 @@ struct Bsr {
     // set on a transpose view: values live in tbase->val, block q = tbase block tperm[q]
     const Bsr* tbase = nullptr;
     DevBuf tperm;
+    // set on a row-prefix view: the first `brows` rows of vbase, its values
+    // read in place (ptr/col are copies of vbase's prefix)
+    const Bsr* vbase = nullptr;
+    std::unique_ptr<Bsr> mat;  // lazily built explicit copy of a transposed view (bsr_materialize)
     DevBuf dpos;  // lazily built: CSR position of each row's diagonal block (-1: none)
     int64_t device_bytes() const { return int64_t(ptr.bytes + col.bytes + val.bytes); }
 };
@@ -131,6 +135,22 @@ const Bsr& bsr_transpose_view(Ctx& ctx, const Bsr& A);
 /// reads it conflict-free (LDGMG_TVIEW=0 forces the explicit copy).
 const Bsr& bsr_transpose_for_sweep(Ctx& ctx, const Bsr& A);
 void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val);
+/// Values of blocks [k0, k0 + nb) from the reference layout (row-major blocks).
+void bsr_set_values(Ctx& ctx, Bsr& A, int64_t k0, int64_t nb, const double* val);
+/// The first `nrows` block rows of `base` (values shared, not copied).
+std::unique_ptr<Bsr> bsr_row_prefix_view(Ctx& ctx, const Bsr& base, int nrows);
+/// A general transposed view: block q of the result is block perm[q] of
+/// `base` read transposed; (ptr, col) its own pattern.  The distributed B^T
+/// of a rank (rows = its columns of B, entries from B's own and ghost rows).
+std::unique_ptr<Bsr> bsr_transposed_view(Ctx& ctx, const Bsr& base, int brows, int bcols, const int* ptr,
+                                         const int* col, const int* perm);
+/// Explicit copy of a view (cached on the view): the split-row kernels of
+/// small passes read stored blocks only.
+const Bsr& bsr_materialize(Ctx& ctx, const Bsr& view);
+/// Values pointer the kernels read for A (its own, or the viewed base's).
+inline const double* bsr_values(const Bsr& A) {
+    return A.tbase ? A.tbase->val.as<double>() : A.vbase ? A.vbase->val.as<double>() : A.val.as<double>();
+}
 
 /// Per-element factors of the block-diagonal solve (smoothers.hpp:464-494).
 struct DiagFactors {

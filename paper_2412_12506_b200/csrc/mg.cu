@@ -146,6 +146,46 @@ void compute_factors_host(Ctx& ctx, const Bsr& A, DiagFactors& F) {
     upload_factors(ctx, F, N, bs, V.data(), lam.data(), sc.data());
 }
 
+// ------------------------------------------- processor-block GS schedule
+/// Wavefronts of the sequential processor-block GS sweep (smoothers.hpp:
+/// 426-436): rows 0..n_rows-1 are relaxed in ascending (reverse: descending)
+/// order within their partition, reading in-partition neighbours live and
+/// everything else (other partitions; columns >= n_cols_own, i.e. a rank's
+/// frozen ghosts) from the sweep-start snapshot.  Row e goes one wavefront
+/// after every in-partition neighbour it reads that precedes it
+/// (read-after-write) and after every earlier row that reads it
+/// (write-after-read: that row must see the OLD x_e; implied by the first
+/// rule on symmetric patterns, explicit so any pattern is exact).  Relaxing
+/// one wavefront per launch reproduces the sequential sweep bit for bit.
+void pgs_wavefronts(int n_rows, const int* ptr, const int* col, const int* part_of, int n_cols_own, bool reverse,
+                    std::vector<int>& rows, std::vector<int>& level_ptr) {
+    const int N = n_rows;
+    auto inpart = [&](int e, int j) { return j < n_cols_own && j != e && part_of[j] == part_of[e]; };
+    std::vector<int> lev(N, 0), need(N, 0);
+    int nlev = N ? 1 : 0;
+    for (int i = 0; i < N; ++i) {
+        const int e = reverse ? N - 1 - i : i;
+        int l = need[e];
+        for (int k = ptr[e]; k < ptr[e + 1]; ++k) {
+            const int j = col[k];
+            if (inpart(e, j) && (reverse ? j > e : j < e)) l = std::max(l, lev[j] + 1);
+        }
+        lev[e] = l;
+        nlev = std::max(nlev, l + 1);
+        for (int k = ptr[e]; k < ptr[e + 1]; ++k) {
+            const int j = col[k];
+            if (inpart(e, j) && (reverse ? j < e : j > e)) need[j] = std::max(need[j], l + 1);
+        }
+    }
+    level_ptr.assign(nlev + 1, 0);
+    std::vector<int> cnt(nlev, 0);
+    for (int e = 0; e < N; ++e) ++cnt[lev[e]];
+    for (int l = 0; l < nlev; ++l) level_ptr[l + 1] = level_ptr[l] + cnt[l];
+    rows.resize(N);
+    std::vector<int> fill(level_ptr.begin(), level_ptr.end() - 1);
+    for (int e = 0; e < N; ++e) rows[fill[lev[e]]++] = e;
+}
+
 // --------------------------------------------------------------- smoother
 void Smoother::init_common(Ctx& ctx) {
     N = A->brows;
@@ -184,38 +224,8 @@ void Smoother::init_common(Ctx& ctx) {
         // precede it in the sweep; relaxing the wavefronts of that DAG one
         // launch at a time reproduces the sequential result bit for bit.
         for (int d = 0; d < 2; ++d) {
-            // need[j]: write-after-read edge -- an element e preceding j in
-            // the sweep that reads x_j (A[e][j] != 0) must see the OLD x_j,
-            // so j goes to a later wavefront than e.  Implied by the
-            // read-after-write edge on symmetric patterns, explicit here so
-            // the schedule is exact for any pattern.
-            std::vector<int> lev(N, 0), need(N, 0);
-            int nlev = N ? 1 : 0;
-            for (int i = 0; i < N; ++i) {
-                const int e = d == 0 ? i : N - 1 - i;
-                int l = need[e];
-                for (int k = A->hptr[e]; k < A->hptr[e + 1]; ++k) {
-                    const int j = A->hcol[k];
-                    if (j == e || part_of[j] != part_of[e]) continue;
-                    if (d == 0 ? j < e : j > e) l = std::max(l, lev[j] + 1);
-                }
-                lev[e] = l;
-                nlev = std::max(nlev, l + 1);
-                for (int k = A->hptr[e]; k < A->hptr[e + 1]; ++k) {
-                    const int j = A->hcol[k];
-                    if (j != e && part_of[j] == part_of[e] && (d == 0 ? j > e : j < e))
-                        need[j] = std::max(need[j], l + 1);
-                }
-            }
             std::vector<int> rows;
-            rows.reserve(N);
-            sched_ptr[d].assign(nlev + 1, 0);
-            std::vector<int> cnt(nlev, 0);
-            for (int e = 0; e < N; ++e) ++cnt[lev[e]];
-            for (int l = 0; l < nlev; ++l) sched_ptr[d][l + 1] = sched_ptr[d][l] + cnt[l];
-            rows.resize(N);
-            std::vector<int> fill(sched_ptr[d].begin(), sched_ptr[d].end() - 1);
-            for (int e = 0; e < N; ++e) rows[fill[lev[e]]++] = e;
+            pgs_wavefronts(N, A->hptr.data(), A->hcol.data(), part_of.data(), N, d == 1, rows, sched_ptr[d]);
             sched_rows[d].alloc(sizeof(int) * std::max(1, N));
             if (N) h2d(ctx, sched_rows[d].p, rows.data(), sizeof(int) * N);
         }

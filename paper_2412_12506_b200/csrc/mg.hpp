@@ -9,6 +9,9 @@
 namespace ldgmg_b200 {
 
 std::vector<int> colour_mesh_host(const Bsr& A);
+/// Processor-block GS wavefront schedule (see mg.cu).
+void pgs_wavefronts(int n_rows, const int* ptr, const int* col, const int* part_of, int n_cols_own, bool reverse,
+                    std::vector<int>& rows, std::vector<int>& level_ptr);
 void upload_factors(Ctx& ctx, DiagFactors& F, int N, int bs, const double* V, const double* lambda,
                     const double* s);
 void compute_factors(Ctx& ctx, const Bsr& A, DiagFactors& F);      // GPU (factors.cu) unless LDGMG_HOST_FACTORS=1

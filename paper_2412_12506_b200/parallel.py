@@ -92,6 +92,101 @@ def transpose_csr(ptr, col, val, n_rows, n_cols, bs):
     return tptr, rows[order].astype(np.int32), np.ascontiguousarray(B[order].transpose(0, 2, 1)).reshape(-1)
 
 
+def partition_depth(sizes, transfers, P, min_rows_per_rank):
+    """Number of leading levels partitioned over the ranks: a level is
+    partitioned while it has >= P * min_rows_per_rank elements and no rank
+    boundary splits a sibling group of its restriction (the coarse residual
+    of a parent must be summed by ONE rank in child order, multigrid.hpp:
+    127-149); the rest of the V-cycle is agglomerated.  At least one level."""
+    depth = len(sizes)
+    if depth < 2:
+        return 0
+    ld = 0
+    while ld < depth - 1 and sizes[ld] >= P * min_rows_per_rank:
+        n, parent = sizes[ld], np.asarray(transfers[ld][0])
+        bounds = [q * n // P for q in range(1, P)]
+        if any(0 < bq < n and int(parent[bq - 1]) == int(parent[bq]) for bq in bounds):
+            break
+        ld += 1
+    return max(ld, 1)
+
+
+def split_b_rows(Bg, n, bs, plan: Plan):
+    """The rank's SAI matrix as ONE device matrix serving both sweep
+    directions: rows [0, n_own) are the rank's B rows (the
+    plan's local column numbering, block order unchanged), rows n_own + g are
+    the plan's ghost rows g restricted to the rank's own columns -- exactly
+    the entries B[j][c], c owned, that the rank's B^T rows need.  Returns
+    (ptr, col, own values (a view of Bg), ghost values (gathered copy)) and
+    the transposed view pattern (tptr, tcol, tperm): B^T row c lists the
+    blocks B[j][c] in ascending GLOBAL row order j (spmv_transpose's scatter
+    order, blockla.hpp:163-175), columns = the local ids of j, which are the
+    ghost-slot numbering of the forward plan (B's pattern is symmetric, so
+    B and B^T reach the same ghosts)."""
+    ptr, col, val = (np.asarray(a) for a in Bg)
+    r0, r1, n_own = plan.r0, plan.r1, plan.n_own
+    lptr = (ptr[r0:r1 + 1] - ptr[r0]).astype(np.int64)
+    k0, k1 = int(ptr[r0]), int(ptr[r1])
+    own_val = val[k0 * bs * bs:k1 * bs * bs]
+    gcols, gcnt, gk = [], [], []
+    for g in plan.ghost_gid:
+        ks = np.arange(ptr[g], ptr[g + 1])
+        cs = col[ks]
+        m = (cs >= r0) & (cs < r1)
+        gcols.append(cs[m] - r0)
+        gk.append(ks[m])
+        gcnt.append(int(m.sum()))
+    gk = np.concatenate(gk) if gk else np.zeros(0, np.int64)
+    gcol = np.concatenate(gcols).astype(np.int32) if gcols else np.zeros(0, np.int32)
+    ghost_val = val.reshape(-1, bs * bs)[gk].reshape(-1) if gk.size else np.zeros(0)
+    fptr = np.concatenate([lptr, lptr[-1] + np.cumsum(np.asarray(gcnt, np.int64))]).astype(np.int32)
+    fcol = np.concatenate([plan.local_col.astype(np.int32), gcol])
+    # every stored B[j][c] with c owned must come from an own or ghost row
+    ghost_set = np.zeros(n, bool)
+    ghost_set[plan.ghost_gid] = True
+    ghost_set[r0:r1] = True
+    rows_of = np.repeat(np.arange(n), np.diff(ptr))
+    hit = (col >= r0) & (col < r1)
+    if not np.all(ghost_set[rows_of[hit]]):
+        raise ValueError("distributed B^T: the SAI pattern is not symmetric (a row outside the ghost layer "
+                         "references an owned column)")
+    # transposed view: entries (j, c) of the local matrix with c < n_own
+    nrows_f = n_own + len(plan.ghost_gid)
+    frow = np.repeat(np.arange(nrows_f), np.diff(fptr))
+    gid = np.concatenate([np.arange(r0, r1), plan.ghost_gid]).astype(np.int64)
+    sel = np.nonzero(fcol < n_own)[0]
+    order = np.lexsort((gid[frow[sel]], fcol[sel]))
+    q = sel[order]
+    tptr = np.zeros(n_own + 1, np.int64)
+    np.add.at(tptr, fcol[q] + 1, 1)
+    tptr = np.cumsum(tptr).astype(np.int32)
+    return (fptr, fcol, own_val, ghost_val), (tptr, frow[q].astype(np.int32), q.astype(np.int32))
+
+
+def boundary_rows(ptr, col, n_own):
+    """(interior, boundary) local rows of a rank's operator: boundary rows
+    read a ghost column (>= n_own), interior rows only owned ones."""
+    ptr, col = np.asarray(ptr), np.asarray(col)
+    rows_of = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    bnd = np.zeros(len(ptr) - 1, bool)
+    bnd[rows_of[col >= n_own]] = True
+    return np.nonzero(~bnd)[0].astype(np.int32), np.nonzero(bnd)[0].astype(np.int32)
+
+
+def pgs_schedule(n_own, ptr, col, reverse):
+    """Wavefronts of the rank's processor-block GS sweep (ldgmg_pgs_schedule):
+    a list of local row arrays, one per launch."""
+    p = np.ascontiguousarray(ptr, np.int32)
+    c = np.ascontiguousarray(col, np.int32)
+    nl = C.c_int()
+    check(lib.ldgmg_pgs_schedule(int(n_own), p.ctypes.data, c.ctypes.data, int(reverse), None, None, C.byref(nl)))
+    rows = np.empty(max(n_own, 1), np.int32)
+    lp = np.empty(nl.value + 1, np.int32)
+    check(lib.ldgmg_pgs_schedule(int(n_own), p.ctypes.data, c.ctypes.data, int(reverse), rows.ctypes.data,
+                                 lp.ctypes.data, C.byref(nl)))
+    return [rows[lp[i]:lp[i + 1]] for i in range(nl.value)]
+
+
 class GpuOps:
     """Local compute through the C ABI (the product path)."""
 
@@ -117,6 +212,45 @@ class GpuOps:
         check(lib.ldgmg_bsr_upload_ex(self.ctx.h, int(brows), int(bcols), bs, bs, p.ctypes.data, c.ctypes.data,
                                       v.ctypes.data, 1, C.byref(h)))  # LDGMG_BSR_UNSORTED_COLUMNS
         return _Handle(h, lib.ldgmg_bsr_destroy)
+
+    def matrix_pieces(self, brows, bcols, bs, ptr, col, pieces):
+        """Upload the pattern, then the values piece by piece (no host
+        concatenation): pieces = [(first_block, row-major values), ...]."""
+        h = C.c_void_p()
+        p = np.ascontiguousarray(ptr, np.int32)
+        c = np.ascontiguousarray(col, np.int32)
+        check(lib.ldgmg_bsr_upload_ex(self.ctx.h, int(brows), int(bcols), bs, bs, p.ctypes.data, c.ctypes.data,
+                                      None, 1, C.byref(h)))
+        M = _Handle(h, lib.ldgmg_bsr_destroy)
+        for k0, v in pieces:
+            v = np.ascontiguousarray(v, np.float64)
+            if v.size:
+                check(lib.ldgmg_bsr_set_values(self.ctx.h, M.h, int(k0), int(v.size // (bs * bs)), v.ctypes.data))
+        return M
+
+    def prefix_view(self, M, nrows):
+        h = C.c_void_p()
+        check(lib.ldgmg_bsr_row_prefix_view(self.ctx.h, M.h, int(nrows), C.byref(h)))
+        V = _Handle(h, lib.ldgmg_bsr_destroy)
+        V.base = M  # keep the values alive
+        return V
+
+    def transposed_view(self, M, brows, bcols, ptr, col, perm):
+        h = C.c_void_p()
+        p, c, q = (np.ascontiguousarray(a, np.int32) for a in (ptr, col, perm))
+        check(lib.ldgmg_bsr_transposed_view(self.ctx.h, M.h, int(brows), int(bcols), p.ctypes.data, c.ctypes.data,
+                                            q.ctypes.data, C.byref(h)))
+        V = _Handle(h, lib.ldgmg_bsr_destroy)
+        V.base = M
+        return V
+
+    def residual_rows(self, A, b, x_ext, r, rows):
+        check(lib.ldgmg_residual_rows(self.ctx.h, A.h, b.data_ptr(), x_ext.data_ptr(), r.data_ptr(),
+                                      rows.data_ptr(), int(rows.numel())))
+
+    def spmv_add_rows(self, B, r_ext, x_own, rows):
+        check(lib.ldgmg_spmv_add_rows(self.ctx.h, B.h, r_ext.data_ptr(), x_own.data_ptr(), rows.data_ptr(),
+                                      int(rows.numel())))
 
     def factors(self, n, bs, V, lam, s):
         h = C.c_void_p()
@@ -186,10 +320,13 @@ class Exchanger:
         self.sendbuf = ops.tensor(max(1, len(plan.send_idx)) * bs)
         self.so, self.ro = plan.send_off, plan.recv_off
 
-    def __call__(self, x_ext):
+    def start(self, x_ext):
+        """Pack and post the exchange; returns the pending works (None when
+        this plan has no traffic).  With NCCL the transfers run on NCCL's
+        stream while the caller's stream goes on (the interior rows)."""
         p, bs = self.plan, self.bs
         if p.n_ghost == 0 and len(p.send_idx) == 0:
-            return
+            return None
         self.ops.gather(x_ext, self.idx, len(p.send_idx), bs, self.sendbuf)
         # the op list only depends on the (fixed) buffers: build it once per target
         key = x_ext.data_ptr() if hasattr(x_ext, "data_ptr") else id(x_ext)
@@ -209,9 +346,16 @@ class Exchanger:
             if not hasattr(self, "_reqs"):
                 self._reqs = {}
             self._reqs[key] = reqs
-        if reqs:
-            for w in self.dist.batch_isend_irecv(reqs):
-                w.wait()
+        return self.dist.batch_isend_irecv(reqs) if reqs else None
+
+    @staticmethod
+    def finish(works):
+        """Make the caller's stream (NCCL) / the host (gloo) wait for the ghosts."""
+        for w in works or ():
+            w.wait()
+
+    def __call__(self, x_ext):
+        self.finish(self.start(x_ext))
 
 
 class DistMultigrid:
@@ -224,8 +368,13 @@ class DistMultigrid:
     agglomerated tail, e.g. an api.Multigrid over levels >= ld)."""
 
     def __init__(self, ops, dist, cfg, levels, transfers, K, dim, bss, ncomp, kernel_offsets, coarse_factory,
-                 group=None, min_rows_per_rank=64):
+                 group=None, min_rows_per_rank=64, overlap=True, overlap_min_rows=2048):
+        """overlap: split every pass of a level with >= overlap_min_rows owned
+        rows into interior rows (run while the ghost layer is in flight) and
+        boundary rows (after it landed); per-row arithmetic is unchanged, so
+        the result is bit-identical either way."""
         self.ops, self.dist, self.cfg, self.group = ops, dist, cfg, group
+        kind = cfg.smoother.kind
         self.dim = dim
         self.rank = dist.get_rank(group)
         self.P = dist.get_world_size(group)
@@ -233,10 +382,7 @@ class DistMultigrid:
         self.koffs = list(kernel_offsets)
         self.N0 = levels[0]["n"]
         depth = len(levels)
-        ld = 0
-        while ld < depth - 1 and levels[ld]["n"] >= self.P * min_rows_per_rank:
-            ld += 1
-        self.ld = max(ld, 1) if depth > 1 else 0
+        self.ld = partition_depth([lv["n"] for lv in levels], transfers, self.P, min_rows_per_rank)
         if self.ld == 0:
             raise ValueError("distributed V-cycle needs at least one partitioned level")
         bs = self.bs
@@ -249,16 +395,34 @@ class DistMultigrid:
             d = {"n": n, "plan": pa, "A": ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs, *lrA),
                  "xA": Exchanger(pa, bs, ops, dist, group, self.rank), "nnzA": int(lrA[0][-1])}
             if "B" in lv:
-                Bg = lv["B"]
-                BTg = transpose_csr(*Bg, n, n, bs)
-                for key, M in (("B", Bg), ("BT", BTg)):
-                    pb = partition_level(M[0], M[1], n, self.P, self.rank)
-                    lr = local_rows(*M, bs, bs, pb)
-                    d[key] = ops.matrix(pb.n_own, pb.n_own + pb.n_ghost, bs, *lr)
-                    d["nnz" + key] = int(lr[0][-1])
-                    d["x" + key] = Exchanger(pb, bs, ops, dist, group, self.rank)
-                    d["ng" + key] = pb.n_ghost
-            if "factors" in lv:
+                # one device matrix for both sweep directions: the rank's B
+                # rows (forward, a row-prefix view) and, behind them, the
+                # ghost rows' owned-column blocks the B^T rows read through
+                # a transposed view (no host transpose, no B^T copy)
+                pb = partition_level(lv["B"][0], lv["B"][1], n, self.P, self.rank)
+                (fptr, fcol, own_val, ghost_val), (tptr, tcol, tperm) = split_b_rows(lv["B"], n, bs, pb)
+                nf = pb.n_own + pb.n_ghost
+                nnz_own = int(fptr[pb.n_own])
+                Bfull = ops.matrix_pieces(nf, nf, bs, fptr, fcol, [(0, own_val), (nnz_own, ghost_val)])
+                d["Bfull"] = Bfull
+                d["B"] = ops.prefix_view(Bfull, pb.n_own)
+                d["BT"] = ops.transposed_view(Bfull, pb.n_own, nf, tptr, tcol, tperm)
+                d["nnzB"], d["nnzBT"] = nnz_own, int(tptr[-1])
+                d["xB"] = Exchanger(pb, bs, ops, dist, group, self.rank)
+                d["ngB"] = d["ngBT"] = pb.n_ghost
+                if overlap and pb.n_own >= overlap_min_rows:
+                    d["splitB"] = tuple(ops.itensor(a) for a in boundary_rows(fptr[:pb.n_own + 1], fcol[:nnz_own],
+                                                                                   pb.n_own))
+                    d["splitBT"] = tuple(ops.itensor(a) for a in boundary_rows(tptr, tcol, pb.n_own))
+            if overlap and pa.n_own >= overlap_min_rows:
+                d["splitA"] = tuple(ops.itensor(a) for a in boundary_rows(lrA[0], lrA[1], pa.n_own))
+            if kind == L.PROC_BLOCK_GS:
+                if cfg.smoother.partitions != self.P:
+                    raise ValueError("distributed processor-block GS needs smoother.partitions == ranks "
+                                     "(each rank is one partition, smoothers.hpp:87-94)")
+                d["pgs"] = [[ops.itensor(w) for w in pgs_schedule(pa.n_own, lrA[0], lrA[1], rev)]
+                            for rev in (0, 1)]
+            if "factors" in lv and kind != L.SAI:  # Jacobi, coloured GS, processor-block GS
                 V, lam, s = lv["factors"]
                 a, b = pa.r0, pa.r1
                 d["F"] = ops.factors(pa.n_own, bs, V[a * bs * bs:b * bs * bs], lam[a * bs:b * bs], s[a * bs:b * bs])
@@ -297,18 +461,38 @@ class DistMultigrid:
         self.rc_part = ops.tensor(nct * bs)  # this rank's restriction contribution
 
     # ---------------------------------------------------------------- smoothing
+    def _pass(self, l, key, xkey, x_ext, full, split):
+        """One operator application after its ghost exchange: with a split,
+        the interior rows run while the ghosts are in flight."""
+        d = self.L[l]
+        if split is None:
+            d[xkey](x_ext)
+            full()
+            return
+        works = d[xkey].start(x_ext)
+        split(d[key][0])
+        Exchanger.finish(works)
+        split(d[key][1])
+
+    def residual(self, l, b, x_ext, r):
+        d = self.L[l]
+        sp = d.get("splitA")
+        self._pass(l, "splitA", "xA", x_ext, lambda: self.ops.residual(d["A"], b, x_ext, r),
+                   sp and (lambda rows: self.ops.residual_rows(d["A"], b, x_ext, r, rows)))
+
     def smooth(self, l, b, sweep):
         d, bs = self.L[l], self.bs
         n_own = d["plan"].n_own
         x_ext = d["x"]
         kind = self.cfg.smoother.kind
         if kind == L.SAI:
-            d["xA"](x_ext)
             rext = d["rext"]
-            self.ops.residual(d["A"], b, x_ext, rext[:n_own * bs])
+            self.residual(l, b, x_ext, rext[:n_own * bs])
             key = "B" if sweep == L.SWEEP_FORWARD else "BT"
-            d["x" + key](rext)
-            self.ops.spmv_add(d[key], rext, x_ext[:n_own * bs])
+            M, x_own = d[key], x_ext[:n_own * bs]
+            sp = d.get("split" + key)
+            self._pass(l, "split" + key, "xB", rext, lambda: self.ops.spmv_add(M, rext, x_own),
+                       sp and (lambda rows: self.ops.spmv_add_rows(M, rext, x_own, rows)))
         elif kind == L.JACOBI:
             d["xA"](x_ext)
             snap = d["snap"]
@@ -324,8 +508,19 @@ class DistMultigrid:
                 if crows[c].numel():
                     self.ops.relax_rows(d["A"], d["F"], b, x_ext, x_ext[:n_own * bs], x_ext[:n_own * bs], 1.0,
                                         crows[c])
+        elif kind == L.PROC_BLOCK_GS:
+            # each rank is one partition (smoothers.hpp:426-436): its ghosts
+            # are exchanged once and stay frozen for the sweep (= the
+            # reference's sweep-start snapshot of the other partitions); its
+            # own rows are relaxed in sequential order, one wavefront of the
+            # dependency DAG per launch, in-partition neighbours read live
+            d["xA"](x_ext)
+            own = x_ext[:n_own * bs]
+            for rows in d["pgs"][0 if sweep == L.SWEEP_FORWARD else 1]:
+                self.ops.relax_rows(d["A"], d["F"], b, x_ext, own, own, self.cfg.smoother.omega, rows)
         else:
-            raise ValueError("distributed V-cycle supports the Jacobi, coloured GS and SAI smoothers")
+            raise ValueError("distributed V-cycle supports the Jacobi, coloured GS, processor-block GS and SAI "
+                             "smoothers")
 
     # ---------------------------------------------------------------- V-cycle
     def _vcycle(self, l, b):
@@ -335,8 +530,7 @@ class DistMultigrid:
         x_ext = d["x"]
         for _ in range(self.cfg.nu1):
             self.smooth(l, b, self.cfg.pre)
-        d["xA"](x_ext)
-        self.ops.residual(d["A"], b, x_ext, d["r"])
+        self.residual(l, b, x_ext, d["r"])
         if l + 1 < self.ld:
             nxt = self.L[l + 1]
             self.ops.restrict(d["T"], d["r"], nxt["b"])
@@ -594,8 +788,13 @@ def sai_halo_hops(spec, smoother) -> int:
     one operator hop, so that the rank sees its neighbours' rows that
     reference it (the ghost send lists are derived from them).  One operator
     hop is one face layer, two for the stress-form Stokes operator (its
-    G_j^T G_i cross terms couple diagonal neighbours)."""
-    r_a = 2 if (spec.kind == L.SYSTEM_STOKES and spec.gamma != 0.0) else 1
+    G_j^T G_i cross terms couple diagonal neighbours) and for any problem with
+    a phase interface: the u-hat donor of an interface face is the more
+    viscous side (ldg_core.hpp:122-127), so G_k^T D G_k couples elements two
+    face layers apart there."""
+    two = (spec.kind == L.SYSTEM_STOKES and spec.gamma != 0.0) or \
+        (spec.phase_shape != L.PHASE_SINGLE and spec.mu_in != spec.mu_out)
+    r_a = 2 if two else 1
     if smoother.kind != L.SAI:
         return r_a
     return (2 * smoother.level + 1) * r_a
@@ -685,10 +884,8 @@ def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_f
     factors (`factors_fn(diag_blocks) -> (V, lam, s)` of the rank's rows)."""
     depth = prob.depth
     shapes = [prob.level_shape(l) for l in range(depth)]
-    ld = 0
-    while ld < depth - 1 and shapes[ld][0] >= nranks * min_rows_per_rank:
-        ld += 1
-    ld = max(ld, 1)
+    ld = partition_depth([sh[0] for sh in shapes], [prob.level_transfer(l) for l in range(depth - 1)], nranks,
+                         min_rows_per_rank)
     levels, transfers = [], []
     for l in range(depth):
         n, bs, _ = shapes[l]
@@ -714,7 +911,7 @@ def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_f
     return levels, transfers
 
 
-def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64):
+def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64, any_n=None, overlap=True):
     """Distributed hierarchy with DISTRIBUTED setup: each rank assembles only
     its rows plus the SAI halo (Problem.partial), solves only the SAI columns
     its rows need (column-masked GPU build), and computes the diagonal
@@ -723,8 +920,10 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64)
     from_problem (tests/test_distributed_setup.py)."""
     from .api import DeviceBsr, Multigrid, MultigridConfig, Problem, Smoother, SmootherConfig, Transfer, sai_build
     rank, P = dist.get_rank(group), dist.get_world_size(group)
+    if any_n is None:  # extension A1 for non-power-of-two meshes (C5 at 48^3)
+        any_n = spec.n & (spec.n - 1) != 0
     prob = Problem.partial(spec, P, rank, sai_halo_hops(spec, cfg.smoother), min_rows_per_rank,
-                           min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
+                           min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements, any_n=any_n)
     depth = prob.depth
     kind = L.SYSTEM_STOKES if prob.n_comp > 1 else L.SYSTEM_SCALAR
 
@@ -765,7 +964,7 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64)
     if prob.kernel_pressure:
         offs.append(prob.dim * prob.bs_scalar)
     dm = DistMultigrid(GpuOps(ctx), dist, cfg, levels, transfers, K, prob.dim, prob.bs_scalar, prob.n_comp, offs,
-                       coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank)
+                       coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank, overlap=overlap)
     dm._problem = prob
     return dm
 

@@ -1,6 +1,7 @@
-"""Profiling target: build a workload (bench C2 by default, or any
-tools/configs_bench.py config), warm up, then run `--cycles` V-cycles between
-cudaProfilerStart/Stop (use ncu --profile-from-start off)."""
+"""Profiling target: build a bench workload (C5 at 48^3 by default, `--n` for
+another size, `--workload C2`), warm up, then run either `--cycles` V-cycles
+or (`--pair`) the level-0 SAI sweep pair between cudaProfilerStart/Stop, so
+`ncu --profile-from-start off` sees exactly that region."""
 import argparse
 import os
 import sys
@@ -12,31 +13,35 @@ import bench  # noqa: E402
 import paper_2412_12506_b200 as g  # noqa: E402
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="C5")
+ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--cycles", type=int, default=2)
-ap.add_argument("--graph", type=int, default=0)
-ap.add_argument("--config", default="")
+ap.add_argument("--graph", type=int, default=1)
+ap.add_argument("--pair", action="store_true", help="profile one level-0 SAI sweep (residual + B r) only")
 a = ap.parse_args()
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx = g.Context(0, stream=stream)
-if a.config:
-    from tools import configs_bench as cb
-    spec, cfg, _ = cb.configs(16)[a.config]
-else:
-    spec, cfg = bench.workload()
-P = g.Problem(spec, min_depth=cfg.min_depth)
+spec, cfg, _ = bench.product_workload(a.workload, a.n)
+pow2 = spec.n & (spec.n - 1) == 0
+P = g.Problem(spec, min_depth=cfg.min_depth, device_assembly=True, any_n=not pow2)
 mg = g.Multigrid(ctx, cfg, P)
-b = torch.as_tensor(bench.rhs(mg.n, mg.bs)).cuda()
+offs = bench.kernel_offsets(spec.kind, P.dim, P.bs_scalar, P.kernel_constants, P.kernel_pressure)
+b = torch.as_tensor(bench.remove_kernel(g.random_rhs(mg.n, mg.bs, 0), mg.n, mg.bs, offs)).cuda()
 x = torch.zeros_like(b)
-for _ in range(3):
-    mg.cycle(x, b)
+mg.cycles(x, b, 3)
+S0 = mg.smoother(0)
+S0.apply(b, x, g.SWEEP_FORWARD)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-for _ in range(a.cycles):
-    if a.graph:
-        mg.cycles(x, b, 1)
-    else:
-        mg.cycle(x, b)
+if a.pair:
+    S0.apply(b, x, g.SWEEP_FORWARD)
+else:
+    for _ in range(a.cycles):
+        if a.graph:
+            mg.cycles(x, b, 1)
+        else:
+            mg.cycle(x, b)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("profiled", a.cycles, "cycles")
+print("profiled", "pair" if a.pair else f"{a.cycles} cycles", flush=True)
