@@ -263,36 +263,31 @@ def run_reference(args):
 
 def run_partitioned(args, ctx, stream, ws, rank, local):
     """N > 1: the mesh-partitioned V-cycle (paper_2412_12506_b200.parallel) on
-    the C2 stencil at 64^3 (262,144 elements = 8x C2), strong scaling over the
-    ranks: contiguous Morton ranges, NCCL ghost-layer exchange before every
-    operator application, agglomerated coarse levels, P-independent kernel
-    projection.  Time = max over ranks of the device time of K cycles."""
+    the headline workload (C5 at 48^3 by default), strong scaling over the
+    ranks: contiguous (restricted-)Morton ranges, one ghost-layer exchange
+    per operator application over NCCL overlapped with the interior rows,
+    B^T read through a per-rank transposed view, agglomerated coarse levels,
+    P-independent kernel projection, distributed setup (each rank assembles
+    its rows + SAI halo and solves its SAI columns).  Time = max over ranks
+    of the device time of K cycles."""
     import torch
     import torch.distributed as dist
     import paper_2412_12506_b200 as g
     from paper_2412_12506_b200 import parallel
 
-    spec, cfg = workload()
-    spec.n = 64
+    spec, cfg, label = product_workload(args.workload, args.n)
     t0 = time.time()
-    if args.replicated_setup:
-        P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements)
-        t_asm = time.time() - t0
-        t0 = time.time()
-        dm = parallel.from_problem(ctx, P, cfg, dist, min_rows_per_rank=512)
-    else:
-        # distributed setup: this rank's rows + SAI halo only (host assembly and
-        # GPU SAI build both ~1/P of the replicated cost)
-        t_asm = 0.0
-        dm = parallel.from_problem_partial(ctx, spec, cfg, dist, min_rows_per_rank=512)
-        P = dm._problem
+    dm = parallel.from_problem_partial(ctx, spec, cfg, dist, min_rows_per_rank=args.min_rows,
+                                       overlap=not args.no_overlap)
+    P = dm._problem
     torch.cuda.synchronize()
-    t_mg = time.time() - t0
+    t_setup = time.time() - t0
     cc = torch.tensor(dm.cycle_costs(), device="cuda", dtype=torch.float64)
     dist.all_reduce(cc)
     dof_cycle, bytes_cycle = float(cc[0]), float(cc[1])
     n, bs = P.level_shape(0)[:2]
-    b_host = rhs(n, bs)
+    offs = kernel_offsets(spec.kind, P.dim, P.bs_scalar, P.kernel_constants, P.kernel_pressure)
+    b_host = remove_kernel(g.random_rhs(n, bs, 0), n, bs, offs)
     r0, r1 = dm.owned_range()
     b_own = torch.as_tensor(b_host[r0 * bs:r1 * bs].copy()).cuda()
     x_own = torch.zeros_like(b_own)
@@ -322,22 +317,24 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = float(tt.item())
     value = dof_cycle * args.steps / t
-    # end to end: per step H2D of the owned b slice from pinned memory, one
-    # cycle, D2H of the owned x slice; wall time, max over ranks
+    # end to end: per step the pinned H2D of the owned b slice, e2e_cycles
+    # cycles, the D2H of the owned x slice; wall time, max over ranks
     b_pin = torch.as_tensor(b_host[r0 * bs:r1 * bs].copy()).pin_memory()
     x_pin = torch.empty_like(b_pin).pin_memory()
     dist.barrier()
+    ne = 2
     te0 = time.perf_counter()
-    for _ in range(max(3, args.steps // 5)):
+    for _ in range(ne):
         b_own.copy_(b_pin, non_blocking=True)
-        dm.cycle(x_own, b_own, fast=True)
+        x_own.zero_()
+        for _ in range(args.e2e_cycles):
+            dm.cycle(x_own, b_own, fast=True)
         x_pin.copy_(x_own, non_blocking=True)
         torch.cuda.synchronize()
     te = time.perf_counter() - te0
-    ne = max(3, args.steps // 5)
     te_t = torch.tensor([te], device="cuda", dtype=torch.float64)
     dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
-    e2e_value = dof_cycle * ne / float(te_t.item())
+    e2e_value = dof_cycle * ne * args.e2e_cycles / float(te_t.item())
     # roofline: this rank's level-0 SAI sweep pair (residual + B r row passes on
     # its rows, no exchange) timed alone with CUDA events; max time over ranks
     roof = None
@@ -354,7 +351,7 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
             pair()
         torch.cuda.synchronize()
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 20
+        reps = 10
         k0.record(stream)
         for _ in range(reps):
             pair()
@@ -370,29 +367,29 @@ def run_partitioned(args, ctx, stream, ws, rank, local):
                 "traffic": None, "alg_bytes_per_launch_pair": alg, "ms": tk * 1e3,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy), per GPU; time = max over ranks",
                 "peak_theoretical": 8000.0, "frac_theoretical": alg / tk / 1e9 / 8000.0}
+    ghosts = torch.tensor([float(d0["plan"].n_ghost)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(ghosts)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 stencil at 64^3 (N=262144, 27x27 FP64 blocks, SAI1, nu=3+3), mesh-partitioned "
-                                   "over the ranks (contiguous Morton ranges, NCCL ghost exchange, agglomerated "
-                                   "coarse levels)",
-                       "fine_dof": n * bs, "dof_updates_per_cycle": dof_cycle, "alg_bytes_per_cycle": bytes_cycle,
-                       "parallelism": f"mesh-partitioned x{ws}", "owned_elements_rank0": r1 - r0,
-                       "partitioned_levels": dm.ld, "cuda_graph": bool(use_graph),
+            "config": {"workload": label + ", mesh-partitioned over the ranks",
+                       "fine_elements": n, "fine_dof": n * bs, "dof_updates_per_cycle": dof_cycle,
+                       "alg_bytes_per_cycle": bytes_cycle, "parallelism": f"mesh-partitioned x{ws}",
+                       "owned_elements_rank0": r1 - r0, "partitioned_levels": dm.ld,
+                       "level0_ghost_elements_all_ranks": float(ghosts.item()),
+                       "overlap": not args.no_overlap, "cuda_graph": bool(use_graph),
                        "graph_note": getattr(dm, "_graph_error", None) or "validated bitwise vs the eager cycle",
                        "projection": "fast (device, 256 fixed ranges, P-independent)",
                        "l2": "no flush: per-rank working set >> 126 MB L2",
-                       "setup_s": {"assembly": round(t_asm, 2), "hierarchy_gpu": round(t_mg, 2),
-                                   "distributed": not args.replicated_setup,
-                                   "note": ("replicated per rank" if args.replicated_setup else
-                                            "each rank assembles its rows + SAI halo and solves its SAI columns")}},
+                       "setup_s": round(t_setup, 2)},
             "vcycle_hbm_GBps_total": bytes_cycle * args.steps / t / 1e9,
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * (r1 - r0) * bs),
                     "d2h_bytes_per_step": int(8 * (r1 - r0) * bs),
-                    "step": "pinned H2D of the owned b slice + one partitioned V-cycle + D2H of the owned x slice"},
+                    "step": f"pinned H2D of the owned b slice + {args.e2e_cycles} partitioned V-cycles + D2H of the "
+                            f"owned x slice (per rank)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }), flush=True)
@@ -519,8 +516,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partitioned", action="store_true", help="force the mesh-partitioned path at N=1 (testing)")
     ap.add_argument("--no-graph", action="store_true", help="N>1: eager distributed cycles (no CUDA graph)")
-    ap.add_argument("--replicated-setup", action="store_true",
-                    help="N>1: build the whole hierarchy on every rank (default: distributed setup)")
+    ap.add_argument("--no-overlap", action="store_true", help="N>1: no interior/boundary split of the passes")
+    ap.add_argument("--min-rows", type=int, default=128, help="N>1: partition levels with >= this many rows per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -163,6 +163,17 @@ int ldgmg_bsr_upload_ex(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int co
                         const int* ptr, const int* col, const double* val, int flags,
                         ldgmg_bsr** out);
 
+/* Batched FP64 GEMM on the tensor cores (mma.sync m8n8k4 DMMA), the kernel
+ * behind the SAI setup's least-squares solves (dense_lstsq blockla.hpp:
+ * 278-309 -> dgels; its compact-WY trailing updates):
+ *   D[b](m, n) = alpha * sum_k A[b](m, k) * B[b](n, k) + beta * D[b](m, n)
+ * A(m, k) at A + b*strideA + m*lda + k, B(n, k) at B + b*strideB + n*ldb + k
+ * (k contiguous in both), D(m, n) at D + b*strideD + m + n*ldd (column-major);
+ * device pointers, batch <= 65535. */
+int ldgmg_dgemm_nt_batched(ldgmg_ctx* ctx, int M, int N, int K, double alpha, const double* A, int64_t lda,
+                           int64_t strideA, const double* B, int64_t ldb, int64_t strideB, double beta, double* D,
+                           int64_t ldd, int64_t strideD, int batch);
+
 /* Values of blocks [first_block, first_block + nblocks) in the reference's
  * layout (row-major blocks, BlockCsr::val order); a matrix uploaded with
  * val == NULL starts from zero blocks.  Streams a BlockBuilder::freeze'd
@@ -170,6 +181,12 @@ int ldgmg_bsr_upload_ex(ldgmg_ctx* ctx, int brows, int bcols, int row_bs, int co
  * rank's rows from several host slices without concatenating them. */
 int ldgmg_bsr_set_values(ldgmg_ctx* ctx, ldgmg_bsr* A, int64_t first_block, int64_t nblocks,
                          const double* val);
+/* A new matrix with pattern (ptr, col) whose block q is a device-side copy
+ * of src's block src_blocks[q] (host int64 array, nnzb entries): a rank's
+ * rows of a device-assembled operator with its local column numbering,
+ * cut without moving the values through the host. */
+int ldgmg_bsr_gather(ldgmg_ctx* ctx, const ldgmg_bsr* src, int brows, int bcols, const int* ptr, const int* col,
+                     const int64_t* src_blocks, ldgmg_bsr** out);
 /* The first nrows block rows of `base` as a matrix of their own (values
  * shared, not copied; `base` must outlive the view).  Distributed B: the
  * forward sweep's rank rows of a matrix that also stores the ghost rows the

@@ -139,7 +139,9 @@ _SIGS = {
     "ldgmg_bsr_upload_ex": ([_P, _I, _I, _I, _I, _P, _P, _P, _I, C.POINTER(_P)], _I),
     "ldgmg_spmv_add": ([_P, _P, _P, _P], _I),
     "ldgmg_bsr_set_values": ([_P, _P, _I64, _I64, _P], _I),
+    "ldgmg_dgemm_nt_batched": ([_P, _I, _I, _I, _D, _P, _I64, _I64, _P, _I64, _I64, _D, _P, _I64, _I64, _I], _I),
     "ldgmg_bsr_row_prefix_view": ([_P, _P, _I, C.POINTER(_P)], _I),
+    "ldgmg_bsr_gather": ([_P, _P, _I, _I, _P, _P, _P, C.POINTER(_P)], _I),
     "ldgmg_bsr_transposed_view": ([_P, _P, _I, _I, _P, _P, _P, C.POINTER(_P)], _I),
     "ldgmg_residual_rows": ([_P, _P, _P, _P, _P, _P, _I], _I),
     "ldgmg_spmv_add_rows": ([_P, _P, _P, _P, _P, _I], _I),

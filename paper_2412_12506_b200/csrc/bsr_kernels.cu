@@ -521,6 +521,17 @@ __global__ void transpose_blocks_kernel(const double* __restrict__ src, double* 
     }
 }
 
+/// dst block q = src block idx[q] (stored layout, same stride), 16-byte words.
+__global__ void gather_blocks_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                                     const int64_t* __restrict__ idx, int64_t nnzb, int words) {
+    const int64_t total = nnzb * words;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = t / words;
+        const int w = int(t - q * words);
+        dst[t] = src[idx[q] * words + w];
+    }
+}
+
 int grid_for(int64_t n, int threads, const Ctx& ctx) {
     return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, ctx.num_sms * 16)));
 }
@@ -678,6 +689,43 @@ void bsr_set_values(Ctx& ctx, Bsr& A, int64_t k0, int64_t nb, const double* val)
         after_launch("upload_permute_kernel");
         LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
     }
+}
+
+std::unique_ptr<Bsr> bsr_gather(Ctx& ctx, const Bsr& src, int brows, int bcols, const int* ptr, const int* col,
+                                const int64_t* src_blocks) {
+    require(!src.tbase && !src.vbase, "bsr_gather: source is a view");
+    require(brows >= 0 && bcols >= 0 && ptr && ptr[0] == 0, "bsr_gather: bad shape");
+    auto A = std::make_unique<Bsr>();
+    A->brows = brows;
+    A->bcols = bcols;
+    A->rbs = src.rbs;
+    A->cbs = src.cbs;
+    A->blk_stride = src.blk_stride;
+    A->hptr.assign(ptr, ptr + brows + 1);
+    for (int i = 0; i < brows; ++i) require(A->hptr[i + 1] >= A->hptr[i], "bsr_gather: ptr must be nondecreasing");
+    A->nnzb = A->hptr[brows];
+    A->hcol.assign(col, col + A->nnzb);
+    for (int64_t q = 0; q < A->nnzb; ++q) {
+        require(A->hcol[q] >= 0 && A->hcol[q] < bcols, "bsr_gather: column out of range");
+        require(src_blocks[q] >= 0 && src_blocks[q] < src.nnzb, "bsr_gather: source block out of range");
+    }
+    set_max_row(*A);
+    A->ptr.alloc(sizeof(int) * (brows + 1));
+    A->col.alloc(sizeof(int) * std::max<int64_t>(1, A->nnzb));
+    A->val.alloc(sizeof(double) * std::max<int64_t>(1, A->nnzb * A->blk_stride));
+    h2d(ctx, A->ptr.p, A->hptr.data(), sizeof(int) * A->hptr.size());
+    if (A->nnzb) {
+        h2d(ctx, A->col.p, A->hcol.data(), sizeof(int) * A->nnzb);
+        DevBuf d_idx(sizeof(int64_t) * A->nnzb);
+        h2d(ctx, d_idx.p, src_blocks, d_idx.bytes);
+        const int words = A->blk_stride / 2;  // blk_stride is even: 16-byte words
+        gather_blocks_kernel<<<grid_for(A->nnzb * words, 256, ctx), 256, 0, ctx.stream>>>(
+            reinterpret_cast<const double2*>(src.val.p), reinterpret_cast<double2*>(A->val.p), d_idx.as<int64_t>(),
+            A->nnzb, words);
+        after_launch("gather_blocks_kernel");
+        LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    return A;
 }
 
 std::unique_ptr<Bsr> bsr_row_prefix_view(Ctx& ctx, const Bsr& base, int nrows) {

@@ -14,6 +14,7 @@
 #include "core.hpp"
 #include "formats.hpp"
 #include "mg.hpp"
+#include "dgemm.hpp"
 #include "host_eig.hpp"
 #include "krylov.hpp"
 #include "setup.hpp"
@@ -122,7 +123,6 @@ int ldgmg_ctx_destroy(ldgmg_ctx* ctx) {
         cudaFree(ctx->d_red);
         cudaFreeHost(ctx->h_red);
         ctx_release_staging(*ctx);
-        ctx_release_blas(*ctx);
         delete ctx;
     });
 }
@@ -338,12 +338,37 @@ int ldgmg_spmv_add(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* 
     });
 }
 
+int ldgmg_dgemm_nt_batched(ldgmg_ctx* ctx, int M, int N, int K, double alpha, const double* A, int64_t lda,
+                           int64_t strideA, const double* B, int64_t ldb, int64_t strideB, double beta, double* D,
+                           int64_t ldd, int64_t strideD, int batch) {
+    return guarded([&] {
+        need(ctx, "dgemm_nt_batched");
+        if (M < 0 || N < 0 || K < 0 || batch < 0) fail(LDGMG_ERR_INVALID_ARGUMENT, "dgemm_nt_batched: negative size");
+        if ((K > 0 && (lda < K || ldb < K)) || ldd < M)
+            fail(LDGMG_ERR_INVALID_ARGUMENT, "dgemm_nt_batched: leading dimension too small");
+        bind(*ctx);
+        dgemm_nt_batched(*ctx, GemmNT{A, lda, strideA, B, ldb, strideB, D, ldd, strideD, M, N, K, alpha, beta}, batch);
+    });
+}
+
 int ldgmg_bsr_set_values(ldgmg_ctx* ctx, ldgmg_bsr* A, int64_t first_block, int64_t nblocks, const double* val) {
     return guarded([&] {
         need(ctx, "ldgmg_bsr_set_values");
         need(A, "ldgmg_bsr_set_values");
         bind(*ctx);
         bsr_set_values(*ctx, *A, first_block, nblocks, val);
+    });
+}
+
+int ldgmg_bsr_gather(ldgmg_ctx* ctx, const ldgmg_bsr* src, int brows, int bcols, const int* ptr, const int* col,
+                     const int64_t* src_blocks, ldgmg_bsr** out) {
+    return guarded([&] {
+        need(ctx, "ldgmg_bsr_gather");
+        need(src, "ldgmg_bsr_gather");
+        need(ptr, "ldgmg_bsr_gather(ptr)");
+        need(out, "ldgmg_bsr_gather(out)");
+        bind(*ctx);
+        *out = static_cast<ldgmg_bsr*>(own_bsr(bsr_gather(*ctx, *src, brows, bcols, ptr, col, src_blocks)));
     });
 }
 

@@ -31,7 +31,6 @@ struct Ctx {
     unsigned char* pin[2] = {nullptr, nullptr};
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     size_t pin_bytes = 0;
-    void* blas = nullptr;  // cuBLAS handle (SAI setup GEMMs), created on first use
 };
 
 /// Large pageable host -> device copy: threaded memcpy into a pinned double
@@ -40,7 +39,6 @@ struct Ctx {
 /// Returns after the copy completed.
 void h2d_staged(Ctx& ctx, void* dst, const void* src, size_t bytes);
 void ctx_release_staging(Ctx& ctx);
-void ctx_release_blas(Ctx& ctx);
 
 struct LevelProgram;  // setup.hpp
 /// Evaluate a deferred-assembly program on the device (assembly_gpu.cu).
@@ -137,6 +135,11 @@ const Bsr& bsr_transpose_for_sweep(Ctx& ctx, const Bsr& A);
 void bsr_download(Ctx& ctx, const Bsr& A, int* ptr, int* col, double* val);
 /// Values of blocks [k0, k0 + nb) from the reference layout (row-major blocks).
 void bsr_set_values(Ctx& ctx, Bsr& A, int64_t k0, int64_t nb, const double* val);
+/// A new matrix with pattern (ptr, col) whose block q is a device copy of
+/// src block src_blocks[q] (rank-local operators cut from a device-assembled
+/// global-shaped one, without a host round trip of the values).
+std::unique_ptr<Bsr> bsr_gather(Ctx& ctx, const Bsr& src, int brows, int bcols, const int* ptr, const int* col,
+                                const int64_t* src_blocks);
 /// The first `nrows` block rows of `base` (values shared, not copied).
 std::unique_ptr<Bsr> bsr_row_prefix_view(Ctx& ctx, const Bsr& base, int nrows);
 /// A general transposed view: block q of the result is block perm[q] of

@@ -321,6 +321,34 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_rea
     }
 }
 
+void Smoother::apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready) const {
+    if (cfg.kind != LDGMG_JACOBI || nu < 1) {
+        for (int i = 0; i < nu; ++i) apply(ctx, b, x, sweep, r_ready && i == 0);
+        return;
+    }
+    // Jacobi: ping-pong between x and the snapshot buffer instead of copying
+    // x before every sweep -- the relax pass reads every input (neighbours
+    // and x_e) from `src` and writes `dst`, exactly the reference's sweep
+    // from a snapshot (smoothers.hpp:411-416), so the bits are unchanged; an
+    // odd count ends with one copy back.
+    double* bufs[2] = {x, snap.as<double>()};
+    for (int i = 0; i < nu; ++i) {
+        RowPass p;
+        p.A = A;
+        p.mode = MODE_RELAX;
+        p.x = bufs[i & 1];
+        p.b = b;
+        p.xe = bufs[i & 1];
+        p.y = bufs[(i + 1) & 1];
+        p.nrows = N;
+        p.F = &F;
+        p.omega = cfg.omega;
+        launch_rowpass(ctx, p);
+    }
+    if (nu & 1)
+        LDGMG_CUDA(cudaMemcpyAsync(x, snap.p, sizeof(double) * size_t(N) * bs, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
 double Smoother::bytes_per_apply() const {
     const double W = 8.0;
     const double nb = double(A->nnzb);
@@ -528,7 +556,7 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready) {
         return;
     }
     const Smoother& S = *sm[l];
-    for (int i = 0; i < cfg.nu1; ++i) S.apply(ctx, b, x, cfg.pre, r0_ready && i == 0);
+    S.apply_sweeps(ctx, b, x, cfg.pre, cfg.nu1, r0_ready);
     RowPass p;
     p.A = A[l];
     p.mode = MODE_RESIDUAL;
@@ -540,7 +568,7 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready) {
     launch_restrict(ctx, *T[l], r[l].as<double>(), bl[l + 1].as<double>(), xl[l + 1].as<double>());
     v_cycle(ctx, l + 1, xl[l + 1].as<double>(), bl[l + 1].as<double>());
     launch_prolong_add(ctx, *T[l], xl[l + 1].as<double>(), x);
-    for (int i = 0; i < cfg.nu2; ++i) S.apply(ctx, b, x, cfg.post);
+    S.apply_sweeps(ctx, b, x, cfg.post, cfg.nu2);
 }
 
 void Mg::project(Ctx& ctx, double* v) {

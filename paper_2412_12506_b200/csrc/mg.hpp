@@ -56,6 +56,9 @@ struct Smoother {
     /// caller's residual check computed it with the same kernel), so the
     /// sweep's own residual pass is skipped; the bits are unchanged.
     void apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready = false) const;
+    /// `nu` consecutive applications (the V-cycle's pre / post smoothing);
+    /// Jacobi ping-pongs x with the snapshot buffer instead of copying.
+    void apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready = false) const;
     double bytes_per_apply() const;
 };
 

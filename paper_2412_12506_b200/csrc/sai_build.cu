@@ -17,7 +17,6 @@
 //      minimum-norm fallback by one-sided Jacobi SVD (dgelsd, :298-308)   GPU, one CTA/problem
 //   7. scatter B(J_b, j) = alpha_J X_b alpha_j (:357-364)         GPU
 // Results are independent of caching (the cache only changes the work done).
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +28,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "dgemm.hpp"
 #include "host_eig.hpp"
 #include "mg.hpp"
 
@@ -42,6 +42,11 @@ __global__ void balance_kernel(const double* __restrict__ val, const int* __rest
                                int* __restrict__ flags) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= N) return;
+    if (dk[e] < 0) {  // row not assembled (distributed setup): never part of a requested problem
+        flags[e] = 0;
+        for (int i = 0; i < bs; ++i) alpha[size_t(e) * bs + i] = 1.0;
+        return;
+    }
     const double* D = val + size_t(dk[e]) * stride;  // column-major (i,j) at j*bs+i
     double svv = 0.0, svp = 0.0;
     for (int i = 0; i < nv; ++i)
@@ -611,6 +616,28 @@ __global__ void qr_wide_t_kernel(const double* __restrict__ G, const double* __r
     }
 }
 
+/// Row-major copy of the wide panel's reflectors (VT(r, c) at r * ldt + c
+/// = V(r, c), V column-major mr x w with leading dimension mr), so the
+/// update C -= V Z reads V with its reflector index contiguous (the GEMM's
+/// k index).  32x32 tiles through shared memory, problem = blockIdx.z.
+__global__ void __launch_bounds__(256) transpose_panel_kernel(const double* __restrict__ V, int64_t sV, int mr,
+                                                              int w, double* __restrict__ VT, int ldt, int64_t sT) {
+    __shared__ double t[32][33];
+    const double* Vp = V + int64_t(blockIdx.z) * sV;
+    double* Tp = VT + int64_t(blockIdx.z) * sT;
+    const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int c = ty; c < 32; c += 8) {
+        const int rr = r0 + tx, cc = c0 + c;
+        t[c][tx] = (rr < mr && cc < w) ? Vp[int64_t(cc) * mr + rr] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int rr = r0 + r, cc = c0 + tx;
+        if (rr < mr && cc < ldt) Tp[int64_t(rr) * ldt + cc] = cc < w ? t[tx][r] : 0.0;
+    }
+}
+
 /// X = R^{-1} (Q^T E)[0:n] for CB right-hand sides per CTA, blocked by 32
 /// rows: solve the 32x32 diagonal block, then update every row above it.
 template <int CB>
@@ -894,27 +921,6 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
     (void)d_X;
 }
 
-namespace {
-void blas_check(cublasStatus_t st, const char* what) {
-    if (st != CUBLAS_STATUS_SUCCESS) fail(LDGMG_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(int(st)));
-}
-cublasHandle_t ctx_blas(Ctx& ctx) {
-    if (!ctx.blas) {
-        cublasHandle_t h;
-        blas_check(cublasCreate(&h), "cublasCreate");
-        ctx.blas = h;
-    }
-    cublasHandle_t h = static_cast<cublasHandle_t>(ctx.blas);
-    blas_check(cublasSetStream(h, ctx.stream), "cublasSetStream");
-    return h;
-}
-}  // namespace
-
-void ctx_release_blas(Ctx& ctx) {
-    if (ctx.blas) cublasDestroy(static_cast<cublasHandle_t>(ctx.blas));
-    ctx.blas = nullptr;
-}
-
 /// Blocked Householder QR least squares for a batch of problems of ONE shape
 /// (m x n, k = bs right-hand sides), compact WY with wide panels of WB = 64
 /// columns: each wide panel is factored as 8-column sub-panels
@@ -922,21 +928,23 @@ void ctx_release_blas(Ctx& ctx) {
 /// qr_trailing_tma_kernel), its T follows from the Gram matrix of its
 /// reflectors (qr_wide_t_kernel), and the trailing matrix and the right-hand
 /// sides get C -= V (T^T (V^T C)) as three strided-batched cuBLAS DGEMMs per
-/// panel.  The trailing update -- all but ~2 % of the flops -- thus runs at
-/// GEMM arithmetic intensity (64 reflectors per pass over C instead of 8).
+/// panel, each a batched FP64 tensor-core GEMM (dgemm_batched.cu; the
+/// reflector block is also kept row-major for the last one).  The trailing
+/// update -- all but ~6 % of the flops -- thus runs at GEMM arithmetic
+/// intensity (64 reflectors per pass over C instead of 8).
 template <int NB>
 void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_X, DevBuf& d_xoff,
                    DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, int bs, int nb, int m, int n) {
     constexpr int WB = 64, TCPW = 4;
     const int k = bs;
-    cublasHandle_t h = ctx_blas(ctx);
     std::vector<int64_t> voff(nb + 1);
     for (int i = 0; i <= nb; ++i) voff[i] = int64_t(i) * m * NB;
     DevBuf d_V(sizeof(double) * std::max<int64_t>(1, voff[nb])), d_voff(sizeof(int64_t) * (nb + 1)),
         d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
         d_Vb(sizeof(double) * size_t(nb) * m * WB), d_G(sizeof(double) * size_t(nb) * WB * WB),
         d_Tb(sizeof(double) * size_t(nb) * WB * WB), d_tau(sizeof(double) * size_t(nb) * WB),
-        d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k));
+        d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k)),
+        d_VbT(sizeof(double) * size_t(nb) * m * WB);
     h2d(ctx, d_voff.p, voff.data(), d_voff.bytes);
     qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
                                                     d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
@@ -948,7 +956,6 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
         fprintf(stderr, "[qr_gemm] NB=%d m=%d n=%d batch=%d\n", NB, m, n, nb);
     const size_t tsmem = sizeof(double) * size_t(TCPW) * (((m + 1) & ~1) + 2);
     ensure_dyn_smem(qr_trailing_tma_kernel<NB, TCPW>, tsmem);
-    const double one = 1.0, zero = 0.0, mone = -1.0;
     double* M = d_M.as<double>();
     double* W = d_W.as<double>();
     const long long sM = (long long)m * n, sW = (long long)m * k, sV = (long long)m * WB, sG = WB * WB,
@@ -983,9 +990,8 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
             }
         }
         // T of the wide panel from the Gram matrix of its reflectors
-        blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, w, mrb, &one, d_Vb.as<double>(), mrb, sV,
-                                             d_Vb.as<double>(), mrb, sV, &zero, d_G.as<double>(), w, sG, nb),
-                   "gram");
+        double* Vb = d_Vb.as<double>();
+        dgemm_nt_batched(ctx, GemmNT{Vb, mrb, sV, Vb, mrb, sV, d_G.as<double>(), w, sG, w, w, mrb, 1.0, 0.0}, nb);
         qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(d_G.as<double>(), d_tau.as<double>(), WB, d_Tb.as<double>(), w,
                                                     sG);
         after_launch("qr_wide_t_kernel");
@@ -996,17 +1002,25 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
             int cols;
         };
         const Part parts[2] = {{M + jb + size_t(jb + w) * m, sM, n - jb - w}, {W + jb, sW, k}};
+        bool vt = false;
         for (const Part& pt : parts) {
             if (pt.cols <= 0) continue;
-            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, pt.cols, mrb, &one, d_Vb.as<double>(),
-                                                 mrb, sV, pt.C, m, pt.stride, &zero, d_Y.as<double>(), w, sY, nb),
-                       "V^T C");
-            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, w, pt.cols, w, &one, d_Tb.as<double>(), w,
-                                                 sG, d_Y.as<double>(), w, sY, &zero, d_Z.as<double>(), w, sY, nb),
-                       "T^T Y");
-            blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, mrb, pt.cols, w, &mone, d_Vb.as<double>(),
-                                                 mrb, sV, d_Z.as<double>(), w, sY, &one, pt.C, m, pt.stride, nb),
-                       "C -= V Z");
+            if (!vt) {  // row-major reflectors for the C -= V Z product
+                transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
+                    Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV);
+                after_launch("transpose_panel_kernel");
+                vt = true;
+            }
+            double* Y = d_Y.as<double>();
+            double* Z = d_Z.as<double>();
+            // Y = V^T C   (w x cols, k = mrb)
+            dgemm_nt_batched(ctx, GemmNT{Vb, mrb, sV, pt.C, m, pt.stride, Y, w, sY, w, pt.cols, mrb, 1.0, 0.0}, nb);
+            // Z = T^T Y   (w x cols, k = w)
+            dgemm_nt_batched(ctx, GemmNT{d_Tb.as<double>(), w, sG, Y, w, sY, Z, w, sY, w, pt.cols, w, 1.0, 0.0}, nb);
+            // C -= V Z    (mrb x cols, k = w)
+            dgemm_nt_batched(ctx, GemmNT{d_VbT.as<double>(), WB, sV, Z, w, sY, pt.C, m, pt.stride, mrb, pt.cols, w,
+                                         -1.0, 1.0},
+                             nb);
         }
     }
     constexpr int CB = 16;
@@ -1046,8 +1060,11 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             rowof[k] = e;
             if (A.hcol[k] == e) dk[e] = k;
         }
+    // with a column mask (distributed setup) rows outside the rank's halo
+    // are empty: they enter no requested problem and get no scaling
     for (int e = 0; e < N; ++e)
-        if (dk[e] < 0) fail(LDGMG_ERR_RUNTIME, "balance_vector: missing diagonal block");
+        if (dk[e] < 0 && !(colmask && A.hptr[e] == A.hptr[e + 1]))
+            fail(LDGMG_ERR_RUNTIME, "balance_vector: missing diagonal block");
     DevBuf d_dk(sizeof(int) * std::max(1, N)), d_flags(sizeof(int) * std::max(1, N)),
         d_alpha(sizeof(double) * std::max<int64_t>(1, int64_t(N) * bs)), d_rowof(sizeof(int) * rowof.size());
     h2d(ctx, d_dk.p, dk.data(), sizeof(int) * N);

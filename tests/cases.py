@@ -46,3 +46,52 @@ def baseline_configs(scale=True):
     c5 = (stokes(4 if scale else 32, 3, P, gamma=0.0, degree=2, beta=4.0, beta_p=1 / 16, delta=0.01, **sph),
           cfg("sai", level=1, zeta=0.107))
     return {"C1": c1, "C2": c2, "C3-GS": c3, "C3-SAI": c3s, "C4": c4, "C5": c5}
+
+
+def baseline_rhs(n, bs, kind, dim, bs_scalar, kernel_constants, kernel_pressure, normal=False, seed=0,
+                 random_rhs=None):
+    """The benchmark right-hand side: the reference's seeded uniform[-1,1]
+    draw (random_rhs, krylov.hpp:279-287) -- Box-Muller N(0,1) on consecutive
+    uniforms of the same stream for C3 (extension A5) -- with the constant
+    mode of every kernel vector removed (krylov.hpp:295-299)."""
+    import numpy as np
+    v = np.array(random_rhs(n, bs, seed), dtype=np.float64)
+    if normal:
+        u = (v + 1.0) / 2.0
+        u1, u2 = u[0::2], u[1::2]
+        z = np.sqrt(-2.0 * np.log(np.maximum(u1, 1e-300)))
+        out = np.empty_like(v)
+        out[0::2] = z * np.cos(2 * np.pi * u2)
+        out[1::2] = z * np.sin(2 * np.pi * u2)
+        v = out
+    offs = []
+    if kernel_constants:
+        offs += [c * bs_scalar for c in range(1 if kind == g.SYSTEM_SCALAR else dim)]
+    if kernel_pressure:
+        offs.append(dim * bs_scalar)
+    for off in offs:
+        idx = np.arange(n) * bs + off
+        v[idx] -= v[idx].mean()
+    return v
+
+
+def fullsize_configs():
+    """The BASELINE.json configs at their stated sizes (C5 at 16^3, the
+    largest the reference can set up in minutes) + the reference-native box
+    interface for C3: (spec, cfg, rhs_is_normal, stationary cycles to run)."""
+    ball = dict(phase_shape=g.PHASE_BALL, center=(0.5, 0.5, 0.5), radii=(0.3, 0.3, 0.3), mu_in=1e4, mu_out=1.0)
+    box = dict(phase_shape=g.PHASE_BOXES, center=(0.25, 0.25, 0.25), radii=(0.75, 0.75, 0.75), mu_in=1e4, mu_out=1.0)
+    ell = dict(phase_shape=g.PHASE_ELLIPSE, center=(0.5, 0.5, 0.5), radii=(0.35, 0.2, 0.2), mu_in=1e3, mu_out=1.0)
+    sph = dict(phase_shape=g.PHASE_BALL, center=(0.5, 0.5, 0.5), radii=(0.25, 0.25, 0.25), mu_in=1e2, mu_out=1.0)
+    return {
+        "C1": (scalar(64, 2, P, degree=3, beta=9.0), cfg("jacobi", omega=0.7, nu=2), False, 40),
+        "C2": (scalar(32, 3, P, degree=2, beta=4.0), cfg("sai", level=1), False, 40),
+        "C3-ball-GS": (scalar(256, 2, D, degree=4, beta=16.0, **ball), cfg("gs"), True, 12),
+        "C3-ball-SAI": (scalar(256, 2, D, degree=4, beta=16.0, **ball), cfg("sai", level=1), True, 12),
+        "C3-box-GS": (scalar(256, 2, D, degree=4, beta=16.0, **box), cfg("gs"), True, 40),
+        "C3-box-SAI": (scalar(256, 2, D, degree=4, beta=16.0, **box), cfg("sai", level=1), True, 40),
+        "C4": (stokes(128, 2, P, gamma=0.0, degree=3, beta=9.0, beta_p=1 / 16, **ell),
+               cfg("sai", level=1, zeta=0.0990), False, 12),
+        "C5-16": (stokes(16, 3, P, gamma=0.0, degree=2, beta=4.0, beta_p=1 / 16, delta=0.01, **sph),
+                  cfg("sai", level=1, zeta=0.107), False, 6),
+    }
