@@ -103,6 +103,23 @@ class DeviceBsr:
     def from_csr(cls, ctx, A) -> "DeviceBsr":
         return cls(ctx, A.brows, A.bcols, A.row_bs, A.col_bs, A.ptr, A.col, A.val)
 
+    @classmethod
+    def adopt(cls, ctx: Context, h) -> "DeviceBsr":
+        """Wrap (and own) a matrix handle returned by the C ABI."""
+        B = cls.__new__(cls)
+        B.ctx, B.h = ctx, h
+        br, bc, rb, cb, nz = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+        check(lib.ldgmg_bsr_shape(h, C.byref(br), C.byref(bc), C.byref(rb), C.byref(cb), C.byref(nz)))
+        B.brows, B.bcols, B.row_bs, B.col_bs, B.nnzb = br.value, bc.value, rb.value, cb.value, nz.value
+        return B
+
+    def pattern(self):
+        """(ptr, col) only -- no value download."""
+        ptr = np.empty(self.brows + 1, np.int32)
+        col = np.empty(max(self.nnzb, 1), np.int32)
+        check(lib.ldgmg_bsr_download(self.ctx.h, self.h, ptr.ctypes.data, col.ctypes.data, None))
+        return ptr, col[: self.nnzb]
+
     def download(self):
         ptr = np.empty(self.brows + 1, np.int32)
         col = np.empty(max(self.nnzb, 1), np.int32)

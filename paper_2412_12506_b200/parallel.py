@@ -111,36 +111,36 @@ def partition_depth(sizes, transfers, P, min_rows_per_rank):
     return max(ld, 1)
 
 
-def split_b_rows(Bg, n, bs, plan: Plan):
+def split_b_index(ptr, col, n, plan: Plan):
     """The rank's SAI matrix as ONE device matrix serving both sweep
     directions: rows [0, n_own) are the rank's B rows (the
     plan's local column numbering, block order unchanged), rows n_own + g are
     the plan's ghost rows g restricted to the rank's own columns -- exactly
-    the entries B[j][c], c owned, that the rank's B^T rows need.  Returns
-    (ptr, col, own values (a view of Bg), ghost values (gathered copy)) and
-    the transposed view pattern (tptr, tcol, tperm): B^T row c lists the
-    blocks B[j][c] in ascending GLOBAL row order j (spmv_transpose's scatter
-    order, blockla.hpp:163-175), columns = the local ids of j, which are the
-    ghost-slot numbering of the forward plan (B's pattern is symmetric, so
-    B and B^T reach the same ghosts)."""
-    ptr, col, val = (np.asarray(a) for a in Bg)
+    the entries B[j][c], c owned, that the rank's B^T rows need.  Index-only:
+    returns (fptr, fcol, src) with src[q] = the global B block behind local
+    block q, and the transposed view pattern (tptr, tcol, tperm): B^T row c
+    lists the blocks B[j][c] in ascending GLOBAL row order j (spmv_transpose's
+    scatter order, blockla.hpp:163-175), columns = the local ids of j, which
+    are the ghost-slot numbering of the forward plan (B's pattern is
+    symmetric, so B and B^T reach the same ghosts)."""
+    ptr, col = np.asarray(ptr, np.int64), np.asarray(col)
     r0, r1, n_own = plan.r0, plan.r1, plan.n_own
-    lptr = (ptr[r0:r1 + 1] - ptr[r0]).astype(np.int64)
-    k0, k1 = int(ptr[r0]), int(ptr[r1])
-    own_val = val[k0 * bs * bs:k1 * bs * bs]
-    gcols, gcnt, gk = [], [], []
-    for g in plan.ghost_gid:
+    lptr = ptr[r0:r1 + 1] - ptr[r0]
+    own_src = np.arange(ptr[r0], ptr[r1], dtype=np.int64)
+    gcnt = np.zeros(len(plan.ghost_gid), np.int64)
+    gsrc, gcol = [], []
+    for i, g in enumerate(plan.ghost_gid):
         ks = np.arange(ptr[g], ptr[g + 1])
         cs = col[ks]
         m = (cs >= r0) & (cs < r1)
-        gcols.append(cs[m] - r0)
-        gk.append(ks[m])
-        gcnt.append(int(m.sum()))
-    gk = np.concatenate(gk) if gk else np.zeros(0, np.int64)
-    gcol = np.concatenate(gcols).astype(np.int32) if gcols else np.zeros(0, np.int32)
-    ghost_val = val.reshape(-1, bs * bs)[gk].reshape(-1) if gk.size else np.zeros(0)
-    fptr = np.concatenate([lptr, lptr[-1] + np.cumsum(np.asarray(gcnt, np.int64))]).astype(np.int32)
+        gsrc.append(ks[m])
+        gcol.append(cs[m] - r0)
+        gcnt[i] = int(m.sum())
+    gsrc = np.concatenate(gsrc).astype(np.int64) if gsrc else np.zeros(0, np.int64)
+    gcol = np.concatenate(gcol).astype(np.int32) if gcol else np.zeros(0, np.int32)
+    fptr = np.concatenate([lptr, lptr[-1] + np.cumsum(gcnt)]).astype(np.int32)
     fcol = np.concatenate([plan.local_col.astype(np.int32), gcol])
+    src = np.concatenate([own_src, gsrc])
     # every stored B[j][c] with c owned must come from an own or ghost row
     ghost_set = np.zeros(n, bool)
     ghost_set[plan.ghost_gid] = True
@@ -160,7 +160,19 @@ def split_b_rows(Bg, n, bs, plan: Plan):
     tptr = np.zeros(n_own + 1, np.int64)
     np.add.at(tptr, fcol[q] + 1, 1)
     tptr = np.cumsum(tptr).astype(np.int32)
-    return (fptr, fcol, own_val, ghost_val), (tptr, frow[q].astype(np.int32), q.astype(np.int32))
+    return (fptr, fcol, src), (tptr, frow[q].astype(np.int32), q.astype(np.int32))
+
+
+def split_b_rows(Bg, n, bs, plan: Plan):
+    """split_b_index with the values gathered on the host: (fptr, fcol, own
+    values (a view of Bg), ghost values), (tptr, tcol, tperm)."""
+    ptr, col, val = (np.asarray(a) for a in Bg)
+    (fptr, fcol, src), tpat = split_b_index(ptr, col, n, plan)
+    k0, k1 = int(ptr[plan.r0]), int(ptr[plan.r1])
+    own_val = val[k0 * bs * bs:k1 * bs * bs]
+    gk = src[k1 - k0:]
+    ghost_val = val.reshape(-1, bs * bs)[gk].reshape(-1) if gk.size else np.zeros(0)
+    return (fptr, fcol, own_val, ghost_val), tpat
 
 
 def boundary_rows(ptr, col, n_own):
@@ -227,6 +239,16 @@ class GpuOps:
             if v.size:
                 check(lib.ldgmg_bsr_set_values(self.ctx.h, M.h, int(k0), int(v.size // (bs * bs)), v.ctypes.data))
         return M
+
+    def gather_matrix(self, M, brows, bcols, ptr, col, src_blocks):
+        """New device matrix: pattern (ptr, col), block q = M's block src_blocks[q] (device copy)."""
+        h = C.c_void_p()
+        p = np.ascontiguousarray(ptr, np.int32)
+        c = np.ascontiguousarray(col, np.int32)
+        q = np.ascontiguousarray(src_blocks, np.int64)
+        check(lib.ldgmg_bsr_gather(self.ctx.h, M.h, int(brows), int(bcols), p.ctypes.data, c.ctypes.data,
+                                   q.ctypes.data, C.byref(h)))
+        return _Handle(h, lib.ldgmg_bsr_destroy)
 
     def prefix_view(self, M, nrows):
         h = C.c_void_p()
@@ -390,20 +412,31 @@ class DistMultigrid:
         for l in range(self.ld):
             lv = levels[l]
             n = lv["n"]
-            pa = partition_level(*lv["A"][:2], n, self.P, self.rank)
-            lrA = local_rows(*lv["A"], bs, bs, pa)
-            d = {"n": n, "plan": pa, "A": ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs, *lrA),
-                 "xA": Exchanger(pa, bs, ops, dist, group, self.rank), "nnzA": int(lrA[0][-1])}
-            if "B" in lv:
+            if "A_local" in lv:  # built on the device already (device_partial_levels)
+                pa, lrA = lv["plan_A"], lv["A_local_pattern"]
+                Aloc = lv["A_local"]
+            else:
+                pa = partition_level(*lv["A"][:2], n, self.P, self.rank)
+                lrA = local_rows(*lv["A"], bs, bs, pa)
+                Aloc = ops.matrix(pa.n_own, pa.n_own + pa.n_ghost, bs, *lrA)
+            d = {"n": n, "plan": pa, "A": Aloc, "xA": Exchanger(pa, bs, ops, dist, group, self.rank),
+                 "nnzA": int(lrA[0][-1])}
+            if "B_full" in lv or "B" in lv:
                 # one device matrix for both sweep directions: the rank's B
                 # rows (forward, a row-prefix view) and, behind them, the
                 # ghost rows' owned-column blocks the B^T rows read through
                 # a transposed view (no host transpose, no B^T copy)
-                pb = partition_level(lv["B"][0], lv["B"][1], n, self.P, self.rank)
-                (fptr, fcol, own_val, ghost_val), (tptr, tcol, tperm) = split_b_rows(lv["B"], n, bs, pb)
-                nf = pb.n_own + pb.n_ghost
-                nnz_own = int(fptr[pb.n_own])
-                Bfull = ops.matrix_pieces(nf, nf, bs, fptr, fcol, [(0, own_val), (nnz_own, ghost_val)])
+                if "B_full" in lv:
+                    pb, Bfull = lv["plan_B"], lv["B_full"]
+                    (fptr, fcol), (tptr, tcol, tperm) = lv["B_index"]
+                    nf = pb.n_own + pb.n_ghost
+                    nnz_own = int(fptr[pb.n_own])
+                else:
+                    pb = partition_level(lv["B"][0], lv["B"][1], n, self.P, self.rank)
+                    (fptr, fcol, own_val, ghost_val), (tptr, tcol, tperm) = split_b_rows(lv["B"], n, bs, pb)
+                    nf = pb.n_own + pb.n_ghost
+                    nnz_own = int(fptr[pb.n_own])
+                    Bfull = ops.matrix_pieces(nf, nf, bs, fptr, fcol, [(0, own_val), (nnz_own, ghost_val)])
                 d["Bfull"] = Bfull
                 d["B"] = ops.prefix_view(Bfull, pb.n_own)
                 d["BT"] = ops.transposed_view(Bfull, pb.n_own, nf, tptr, tcol, tperm)
@@ -422,7 +455,9 @@ class DistMultigrid:
                                      "(each rank is one partition, smoothers.hpp:87-94)")
                 d["pgs"] = [[ops.itensor(w) for w in pgs_schedule(pa.n_own, lrA[0], lrA[1], rev)]
                             for rev in (0, 1)]
-            if "factors" in lv and kind != L.SAI:  # Jacobi, coloured GS, processor-block GS
+            if "factors_own" in lv and kind != L.SAI:
+                d["F"] = ops.factors(pa.n_own, bs, *lv["factors_own"])
+            elif "factors" in lv and kind != L.SAI:  # Jacobi, coloured GS, processor-block GS
                 V, lam, s = lv["factors"]
                 a, b = pa.r0, pa.r1
                 d["F"] = ops.factors(pa.n_own, bs, V[a * bs * bs:b * bs * bs], lam[a * bs:b * bs], s[a * bs:b * bs])
@@ -911,33 +946,92 @@ def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_f
     return levels, transfers
 
 
-def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64, any_n=None, overlap=True):
-    """Distributed hierarchy with DISTRIBUTED setup: each rank assembles only
-    its rows plus the SAI halo (Problem.partial), solves only the SAI columns
-    its rows need (column-masked GPU build), and computes the diagonal
-    factors of its own rows on the GPU.  The agglomerated tail is set up in
-    full on every rank (it is small).  Results are identical to
-    from_problem (tests/test_distributed_setup.py)."""
+def device_partial_levels(ctx, prob, cfg, nranks, rank, min_rows_per_rank, bcast):
+    """Per-level data for DistMultigrid with every operator value kept on
+    the device: the rank's rows + halo are ASSEMBLED on the device
+    (Problem.partial with device assembly, global numbering, other rows
+    empty); its SAI columns pattern^l(range) are solved by the column-masked
+    GPU build directly on that operator (rows outside the halo enter no
+    requested problem); the rank's local A and its B (own rows + the ghost
+    rows' owned-column blocks, split_b_index) are cut out of the global-
+    shaped device matrices by block gathers.  Only index arrays (ptr / col /
+    plans) live on the host; the values never cross PCIe.  Levels past the
+    partitioned ones are built in full (device operators) for the
+    agglomerated tail."""
+    from .api import DeviceBsr, Smoother, SmootherConfig, sai_build
+    ops = GpuOps(ctx)
+    depth = prob.depth
+    shapes = [prob.level_shape(l) for l in range(depth)]
+    transfers = [prob.level_transfer(l) for l in range(depth - 1)]
+    ld = partition_depth([sh[0] for sh in shapes], transfers, nranks, min_rows_per_rank)
+    kind = L.SYSTEM_STOKES if prob.n_comp > 1 else L.SYSTEM_SCALAR
+    levels = []
+    for l in range(depth):
+        n, bs, _ = shapes[l]
+        ptr, col = prob.level_pattern(l)
+        lv = {"n": n, "bs": bs, "pattern": (ptr, col)}
+        if l < ld:
+            r0, r1 = rank * n // nranks, (rank + 1) * n // nranks
+            Ad = prob.device_operator(ctx, l)
+            pa = partition_level(ptr, col, n, nranks, rank)
+            lptr = (np.asarray(ptr[r0:r1 + 1], np.int64) - int(ptr[r0])).astype(np.int32)
+            lv["plan_A"], lv["A_local_pattern"] = pa, (lptr, pa.local_col)
+            whole = pa.n_ghost == 0 and r0 == 0 and r1 == n  # one rank: the local operator IS the global one
+            lv["A_local"] = Ad if whole else ops.gather_matrix(
+                Ad, pa.n_own, pa.n_own + pa.n_ghost, lptr, pa.local_col,
+                np.arange(int(ptr[r0]), int(ptr[r1]), dtype=np.int64))
+            if cfg.smoother.kind == L.SAI:
+                own = np.zeros(n, bool)
+                own[r0:r1] = True
+                want = csr_ring(ptr, col, own, cfg.smoother.level)
+                Bd, _ = sai_build(ctx, Ad, kind, prob.n_velocity, cfg.smoother.level, cfg.smoother.zeta,
+                                  cfg.smoother.cache, col_mask=want)
+                del Ad
+                Bp, Bc = Bd.pattern()
+                pb = partition_level(Bp, Bc, n, nranks, rank)
+                (fptr, fcol, src), tpat = split_b_index(Bp, Bc, n, pb)
+                nf = pb.n_own + pb.n_ghost
+                lv["B_full"] = Bd if (whole and pb.n_ghost == 0) else ops.gather_matrix(Bd, nf, nf, fptr, fcol, src)
+                del Bd
+                lv["plan_B"], lv["B_index"] = pb, ((fptr, fcol), tpat)
+            else:
+                dk = np.array([int(ptr[e]) + int(np.nonzero(col[ptr[e]:ptr[e + 1]] == e)[0][0])
+                               for e in range(r0, r1)], np.int64)
+                n_own = r1 - r0
+                Dm = ops.gather_matrix(Ad, n_own, n_own, np.arange(n_own + 1, dtype=np.int32),
+                                       np.arange(n_own, dtype=np.int32), dk)
+                del Ad
+                Dw = DeviceBsr.adopt(ctx, Dm.h)
+                Dm.h = None  # ownership moves to Dw
+                lv["factors_own"] = Smoother(ctx, Dw, SmootherConfig.jacobi(cfg.smoother.omega)).diag_factors()
+                if cfg.smoother.kind == L.COLOURED_GS:
+                    lv["colour"] = distributed_colouring(ptr, col, n, nranks, rank, bcast)
+        else:
+            lv["A_dev"] = prob.device_operator(ctx, l)
+        levels.append(lv)
+    return levels, transfers
+
+
+def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64, any_n=None, overlap=True,
+                         device=True):
+    """Distributed hierarchy with DISTRIBUTED setup: each rank builds only
+    its rows plus the SAI halo, solves only the SAI columns its rows need
+    (column-masked GPU build), and computes the diagonal factors of its own
+    rows on the GPU.  device=True (default): operators assembled and cut on
+    the device (device_partial_levels, no operator values on the host);
+    False: host assembly (Problem.partial + partial_levels, the path the CPU
+    tests drive).  The agglomerated tail is set up in full on every rank (it
+    is small).  Results are identical either way and to from_problem
+    (tests/test_distributed_setup.py)."""
     from .api import DeviceBsr, Multigrid, MultigridConfig, Problem, Smoother, SmootherConfig, Transfer, sai_build
     rank, P = dist.get_rank(group), dist.get_world_size(group)
     if any_n is None:  # extension A1 for non-power-of-two meshes (C5 at 48^3)
         any_n = spec.n & (spec.n - 1) != 0
     prob = Problem.partial(spec, P, rank, sai_halo_hops(spec, cfg.smoother), min_rows_per_rank,
-                           min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements, any_n=any_n)
+                           min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements, any_n=any_n,
+                           device_assembly=device)
     depth = prob.depth
     kind = L.SYSTEM_STOKES if prob.n_comp > 1 else L.SYSTEM_SCALAR
-
-    def gpu_sai(lptr, lcol, lval, nH, mask):
-        A = DeviceBsr(ctx, nH, nH, prob.bs, prob.bs, lptr, lcol, lval)
-        B, _ = sai_build(ctx, A, kind, prob.n_velocity, cfg.smoother.level, cfg.smoother.zeta,
-                         cfg.smoother.cache, col_mask=mask)
-        return B.download()
-
-    def gpu_factors(l, r0, r1, bs, D):
-        n_own = r1 - r0
-        Ad = DeviceBsr(ctx, n_own, n_own, bs, bs, np.arange(n_own + 1, dtype=np.int32),
-                       np.arange(n_own, dtype=np.int32), D)
-        return Smoother(ctx, Ad, SmootherConfig.jacobi(cfg.smoother.omega)).diag_factors()
 
     def bcast(q, mine):
         import torch
@@ -945,11 +1039,27 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64,
         dist.broadcast(t, src=dist.get_global_rank(group, q) if group is not None else q, group=group)
         return t.cpu().numpy().astype(np.int32)
 
-    levels, transfers = partial_levels(prob, cfg, P, rank, min_rows_per_rank, gpu_sai, gpu_factors, bcast)
+    if device:
+        levels, transfers = device_partial_levels(ctx, prob, cfg, P, rank, min_rows_per_rank, bcast)
+    else:
+        def gpu_sai(lptr, lcol, lval, nH, mask):
+            A = DeviceBsr(ctx, nH, nH, prob.bs, prob.bs, lptr, lcol, lval)
+            B, _ = sai_build(ctx, A, kind, prob.n_velocity, cfg.smoother.level, cfg.smoother.zeta,
+                             cfg.smoother.cache, col_mask=mask)
+            return B.download()
+
+        def gpu_factors(l, r0, r1, bs, D):
+            n_own = r1 - r0
+            Ad = DeviceBsr(ctx, n_own, n_own, bs, bs, np.arange(n_own + 1, dtype=np.int32),
+                           np.arange(n_own, dtype=np.int32), D)
+            return Smoother(ctx, Ad, SmootherConfig.jacobi(cfg.smoother.omega)).diag_factors()
+
+        levels, transfers = partial_levels(prob, cfg, P, rank, min_rows_per_rank, gpu_sai, gpu_factors, bcast)
     K = prob.injection()
 
     def coarse_factory(ld_):
-        As = [DeviceBsr(ctx, levels[l]["n"], levels[l]["n"], levels[l]["bs"], levels[l]["bs"], *levels[l]["A"])
+        As = [levels[l]["A_dev"] if "A_dev" in levels[l] else
+              DeviceBsr(ctx, levels[l]["n"], levels[l]["n"], levels[l]["bs"], levels[l]["bs"], *levels[l]["A"])
               for l in range(ld_, depth)]
         Ts = [Transfer(ctx, levels[l]["n"], levels[l + 1]["n"], *transfers[l], prob.dim, prob.bs_scalar,
                        prob.n_comp, K) for l in range(ld_, depth - 1)]
@@ -967,7 +1077,6 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64,
                        coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank, overlap=overlap)
     dm._problem = prob
     return dm
-
 
 
 # ------------------------------------------------------ distributed Krylov

@@ -54,17 +54,29 @@ def test_partitioned_path_world1_bitwise(ctx, dist1, name, spec, cfg, min_rows):
     assert np.array_equal(xd.cpu().numpy(), xf.cpu().numpy())
 
 
+SPH = dict(phase_shape=g.PHASE_BALL, center=(0.5, 0.5, 0.5), radii=(0.25, 0.25, 0.25), mu_in=1e2, mu_out=1.0)
+
+
+@pytest.mark.parametrize("device", [True, False])
 @pytest.mark.parametrize("name,spec,cfg,min_rows", [
     ("sai-2d-dirichlet", K.scalar(16, 2, K.D, degree=2), K.cfg("sai", level=1, nu=2), 16),
     ("jacobi-2d", K.scalar(16, 2, K.P, degree=3, beta=9.0), K.cfg("jacobi", omega=0.7, nu=2), 16),
     ("gs-2d", K.scalar(16, 2, K.D, degree=2), K.cfg("gs", nu=2), 16),
+    ("pgs-2d", K.scalar(16, 2, K.D, degree=2), K.cfg("pgs", nu=1, partitions=1), 16),
+    # C5's physics on a non-power-of-two mesh (extension A1)
+    ("sai-stokes3d-anyn", K.stokes(6, 3, K.P, gamma=0.0, degree=1, beta=1.0, beta_p=1 / 16, delta=0.01, **SPH),
+     K.cfg("sai", level=1, zeta=0.107, nu=1), 16),
 ])
-def test_distributed_setup_world1_matches_replicated(ctx, dist1, name, spec, cfg, min_rows):
-    """from_problem_partial (distributed setup path, GPU SAI / GPU factors on
-    the rank's rows) gives the same cycles as the replicated setup."""
+def test_distributed_setup_world1_matches_replicated(ctx, dist1, name, spec, cfg, min_rows, device):
+    """from_problem_partial (distributed setup: device-assembled operators cut
+    by block gathers, or host assembly; GPU SAI / GPU factors on the rank's
+    rows; B^T through the transposed view) gives the same cycles as the
+    replicated setup, bit for bit."""
     from paper_2412_12506_b200 import parallel
-    a = parallel.from_problem(ctx, g.Problem(spec, min_depth=cfg.min_depth), cfg, dist1, min_rows_per_rank=min_rows)
-    b = parallel.from_problem_partial(ctx, spec, cfg, dist1, min_rows_per_rank=min_rows)
+    any_n = spec.n & (spec.n - 1) != 0
+    a = parallel.from_problem(ctx, g.Problem(spec, min_depth=cfg.min_depth, any_n=any_n), cfg, dist1,
+                              min_rows_per_rank=min_rows)
+    b = parallel.from_problem_partial(ctx, spec, cfg, dist1, min_rows_per_rank=min_rows, device=device)
     n, bs = a._full.n, a._full.bs
     rhs = torch.as_tensor(np.random.default_rng(4).uniform(-1, 1, n * bs)).cuda()
     xa, xb = torch.zeros_like(rhs), torch.zeros_like(rhs)
