@@ -200,6 +200,13 @@ int ldgmg_bsr_row_prefix_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int nrows, 
 int ldgmg_bsr_transposed_view(ldgmg_ctx* ctx, const ldgmg_bsr* base, int brows, int bcols, const int* ptr,
                               const int* col, const int* perm, ldgmg_bsr** out);
 
+/* Memory-safety net (no reference counterpart): with LDGMG_GUARD_BYTES=G in
+ * the environment every library allocation carries G-byte guard zones; the
+ * check returns how many zones were overwritten so far (out-of-bounds
+ * writes), -1 when guards are off.  live = guarded allocations alive. */
+int64_t ldgmg_debug_guard_check(void);
+int64_t ldgmg_debug_guard_live(void);
+
 /* replaces spmv(const BlockCsr&, const BlockVec&, BlockVec&)  blockla.hpp:136-154 */
 int ldgmg_spmv(ldgmg_ctx* ctx, const ldgmg_bsr* A, const double* x, double* y);
 /* replaces spmv_transpose(...)                                 blockla.hpp:157-176 */

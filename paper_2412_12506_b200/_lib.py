@@ -118,6 +118,8 @@ _SIGS = {
     "ldgmg_last_error": ([], C.c_char_p),
     "ldgmg_abi_version": ([], _I),
     "ldgmg_launch_count": ([], _I64),
+    "ldgmg_debug_guard_check": ([], _I64),
+    "ldgmg_debug_guard_live": ([], _I64),
     "ldgmg_ctx_create": ([_I, C.POINTER(_P)], _I),
     "ldgmg_ctx_destroy": ([_P], _I),
     "ldgmg_ctx_set_stream": ([_P, _P], _I),

@@ -539,14 +539,10 @@ int grid_for(int64_t n, int threads, const Ctx& ctx) {
 }  // namespace
 
 void* pinned_alloc(size_t bytes) {
-    static int env = -1;
-    if (env < 0) {
-        // off by default: page-locking a multi-GB allocation cost ~0.5 s/GB on
-        // the box (C5 32^3: +10.5 s assembly for -2.3 s upload)
-        const char* e = getenv("LDGMG_PINNED_SETUP");
-        env = e ? atoi(e) : 0;
-    }
-    if (!env) return nullptr;
+    // page-locking a multi-GB allocation cost ~0.5 s/GB on the box (C5 32^3:
+    // +10.5 s assembly for -2.3 s upload), so setup buffers stay pageable
+    constexpr bool kPinnedSetup = false;
+    if (!kPinnedSetup) return nullptr;
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
         cudaGetLastError();
@@ -1109,11 +1105,7 @@ void launch_rowpass(Ctx& ctx, const RowPass& p) {
     const int GT = wide <= 32 ? 32 : wide <= 64 ? 64 : wide <= 128 ? 128 : 256;
     // ring depth: keep >= ~3 blocks in flight per group within a 200 KB budget
     const size_t stage_bytes = size_t(a.stage_doubles) * 8;
-    static int ns_env = -2;
-    if (ns_env == -2) {
-        const char* e = getenv("LDGMG_NS");
-        ns_env = e ? atoi(e) : -1;
-    }
+    constexpr int ns_env = -1;  // ring depth chosen per pass (configure_and_launch)
     const bool sq = A.rbs == A.cbs;
     if (sq && A.rbs == 16) configure_and_launch<32, 16>(ctx, a, stage_bytes, ns_env);
     else if (sq && A.rbs == 25) configure_and_launch<32, 25>(ctx, a, stage_bytes, ns_env);

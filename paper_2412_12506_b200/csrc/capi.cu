@@ -152,13 +152,15 @@ int ldgmg_device_alloc(ldgmg_ctx* ctx, size_t bytes, void** ptr) {
     return guarded([&] {
         need(ctx, "ldgmg_device_alloc");
         bind(*ctx);
-        LDGMG_CUDA(cudaMalloc(ptr, bytes ? bytes : 16));
+        *ptr = dev_alloc(bytes ? bytes : 16);
     });
 }
+int64_t ldgmg_debug_guard_check(void) { return dev_guard_check(); }
+int64_t ldgmg_debug_guard_live(void) { return dev_guard_live(); }
 int ldgmg_device_free(ldgmg_ctx* ctx, void* ptr) {
     return guarded([&] {
         need(ctx, "ldgmg_device_free");
-        LDGMG_CUDA(cudaFree(ptr));
+        dev_free(ptr);
     });
 }
 int ldgmg_copy_h2d(ldgmg_ctx* ctx, void* dst, const void* src, size_t bytes) {
@@ -967,12 +969,9 @@ struct SolveState {
 };
 constexpr int kSolveHist = int(sizeof(SolveState) / sizeof(double));
 
-/// LDGMG_SOLVE_SNAP=1: copy every iterate to the host inside the loop body
-/// (overlapped with the check); default 0: one copy of the final x after it
-bool solve_snap_in_loop() {
-    static const int v = getenv("LDGMG_SOLVE_SNAP") ? atoi(getenv("LDGMG_SOLVE_SNAP")) : 0;
-    return v != 0;
-}
+/// The device loop copies the final x once after it (copying every iterate
+/// inside the loop body measured slower).
+constexpr bool solve_snap_in_loop() { return false; }
 
 /// The loop test of ldgmg_mg_solve_host on the device: rr = ||r|| / ||b||
 /// (IEEE sqrt and division, the host loop's bits), history entry, and the
@@ -1150,11 +1149,7 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
         auto tsec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count() * 1e3; };
         const auto T0 = tnow();
         // pageable -> pinned with host threads, then one DMA
-        static const int h2d_mode = getenv("LDGMG_SOLVE_H2D") ? atoi(getenv("LDGMG_SOLVE_H2D")) : 0;
-        if (h2d_mode == 1) parallel_memcpy(m.h_stage, b_host, sizeof(double) * n);
-        const auto T0a = tnow();
-        LDGMG_CUDA(cudaMemcpyAsync(b.p, h2d_mode == 1 ? m.h_stage : b_host, sizeof(double) * n,
-                                   cudaMemcpyHostToDevice, ctx->stream));
+        LDGMG_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
         if (timing) LDGMG_CUDA(cudaStreamSynchronize(ctx->stream));
         const auto T0b = tnow();
         // With an SAI level-0 smoother the residual check of iterate k is the
@@ -1258,8 +1253,8 @@ int ldgmg_mg_solve_host(ldgmg_ctx* ctx, ldgmg_mg* mg, const double* b_host, doub
             std::memset(x_host, 0, sizeof(double) * n);  // x = 0 exactly (no cycle ran)
         }
         if (timing)
-            fprintf(stderr, "[solve_host] memcpy %.3f dma %.3f norm %.3f ms, %d cycles+checks %.3f ms, d2h %.3f ms\n",
-                    tsec(T0, T0a), tsec(T0a, T0b), tsec(T0b, T1), it, tsec(T1, T2), tsec(T2, tnow()));
+            fprintf(stderr, "[solve_host] h2d %.3f norm %.3f ms, %d cycles+checks %.3f ms, d2h %.3f ms\n",
+                    tsec(T0, T0b), tsec(T0b, T1), it, tsec(T1, T2), tsec(T2, tnow()));
     });
 }
 

@@ -54,17 +54,10 @@ inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
 /// trigger made it 5-10 % SLOWER (dependent CTAs parked on the SMs), the
 /// implicit trigger at grid end is neutral (3.295 vs 3.300 ms), so it is off
 /// by default and the device-side trigger is not issued.
-inline bool pdl_enabled() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("LDGMG_PDL");
-        env = e ? std::atoi(e) : 0;
-    }
-    return env != 0;
-}
+inline bool pdl_enabled() { return false; }
 
 /// PDL for the SMALL kernels only (split-row passes of the coarse levels,
-/// transfers, bottom, projection; LDGMG_PDL_SMALL=0 disables): they trigger
+/// transfers, bottom, projection): they trigger
 /// their dependents at entry and issue their immutable prologue (barrier
 /// init, TMA of the first row's blocks / injection matrices) before
 /// griddepcontrol.wait, so a chain of latency-bound small passes overlaps
@@ -72,14 +65,7 @@ inline bool pdl_enabled() {
 /// launched without the attribute (an early trigger there parked dependent
 /// CTAs on the SMs, see pdl_enabled), which also keeps any small kernel from
 /// starting before a big pass ends.
-inline bool pdl_small_enabled() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("LDGMG_PDL_SMALL");
-        env = e ? std::atoi(e) : 1;
-    }
-    return env != 0;
-}
+inline bool pdl_small_enabled() { return true; }
 
 template <class... KArgs, class... Args>
 inline void launch_pdl_small(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
@@ -147,15 +133,10 @@ inline void ensure_dyn_smem(K* kernel, size_t bytes) {
 /// The V-cycle alternates the TMA row pass (large carveout) with small
 /// kernels; letting the driver pick a smaller carveout for those forces an
 /// SM reconfiguration (L1 drain) at every switch, which measured as a
-/// ~15 us bubble per small launch on B200.  LDGMG_CARVEOUT=0 disables.
+/// ~15 us bubble per small launch on B200.
 template <class K>
 inline void max_carveout(K* kernel) {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("LDGMG_CARVEOUT");
-        env = e ? std::atoi(e) : 1;
-    }
-    if (env) cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
+    cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel),
                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100),
                         "carveout");
 }

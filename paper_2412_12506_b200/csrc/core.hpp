@@ -57,6 +57,13 @@ inline void d2h(Ctx& ctx, void* dst, const void* src, size_t bytes) {
     LDGMG_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
+/// Device allocation of the library (devmem.cpp): plain cudaMalloc, or with
+/// guard zones checked for out-of-bounds writes (LDGMG_GUARD_BYTES).
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+int64_t dev_guard_check();  // corrupted zones so far (-1: guards off)
+int64_t dev_guard_live();
+
 /// RAII device allocation.
 struct DevBuf {
     void* p = nullptr;
@@ -78,10 +85,10 @@ struct DevBuf {
     void alloc(size_t n) {
         release();
         bytes = n;
-        if (n) LDGMG_CUDA(cudaMalloc(&p, n));
+        if (n) p = dev_alloc(n);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         bytes = 0;
     }

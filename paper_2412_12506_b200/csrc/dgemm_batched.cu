@@ -208,12 +208,10 @@ void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch) {
         case 5: launch<64, 128, 2, 4, 16, 3>(ctx, g, batch, vec); return;
         default: break;
     }
-    // default: tall outputs (C -= V Z) take 128-row tiles, the 64-row
-    // products (V^T C, Gram, T^T Y) 64 x 64
-    if (g.M > 64)
-        launch<128, 64, 4, 2, 16, 3>(ctx, g, batch, vec);
-    else
-        launch<64, 64, 2, 2, 16, 3>(ctx, g, batch, vec);
+    // default: 64 x 64 tiles, 4 warps, 3 stages -- measured best on every
+    // product of the C5 QR (tools/dgemm_bench.py, B200: V^T C 30.7, Gram
+    // 20.9, T^T Y 21.7, C -= V Z 20.1 TF/s; 128-row tiles 15-19 TF/s)
+    launch<64, 64, 2, 2, 16, 3>(ctx, g, batch, vec);
 }
 
 }  // namespace ldgmg_b200

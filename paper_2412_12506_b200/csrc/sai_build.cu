@@ -875,18 +875,11 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
     // TMA-staged trailing tiles of tcpw columns (needs the 2-double tail pad
     // on M and W that build_sai_gpu allocates).  Wider tiles re-read the
     // reflectors from L2 fewer times; the widest tile that fits is used.
-    static int tma_env = -2, tcpw_env = -2;
-    if (tma_env == -2) {
-        const char* e = getenv("LDGMG_QR_TMA");
-        tma_env = e ? atoi(e) : 1;
-        e = getenv("LDGMG_QR_TCPW");
-        tcpw_env = e ? atoi(e) : 0;
-    }
     const size_t col_bytes = sizeof(double) * size_t(((max_m + 1) & ~1) + 2);
     int tcpw = 0;
     for (int c : {8, 4, 2})
-        if (!tcpw && col_bytes * c <= 200 * 1024 && (tcpw_env == 0 || tcpw_env == c)) tcpw = c;
-    const bool tma = tma_env != 0 && tcpw > 0;
+        if (!tcpw && col_bytes * c <= 200 * 1024) tcpw = c;
+    const bool tma = tcpw > 0;
     const size_t tsmem = col_bytes * tcpw;
     auto tma_kernel = tcpw == 8 ? qr_trailing_tma_kernel<NB, 8>
                                 : tcpw == 4 ? qr_trailing_tma_kernel<NB, 4> : qr_trailing_tma_kernel<NB, 2>;
@@ -1307,8 +1300,8 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         // batched together with their M (and right-hand side) padded by zero
         // rows at the end: the least-squares minimiser and ||M||_F are
         // unchanged, and a few large batches replace many latency-bound small
-        // ones.  LDGMG_SAI_PAD=1 keeps exact shapes.
-        static const double pad = getenv("LDGMG_SAI_PAD") ? atof(getenv("LDGMG_SAI_PAD")) : 1.25;
+        // ones.
+        constexpr double pad = 1.25;
         std::vector<std::pair<int, int>> batches;
         std::vector<int> batch_ni;
         size_t max_mn = 0, max_mk = 0;
@@ -1377,25 +1370,18 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 max_m = std::max(max_m, hni[i] * bs);
                 max_n = std::max(max_n, hnj[i] * bs);
             }
-            static int qr_env = -2;
-            if (qr_env == -2) {
-                const char* e = getenv("LDGMG_QR_UNBLOCKED");
-                qr_env = e ? atoi(e) : 0;
-            }
+            // wide problems: compact-WY panels + DMMA GEMM updates; narrow
+            // ones (n < 128): in-kernel blocked updates; panels too tall for
+            // shared memory: the one-CTA-per-problem unblocked kernel
             const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
-            static int gemm_env = -2;
-            if (gemm_env == -2) {
-                const char* e = getenv("LDGMG_QR_GEMM");
-                gemm_env = e ? atoi(e) : 1;
-            }
-            if (!qr_env && gemm_env && smem8 <= 200 * 1024 && max_n >= 128)
+            if (smem8 <= 200 * 1024 && max_n >= 128)
                 qr_gemm_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
-            else if (!qr_env && gemm_env && smem4 <= 200 * 1024 && max_n >= 128)
+            else if (smem4 <= 200 * 1024 && max_n >= 128)
                 qr_gemm_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
-            else if (!qr_env && smem8 <= 200 * 1024)
+            else if (smem8 <= 200 * 1024)
                 qr_blocked_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
                                     max_n);
-            else if (!qr_env && smem4 <= 200 * 1024)
+            else if (smem4 <= 200 * 1024)
                 qr_blocked_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
                                     max_n);
             else {

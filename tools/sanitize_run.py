@@ -1,4 +1,4 @@
-"""compute-sanitizer target: every kernel family of the product on tiny
+"""Memory-safety and determinism target: every kernel family of the product on tiny
 problems -- GPU setup (device assembly, diagonal-factor eig, batched SAI
 least squares incl. the rank-deficient refit, bottom eig), Jacobi / coloured
 GS / processor-block GS / SAI forward + reverse sweeps (B^T as copy or view:
@@ -6,7 +6,12 @@ LDGMG_TVIEW=0/1), restriction / prolongation, bottom pseudoinverse, kernel
 projection (tree and strict), the graph-captured cycle, the device-loop
 solve and GMRES.  Small enough for racecheck (~100x slowdown).
 
-  compute-sanitizer --tool {memcheck,racecheck,synccheck} python tools/sanitize_run.py
+  LDGMG_GUARD_BYTES=4096 python tools/sanitize_run.py   (tests/test_gpu_guards.py)
+
+Every device allocation of the library then carries guard zones that are
+checked at the end (out-of-bounds writes), and every case runs its cycles
+twice, direct and graph-replayed, and must agree bit for bit (races).
+compute-sanitizer itself is closed on the GPU pool this was built on.
 """
 import os
 import sys
@@ -29,6 +34,14 @@ def run(ctx, spec, cfg, any_n=False, device_assembly=True, strict=False):
     x = torch.zeros_like(b)
     mg.cycle(x, b)        # direct launches
     mg.cycles(x, b, 2)    # graph capture + replay
+    # determinism (a data race shows up as run-to-run differences): the same
+    # cycles from the same start, direct and graph-replayed, bit for bit
+    x1, x2 = torch.zeros_like(b), torch.zeros_like(b)
+    mg.cycle(x1, b)
+    mg.cycle(x1, b)
+    mg.cycles(x2, b, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, x2), "nondeterministic V-cycle"
     y = torch.empty_like(b)
     mg.apply(b, y)
     _, hist, its = mg.solve_host(b.cpu().numpy(), tol=0.0, maxit=2)
@@ -63,6 +76,12 @@ def main():
     for name, spec, cfg, any_n, strict in cases:
         its = run(ctx, spec, cfg, any_n=any_n, strict=strict)
         print(f"{name}: ok ({its} solve iterations)", flush=True)
+    g_bad = int(g._lib.lib.ldgmg_debug_guard_check())
+    if g_bad >= 0:
+        print(f"guard zones: {g_bad} violations, {int(g._lib.lib.ldgmg_debug_guard_live())} live buffers checked",
+              flush=True)
+        if g_bad:
+            sys.exit(3)
     print("sanitize_run: all cases ok", flush=True)
 
 
