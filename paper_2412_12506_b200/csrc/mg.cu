@@ -236,7 +236,7 @@ void Smoother::init_common(Ctx& ctx) {
     (void)ctx;
 }
 
-void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready) const {
+void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready, const double* r_in) const {
     switch (cfg.kind) {
         case LDGMG_JACOBI: {
             LDGMG_CUDA(cudaMemcpyAsync(snap.p, x, sizeof(double) * size_t(N) * bs,
@@ -295,14 +295,14 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_rea
             break;
         }
         case LDGMG_SAI: {
-            double* r = snap.as<double>();
-            if (!r_ready) {
+            const double* r = r_in ? r_in : snap.as<double>();
+            if (!r_ready && !r_in) {
                 RowPass p;
                 p.A = A;
                 p.mode = MODE_RESIDUAL;
                 p.x = x;
                 p.b = b;
-                p.y = r;
+                p.y = snap.as<double>();
                 p.nrows = N;
                 launch_rowpass(ctx, p);
             }
@@ -321,9 +321,14 @@ void Smoother::apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_rea
     }
 }
 
-void Smoother::apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready) const {
+void Smoother::apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready,
+                            bool x_zero) const {
     if (cfg.kind != LDGMG_JACOBI || nu < 1) {
-        for (int i = 0; i < nu; ++i) apply(ctx, b, x, sweep, r_ready && i == 0);
+        // SAI from x = 0 (the coarse levels' pre-smoothing): the first
+        // residual b - A 0 is b bit for bit (every block product is +0 and
+        // b - (+0) = b), so the sweep reads b instead of a residual pass
+        const double* r0 = x_zero && cfg.kind == LDGMG_SAI ? b : nullptr;
+        for (int i = 0; i < nu; ++i) apply(ctx, b, x, sweep, r_ready && i == 0, i == 0 ? r0 : nullptr);
         return;
     }
     // Jacobi: ping-pong between x and the snapshot buffer instead of copying
@@ -556,7 +561,8 @@ void Mg::v_cycle(Ctx& ctx, int l, double* x, const double* b, bool r0_ready) {
         return;
     }
     const Smoother& S = *sm[l];
-    S.apply_sweeps(ctx, b, x, cfg.pre, cfg.nu1, r0_ready);
+    // coarse levels start from x = 0 (zeroed by the restriction)
+    S.apply_sweeps(ctx, b, x, cfg.pre, cfg.nu1, r0_ready, l > 0 && x == xl[l].as<double>());
     RowPass p;
     p.A = A[l];
     p.mode = MODE_RESIDUAL;
@@ -672,6 +678,8 @@ double Mg::bytes_per_cycle() const {
     for (int l = 0; l + 1 < depth; ++l) {
         const double N = A[l]->brows, Nc = A[l + 1]->brows;
         s += double(cfg.nu1 + cfg.nu2) * sm[l]->bytes_per_apply();
+        if (l > 0 && cfg.nu1 > 0 && sm[l]->cfg.kind == LDGMG_SAI)  // first coarse sweep from x = 0: no residual pass
+            s -= W * (double(bs) * bs * double(A[l]->nnzb) + 3.0 * bs * N);
         s += W * (double(bs) * bs * double(A[l]->nnzb) + 3.0 * bs * N);  // residual
         s += W * (bs * N + bs * Nc) + W * (bs * Nc + 2.0 * bs * N);      // transfers
     }

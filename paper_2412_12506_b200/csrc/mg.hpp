@@ -55,10 +55,14 @@ struct Smoother {
     /// `r_ready`: SAI only -- `snap` already holds b - A x for this x (the
     /// caller's residual check computed it with the same kernel), so the
     /// sweep's own residual pass is skipped; the bits are unchanged.
-    void apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready = false) const;
+    /// `r_in` (SAI only): a vector known to equal b - A x (e.g. b when x = 0).
+    void apply(Ctx& ctx, const double* b, double* x, int sweep, bool r_ready = false,
+               const double* r_in = nullptr) const;
     /// `nu` consecutive applications (the V-cycle's pre / post smoothing);
-    /// Jacobi ping-pongs x with the snapshot buffer instead of copying.
-    void apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready = false) const;
+    /// Jacobi ping-pongs x with the snapshot buffer instead of copying;
+    /// `x_zero`: x is exactly zero on entry (coarse levels).
+    void apply_sweeps(Ctx& ctx, const double* b, double* x, int sweep, int nu, bool r_ready = false,
+                      bool x_zero = false) const;
     double bytes_per_apply() const;
 };
 

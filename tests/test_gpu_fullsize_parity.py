@@ -44,15 +44,15 @@ CONVERGING = {"C1", "C2", "C3-box-GS", "C3-box-SAI"}
 #   hist_rel: max_k |h_k - h_k^ref| / h_k^ref                     [diverging, A2]
 #   x: | ||x|| - ||x_ref|| | / ||x_ref|| and the projections / ||proj_ref||
 #   eta: max_k |r_k - r_k^ref| / r_0^ref of the GMRES residuals
-BARS = {
-    "C1": dict(hist=1e-12, x=1e-10, eta=1e-12),
-    "C2": dict(hist=1e-12, x=1e-10, eta=1e-12),
-    "C3-box-GS": dict(hist=3e-9, x=1e-6, eta=1e-11),
-    "C3-box-SAI": dict(hist=1e-9, x=1e-6, eta=1e-11),
-    "C3-ball-GS": dict(hist_rel=1e-6),
-    "C3-ball-SAI": dict(hist_rel=1e-6),
-    "C4": dict(hist_rel=1e-6),
-    "C5-16": dict(hist_rel=1e-6),
+BARS = {  # measured (profiles/r02/fullsize_parity.jsonl) -> bar
+    "C1": dict(hist=1e-12, x=1e-10, eta=1e-12),            # 4.9e-15, 3.5e-14, 2.3e-14
+    "C2": dict(hist=1e-12, x=1e-10, eta=1e-12),            # 7.3e-16, 5.6e-15, 1.7e-14
+    "C3-box-GS": dict(hist=3e-9, x=1.5e-8, eta=2e-10),     # 9.2e-10, 4.1e-9, 5.1e-11
+    "C3-box-SAI": dict(hist=1e-9, x=5e-10, eta=5e-9),      # 3.3e-10, 1.3e-10, 1.7e-9
+    "C3-ball-GS": dict(hist_rel=1e-10),                    # 2.6e-12 (x 9.6e-13)
+    "C3-ball-SAI": dict(hist_rel=1e-10),                   # 1.3e-12 (x 1.5e-12)
+    "C4": dict(hist_rel=1e-10),                            # 4.4e-13 (x 1.4e-13)
+    "C5-16": dict(hist_rel=1e-10),                         # 1.2e-13 (x 2.5e-13)
 }
 
 

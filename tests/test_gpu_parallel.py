@@ -137,3 +137,44 @@ def _fast_projection_and_graph(ctx, dist1):
         dm._cycle_body(xe, b, True)       # eager
     torch.cuda.synchronize()
     assert np.array_equal(xg.cpu().numpy(), xe.cpu().numpy())
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_device_partial_levels_match_global_build(ctx, P):
+    """The device-resident distributed setup (device_partial_levels) for
+    every rank of a P-rank job, emulated on one GPU (the setup needs no
+    communication for SAI): each rank's partial problem is assembled on the
+    device (its rows + halo, the other rows empty), its SAI columns solved
+    by the masked build on that operator, and its local A and B cut out by
+    block gathers -- every block equals the corresponding block of the
+    replicated global build (the host-path split of the global B), bit for
+    bit."""
+    from paper_2412_12506_b200 import parallel
+    spec = K.stokes(12, 3, K.P, gamma=0.0, degree=1, beta=1.0, beta_p=1 / 16, delta=0.01, **SPH)
+    cfg = K.cfg("sai", level=1, zeta=0.107, nu=1)
+    full = g.Problem(spec, min_depth=cfg.min_depth, any_n=True)
+    mgf = g.Multigrid(ctx, cfg, full)
+    n, bs, _ = full.level_shape(0)
+    Ag = full.level_matrix(0)
+    Bg = mgf.smoother(0).sai_matrix()
+    for rank in range(P):
+        prob = g.Problem.partial(spec, P, rank, parallel.sai_halo_hops(spec, cfg.smoother), 8,
+                                 min_depth=cfg.min_depth, any_n=True, device_assembly=True)
+        levels, _ = parallel.device_partial_levels(ctx, prob, cfg, P, rank, 8, None)
+        lv = levels[0]
+        pa, pb = lv["plan_A"], lv["plan_B"]
+        # A: the rank's rows with the plan's local columns
+        lptr, lcol, lval = parallel.local_rows(*Ag, bs, bs, pa)
+        A_dev = g.DeviceBsr.adopt(ctx, lv["A_local"].h)
+        lv["A_local"].h = None
+        p_, c_, v_ = A_dev.download()
+        assert np.array_equal(p_, lptr) and np.array_equal(c_, lcol)
+        assert np.array_equal(v_.view(np.int64), np.ascontiguousarray(lval).view(np.int64)), rank
+        # B: own rows + ghost rows' owned columns (host split of the global build)
+        (fptr, fcol, own_val, ghost_val), _ = parallel.split_b_rows(Bg, n, bs, pb)
+        B_dev = g.DeviceBsr.adopt(ctx, lv["B_full"].h)
+        lv["B_full"].h = None
+        p_, c_, v_ = B_dev.download()
+        want = np.concatenate([np.ascontiguousarray(own_val), ghost_val])
+        assert np.array_equal(p_, fptr) and np.array_equal(c_, fcol)
+        assert np.array_equal(v_.view(np.int64), want.view(np.int64)), rank
