@@ -64,33 +64,63 @@ void dev_free(void* p);
 int64_t dev_guard_check();  // corrupted zones so far (-1: guards off)
 int64_t dev_guard_live();
 
+/// Stream-ordered allocation scope: DevBufs allocated on this thread while
+/// a scope is alive come from cudaMallocAsync on its stream and go back with
+/// cudaFreeAsync (no device-wide synchronisation at free), so independent
+/// work on several streams keeps overlapping.  Off under guard zones (the
+/// guarded path stays synchronous and checked).
+cudaStream_t dev_async_stream();
+struct DevAsyncScope {
+    cudaStream_t prev;
+    explicit DevAsyncScope(cudaStream_t s);
+    ~DevAsyncScope();
+};
+
 /// RAII device allocation.
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t astream = nullptr;  // stream-ordered allocation (DevAsyncScope)
     DevBuf() = default;
     explicit DevBuf(size_t n) { alloc(n); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), astream(o.astream) {
+        o.p = nullptr;
+        o.bytes = 0;
+        o.astream = nullptr;
+    }
     DevBuf& operator=(DevBuf&& o) noexcept {
         release();
         p = o.p;
         bytes = o.bytes;
+        astream = o.astream;
         o.p = nullptr;
         o.bytes = 0;
+        o.astream = nullptr;
         return *this;
     }
     ~DevBuf() { release(); }
     void alloc(size_t n) {
         release();
         bytes = n;
-        if (n) p = dev_alloc(n);
+        if (!n) return;
+        astream = dev_async_stream();
+        if (astream)
+            LDGMG_CUDA(cudaMallocAsync(&p, n, astream));
+        else
+            p = dev_alloc(n);
     }
     void release() {
-        if (p) dev_free(p);
+        if (p) {
+            if (astream)
+                cudaFreeAsync(p, astream);
+            else
+                dev_free(p);
+        }
         p = nullptr;
         bytes = 0;
+        astream = nullptr;
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }

@@ -15,7 +15,7 @@
 #include <unordered_map>
 #include <vector>
 
-#include "common.cuh"
+#include "core.hpp"
 
 namespace ldgmg_b200 {
 
@@ -110,6 +110,13 @@ int64_t dev_guard_check() {
         }
     return bad;
 }
+
+namespace {
+thread_local cudaStream_t tl_async = nullptr;
+}
+cudaStream_t dev_async_stream() { return tl_async; }
+DevAsyncScope::DevAsyncScope(cudaStream_t s) : prev(tl_async) { tl_async = guard_bytes() ? nullptr : s; }
+DevAsyncScope::~DevAsyncScope() { tl_async = prev; }
 
 int64_t dev_guard_live() {
     std::lock_guard<std::mutex> lk(reg().mu);

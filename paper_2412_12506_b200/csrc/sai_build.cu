@@ -1325,9 +1325,39 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             max_mk = std::max(max_mk, size_t(p1 - p0) * size_t(m * bs));
             p0 = p1;
         }
-        DevBuf d_M(sizeof(double) * (max_mn + 2)), d_W(sizeof(double) * (max_mk + 2));
+        // The batches are independent: they run on kSlots streams, each with
+        // its own workspace, so one batch's latency-bound panel kernels
+        // overlap another's GEMMs.  Temporaries inside a batch are
+        // stream-ordered (DevAsyncScope): no free synchronises the device.
+        // The rank-deficient refits follow after all batches.
+        constexpr int kSlots = 2;
+        const int nslots = int(std::min<size_t>(kSlots, batches.size()));
+        std::vector<DevBuf> slot_M(nslots), slot_W(nslots);
+        std::vector<cudaStream_t> slot_s(nslots, nullptr);
+        cudaEvent_t ev_ready = nullptr;
+        LDGMG_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+        LDGMG_CUDA(cudaEventRecord(ev_ready, ctx.stream));  // d_At, d_X are ready on the context stream
+        for (int sl = 0; sl < nslots; ++sl) {
+            slot_M[sl].alloc(sizeof(double) * (max_mn + 2));
+            slot_W[sl].alloc(sizeof(double) * (max_mk + 2));
+            LDGMG_CUDA(cudaStreamCreateWithFlags(&slot_s[sl], cudaStreamNonBlocking));
+            LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], ev_ready, 0));
+        }
+        struct BatchState {
+            int p0 = 0, p1 = 0, slot = 0;
+            std::vector<int64_t> moff, xo;
+            std::vector<int> hni, hnj;
+            DevBuf d_boff, d_blk, d_ni, d_nj, d_moff, d_def;
+        };
+        std::vector<BatchState> states(batches.size());
         for (size_t bi = 0; bi < batches.size(); ++bi) {
             const auto [p0, p1] = batches[bi];
+            const int sl = int(bi % size_t(nslots));
+            Ctx bctx = ctx;
+            bctx.stream = slot_s[sl];
+            DevAsyncScope async_scope(bctx.stream);
+            DevBuf& d_M = slot_M[sl];
+            DevBuf& d_W = slot_W[sl];
             const int ni_pad = batch_ni[bi];
             std::vector<int64_t> moff(1, 0), woff(1, 0), boff(1, 0), xo;
             std::vector<int> hni, hnj, hblk;
@@ -1352,19 +1382,18 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             DevBuf d_moff(sizeof(int64_t) * moff.size()), d_woff(sizeof(int64_t) * woff.size()),
                 d_boff(sizeof(int64_t) * boff.size()), d_blk(sizeof(int) * std::max<size_t>(1, hblk.size())),
                 d_ni(sizeof(int) * nb), d_nj(sizeof(int) * nb), d_xoff(sizeof(int64_t) * nb), d_def(sizeof(int) * nb);
-            h2d(ctx, d_moff.p, moff.data(), d_moff.bytes);
-            h2d(ctx, d_woff.p, woff.data(), d_woff.bytes);
-            h2d(ctx, d_boff.p, boff.data(), d_boff.bytes);
-            h2d(ctx, d_blk.p, hblk.data(), sizeof(int) * hblk.size());
-            h2d(ctx, d_ni.p, hni.data(), sizeof(int) * nb);
-            h2d(ctx, d_nj.p, hnj.data(), sizeof(int) * nb);
-            h2d(ctx, d_xoff.p, xo.data(), sizeof(int64_t) * nb);
+            h2d(bctx, d_moff.p, moff.data(), d_moff.bytes);
+            h2d(bctx, d_woff.p, woff.data(), d_woff.bytes);
+            h2d(bctx, d_boff.p, boff.data(), d_boff.bytes);
+            h2d(bctx, d_blk.p, hblk.data(), sizeof(int) * hblk.size());
+            h2d(bctx, d_ni.p, hni.data(), sizeof(int) * nb);
+            h2d(bctx, d_nj.p, hnj.data(), sizeof(int) * nb);
+            h2d(bctx, d_xoff.p, xo.data(), sizeof(int64_t) * nb);
             const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
-            assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
+            assemble_m_kernel<<<ga, 256, 0, bctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
                                                          d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                          d_moff.as<int64_t>(), d_M.as<double>());
             after_launch("assemble_m_kernel");
-            stamp("assemble M");
             int max_m = 0, max_n = 0;
             for (int i = 0; i < nb; ++i) {
                 max_m = std::max(max_m, hni[i] * bs);
@@ -1375,23 +1404,52 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             // shared memory: the one-CTA-per-problem unblocked kernel
             const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
             if (smem8 <= 200 * 1024 && max_n >= 128)
-                qr_gemm_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
+                qr_gemm_batch<8>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
             else if (smem4 <= 200 * 1024 && max_n >= 128)
-                qr_gemm_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
+                qr_gemm_batch<4>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
             else if (smem8 <= 200 * 1024)
-                qr_blocked_batch<8>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
+                qr_blocked_batch<8>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
                                     max_n);
             else if (smem4 <= 200 * 1024)
-                qr_blocked_batch<4>(ctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
+                qr_blocked_batch<4>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
                                     max_n);
             else {
-                qr_ls_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
+                qr_ls_kernel<256><<<nb, 256, 0, bctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
                                                               d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
                                                               d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
                                                               d_def.as<int>());
                 after_launch("qr_ls_kernel");
             }
-            stamp("QR least squares");
+            BatchState& st = states[bi];
+            st.p0 = p0;
+            st.p1 = p1;
+            st.slot = sl;
+            st.moff = std::move(moff);
+            st.xo = std::move(xo);
+            st.hni = std::move(hni);
+            st.hnj = std::move(hnj);
+            st.d_boff = std::move(d_boff);
+            st.d_blk = std::move(d_blk);
+            st.d_ni = std::move(d_ni);
+            st.d_nj = std::move(d_nj);
+            st.d_moff = std::move(d_moff);
+            st.d_def = std::move(d_def);
+        }
+        for (cudaStream_t st : slot_s) LDGMG_CUDA(cudaStreamSynchronize(st));
+        stamp("QR least squares (all batches)");
+        // rank-deficient problems: minimum-norm refit from a fresh copy of M
+        // (on the context stream, slot 0's workspace)
+        for (size_t bi = 0; bi < batches.size(); ++bi) {
+            BatchState& st = states[bi];
+            const int p0 = st.p0, nb = st.p1 - st.p0;
+            const std::vector<int>& hni = st.hni;
+            const std::vector<int>& hnj = st.hnj;
+            const std::vector<int64_t>& moff = st.moff;
+            const std::vector<int64_t>& xo = st.xo;
+            DevBuf& d_M = slot_M[0];
+            const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
+            DevBuf &d_blk = st.d_blk, &d_boff = st.d_boff, &d_ni = st.d_ni, &d_nj = st.d_nj, &d_moff = st.d_moff,
+                   &d_def = st.d_def;
             std::vector<int> def(nb);
             d2h(ctx, def.data(), d_def.p, sizeof(int) * nb);
             // rank-deficient problems: minimum-norm refit from a fresh copy of M
@@ -1431,6 +1489,12 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             }
             for (int i = 0; i < nb; ++i) deficient[bord[p0 + i]] = def[i];
         }
+        states.clear();  // stream-ordered frees on the batch streams
+        for (cudaStream_t st : slot_s) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+        cudaEventDestroy(ev_ready);
     }
 
     // cache inserts (device copies of the fresh solutions)
