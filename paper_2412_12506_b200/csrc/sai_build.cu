@@ -1330,8 +1330,8 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         // overlap another's GEMMs.  Temporaries inside a batch are
         // stream-ordered (DevAsyncScope): no free synchronises the device.
         // The rank-deficient refits follow after all batches.
-        constexpr int kSlots = 2;
-        const int nslots = int(std::min<size_t>(kSlots, batches.size()));
+        static const int kSlots = getenv("LDGMG_SAI_STREAMS") ? std::max(1, atoi(getenv("LDGMG_SAI_STREAMS"))) : 2;
+        const int nslots = int(std::min<size_t>(size_t(kSlots), batches.size()));
         std::vector<DevBuf> slot_M(nslots), slot_W(nslots);
         std::vector<cudaStream_t> slot_s(nslots, nullptr);
         cudaEvent_t ev_ready = nullptr;

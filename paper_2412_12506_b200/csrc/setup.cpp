@@ -1047,6 +1047,7 @@ void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int botto
 
     P.levels.clear();
     P.levels.resize(meshes.size());
+    bool partial_prefix = true;
     for (size_t l = 0; l < meshes.size(); ++l) {
         LevelMesh& m = meshes[l];
         std::vector<Region> lregs = regs;
@@ -1092,7 +1093,15 @@ void problem_build_partial(const ldgmg_problem_spec& s, int min_depth, int botto
         L.partial = false;
         // distributed levels (the same rule as parallel.DistMultigrid): the
         // rank's range plus `halo_hops` face layers; smaller levels in full
-        if (nranks > 1 && N >= nranks * min_rows_per_rank && l + 1 < meshes.size()) {
+        // the partitioned levels are a prefix of the hierarchy, and a level is
+        // partitioned only if no rank boundary splits a sibling group of its
+        // restriction (parallel.partition_depth applies the same rule)
+        bool aligned = true;
+        for (int q = 1; q < nranks; ++q)
+            aligned &= int(int64_t(q) * N / nranks) % (1 << s.dim) == 0;
+        partial_prefix = partial_prefix && nranks > 1 && N >= nranks * min_rows_per_rank && l + 1 < meshes.size() &&
+                         aligned;
+        if (partial_prefix) {
             const int r0 = int(int64_t(rank) * N / nranks), r1 = int(int64_t(rank + 1) * N / nranks);
             c.rows = halo_rows(m, r0, r1, halo_hops);
             c.grows = with_neighbours(m, c.rows);

@@ -925,6 +925,9 @@ def partial_levels(prob, cfg, nranks, rank, min_rows_per_rank, sai_fn, factors_f
     for l in range(depth):
         n, bs, _ = shapes[l]
         lv = {"n": n, "bs": bs, "A": prob.level_matrix(l)}
+        if l >= ld and prob.level_partial(l):
+            raise ValueError(f"distributed setup: level {l} is assembled per rank but agglomerated by the "
+                             "V-cycle (a rank boundary splits a sibling group); raise min_rows_per_rank")
         if l + 1 < depth:
             transfers.append(prob.level_transfer(l))
             if l < ld:
@@ -1007,6 +1010,9 @@ def device_partial_levels(ctx, prob, cfg, nranks, rank, min_rows_per_rank, bcast
                 if cfg.smoother.kind == L.COLOURED_GS:
                     lv["colour"] = distributed_colouring(ptr, col, n, nranks, rank, bcast)
         else:
+            if prob.level_partial(l):  # the setup assembled only a halo here, but the V-cycle agglomerates it
+                raise ValueError(f"distributed setup: level {l} is assembled per rank but agglomerated by the "
+                                 "V-cycle (a rank boundary splits a sibling group); raise min_rows_per_rank")
             lv["A_dev"] = prob.device_operator(ctx, l)
         levels.append(lv)
     return levels, transfers
