@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <unordered_map>
 #include <vector>
 
@@ -841,8 +842,11 @@ struct ColumnPlan {
 
 struct SaiCacheEntry {
     int nj = 0, bs = 0;
-    DevBuf X;  // (nj*bs) x bs column-major
+    std::shared_ptr<DevBuf> slab;  // one allocation per build, shared by its entries
+    int64_t off = 0;               // X ((nj*bs) x bs column-major) at slab + off doubles
     bool deficient = false;
+    const double* X() const { return slab->as<double>() + off; }
+    size_t bytes() const { return sizeof(double) * size_t(nj) * bs * bs; }
 };
 
 struct SaiCache {
@@ -1499,17 +1503,25 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         cudaEventDestroy(ev_ready);
     }
 
-    // cache inserts (device copies of the fresh solutions)
-    for (auto& [pid, key] : inserts) {
-        SaiCacheEntry e;
-        e.nj = probs[pid].nj;
-        e.bs = bs;
-        e.deficient = deficient[pid] != 0;
-        e.X.alloc(sizeof(double) * size_t(e.nj) * bs * bs);
-        LDGMG_CUDA(cudaMemcpyAsync(e.X.p, d_X.as<double>() + xoff[pid], e.X.bytes, cudaMemcpyDeviceToDevice,
-                                   ctx.stream));
-        cache->map.emplace(key, std::move(e));
-        cache->bytes += size_t(probs[pid].nj) * bs * bs * sizeof(double);
+    // cache inserts (device copies of the fresh solutions), one slab per build
+    if (!inserts.empty()) {
+        int64_t total = 0;
+        for (auto& ins : inserts) total += int64_t(probs[ins.first].nj) * bs * bs;
+        auto slab = std::make_shared<DevBuf>(sizeof(double) * size_t(total));
+        int64_t off = 0;
+        for (auto& [pid, key] : inserts) {
+            SaiCacheEntry e;
+            e.nj = probs[pid].nj;
+            e.bs = bs;
+            e.deficient = deficient[pid] != 0;
+            e.slab = slab;
+            e.off = off;
+            off += int64_t(e.nj) * bs * bs;
+            LDGMG_CUDA(cudaMemcpyAsync(slab->as<double>() + e.off, d_X.as<double>() + xoff[pid], e.bytes(),
+                                       cudaMemcpyDeviceToDevice, ctx.stream));
+            cache->map.emplace(key, std::move(e));
+            cache->bytes += size_t(probs[pid].nj) * bs * bs * sizeof(double);
+        }
     }
 
     // ---- 7. B on the pattern and the scatter
@@ -1554,7 +1566,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
     if (xoff[np])
         LDGMG_CUDA(cudaMemcpyAsync(d_Xall.p, d_X.p, sizeof(double) * xoff[np], cudaMemcpyDeviceToDevice, ctx.stream));
     for (size_t i = 0; i < cached_list.size(); ++i) {
-        LDGMG_CUDA(cudaMemcpyAsync(d_Xall.as<double>() + cxoff[i], cached_list[i]->X.p, cached_list[i]->X.bytes,
+        LDGMG_CUDA(cudaMemcpyAsync(d_Xall.as<double>() + cxoff[i], cached_list[i]->X(), cached_list[i]->bytes(),
                                    cudaMemcpyDeviceToDevice, ctx.stream));
         sxoff.push_back(cxoff[i]);
     }

@@ -133,3 +133,41 @@ def test_c5_dropin_bitwise_8cubed(ctx, ref):
     mg.apply(bd, yd)
     torch.cuda.synchronize()
     assert np.array_equal(yd.cpu().numpy().view(np.int64), R.apply(b).view(np.int64))
+
+
+def test_c5_bottom_pinv_matches_oracle_sym_eig(ctx, ref):
+    """The C5 48^3 bottom (3^3 elements x 108 = 2,916 unknowns, the size the
+    device eigensolver is used for) -- built here from C5 at 24^3, whose
+    hierarchy 24 -> 12 -> 6 -> 3 ends in the same 3^3 bottom -- applied as
+    the pseudoinverse (multigrid.hpp:249-253, cutoff 1e-10 max|lambda|) on
+    the GPU (cuSOLVER dsyevd eigenpairs) and from the oracle's sym_eig
+    (blockla.hpp:318-326, LAPACK dsyevd through the shim) on the same dense
+    operator: the same action within 1e-10, the same null space."""
+    spec, cfg, _, _ = K.fullsize_configs()["C5-16"]
+    spec.n = 24
+    P = g.Problem(spec, min_depth=cfg.min_depth, bottom_max_elements=cfg.bottom_max_elements, any_n=True)
+    lb = P.depth - 1
+    nb, bs, _ = P.level_shape(lb)
+    assert nb == 27 and nb * bs == 2916
+    ptr, col, val = P.level_matrix(lb)
+    n = nb * bs
+    D = np.zeros((n, n))
+    for i in range(nb):
+        for k in range(ptr[i], ptr[i + 1]):
+            D[i * bs:(i + 1) * bs, col[k] * bs:(col[k] + 1) * bs] = val[k * bs * bs:(k + 1) * bs * bs].reshape(bs, bs)
+    lam, V = ref.sym_eig(D)
+    V = V.reshape(n, n, order="F")
+    # GPU: a depth-1 hierarchy on the bottom operator: its v_cycle IS the bottom pseudoinverse
+    A = g.DeviceBsr(ctx, nb, nb, bs, bs, ptr, col, val)
+    cfg1 = K.cfg("sai", level=1, zeta=0.107, min_depth=1, bottom_max=27)
+    mg = g.Multigrid(ctx, cfg1, levels=[A], transfers=[], system_kind=g.SYSTEM_STOKES, dim=3, n_comp=4,
+                     bs_scalar=27, kernel_constants=False, kernel_pressure=True)
+    b = np.random.default_rng(9).uniform(-1, 1, n)
+    xd = torch.zeros(n, dtype=torch.float64, device="cuda")
+    mg.vcycle(xd, torch.as_tensor(b).cuda())
+    torch.cuda.synchronize()
+    got = xd.cpu().numpy()
+    cut = 1e-10 * np.max(np.abs(lam))
+    inv = np.where(np.abs(lam) > cut, 1.0 / np.where(lam == 0, 1.0, lam), 0.0)
+    want = V @ (inv * (V.T @ b))
+    assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want), np.linalg.norm(got - want) / np.linalg.norm(want)
