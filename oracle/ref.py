@@ -370,10 +370,10 @@ def cycles_multi(hierarchies, b, ncycles):
 def sym_eig(A):
     """sym_eig (blockla.hpp:318-326) of a dense symmetric matrix: (lambda
     ascending, V column-major flattened)."""
-    A = np.asfortranarray(A, np.float64)
     n = A.shape[0]
+    a = np.ascontiguousarray(np.asarray(A, np.float64).reshape(-1, order="F"))  # kept alive over the call
     lam, V = np.empty(n), np.empty(n * n)
-    _chk(lib().ref_sym_eig(n, _p(A.reshape(-1, order="F").copy()), _p(lam), _p(V)))
+    _chk(lib().ref_sym_eig(n, _p(a), _p(lam), _p(V)))
     return lam, V
 
 
@@ -427,7 +427,8 @@ def sai_build(kind, dim, ncomp, bs_scalar, N, ptr, col, val, level, zeta, cache=
 def balance_vector(kind, dim, ncomp, bs_scalar, N, ptr, col, val, zeta):
     bs = ncomp * bs_scalar
     a = np.empty(N * bs)
-    _chk(lib().ref_balance_vector(kind, dim, ncomp, bs_scalar, N, _p(np.ascontiguousarray(ptr, np.int32)),
-                                  _p(np.ascontiguousarray(col, np.int32)), _p(np.ascontiguousarray(val)), zeta,
-                                  _p(a)))
+    ptr = np.ascontiguousarray(ptr, np.int32)  # kept alive over the call
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    _chk(lib().ref_balance_vector(kind, dim, ncomp, bs_scalar, N, _p(ptr), _p(col), _p(val), zeta, _p(a)))
     return a

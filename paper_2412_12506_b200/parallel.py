@@ -1019,7 +1019,7 @@ def device_partial_levels(ctx, prob, cfg, nranks, rank, min_rows_per_rank, bcast
 
 
 def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64, any_n=None, overlap=True,
-                         device=True):
+                         device=True, overlap_min_rows=2048):
     """Distributed hierarchy with DISTRIBUTED setup: each rank builds only
     its rows plus the SAI halo, solves only the SAI columns its rows need
     (column-masked GPU build), and computes the diagonal factors of its own
@@ -1080,7 +1080,8 @@ def from_problem_partial(ctx, spec, cfg, dist, group=None, min_rows_per_rank=64,
     if prob.kernel_pressure:
         offs.append(prob.dim * prob.bs_scalar)
     dm = DistMultigrid(GpuOps(ctx), dist, cfg, levels, transfers, K, prob.dim, prob.bs_scalar, prob.n_comp, offs,
-                       coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank, overlap=overlap)
+                       coarse_factory, group=group, min_rows_per_rank=min_rows_per_rank, overlap=overlap,
+                       overlap_min_rows=overlap_min_rows)
     dm._problem = prob
     return dm
 

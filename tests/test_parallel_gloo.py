@@ -114,3 +114,57 @@ def test_distributed_krylov_matches_reference(ref, tmp_path, case, kind, world):
         assert np.array_equal(z["residuals"], want["residuals"]), rank
         assert int(z["iterations"]) == want["iterations"]
         assert float(z["rho"]) == want["rho"] and float(z["eta"]) == want["eta"]
+
+
+def test_partition_depth_c5_48():
+    """C5 at 48^3 (levels 110592, 13824, 1728, 216, 27; children of c are
+    8c..8c+7): with 128 rows per rank the partitioned prefix is 3 levels at
+    P = 2, 4, 8 (every rank boundary lands on a sibling-group boundary), and a
+    boundary inside a sibling group stops the prefix."""
+    from paper_2412_12506_b200.parallel import partition_depth
+    sizes = [110592, 13824, 1728, 216, 27]
+    transfers = [(np.arange(n) // 8, np.arange(n) % 8) for n in sizes[:-1]]
+    for P in (2, 4, 8):
+        assert partition_depth(sizes, transfers, P, 128) == 3
+    assert partition_depth(sizes, transfers, 2, 8) == 3  # 216 / 2 = 108 = 13.5 groups: level 3 stays whole
+    assert partition_depth(sizes, transfers, 16, 1) == 2  # 1728 / 16 = 108: level 2 stays whole
+    assert partition_depth([36, 9], [(np.arange(36) // 4, np.arange(36) % 4)], 3, 1) == 1  # forced first level
+
+
+def test_split_b_index_and_boundary_rows():
+    """The rank-local B layout (own rows, then the ghost rows' owned-column
+    blocks) and its transposed view reproduce B's rows and B^T's rows of the
+    rank, the latter in ascending global row order; interior / boundary
+    rows partition the rank's rows by ghost references."""
+    from paper_2412_12506_b200.parallel import boundary_rows, partition_level, split_b_rows
+    import paper_2412_12506_b200 as g
+    from tests import cases as K
+    P_ = g.Problem(K.scalar(8, 2, K.P, degree=1), min_depth=1)
+    ptr, col, _ = P_.level_matrix(0)
+    n, bs = P_.level_shape(0)[:2]
+    rng = np.random.default_rng(0)
+    val = rng.standard_normal(len(col) * bs * bs)
+    dense = np.zeros((n * bs, n * bs))
+    for i in range(n):
+        for k in range(ptr[i], ptr[i + 1]):
+            dense[i * bs:(i + 1) * bs, col[k] * bs:(col[k] + 1) * bs] = val[k * bs * bs:(k + 1) * bs * bs].reshape(bs, bs)
+    for world in (2, 3):
+        for rank in range(world):
+            pl = partition_level(ptr, col, n, world, rank)
+            (fptr, fcol, own_val, ghost_val), (tptr, tcol, tperm) = split_b_rows((ptr, col, val), n, bs, pl)
+            gid = np.concatenate([np.arange(pl.r0, pl.r1), pl.ghost_gid])
+            fval = np.concatenate([own_val, ghost_val]).reshape(-1, bs, bs)
+            for c in range(pl.n_own):  # B^T row c of the rank = column (r0 + c) of B, rows ascending
+                js = tcol[tptr[c]:tptr[c + 1]]
+                assert np.all(np.diff(gid[js]) > 0)
+                got = np.zeros((bs, n * bs))
+                for q, j in zip(range(tptr[c], tptr[c + 1]), js):
+                    got[:, gid[j] * bs:(gid[j] + 1) * bs] = fval[tperm[q]].T
+                want = dense[:, (pl.r0 + c) * bs:(pl.r0 + c + 1) * bs].T
+                assert np.array_equal(got, want)
+            interior, boundary = boundary_rows(fptr[:pl.n_own + 1], fcol[:fptr[pl.n_own]], pl.n_own)
+            assert sorted(np.concatenate([interior, boundary]).tolist()) == list(range(pl.n_own))
+            for r in boundary:
+                assert np.any(fcol[fptr[r]:fptr[r + 1]] >= pl.n_own)
+            for r in interior:
+                assert np.all(fcol[fptr[r]:fptr[r + 1]] < pl.n_own)

@@ -22,7 +22,11 @@ a = ap.parse_args()
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx = g.Context(0, stream=stream)
-spec, cfg, _ = bench.product_workload(a.workload, a.n)
+if a.workload in ("C5", "C2"):
+    spec, cfg, _ = bench.product_workload(a.workload, a.n)
+else:  # any tools/configs_bench.py config (C1, C3-GS, C4, ...)
+    from tools import configs_bench as cb
+    spec, cfg, _ = cb.configs(a.n or 16)[a.workload]
 pow2 = spec.n & (spec.n - 1) == 0
 P = g.Problem(spec, min_depth=cfg.min_depth, device_assembly=True, any_n=not pow2)
 mg = g.Multigrid(ctx, cfg, P)
@@ -31,7 +35,8 @@ b = torch.as_tensor(bench.remove_kernel(g.random_rhs(mg.n, mg.bs, 0), mg.n, mg.b
 x = torch.zeros_like(b)
 mg.cycles(x, b, 3)
 S0 = mg.smoother(0)
-S0.apply(b, x, g.SWEEP_FORWARD)
+if a.pair:
+    S0.apply(b, x, g.SWEEP_FORWARD)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
 if a.pair:
