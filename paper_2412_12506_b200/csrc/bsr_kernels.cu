@@ -22,6 +22,8 @@
 //              the Eigen-shim product order, oracle/shim/Eigen/Dense).
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <algorithm>
 #include <cstdio>
 #include <chrono>
@@ -431,6 +433,9 @@ __global__ void __launch_bounds__(GT) rowpass_kernel(const RowPassArgs a) {
 
 template <int GT, int BS>
 int rowpass_occupancy(Ctx& ctx, size_t smem) {
+    // host threads may drive several contexts at once (one per rank)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     static int attr_set_device = -1;
     if (attr_set_device != ctx.device) {
         LDGMG_CUDA(cudaFuncSetAttribute(rowpass_kernel<GT, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -4,6 +4,7 @@
 // = TMA `cp.async.bulk`, SASS UBLKCP).
 #pragma once
 
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -111,6 +112,8 @@ inline void ensure_dyn_smem(K* kernel, size_t bytes) {
         size_t bytes;  // current cudaFuncAttributeMaxDynamicSharedMemorySize
     };
     static std::vector<Entry> set;
+    static std::mutex mu;  // host threads launch concurrently (SAI batch slots, one context per rank)
+    std::lock_guard<std::mutex> lk(mu);
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     const void* f = reinterpret_cast<const void*>(kernel);

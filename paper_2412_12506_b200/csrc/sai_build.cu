@@ -23,8 +23,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -860,14 +862,13 @@ void sai_cache_free(SaiCache* c) { delete c; }
 /// Host driver of the blocked batch QR (see qr_init_kernel).
 template <int NB>
 void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_X,
-                      DevBuf& d_xoff, DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, const std::vector<int>& hni, int bs,
-                      int nb, int max_m, int max_n) {
+                      DevBuf& d_xoff, DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, DevBuf& d_voff,
+                      const std::vector<int>& hni, int bs, int nb, int max_m, int max_n) {
     constexpr int CPW = 4;
-    std::vector<int64_t> voff(nb + 1, 0);
-    for (int i = 0; i < nb; ++i) voff[i + 1] = voff[i] + int64_t(hni[i]) * bs * NB;
-    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, voff[nb])), d_voff(sizeof(int64_t) * (nb + 1)),
-        d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb);
-    h2d(ctx, d_voff.p, voff.data(), d_voff.bytes);
+    int64_t vtotal = 0;  // d_voff (uploaded by the caller): prefix sums of ni * bs * NB
+    for (int i = 0; i < nb; ++i) vtotal += int64_t(hni[i]) * bs * NB;
+    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, vtotal)), d_T(sizeof(double) * size_t(nb) * NB * NB),
+        d_tol(sizeof(double) * nb);
     qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
                                                     d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
                                                     d_tol.as<double>(), d_def.as<int>());
@@ -931,18 +932,17 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
 /// intensity (64 reflectors per pass over C instead of 8).
 template <int NB>
 void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_X, DevBuf& d_xoff,
-                   DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, int bs, int nb, int m, int n) {
+                   DevBuf& d_ni, DevBuf& d_nj, DevBuf& d_def, DevBuf& d_voff, int bs, int nb, int m, int n) {
     constexpr int WB = 64, TCPW = 4;
     const int k = bs;
-    std::vector<int64_t> voff(nb + 1);
-    for (int i = 0; i <= nb; ++i) voff[i] = int64_t(i) * m * NB;
-    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, voff[nb])), d_voff(sizeof(int64_t) * (nb + 1)),
+    // d_voff (uploaded by the caller): voff[i] = i * m * NB
+    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, int64_t(nb) * m * NB)),
         d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
         d_Vb(sizeof(double) * size_t(nb) * m * WB), d_G(sizeof(double) * size_t(nb) * WB * WB),
         d_Tb(sizeof(double) * size_t(nb) * WB * WB), d_tau(sizeof(double) * size_t(nb) * WB),
         d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k)),
         d_VbT(sizeof(double) * size_t(nb) * m * WB);
-    h2d(ctx, d_voff.p, voff.data(), d_voff.bytes);
+    
     qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
                                                     d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
                                                     d_tol.as<double>(), d_def.as<int>());
@@ -1331,39 +1331,26 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         }
         // The batches are independent: they run on kSlots streams, each with
         // its own workspace, so one batch's latency-bound panel kernels
-        // overlap another's GEMMs.  Temporaries inside a batch are
-        // stream-ordered (DevAsyncScope): no free synchronises the device.
-        // The rank-deficient refits follow after all batches.
-        // measured on C5 16^3 level 0 (881 problems, 7 batches): QR 0.45-0.54 s
-        // on one stream, 0.39-0.41 on two, 0.36 on three, 0.35 on four
+        // overlap another's GEMMs.  Every batch's index arrays are uploaded
+        // up front (nothing synchronises a slot stream once batches run),
+        // batches go to slots longest-first onto the least-loaded slot, and
+        // each slot is fed by its own host thread (a slot whose launch queue
+        // is full then holds back only its own thread).  Temporaries inside a
+        // batch are stream-ordered (DevAsyncScope).  The rank-deficient
+        // refits follow after all batches.
         constexpr int kSlots = 4;
         const int nslots = int(std::min<size_t>(size_t(kSlots), batches.size()));
-        std::vector<DevBuf> slot_M(nslots), slot_W(nslots);
-        std::vector<cudaStream_t> slot_s(nslots, nullptr);
-        cudaEvent_t ev_ready = nullptr;
-        LDGMG_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
-        LDGMG_CUDA(cudaEventRecord(ev_ready, ctx.stream));  // d_At, d_X are ready on the context stream
-        for (int sl = 0; sl < nslots; ++sl) {
-            slot_M[sl].alloc(sizeof(double) * (max_mn + 2));
-            slot_W[sl].alloc(sizeof(double) * (max_mk + 2));
-            LDGMG_CUDA(cudaStreamCreateWithFlags(&slot_s[sl], cudaStreamNonBlocking));
-            LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], ev_ready, 0));
-        }
         struct BatchState {
-            int p0 = 0, p1 = 0, slot = 0;
+            int p0 = 0, p1 = 0, slot = 0, path = 0, max_m = 0, max_n = 0;
+            double cost = 0.0;
             std::vector<int64_t> moff, xo;
             std::vector<int> hni, hnj;
-            DevBuf d_boff, d_blk, d_ni, d_nj, d_moff, d_def;
+            DevBuf d_boff, d_blk, d_ni, d_nj, d_moff, d_woff, d_xoff, d_def, d_voff;
         };
         std::vector<BatchState> states(batches.size());
         for (size_t bi = 0; bi < batches.size(); ++bi) {
+            BatchState& st = states[bi];
             const auto [p0, p1] = batches[bi];
-            const int sl = int(bi % size_t(nslots));
-            Ctx bctx = ctx;
-            bctx.stream = slot_s[sl];
-            DevAsyncScope async_scope(bctx.stream);
-            DevBuf& d_M = slot_M[sl];
-            DevBuf& d_W = slot_W[sl];
             const int ni_pad = batch_ni[bi];
             std::vector<int64_t> moff(1, 0), woff(1, 0), boff(1, 0), xo;
             std::vector<int> hni, hnj, hblk;
@@ -1385,63 +1372,170 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 xo.push_back(xoff[pid]);
             }
             const int nb = p1 - p0;
-            DevBuf d_moff(sizeof(int64_t) * moff.size()), d_woff(sizeof(int64_t) * woff.size()),
-                d_boff(sizeof(int64_t) * boff.size()), d_blk(sizeof(int) * std::max<size_t>(1, hblk.size())),
-                d_ni(sizeof(int) * nb), d_nj(sizeof(int) * nb), d_xoff(sizeof(int64_t) * nb), d_def(sizeof(int) * nb);
-            h2d(bctx, d_moff.p, moff.data(), d_moff.bytes);
-            h2d(bctx, d_woff.p, woff.data(), d_woff.bytes);
-            h2d(bctx, d_boff.p, boff.data(), d_boff.bytes);
-            h2d(bctx, d_blk.p, hblk.data(), sizeof(int) * hblk.size());
-            h2d(bctx, d_ni.p, hni.data(), sizeof(int) * nb);
-            h2d(bctx, d_nj.p, hnj.data(), sizeof(int) * nb);
-            h2d(bctx, d_xoff.p, xo.data(), sizeof(int64_t) * nb);
-            const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
-            assemble_m_kernel<<<ga, 256, 0, bctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
-                                                         d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
-                                                         d_moff.as<int64_t>(), d_M.as<double>());
-            after_launch("assemble_m_kernel");
-            int max_m = 0, max_n = 0;
             for (int i = 0; i < nb; ++i) {
-                max_m = std::max(max_m, hni[i] * bs);
-                max_n = std::max(max_n, hnj[i] * bs);
+                st.max_m = std::max(st.max_m, hni[i] * bs);
+                st.max_n = std::max(st.max_n, hnj[i] * bs);
             }
             // wide problems: compact-WY panels + DMMA GEMM updates; narrow
             // ones (n < 128): in-kernel blocked updates; panels too tall for
             // shared memory: the one-CTA-per-problem unblocked kernel
-            const size_t smem8 = sizeof(double) * size_t(max_m) * 8, smem4 = sizeof(double) * size_t(max_m) * 4;
-            if (smem8 <= 200 * 1024 && max_n >= 128)
-                qr_gemm_batch<8>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
-            else if (smem4 <= 200 * 1024 && max_n >= 128)
-                qr_gemm_batch<4>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, bs, nb, max_m, max_n);
-            else if (smem8 <= 200 * 1024)
-                qr_blocked_batch<8>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
-                                    max_n);
-            else if (smem4 <= 200 * 1024)
-                qr_blocked_batch<4>(bctx, d_M, d_moff, d_W, d_woff, d_X, d_xoff, d_ni, d_nj, d_def, hni, bs, nb, max_m,
-                                    max_n);
-            else {
-                qr_ls_kernel<256><<<nb, 256, 0, bctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
-                                                              d_W.as<double>(), d_woff.as<int64_t>(), d_X.as<double>(),
-                                                              d_xoff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
-                                                              d_def.as<int>());
-                after_launch("qr_ls_kernel");
-            }
-            BatchState& st = states[bi];
+            const size_t smem8 = sizeof(double) * size_t(st.max_m) * 8, smem4 = sizeof(double) * size_t(st.max_m) * 4;
+            st.path = smem8 <= 200 * 1024 && st.max_n >= 128   ? 0
+                      : smem4 <= 200 * 1024 && st.max_n >= 128 ? 1
+                      : smem8 <= 200 * 1024                    ? 2
+                      : smem4 <= 200 * 1024                    ? 3
+                                                               : 4;
+            const int NB = (st.path == 0 || st.path == 2) ? 8 : 4;
+            std::vector<int64_t> voff(nb + 1, 0);
+            for (int i = 0; i < nb; ++i)
+                voff[i + 1] = voff[i] + (st.path <= 1 ? int64_t(st.max_m) : int64_t(hni[i]) * bs) * NB;
+            st.d_moff.alloc(sizeof(int64_t) * moff.size());
+            st.d_woff.alloc(sizeof(int64_t) * woff.size());
+            st.d_boff.alloc(sizeof(int64_t) * boff.size());
+            st.d_blk.alloc(sizeof(int) * std::max<size_t>(1, hblk.size()));
+            st.d_ni.alloc(sizeof(int) * nb);
+            st.d_nj.alloc(sizeof(int) * nb);
+            st.d_xoff.alloc(sizeof(int64_t) * nb);
+            st.d_def.alloc(sizeof(int) * nb);
+            st.d_voff.alloc(sizeof(int64_t) * voff.size());
+            h2d(ctx, st.d_moff.p, moff.data(), st.d_moff.bytes);
+            h2d(ctx, st.d_woff.p, woff.data(), st.d_woff.bytes);
+            h2d(ctx, st.d_boff.p, boff.data(), st.d_boff.bytes);
+            h2d(ctx, st.d_blk.p, hblk.data(), sizeof(int) * hblk.size());
+            h2d(ctx, st.d_ni.p, hni.data(), sizeof(int) * nb);
+            h2d(ctx, st.d_nj.p, hnj.data(), sizeof(int) * nb);
+            h2d(ctx, st.d_xoff.p, xo.data(), sizeof(int64_t) * nb);
+            h2d(ctx, st.d_voff.p, voff.data(), st.d_voff.bytes);
+            // modelled seconds: the flops at ~15 TF/s plus the latency-bound
+            // launch chain (one panel + one trailing launch per NB columns)
+            const double m = st.max_m, n = st.max_n;
+            st.cost = nb * (2.0 * m * n * n + 4.0 * m * n * bs) / 15e12 + (2.0 * n / NB + 9.0 * n / 64) * 20e-6;
             st.p0 = p0;
             st.p1 = p1;
-            st.slot = sl;
             st.moff = std::move(moff);
             st.xo = std::move(xo);
             st.hni = std::move(hni);
             st.hnj = std::move(hnj);
-            st.d_boff = std::move(d_boff);
-            st.d_blk = std::move(d_blk);
-            st.d_ni = std::move(d_ni);
-            st.d_nj = std::move(d_nj);
-            st.d_moff = std::move(d_moff);
-            st.d_def = std::move(d_def);
+        }
+        // longest batch first onto the least-loaded slot
+        std::vector<std::vector<int>> slot_batches(nslots);
+        {
+            std::vector<int> order(batches.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int a, int b) { return states[a].cost > states[b].cost; });
+            std::vector<double> load(nslots, 0.0);
+            for (int bi : order) {
+                const int sl = int(std::min_element(load.begin(), load.end()) - load.begin());
+                load[sl] += states[bi].cost;
+                states[bi].slot = sl;
+                slot_batches[sl].push_back(bi);
+            }
+        }
+        std::vector<size_t> slot_mn(nslots, 0), slot_mk(nslots, 0);
+        for (size_t bi = 0; bi < batches.size(); ++bi) {
+            const auto [p0, p1] = batches[bi];
+            const size_t m = size_t(batch_ni[bi]) * bs, n = size_t(probs[bord[p0]].nj) * bs;
+            slot_mn[states[bi].slot] = std::max(slot_mn[states[bi].slot], size_t(p1 - p0) * m * n);
+            slot_mk[states[bi].slot] = std::max(slot_mk[states[bi].slot], size_t(p1 - p0) * m * bs);
+        }
+        (void)max_mn;
+        (void)max_mk;
+        std::vector<DevBuf> slot_M(nslots), slot_W(nslots);
+        std::vector<cudaStream_t> slot_s(nslots, nullptr);
+        cudaEvent_t ev_ready = nullptr;
+        LDGMG_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+        LDGMG_CUDA(cudaEventRecord(ev_ready, ctx.stream));  // d_At, d_X, the index arrays are ready
+        for (int sl = 0; sl < nslots; ++sl) {
+            slot_M[sl].alloc(sizeof(double) * (slot_mn[sl] + 2));
+            slot_W[sl].alloc(sizeof(double) * (slot_mk[sl] + 2));
+            LDGMG_CUDA(cudaStreamCreateWithFlags(&slot_s[sl], cudaStreamNonBlocking));
+            LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], ev_ready, 0));
+        }
+        // LDGMG_SAI_TIMING: per-batch start / end on the device clock
+        std::vector<cudaEvent_t> tev;
+        if (timing) {
+            tev.resize(2 * batches.size() + 1);
+            for (auto& e : tev) LDGMG_CUDA(cudaEventCreate(&e));
+            LDGMG_CUDA(cudaEventRecord(tev[0], ctx.stream));
+            for (int sl = 0; sl < nslots; ++sl) LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], tev[0], 0));
+        }
+        auto run_slot = [&](int sl) {
+            int dev = 0;
+            LDGMG_CUDA(cudaGetDevice(&dev));
+            Ctx bctx = ctx;
+            bctx.stream = slot_s[sl];
+            DevAsyncScope async_scope(bctx.stream);
+            DevBuf& d_M = slot_M[sl];
+            DevBuf& d_W = slot_W[sl];
+            for (int bi : slot_batches[sl]) {
+                BatchState& st = states[bi];
+                const int nb = st.p1 - st.p0;
+                if (timing) LDGMG_CUDA(cudaEventRecord(tev[1 + 2 * bi], bctx.stream));
+                const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
+                assemble_m_kernel<<<ga, 256, 0, bctx.stream>>>(d_At, stride, bs, st.d_blk.as<int>(),
+                                                             st.d_boff.as<int64_t>(), st.d_ni.as<int>(),
+                                                             st.d_nj.as<int>(), st.d_moff.as<int64_t>(),
+                                                             d_M.as<double>());
+                after_launch("assemble_m_kernel");
+                switch (st.path) {
+                    case 0:
+                        qr_gemm_batch<8>(bctx, d_M, st.d_moff, d_W, st.d_woff, d_X, st.d_xoff, st.d_ni, st.d_nj,
+                                         st.d_def, st.d_voff, bs, nb, st.max_m, st.max_n);
+                        break;
+                    case 1:
+                        qr_gemm_batch<4>(bctx, d_M, st.d_moff, d_W, st.d_woff, d_X, st.d_xoff, st.d_ni, st.d_nj,
+                                         st.d_def, st.d_voff, bs, nb, st.max_m, st.max_n);
+                        break;
+                    case 2:
+                        qr_blocked_batch<8>(bctx, d_M, st.d_moff, d_W, st.d_woff, d_X, st.d_xoff, st.d_ni, st.d_nj,
+                                            st.d_def, st.d_voff, st.hni, bs, nb, st.max_m, st.max_n);
+                        break;
+                    case 3:
+                        qr_blocked_batch<4>(bctx, d_M, st.d_moff, d_W, st.d_woff, d_X, st.d_xoff, st.d_ni, st.d_nj,
+                                            st.d_def, st.d_voff, st.hni, bs, nb, st.max_m, st.max_n);
+                        break;
+                    default:
+                        qr_ls_kernel<256><<<nb, 256, 0, bctx.stream>>>(
+                            d_M.as<double>(), st.d_moff.as<int64_t>(), d_W.as<double>(), st.d_woff.as<int64_t>(),
+                            d_X.as<double>(), st.d_xoff.as<int64_t>(), st.d_ni.as<int>(), st.d_nj.as<int>(), bs,
+                            st.d_def.as<int>());
+                        after_launch("qr_ls_kernel");
+                }
+                if (timing) LDGMG_CUDA(cudaEventRecord(tev[2 + 2 * bi], bctx.stream));
+            }
+            (void)dev;
+        };
+        {
+            std::vector<std::exception_ptr> errs(nslots);
+            std::vector<std::thread> th;
+            int dev = 0;
+            LDGMG_CUDA(cudaGetDevice(&dev));
+            for (int sl = 0; sl < nslots; ++sl)
+                th.emplace_back([&, sl] {
+                    try {
+                        LDGMG_CUDA(cudaSetDevice(dev));
+                        run_slot(sl);
+                    } catch (...) {
+                        errs[sl] = std::current_exception();
+                    }
+                });
+            for (auto& t : th) t.join();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
         }
         for (cudaStream_t st : slot_s) LDGMG_CUDA(cudaStreamSynchronize(st));
+        if (timing) {
+            for (size_t bi = 0; bi < batches.size(); ++bi) {
+                float t0 = 0.f, t1 = 0.f;
+                LDGMG_CUDA(cudaEventElapsedTime(&t0, tev[0], tev[1 + 2 * bi]));
+                LDGMG_CUDA(cudaEventElapsedTime(&t1, tev[0], tev[2 + 2 * bi]));
+                fprintf(stderr, "[sai batch %zu] slot %d problems %d m %d n %d: %8.2f -> %8.2f ms (%7.2f ms)\n", bi,
+                        states[bi].slot, batches[bi].second - batches[bi].first, batch_ni[bi] * bs,
+                        probs[bord[batches[bi].first]].nj * bs, t0, t1, t1 - t0);
+            }
+            for (auto e : tev) cudaEventDestroy(e);
+        }
         stamp("QR least squares (all batches)");
         // rank-deficient problems: minimum-norm refit from a fresh copy of M
         // (on the context stream, slot 0's workspace)
@@ -1452,7 +1546,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             const std::vector<int>& hnj = st.hnj;
             const std::vector<int64_t>& moff = st.moff;
             const std::vector<int64_t>& xo = st.xo;
-            DevBuf& d_M = slot_M[0];
+            DevBuf d_M;  // a fresh copy of the batch's M (only when a refit is needed)
             const dim3 ga(std::max(1, std::min(64, ctx.num_sms)), nb);
             DevBuf &d_blk = st.d_blk, &d_boff = st.d_boff, &d_ni = st.d_ni, &d_nj = st.d_nj, &d_moff = st.d_moff,
                    &d_def = st.d_def;
@@ -1463,6 +1557,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             for (int i = 0; i < nb; ++i)
                 if (def[i]) defl.push_back(i);
             if (!defl.empty()) {
+                d_M.alloc(sizeof(double) * size_t(std::max<int64_t>(1, moff.back())));
                 assemble_m_kernel<<<ga, 256, 0, ctx.stream>>>(d_At, stride, bs, d_blk.as<int>(),
                                                              d_boff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(),
                                                              d_moff.as<int64_t>(), d_M.as<double>());

@@ -5,8 +5,10 @@ shared mailbox.  Lets the partitioned V-cycle's GPU path (device setup,
 ghost exchange with the interior/boundary overlap split, transposed views,
 processor-block GS) run with P > 1 where only one GPU exists.  Transfers are
 device-to-device copies after a device synchronisation -- correctness only,
-no NVLink timing."""
+no NVLink timing.  Every value crosses threads as a HOST copy made after a
+device synchronisation, so no rank's stream reads another rank's memory."""
 import threading
+import traceback
 
 import torch
 
@@ -58,19 +60,27 @@ class FakeDist:
         return True
 
     # point to point ---------------------------------------------------------
+    # two DISTINCT functions: P2POp.op is compared against them to tell the
+    # sends from the receives of a batch
     def isend(self, *a, **k):
         raise RuntimeError("use batch_isend_irecv")
 
-    irecv = isend
+    def irecv(self, *a, **k):
+        raise RuntimeError("use batch_isend_irecv")
 
     def batch_isend_irecv(self, ops):
         torch.cuda.synchronize()  # the packed send buffers are complete
+        # host copies: a device clone made on this rank's stream could be read
+        # by the receiving thread's stream before it completes (and its
+        # memory recycled by this rank's allocator stream)
+        sends = [(o.peer, o.tensor.detach().cpu().clone(), "".join(traceback.format_stack(limit=8)[:-1]))
+                 for o in ops if o.op == self.isend]
         with self.w.cv:
-            for o in ops:
-                if o.op == self.isend:
-                    self.w.mail.setdefault((self.rank, o.peer), []).append(o.tensor.clone())
+            for peer, t, where in sends:
+                self.w.mail.setdefault((self.rank, peer), []).append((t, where))
             self.w.cv.notify_all()
         recvs = [o for o in ops if o.op == self.irecv]
+        here = "".join(traceback.format_stack(limit=8)[:-1])
 
         def finish():
             for o in recvs:
@@ -79,7 +89,10 @@ class FakeDist:
                     ok = self.w.cv.wait_for(lambda: self.w.mail.get(key), timeout=self.w.timeout)
                     if not ok:
                         raise TimeoutError(f"rank {self.rank}: no message from {o.peer}")
-                    t = self.w.mail[key].pop(0)
+                    t, where = self.w.mail[key].pop(0)
+                if t.numel() != o.tensor.numel():
+                    raise RuntimeError(f"rank {self.rank} <- {o.peer}: message of {t.numel()} values for a "
+                                       f"{o.tensor.numel()}-value receive\n-- sent at:\n{where}\n-- received at:\n{here}")
                 o.tensor.copy_(t)
             torch.cuda.synchronize()
         return [_Work(finish)]
@@ -103,14 +116,14 @@ class FakeDist:
 
     def all_gather(self, out, tensor, group=None):
         torch.cuda.synchronize()
-        vals = self._gather(tensor.clone())
+        vals = self._gather(tensor.detach().cpu().clone())
         for o, v in zip(out, vals):
             o.copy_(v)
         torch.cuda.synchronize()
 
     def all_reduce(self, tensor, op="sum", group=None):
         torch.cuda.synchronize()
-        vals = self._gather(tensor.clone())
+        vals = self._gather(tensor.detach().cpu().clone())
         acc = vals[0].clone()
         for v in vals[1:]:
             acc = acc + v if op == "sum" else (torch.minimum(acc, v) if op == "min" else torch.maximum(acc, v))
@@ -119,7 +132,7 @@ class FakeDist:
 
     def broadcast(self, tensor, src=0, group=None):
         torch.cuda.synchronize()
-        vals = self._gather(tensor.clone())
+        vals = self._gather(tensor.detach().cpu().clone())
         tensor.copy_(vals[src])
         torch.cuda.synchronize()
 
