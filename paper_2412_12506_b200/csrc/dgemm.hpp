@@ -18,6 +18,15 @@ struct GemmNT {
     int64_t ldd, sD;
     int M, N, K;
     double alpha, beta;
+    // optional second segment of the N index: rows n >= nsplit of B and
+    // columns n >= nsplit of D live at B2 + (n - nsplit) ldb (batch stride
+    // sB2) and D2 + (n - nsplit) ldd (sD2) -- one launch for the trailing
+    // columns of M and the right-hand sides W of the QR update
+    const double* B2 = nullptr;
+    int64_t sB2 = 0;
+    double* D2 = nullptr;
+    int64_t sD2 = 0;
+    int nsplit = 1 << 30;
 };
 void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch);
 

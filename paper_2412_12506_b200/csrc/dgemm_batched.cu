@@ -62,7 +62,8 @@ struct Cfg {
 /// rows [r0, r0+ROWS) x k [k0, k0+BK) of an operand into a padded [row][k]
 /// tile; zero fill outside the matrix.
 template <int ROWS, int BK, int LDK, int THREADS, bool VEC>
-__device__ __forceinline__ void load_tile(double* s, const double* G, int64_t ld, int rows, int K, int r0, int k0) {
+__device__ __forceinline__ void load_tile(double* s, const double* G, int64_t ld, int rows, int K, int r0, int k0,
+                                          const double* G2 = nullptr, int split = 1 << 30) {
     constexpr int PER = VEC ? 2 : 1;                 // doubles per copy
     constexpr int COPIES = ROWS * BK / PER;          // copies per tile
     static_assert(COPIES % THREADS == 0, "tile copies divide over the threads");
@@ -73,7 +74,9 @@ __device__ __forceinline__ void load_tile(double* s, const double* G, int64_t ld
         const int r = id / CPR, kk = (id - r * CPR) * PER;
         const int k = k0 + kk;
         const bool rv = r0 + r < rows;
-        const double* src = G + (rv ? int64_t(r0 + r) * ld : 0) + (rv && k < K ? k : 0);
+        // rows past `split` come from the second segment (G2 is pre-offset)
+        const double* base = r0 + r < split ? G : G2;
+        const double* src = rv ? base + int64_t(r0 + r) * ld + (k < K ? k : 0) : G;
         if constexpr (VEC) {
             const int bytes = (rv && k < K) ? (k + 1 < K ? 16 : 8) : 0;
             cp_async16(s + r * LDK + kk, src, bytes);
@@ -95,6 +98,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
     const double* A = g.A + int64_t(b) * g.sA;
     const double* B = g.B + int64_t(b) * g.sB;
     double* D = g.D + int64_t(b) * g.sD;
+    // second N segment, offset so that row / column n indexes it directly
+    const double* B2 = g.B2 ? g.B2 + int64_t(b) * g.sB2 - int64_t(g.nsplit) * g.ldb : B;
+    double* D2 = g.D2 ? g.D2 + int64_t(b) * g.sD2 - int64_t(g.nsplit) * g.ldd : D;
+    const int bsplit = g.B2 ? g.nsplit : 1 << 30;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = (warp / WN) * (TM * 8), wn = (warp % WN) * (TN * 8);
@@ -104,13 +111,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) {
             load_tile<BM, BK, LDK, THREADS, VEC>(sA + s * BM * LDK, A, g.lda, g.M, g.K, m0, s * BK);
-            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, s * BK);
+            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, s * BK, B2, bsplit);
         }
         cp_async_commit();
     }
     // D prefetch (beta != 0): in flight during the whole K loop
     double dold[BETA ? TM : 1][BETA ? TN : 1][2];
-    constexpr bool use_d = BETA;
     if constexpr (BETA)
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -119,7 +125,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int m = m0 + wm + i * 8 + fr, n = n0 + wn + j * 8 + fk * 2 + h;
-                if constexpr (BETA) dold[i][j][h] = (m < g.M && n < g.N) ? D[m + int64_t(n) * g.ldd] : 0.0;
+                const double* Dn = n < g.nsplit ? D : D2;
+                dold[i][j][h] = (m < g.M && n < g.N) ? Dn[m + int64_t(n) * g.ldd] : 0.0;
             }
     double acc[TM][TN][2];
 #pragma unroll
@@ -133,7 +140,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
         if (nxt < nk) {
             const int s = nxt % STAGES;
             load_tile<BM, BK, LDK, THREADS, VEC>(sA + s * BM * LDK, A, g.lda, g.M, g.K, m0, nxt * BK);
-            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, nxt * BK);
+            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, nxt * BK, B2, bsplit);
         }
         cp_async_commit();
         const double* tA = sA + (kt % STAGES) * BM * LDK + (wm + fr) * LDK + fk;
@@ -161,11 +168,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int n = n0 + wn + j * 8 + fk * 2 + h;
+                double* Dn = n < g.nsplit ? D : D2;
                 if (m < g.M && n < g.N) {
-                    if constexpr (use_d)
-                        D[m + int64_t(n) * g.ldd] = g.alpha * acc[i][j][h] + g.beta * dold[i][j][h];
-                    else
-                        D[m + int64_t(n) * g.ldd] = g.alpha * acc[i][j][h];
+                    double v = g.alpha * acc[i][j][h];
+                    if constexpr (BETA) v += g.beta * dold[i][j][h];
+                    Dn[m + int64_t(n) * g.ldd] = v;
                 }
             }
     }
@@ -194,7 +201,7 @@ void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch) {
     require(batch <= 65535, "dgemm_nt_batched: batch above 65535");
     // 16-byte copies need every operand row to start 16-byte aligned
     const bool vec = aligned16(g.A) && aligned16(g.B) && !(g.lda & 1) && !(g.ldb & 1) && !(g.sA & 1) &&
-                     !(g.sB & 1);
+                     !(g.sB & 1) && (!g.B2 || (aligned16(g.B2) && !(g.sB2 & 1)));
     static int variant = -1;
     if (variant < 0) {
         const char* e = std::getenv("LDGMG_DGEMM_VARIANT");  // measurement only (tools/dgemm_bench.py)
@@ -210,7 +217,11 @@ void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch) {
     }
     // default: 64 x 64 tiles, 4 warps, 3 stages -- measured best on every
     // product of the C5 QR (tools/dgemm_bench.py, B200: V^T C 30.7, Gram
-    // 20.9, T^T Y 21.7, C -= V Z 20.1 TF/s; 128-row tiles 15-19 TF/s)
+    // 20.9, T^T Y 21.7, C -= V Z 20.1 TF/s; 128-row tiles 15-19 TF/s).  The
+    // K = 64 update is bound by its per-tile pipeline fill and barriers, not
+    // by the 194 registers of the D prefetch: the accumulators seeded with D
+    // (128 registers, 3 CTAs per SM) measured 6 % slower, D staged in shared
+    // memory by bulk copies (2 stages) 11 % slower
     launch<64, 64, 2, 2, 16, 3>(ctx, g, batch, vec);
 }
 

@@ -256,27 +256,52 @@ __global__ void __launch_bounds__(NT) qr_ls_kernel(double* __restrict__ Ms, cons
 // Per panel the trailing block is read twice and written once: 24 B per
 // element, NB-fold less than the unblocked column-by-column kernel.
 // ---------------------------------------------------------------------------
-template <int NT>
-__global__ void __launch_bounds__(NT) qr_init_kernel(const double* __restrict__ Ms, const int64_t* __restrict__ moff,
-                                                     double* __restrict__ Ws, const int64_t* __restrict__ woff,
-                                                     const int* __restrict__ ni, const int* __restrict__ nj, int bs,
-                                                     double* __restrict__ tol_out, int* __restrict__ deficient) {
-    __shared__ double red[NT / 32];
-    const int p = blockIdx.x;
+/// W = E and the partial sums of ||M||_F^2, INIT_SLICES CTAs per problem
+/// (grid-strided slices, fixed order), then qr_tol_kernel adds the slices in
+/// order: tol = 1e-12 ||M||_F (the rank test of dgels' caller, blockla.hpp).
+constexpr int INIT_SLICES = 32;
+__global__ void __launch_bounds__(256) qr_init_kernel(const double* __restrict__ Ms, const int64_t* __restrict__ moff,
+                                                      double* __restrict__ Ws, const int64_t* __restrict__ woff,
+                                                      const int* __restrict__ ni, const int* __restrict__ nj, int bs,
+                                                      double* __restrict__ part) {
+    __shared__ double red[8];
+    const int p = blockIdx.y, x = blockIdx.x;
     const int m = ni[p] * bs, n = nj[p] * bs, k = bs;
     const double* M = Ms + moff[p];
     double* W = Ws + woff[p];
-    for (int64_t t = threadIdx.x; t < int64_t(m) * k; t += NT) {
+    const int64_t stride = int64_t(INIT_SLICES) * 256;
+    for (int64_t t = int64_t(x) * 256 + threadIdx.x; t < int64_t(m) * k; t += stride) {
         const int c = int(t / m), r = int(t - int64_t(c) * m);
         W[t] = r == c ? 1.0 : 0.0;
     }
     double acc = 0.0;
-    for (int64_t t = threadIdx.x; t < int64_t(m) * n; t += NT) acc += M[t] * M[t];
-    acc = block_sum<NT>(acc, red);
-    if (threadIdx.x == 0) {
-        tol_out[p] = 1e-12 * sqrt(acc);
-        deficient[p] = 0;
-    }
+    for (int64_t t = int64_t(x) * 256 + threadIdx.x; t < int64_t(m) * n; t += stride) acc += M[t] * M[t];
+    acc = block_sum<256>(acc, red);
+    if (threadIdx.x == 0) part[int64_t(p) * INIT_SLICES + x] = acc;
+}
+
+__global__ void qr_tol_kernel(const double* __restrict__ part, int nb, double* __restrict__ tol_out,
+                              int* __restrict__ deficient) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nb) return;
+    double s = 0.0;
+    for (int x = 0; x < INIT_SLICES; ++x) s += part[int64_t(p) * INIT_SLICES + x];
+    tol_out[p] = 1e-12 * sqrt(s);
+    deficient[p] = 0;
+}
+
+/// qr_init_kernel + qr_tol_kernel for a batch.
+void qr_init(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff, DevBuf& d_ni, DevBuf& d_nj, int bs,
+             int nb, DevBuf& d_tol, DevBuf& d_def) {
+    DevBuf d_part(sizeof(double) * size_t(nb) * INIT_SLICES);
+    qr_init_kernel<<<dim3(INIT_SLICES, nb), 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
+                                                                   d_W.as<double>(), d_woff.as<int64_t>(),
+                                                                   d_ni.as<int>(), d_nj.as<int>(), bs,
+                                                                   d_part.as<double>());
+    after_launch("qr_init_kernel");
+    qr_tol_kernel<<<div_up(nb, 128), 128, 0, ctx.stream>>>(d_part.as<double>(), nb, d_tol.as<double>(),
+                                                          d_def.as<int>());
+    after_launch("qr_tol_kernel");
 }
 
 template <int NT, int NB>
@@ -869,10 +894,7 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
     for (int i = 0; i < nb; ++i) vtotal += int64_t(hni[i]) * bs * NB;
     DevBuf d_V(sizeof(double) * std::max<int64_t>(1, vtotal)), d_T(sizeof(double) * size_t(nb) * NB * NB),
         d_tol(sizeof(double) * nb);
-    qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
-                                                    d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
-                                                    d_tol.as<double>(), d_def.as<int>());
-    after_launch("qr_init_kernel");
+    qr_init(ctx, d_M, d_moff, d_W, d_woff, d_ni, d_nj, bs, nb, d_tol, d_def);
     const size_t smem = sizeof(double) * size_t(max_m) * NB;
     ensure_dyn_smem(qr_panel_kernel<256, NB>, size_t(smem));
     if (getenv("LDGMG_SAI_TIMING") && atoi(getenv("LDGMG_SAI_TIMING")))
@@ -943,10 +965,7 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
         d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k)),
         d_VbT(sizeof(double) * size_t(nb) * m * WB);
     
-    qr_init_kernel<256><<<nb, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(),
-                                                    d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs,
-                                                    d_tol.as<double>(), d_def.as<int>());
-    after_launch("qr_init_kernel");
+    qr_init(ctx, d_M, d_moff, d_W, d_woff, d_ni, d_nj, bs, nb, d_tol, d_def);
     const size_t psmem = sizeof(double) * size_t(m) * NB;
     ensure_dyn_smem(qr_panel_kernel<256, NB>, psmem);
     if (getenv("LDGMG_SAI_TIMING") && atoi(getenv("LDGMG_SAI_TIMING")))
@@ -992,33 +1011,34 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
         qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(d_G.as<double>(), d_tau.as<double>(), WB, d_Tb.as<double>(), w,
                                                     sG);
         after_launch("qr_wide_t_kernel");
-        // C -= V (T^T (V^T C)) on the trailing columns of M and on W
-        struct Part {
-            double* C;
-            long long stride;
-            int cols;
-        };
-        const Part parts[2] = {{M + jb + size_t(jb + w) * m, sM, n - jb - w}, {W + jb, sW, k}};
-        bool vt = false;
-        for (const Part& pt : parts) {
-            if (pt.cols <= 0) continue;
-            if (!vt) {  // row-major reflectors for the C -= V Z product
-                transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
-                    Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV);
-                after_launch("transpose_panel_kernel");
-                vt = true;
-            }
-            double* Y = d_Y.as<double>();
-            double* Z = d_Z.as<double>();
-            // Y = V^T C   (w x cols, k = mrb)
-            dgemm_nt_batched(ctx, GemmNT{Vb, mrb, sV, pt.C, m, pt.stride, Y, w, sY, w, pt.cols, mrb, 1.0, 0.0}, nb);
-            // Z = T^T Y   (w x cols, k = w)
-            dgemm_nt_batched(ctx, GemmNT{d_Tb.as<double>(), w, sG, Y, w, sY, Z, w, sY, w, pt.cols, w, 1.0, 0.0}, nb);
-            // C -= V Z    (mrb x cols, k = w)
-            dgemm_nt_batched(ctx, GemmNT{d_VbT.as<double>(), WB, sV, Z, w, sY, pt.C, m, pt.stride, mrb, pt.cols, w,
-                                         -1.0, 1.0},
-                             nb);
+        // C -= V (T^T (V^T C)) on the trailing columns of M and on W, ONE
+        // launch per product: the N index runs over M's trailing columns,
+        // then (second segment) the k right-hand sides
+        const int nM = n - jb - w, ncols = nM + k;
+        double* CM = M + jb + size_t(jb + w) * m;
+        double* CW = W + jb;
+        transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
+            Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV);
+        after_launch("transpose_panel_kernel");
+        double* Y = d_Y.as<double>();
+        double* Z = d_Z.as<double>();
+        GemmNT gy{Vb, mrb, sV, nM > 0 ? CM : CW, m, nM > 0 ? sM : sW, Y, w, sY, w, ncols, mrb, 1.0, 0.0};
+        if (nM > 0) {
+            gy.B2 = CW;
+            gy.sB2 = sW;
+            gy.nsplit = nM;
         }
+        dgemm_nt_batched(ctx, gy, nb);  // Y = V^T C   (w x ncols, k = mrb)
+        dgemm_nt_batched(ctx, GemmNT{d_Tb.as<double>(), w, sG, Y, w, sY, Z, w, sY, w, ncols, w, 1.0, 0.0},
+                         nb);  // Z = T^T Y
+        GemmNT gu{d_VbT.as<double>(), WB, sV, Z, w, sY, nM > 0 ? CM : CW, m, nM > 0 ? sM : sW, mrb, ncols, w,
+                  -1.0, 1.0};
+        if (nM > 0) {
+            gu.D2 = CW;
+            gu.sD2 = sW;
+            gu.nsplit = nM;
+        }
+        dgemm_nt_batched(ctx, gu, nb);  // C -= V Z   (mrb x ncols, k = w)
     }
     constexpr int CB = 16;
     qr_backsub_kernel<CB><<<dim3(div_up(bs, CB), nb), 256, 0, ctx.stream>>>(
@@ -1338,8 +1358,12 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         // is full then holds back only its own thread).  Temporaries inside a
         // batch are stream-ordered (DevAsyncScope).  The rank-deficient
         // refits follow after all batches.
-        constexpr int kSlots = 4;
-        const int nslots = int(std::min<size_t>(size_t(kSlots), batches.size()));
+        // up to kSlots concurrent batches (every batch its own stream when
+        // they fit: the small batches' latency-bound chains then run beside
+        // the large ones instead of after them), fewer when the workspaces
+        // would not fit in 40 % of the free device memory
+        constexpr int kSlots = 8;
+        int nslots = int(std::min<size_t>(size_t(kSlots), batches.size()));
         struct BatchState {
             int p0 = 0, p1 = 0, slot = 0, path = 0, max_m = 0, max_n = 0;
             double cost = 0.0;
@@ -1417,9 +1441,14 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             st.hni = std::move(hni);
             st.hnj = std::move(hnj);
         }
+        stamp("QR batch index uploads");
         // longest batch first onto the least-loaded slot
-        std::vector<std::vector<int>> slot_batches(nslots);
-        {
+        std::vector<std::vector<int>> slot_batches;
+        std::vector<size_t> slot_mn, slot_mk;
+        size_t free_b = 0, total_b = 0;
+        LDGMG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        for (;; --nslots) {
+            slot_batches.assign(nslots, {});
             std::vector<int> order(batches.size());
             for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
             std::stable_sort(order.begin(), order.end(),
@@ -1431,13 +1460,20 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 states[bi].slot = sl;
                 slot_batches[sl].push_back(bi);
             }
-        }
-        std::vector<size_t> slot_mn(nslots, 0), slot_mk(nslots, 0);
-        for (size_t bi = 0; bi < batches.size(); ++bi) {
-            const auto [p0, p1] = batches[bi];
-            const size_t m = size_t(batch_ni[bi]) * bs, n = size_t(probs[bord[p0]].nj) * bs;
-            slot_mn[states[bi].slot] = std::max(slot_mn[states[bi].slot], size_t(p1 - p0) * m * n);
-            slot_mk[states[bi].slot] = std::max(slot_mk[states[bi].slot], size_t(p1 - p0) * m * bs);
+            slot_mn.assign(nslots, 0);
+            slot_mk.assign(nslots, 0);
+            size_t work = 0;  // + the per-batch temporaries (reflector blocks, Y, Z)
+            std::vector<size_t> slot_tmp(nslots, 0);
+            for (size_t bi = 0; bi < batches.size(); ++bi) {
+                const auto [p0, p1] = batches[bi];
+                const size_t m = size_t(batch_ni[bi]) * bs, n = size_t(probs[bord[p0]].nj) * bs;
+                const int sl = states[bi].slot;
+                slot_mn[sl] = std::max(slot_mn[sl], size_t(p1 - p0) * m * n);
+                slot_mk[sl] = std::max(slot_mk[sl], size_t(p1 - p0) * m * bs);
+                slot_tmp[sl] = std::max(slot_tmp[sl], size_t(p1 - p0) * (3 * m * 64 + 2 * 64 * (n + bs)));
+            }
+            for (int sl = 0; sl < nslots; ++sl) work += sizeof(double) * (slot_mn[sl] + slot_mk[sl] + slot_tmp[sl]);
+            if (nslots == 1 || work <= free_b / 10 * 4) break;
         }
         (void)max_mn;
         (void)max_mk;
@@ -1452,6 +1488,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             LDGMG_CUDA(cudaStreamCreateWithFlags(&slot_s[sl], cudaStreamNonBlocking));
             LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], ev_ready, 0));
         }
+        stamp("QR slot workspaces");
         // LDGMG_SAI_TIMING: per-batch start / end on the device clock
         std::vector<cudaEvent_t> tev;
         if (timing) {
