@@ -18,15 +18,19 @@ struct GemmNT {
     int64_t ldd, sD;
     int M, N, K;
     double alpha, beta;
-    // optional second segment of the N index: rows n >= nsplit of B and
-    // columns n >= nsplit of D live at B2 + (n - nsplit) ldb (batch stride
-    // sB2) and D2 + (n - nsplit) ldd (sD2) -- one launch for the trailing
-    // columns of M and the right-hand sides W of the QR update
+    // optional further segments of the N index: rows n of B with
+    // nsplit <= n < nsplit2 live at B2 + (n - nsplit) ldb (batch stride sB2),
+    // those with n >= nsplit2 at B3 + (n - nsplit2) ldb (sB3); columns n >=
+    // nsplit of D at D2 + (n - nsplit) ldd (sD2) -- one launch for the QR's
+    // reflector Gram, the trailing columns of M and the right-hand sides W
     const double* B2 = nullptr;
     int64_t sB2 = 0;
     double* D2 = nullptr;
     int64_t sD2 = 0;
     int nsplit = 1 << 30;
+    const double* B3 = nullptr;
+    int64_t sB3 = 0;
+    int nsplit2 = 1 << 30;
 };
 void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch);
 

@@ -63,7 +63,8 @@ struct Cfg {
 /// tile; zero fill outside the matrix.
 template <int ROWS, int BK, int LDK, int THREADS, bool VEC>
 __device__ __forceinline__ void load_tile(double* s, const double* G, int64_t ld, int rows, int K, int r0, int k0,
-                                          const double* G2 = nullptr, int split = 1 << 30) {
+                                          const double* G2 = nullptr, int split = 1 << 30,
+                                          const double* G3 = nullptr, int split2 = 1 << 30) {
     constexpr int PER = VEC ? 2 : 1;                 // doubles per copy
     constexpr int COPIES = ROWS * BK / PER;          // copies per tile
     static_assert(COPIES % THREADS == 0, "tile copies divide over the threads");
@@ -74,8 +75,8 @@ __device__ __forceinline__ void load_tile(double* s, const double* G, int64_t ld
         const int r = id / CPR, kk = (id - r * CPR) * PER;
         const int k = k0 + kk;
         const bool rv = r0 + r < rows;
-        // rows past `split` come from the second segment (G2 is pre-offset)
-        const double* base = r0 + r < split ? G : G2;
+        // rows past `split` / `split2` come from the second / third segment (pre-offset)
+        const double* base = r0 + r < split ? G : r0 + r < split2 ? G2 : G3;
         const double* src = rv ? base + int64_t(r0 + r) * ld + (k < K ? k : 0) : G;
         if constexpr (VEC) {
             const int bytes = (rv && k < K) ? (k + 1 < K ? 16 : 8) : 0;
@@ -98,10 +99,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
     const double* A = g.A + int64_t(b) * g.sA;
     const double* B = g.B + int64_t(b) * g.sB;
     double* D = g.D + int64_t(b) * g.sD;
-    // second N segment, offset so that row / column n indexes it directly
+    // second / third N segments, offset so that row / column n indexes them directly
     const double* B2 = g.B2 ? g.B2 + int64_t(b) * g.sB2 - int64_t(g.nsplit) * g.ldb : B;
     double* D2 = g.D2 ? g.D2 + int64_t(b) * g.sD2 - int64_t(g.nsplit) * g.ldd : D;
-    const int bsplit = g.B2 ? g.nsplit : 1 << 30;
+    const double* B3 = g.B3 ? g.B3 + int64_t(b) * g.sB3 - int64_t(g.nsplit2) * g.ldb : B2;
+    const int bsplit = g.B2 ? g.nsplit : 1 << 30, bsplit2 = g.B3 ? g.nsplit2 : 1 << 30;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = (warp / WN) * (TM * 8), wn = (warp % WN) * (TN * 8);
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) {
             load_tile<BM, BK, LDK, THREADS, VEC>(sA + s * BM * LDK, A, g.lda, g.M, g.K, m0, s * BK);
-            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, s * BK, B2, bsplit);
+            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, s * BK, B2, bsplit, B3, bsplit2);
         }
         cp_async_commit();
     }
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, BK, STAGES>::THREADS)
         if (nxt < nk) {
             const int s = nxt % STAGES;
             load_tile<BM, BK, LDK, THREADS, VEC>(sA + s * BM * LDK, A, g.lda, g.M, g.K, m0, nxt * BK);
-            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, nxt * BK, B2, bsplit);
+            load_tile<BN, BK, LDK, THREADS, VEC>(sB + s * BN * LDK, B, g.ldb, g.N, g.K, n0, nxt * BK, B2, bsplit, B3, bsplit2);
         }
         cp_async_commit();
         const double* tA = sA + (kt % STAGES) * BM * LDK + (wm + fr) * LDK + fk;
@@ -201,7 +203,8 @@ void dgemm_nt_batched(Ctx& ctx, const GemmNT& g, int batch) {
     require(batch <= 65535, "dgemm_nt_batched: batch above 65535");
     // 16-byte copies need every operand row to start 16-byte aligned
     const bool vec = aligned16(g.A) && aligned16(g.B) && !(g.lda & 1) && !(g.ldb & 1) && !(g.sA & 1) &&
-                     !(g.sB & 1) && (!g.B2 || (aligned16(g.B2) && !(g.sB2 & 1)));
+                     !(g.sB & 1) && (!g.B2 || (aligned16(g.B2) && !(g.sB2 & 1))) &&
+                     (!g.B3 || (aligned16(g.B3) && !(g.sB3 & 1)));
     static int variant = -1;
     if (variant < 0) {
         const char* e = std::getenv("LDGMG_DGEMM_VARIANT");  // measurement only (tools/dgemm_bench.py)

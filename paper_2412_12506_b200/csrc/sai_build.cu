@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
                                                       const int64_t* __restrict__ voff, double* __restrict__ Tg,
                                                       int* __restrict__ deficient, double* __restrict__ Vbig = nullptr,
                                                       int ldbig = 0, int64_t bigstride = 0, int bigcol = 0,
-                                                      double* __restrict__ taus = nullptr, int taustride = 0) {
+                                                      double* __restrict__ taus = nullptr, int taustride = 0,
+                                                      int ldv = 0) {
     extern __shared__ __align__(16) double Vp[];  // mr x NB panel, column-major (row j0 stored at 0)
     __shared__ double red[NT / 32];
     __shared__ double sT[NB * NB], stau[NB], sh_beta;
@@ -395,12 +396,14 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
         V[t] = (c < nb && r >= c) ? Vp[size_t(c) * mr + r] : 0.0;
     }
     for (int t = tid; t < NB * NB; t += NT) Tg[size_t(p) * NB * NB + t] = sT[t];
-    if (Vbig) {  // also into the wide panel: columns bigcol.., rows shifted by bigcol (zeros above)
-        double* VB = Vbig + size_t(p) * bigstride + size_t(bigcol) * ldbig;
+    if (Vbig) {  // also into the wide panel (ldbig rows, leading dimension ldv): columns bigcol.., rows
+                 // shifted by bigcol (zeros above)
+        if (!ldv) ldv = ldbig;
+        double* VB = Vbig + size_t(p) * bigstride + size_t(bigcol) * ldv;
         for (int t = tid; t < ldbig * nb; t += NT) {
             const int c = t / ldbig, r = t - c * ldbig;
             const int rr = r - bigcol;  // row within this panel
-            VB[size_t(c) * ldbig + r] = (rr >= c && rr < mr) ? Vp[size_t(c) * mr + rr] : 0.0;
+            VB[size_t(c) * ldv + r] = (rr >= c && rr < mr) ? Vp[size_t(c) * mr + rr] : 0.0;
         }
         for (int t = tid; t < nb; t += NT) taus[size_t(p) * taustride + bigcol + t] = stau[t];
     }
@@ -624,10 +627,10 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
 /// T of the wide compact-WY panel (dlarft, forward / columnwise) from the
 /// Gram matrix G = V^T V of its reflectors and their taus: T(i,i) = tau_i,
 /// T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i).  One CTA per problem, column-major.
-__global__ void qr_wide_t_kernel(const double* __restrict__ G, const double* __restrict__ taus, int taustride,
-                                 double* __restrict__ T, int w, int64_t mstride) {
+__global__ void qr_wide_t_kernel(const double* __restrict__ G, int64_t gstride, const double* __restrict__ taus,
+                                 int taustride, double* __restrict__ T, int w, int64_t mstride) {
     const int p = blockIdx.x;
-    const double* Gp = G + size_t(p) * mstride;  // w x w, ld w, problem stride mstride
+    const double* Gp = G + size_t(p) * gstride;  // w x w, ld w, problem stride gstride
     const double* tp = taus + size_t(p) * taustride;
     double* Tp = T + size_t(p) * mstride;
     for (int t = threadIdx.x; t < w * w; t += blockDim.x) Tp[t] = 0.0;
@@ -645,11 +648,12 @@ __global__ void qr_wide_t_kernel(const double* __restrict__ G, const double* __r
 }
 
 /// Row-major copy of the wide panel's reflectors (VT(r, c) at r * ldt + c
-/// = V(r, c), V column-major mr x w with leading dimension mr), so the
+/// = V(r, c), V column-major mr x w with leading dimension ldv), so the
 /// update C -= V Z reads V with its reflector index contiguous (the GEMM's
 /// k index).  32x32 tiles through shared memory, problem = blockIdx.z.
 __global__ void __launch_bounds__(256) transpose_panel_kernel(const double* __restrict__ V, int64_t sV, int mr,
-                                                              int w, double* __restrict__ VT, int ldt, int64_t sT) {
+                                                              int w, double* __restrict__ VT, int ldt, int64_t sT,
+                                                              int ldv) {
     __shared__ double t[32][33];
     const double* Vp = V + int64_t(blockIdx.z) * sV;
     double* Tp = VT + int64_t(blockIdx.z) * sT;
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(256) transpose_panel_kernel(const double* __re
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int c = ty; c < 32; c += 8) {
         const int rr = r0 + tx, cc = c0 + c;
-        t[c][tx] = (rr < mr && cc < w) ? Vp[int64_t(cc) * mr + rr] : 0.0;
+        t[c][tx] = (rr < mr && cc < w) ? Vp[int64_t(cc) * ldv + rr] : 0.0;
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
@@ -960,10 +964,9 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
     // d_voff (uploaded by the caller): voff[i] = i * m * NB
     DevBuf d_V(sizeof(double) * std::max<int64_t>(1, int64_t(nb) * m * NB)),
         d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
-        d_Vb(sizeof(double) * size_t(nb) * m * WB), d_G(sizeof(double) * size_t(nb) * WB * WB),
-        d_Tb(sizeof(double) * size_t(nb) * WB * WB), d_tau(sizeof(double) * size_t(nb) * WB),
-        d_Y(sizeof(double) * size_t(nb) * WB * (n + k)), d_Z(sizeof(double) * size_t(nb) * WB * (n + k)),
-        d_VbT(sizeof(double) * size_t(nb) * m * WB);
+        d_Vb(sizeof(double) * size_t(nb) * m * WB), d_Tb(sizeof(double) * size_t(nb) * WB * WB),
+        d_tau(sizeof(double) * size_t(nb) * WB), d_Y(sizeof(double) * size_t(nb) * WB * (WB + n + k)),
+        d_Z(sizeof(double) * size_t(nb) * WB * (n + k)), d_VbT(sizeof(double) * size_t(nb) * m * WB);
     
     qr_init(ctx, d_M, d_moff, d_W, d_woff, d_ni, d_nj, bs, nb, d_tol, d_def);
     const size_t psmem = sizeof(double) * size_t(m) * NB;
@@ -975,7 +978,7 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
     double* M = d_M.as<double>();
     double* W = d_W.as<double>();
     const long long sM = (long long)m * n, sW = (long long)m * k, sV = (long long)m * WB, sG = WB * WB,
-                    sY = (long long)WB * (n + k);
+                    sY = (long long)WB * (WB + n + k), sZ = (long long)WB * (n + k);
     for (int jb = 0; jb < n; jb += WB) {
         const int w = std::min(WB, n - jb), mrb = m - jb;
         for (int s0 = 0; s0 < w; s0 += NB) {
@@ -983,7 +986,7 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
             qr_panel_kernel<256, NB><<<nb, 256, psmem, ctx.stream>>>(
                 M, d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(), d_V.as<double>(),
                 d_voff.as<int64_t>(), d_T.as<double>(), d_def.as<int>(), d_Vb.as<double>(), mrb, sV, s0,
-                d_tau.as<double>(), WB);
+                d_tau.as<double>(), WB, m);
             {
                 const cudaError_t e = cudaGetLastError();
                 if (e != cudaSuccess) {
@@ -1005,33 +1008,36 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
                 after_launch("qr_trailing_tma_kernel");
             }
         }
-        // T of the wide panel from the Gram matrix of its reflectors
+        // ONE launch for [G | Y] = V^T [V | C_M | W]: the Gram matrix of the
+        // reflectors (for T) and V^T of the trailing columns of M and of the
+        // right-hand sides -- three segments of the N index, all with the
+        // leading dimension m (V is stored with ld m)
         double* Vb = d_Vb.as<double>();
-        dgemm_nt_batched(ctx, GemmNT{Vb, mrb, sV, Vb, mrb, sV, d_G.as<double>(), w, sG, w, w, mrb, 1.0, 0.0}, nb);
-        qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(d_G.as<double>(), d_tau.as<double>(), WB, d_Tb.as<double>(), w,
-                                                    sG);
-        after_launch("qr_wide_t_kernel");
-        // C -= V (T^T (V^T C)) on the trailing columns of M and on W, ONE
-        // launch per product: the N index runs over M's trailing columns,
-        // then (second segment) the k right-hand sides
         const int nM = n - jb - w, ncols = nM + k;
         double* CM = M + jb + size_t(jb + w) * m;
         double* CW = W + jb;
-        transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
-            Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV);
-        after_launch("transpose_panel_kernel");
-        double* Y = d_Y.as<double>();
+        double* Y = d_Y.as<double>();  // w x (w + ncols): G, then Y
         double* Z = d_Z.as<double>();
-        GemmNT gy{Vb, mrb, sV, nM > 0 ? CM : CW, m, nM > 0 ? sM : sW, Y, w, sY, w, ncols, mrb, 1.0, 0.0};
+        GemmNT gy{Vb, m, sV, Vb, m, sV, Y, w, sY, w, w + ncols, mrb, 1.0, 0.0};
+        gy.B2 = nM > 0 ? CM : CW;
+        gy.sB2 = nM > 0 ? sM : sW;
+        gy.nsplit = w;
         if (nM > 0) {
-            gy.B2 = CW;
-            gy.sB2 = sW;
-            gy.nsplit = nM;
+            gy.B3 = CW;
+            gy.sB3 = sW;
+            gy.nsplit2 = w + nM;
         }
-        dgemm_nt_batched(ctx, gy, nb);  // Y = V^T C   (w x ncols, k = mrb)
-        dgemm_nt_batched(ctx, GemmNT{d_Tb.as<double>(), w, sG, Y, w, sY, Z, w, sY, w, ncols, w, 1.0, 0.0},
+        dgemm_nt_batched(ctx, gy, nb);
+        qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(Y, sY, d_tau.as<double>(), WB, d_Tb.as<double>(), w, sG);
+        after_launch("qr_wide_t_kernel");
+        transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
+            Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV, m);
+        after_launch("transpose_panel_kernel");
+        // C -= V (T^T Y) on the trailing columns of M and on W (two segments)
+        dgemm_nt_batched(ctx, GemmNT{d_Tb.as<double>(), w, sG, Y + size_t(w) * w, w, sY, Z, w, sZ, w, ncols, w, 1.0,
+                                     0.0},
                          nb);  // Z = T^T Y
-        GemmNT gu{d_VbT.as<double>(), WB, sV, Z, w, sY, nM > 0 ? CM : CW, m, nM > 0 ? sM : sW, mrb, ncols, w,
+        GemmNT gu{d_VbT.as<double>(), WB, sV, Z, w, sZ, nM > 0 ? CM : CW, m, nM > 0 ? sM : sW, mrb, ncols, w,
                   -1.0, 1.0};
         if (nM > 0) {
             gu.D2 = CW;
