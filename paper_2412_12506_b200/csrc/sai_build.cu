@@ -304,6 +304,16 @@ void qr_init(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d_woff,
     after_launch("qr_tol_kernel");
 }
 
+/// Factor the NB-column sub-panel M[j0:, j0:j0+nb] of every problem (one
+/// CTA per problem, the sub-panel in shared memory): dgeqr2 column by column,
+/// write R (rows <= the diagonal) to M, the reflectors with explicit unit
+/// heads and zeros above to Vg (and, for the compact-WY path, into the wide
+/// panel Vbig with its taus) and T of H_0..H_{nb-1} = I - V T V^T to Tg.
+/// Every thread owns the rows r = tid (mod NT) of every column, so the only
+/// cross-thread traffic of a column step is two block reductions: the norm of
+/// the column (computed while the previous column's update ran) and, in ONE
+/// pass that also scales the column, its dots with all later columns; T comes
+/// from a single Gram pass at the end (T(0:i, i) = -tau_i T(0:i,0:i) G(0:i, i)).
 template <int NT, int NB>
 __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, const int64_t* __restrict__ moff,
                                                       const int* __restrict__ ni, const int* __restrict__ nj, int bs,
@@ -314,8 +324,10 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
                                                       double* __restrict__ taus = nullptr, int taustride = 0,
                                                       int ldv = 0) {
     extern __shared__ __align__(16) double Vp[];  // mr x NB panel, column-major (row j0 stored at 0)
-    __shared__ double red[NT / 32];
-    __shared__ double sT[NB * NB], stau[NB], sh_beta;
+    constexpr int NW = NT / 32, NG = NB * (NB - 1) / 2;
+    __shared__ double sred[2][NW][NB + 1];  // per-warp partials: dots at [c], the column norm at [NB]
+    __shared__ double sgram[NW][NG > 0 ? NG : 1];
+    __shared__ double salpha[2], stau[NB], sT[NB * NB];
     const int p = blockIdx.x;
     const int m = ni[p] * bs, n = nj[p] * bs;
     if (j0 >= n) return;
@@ -324,87 +336,147 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
     const int nb = min(NB, n - j0), mr = m - j0;
     const double tol = tolv[p];
     int def = 0;
-    for (int t = tid; t < mr * nb; t += NT) {
-        const int c = t / mr, r = t - c * mr;
-        Vp[size_t(c) * mr + r] = M[size_t(j0 + c) * m + j0 + r];
-    }
-    __syncthreads();
+    for (int c = 0; c < nb; ++c)
+        for (int r = tid; r < mr; r += NT) Vp[c * mr + r] = M[int64_t(j0 + c) * m + j0 + r];
+    // the norm of column 0 below its diagonal (own rows), alpha of column 0
+    double nrm = 0.0;
+    for (int r = tid; r < mr; r += NT)
+        if (r > 0) nrm = fma(Vp[r], Vp[r], nrm);
+    if (tid == 0) salpha[0] = Vp[0];
     for (int jj = 0; jj < nb; ++jj) {
-        double* cj = Vp + size_t(jj) * mr;
+        const int buf = jj & 1;
+        double* cj = Vp + jj * mr;
+        for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+        if (lane == 0) sred[buf][warp][NB] = nrm;
+        __syncthreads();  // (A) norm partials and alpha
         double s = 0.0;
-        for (int i = jj + 1 + tid; i < mr; i += NT) s += cj[i] * cj[i];
-        s = block_sum<NT>(s, red);
-        const double alpha = cj[jj];
-        double tau = 0.0, beta = alpha;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += sred[buf][w][NB];
+        const double alpha = salpha[buf];
+        double tau = 0.0, beta = alpha, scal = 1.0;
         if (s != 0.0) {
-            const double nrm = sqrt(alpha * alpha + s);
-            beta = alpha >= 0.0 ? -nrm : nrm;
+            const double nr = sqrt(alpha * alpha + s);
+            beta = alpha >= 0.0 ? -nr : nr;
             tau = (beta - alpha) / beta;
-            const double scal = 1.0 / (alpha - beta);
-            for (int i = jj + 1 + tid; i < mr; i += NT) cj[i] *= scal;
+            scal = 1.0 / (alpha - beta);
         }
-        __syncthreads();
-        if (tid == 0) {
-            cj[jj] = 1.0;  // implicit unit head of v; R_jj goes straight to M
-            stau[jj] = tau;
-            sh_beta = beta;
-        }
-        __syncthreads();
-        const double bj = sh_beta;
-        if (!(fabs(bj) > tol)) def = 1;
-        for (int c = jj + 1 + warp; c < nb; c += NT / 32) {
-            double* ct = Vp + size_t(c) * mr;
-            double w = 0.0;
-            for (int i = jj + lane; i < mr; i += 32) w += cj[i] * ct[i];
-            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-            w *= tau;
-            for (int i = jj + lane; i < mr; i += 32) ct[i] -= w * cj[i];
-        }
-        __syncthreads();
-        if (tid == 0) M[size_t(j0 + jj) * m + j0 + jj] = bj;
-        for (int i = tid; i < jj; i += NT) M[size_t(j0 + jj) * m + j0 + i] = Vp[size_t(jj) * mr + i];
-    }
-    __syncthreads();
-    // T of H_0 ... H_{nb-1} = I - V T V^T (upper triangular)
-    for (int t = tid; t < NB * NB; t += NT) sT[t] = 0.0;
-    __syncthreads();
-    if (tid < nb) sT[tid * NB + tid] = stau[tid];
-    __syncthreads();
-    for (int i = 1; i < nb; ++i) {
-        for (int c = warp; c < i; c += NT / 32) {  // z_c = v_c^T v_i over rows >= i
-            double w = 0.0;
-            for (int r = i + lane; r < mr; r += 32) w += Vp[size_t(c) * mr + r] * Vp[size_t(i) * mr + r];
-            for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-            if (lane == 0) sT[c * NB + i] = w;
-        }
-        __syncthreads();
-        if (tid == 0) {  // T(0:i, i) = -tau_i T(0:i,0:i) z
-            double tmp[NB];
-            for (int a = 0; a < i; ++a) {
-                double s = 0.0;
-                for (int b2 = a; b2 < i; ++b2) s += sT[a * NB + b2] * sT[b2 * NB + i];
-                tmp[a] = -stau[i] * s;
+        if (!(fabs(beta) > tol)) def = 1;
+        // scale the column (unit head at jj) and, in the same pass, the dots
+        // of v with every later column over rows >= jj
+        double dots[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) dots[c] = 0.0;
+        for (int r = tid; r < mr; r += NT) {
+            if (r < jj) continue;
+            double v = 1.0;
+            if (r > jj) {
+                v = s != 0.0 ? cj[r] * scal : cj[r];
+                cj[r] = v;
+            } else {
+                cj[r] = 1.0;
             }
-            for (int a = 0; a < i; ++a) sT[a * NB + i] = tmp[a];
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c > jj && c < nb) dots[c] = fma(v, Vp[c * mr + r], dots[c]);
         }
-        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < NB; ++c)
+            if (c > jj && c < nb) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dots[c] += __shfl_xor_sync(0xffffffffu, dots[c], o);
+                if (lane == 0) sred[buf][warp][c] = dots[c];
+            }
+        if (tid == 0) {
+            stau[jj] = tau;
+            M[int64_t(j0 + jj) * m + j0 + jj] = beta;
+        }
+        __syncthreads();  // (B) dot partials
+        double Wc[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+            Wc[c] = 0.0;
+            if (c > jj && c < nb) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) Wc[c] += sred[buf][w][c];
+                Wc[c] *= tau;
+            }
+        }
+        // apply H_jj to the later columns; the next column's norm and alpha
+        nrm = 0.0;
+        for (int r = tid; r < mr; r += NT) {
+            if (r < jj) {
+                // R entries of column jj are final
+                M[int64_t(j0 + jj) * m + j0 + r] = cj[r];
+                continue;
+            }
+            const double v = cj[r];
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c > jj && c < nb) Vp[c * mr + r] -= Wc[c] * v;
+            if (jj + 1 < nb) {
+                const double x = Vp[(jj + 1) * mr + r];
+                if (r > jj + 1) nrm = fma(x, x, nrm);
+                if (r == jj + 1) salpha[buf ^ 1] = x;
+            }
+        }
     }
+    __syncthreads();
+    // T from the Gram matrix of the reflectors (unit heads, zeros above)
+    if constexpr (NG > 0) {
+        double g[NG];
+#pragma unroll
+        for (int q = 0; q < NG; ++q) g[q] = 0.0;
+        for (int r = tid; r < mr; r += NT) {
+            double v[NB];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) v[c] = (c < nb && r >= c) ? Vp[c * mr + r] : 0.0;
+            int q = 0;
+#pragma unroll
+            for (int a2 = 0; a2 < NB; ++a2)
+#pragma unroll
+                for (int b2 = a2 + 1; b2 < NB; ++b2) g[q] = fma(v[a2], v[b2], g[q]), ++q;
+        }
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) g[q] += __shfl_xor_sync(0xffffffffu, g[q], o);
+            if (lane == 0) sgram[warp][q] = g[q];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int t = 0; t < NB * NB; ++t) sT[t] = 0.0;
+        for (int i = 0; i < nb; ++i) {
+            double z[NB];
+            for (int c = 0; c < i; ++c) {  // G(c, i), c < i: index of pair (c, i)
+                const int q = c * NB - c * (c + 1) / 2 + (i - c - 1);
+                double gs = 0.0;
+                for (int w = 0; w < NW; ++w) gs += sgram[w][q];
+                z[c] = gs;
+            }
+            for (int a2 = 0; a2 < i; ++a2) {  // T(0:i, i) = -tau_i T(0:i, 0:i) z
+                double acc = 0.0;
+                for (int b2 = a2; b2 < i; ++b2) acc += sT[a2 * NB + b2] * z[b2];
+                sT[a2 * NB + i] = -stau[i] * acc;
+            }
+            sT[i * NB + i] = stau[i];
+        }
+    }
+    __syncthreads();
     // V with explicit zeros above the unit heads (padded to NB columns)
     double* V = Vg + voff[p];
-    for (int t = tid; t < mr * NB; t += NT) {
-        const int c = t / mr, r = t - c * mr;
-        V[t] = (c < nb && r >= c) ? Vp[size_t(c) * mr + r] : 0.0;
-    }
+    for (int c = 0; c < NB; ++c)
+        for (int r = tid; r < mr; r += NT) V[int64_t(c) * mr + r] = (c < nb && r >= c) ? Vp[c * mr + r] : 0.0;
     for (int t = tid; t < NB * NB; t += NT) Tg[size_t(p) * NB * NB + t] = sT[t];
     if (Vbig) {  // also into the wide panel (ldbig rows, leading dimension ldv): columns bigcol.., rows
                  // shifted by bigcol (zeros above)
         if (!ldv) ldv = ldbig;
         double* VB = Vbig + size_t(p) * bigstride + size_t(bigcol) * ldv;
-        for (int t = tid; t < ldbig * nb; t += NT) {
-            const int c = t / ldbig, r = t - c * ldbig;
-            const int rr = r - bigcol;  // row within this panel
-            VB[size_t(c) * ldv + r] = (rr >= c && rr < mr) ? Vp[size_t(c) * mr + rr] : 0.0;
-        }
+        for (int c = 0; c < nb; ++c)
+            for (int r = tid; r < ldbig; r += NT) {
+                const int rr = r - bigcol;  // row within this panel
+                VB[size_t(c) * ldv + r] = (rr >= c && rr < mr) ? Vp[c * mr + rr] : 0.0;
+            }
         for (int t = tid; t < nb; t += NT) taus[size_t(p) * taustride + bigcol + t] = stau[t];
     }
     if (def && tid == 0) deficient[p] = 1;
