@@ -26,6 +26,7 @@
 #include <exception>
 #include <map>
 #include <memory>
+#include <string>
 #include <thread>
 #include <unordered_map>
 #include <vector>
@@ -1567,6 +1568,19 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], ev_ready, 0));
         }
         stamp("QR slot workspaces");
+        // the batches' stream-ordered temporaries stay in the device's default
+        // pool until the end of the QR (a release at every synchronisation
+        // would unmap and remap them), then go back in one trim
+        cudaMemPool_t pool = nullptr;
+        uint64_t pool_thr_old = 0;
+        {
+            int dev = 0;
+            LDGMG_CUDA(cudaGetDevice(&dev));
+            LDGMG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+            LDGMG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &pool_thr_old));
+            uint64_t keep = UINT64_MAX;
+            LDGMG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
         // LDGMG_SAI_TIMING: per-batch start / end on the device clock
         std::vector<cudaEvent_t> tev;
         if (timing) {
@@ -1575,7 +1589,9 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             LDGMG_CUDA(cudaEventRecord(tev[0], ctx.stream));
             for (int sl = 0; sl < nslots; ++sl) LDGMG_CUDA(cudaStreamWaitEvent(slot_s[sl], tev[0], 0));
         }
+        std::vector<double> slot_host_s(nslots, 0.0);
         auto run_slot = [&](int sl) {
+            const auto h0 = std::chrono::steady_clock::now();
             int dev = 0;
             LDGMG_CUDA(cudaGetDevice(&dev));
             Ctx bctx = ctx;
@@ -1620,6 +1636,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 if (timing) LDGMG_CUDA(cudaEventRecord(tev[2 + 2 * bi], bctx.stream));
             }
             (void)dev;
+            slot_host_s[sl] = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         };
         {
             std::vector<std::exception_ptr> errs(nslots);
@@ -1636,10 +1653,20 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                     }
                 });
             for (auto& t : th) t.join();
+            if (timing)
+                fprintf(stderr, "[sai] host enqueue per slot (s):%s\n", [&] {
+                    std::string o;
+                    for (double v : slot_host_s) o += " " + std::to_string(v).substr(0, 5);
+                    return o;
+                }().c_str());
             for (auto& e : errs)
                 if (e) std::rethrow_exception(e);
         }
         for (cudaStream_t st : slot_s) LDGMG_CUDA(cudaStreamSynchronize(st));
+        stamp("QR least squares (device work)");
+        LDGMG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &pool_thr_old));
+        LDGMG_CUDA(cudaMemPoolTrimTo(pool, 0));
+        stamp("QR temporaries released");
         if (timing) {
             for (size_t bi = 0; bi < batches.size(); ++bi) {
                 float t0 = 0.f, t1 = 0.f;
@@ -1651,7 +1678,6 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             }
             for (auto e : tev) cudaEventDestroy(e);
         }
-        stamp("QR least squares (all batches)");
         // rank-deficient problems: minimum-norm refit from a fresh copy of M
         // (on the context stream, slot 0's workspace)
         for (size_t bi = 0; bi < batches.size(); ++bi) {
