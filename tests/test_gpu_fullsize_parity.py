@@ -181,3 +181,34 @@ def test_c5_bottom_pinv_matches_oracle_sym_eig(ctx, ref):
     bar = 64 * np.finfo(float).eps * kappa
     rel = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert rel <= bar, (rel, kappa, bar)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3-ball-GS", "C3-ball-SAI", "C4"])
+def test_fullsize_dropin_bitwise(ctx, ref, name):
+    """The BASELINE configs at their STATED sizes on the drop-in route (the
+    reference's own level operators, diagonal factors / SAI matrices,
+    transfers and bottom eigenpairs uploaded, strict order): two V-cycles and
+    `apply` bit-identical to the reference's (multigrid.hpp:82-101) on the
+    benchmark right-hand side -- C1 64^2 Jacobi, C3 256^2 (ball interface,
+    extension A2) with 4-colour GS and with SAI1, C4 128^2 Stokes SAI1.  (C2 at
+    32^3: test_gpu_fullsize.py; C5's physics at 8^3: above.)"""
+    from tests.test_gpu_vcycle import dropin_mg
+    spec, cfg, normal, _ = K.fullsize_configs()[name]
+    R = ref.RefMultigrid(spec, cfg)
+    n, bs, _ = R.shape(0)
+    mg = dropin_mg(ctx, R, cfg)
+    mg.set_strict_order(True)
+    b = K.baseline_rhs(n, bs, spec.kind, R.dim, R.bs_scalar, R.kernel_constants, R.kernel_pressure, normal=normal,
+                       random_rhs=ref.random_rhs)
+    x = np.zeros(n * bs)
+    xd = torch.as_tensor(x).cuda()
+    bd = torch.as_tensor(b).cuda()
+    for _ in range(2):
+        mg.cycle(xd, bd)
+        x = R.cycle(x, b)
+        torch.cuda.synchronize()
+        assert np.array_equal(xd.cpu().numpy().view(np.int64), x.view(np.int64)), name
+    yd = torch.empty_like(bd)
+    mg.apply(bd, yd)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy().view(np.int64), R.apply(b).view(np.int64)), name
