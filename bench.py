@@ -251,7 +251,7 @@ def run_reference(args):
     value, info = cpu_reference(name, args.cpu_n, max(1, args.steps), args.warmup)
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cpu_sample": info["sample"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
@@ -576,7 +576,7 @@ def main():
         line = {
             "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": cfgd,
             "roofline": r["roofline"],
             "vcycle_hbm_GBps": r["vcycle_hbm_GBps"],
