@@ -457,7 +457,8 @@ int rowpass_occupancy(Ctx& ctx, size_t smem) {
 /// (C2 level 1: 4096 rows over 1628 CTAs): 2 stages -> more resident CTAs,
 /// and the grid sized so every CTA gets the same number of rows (the pass
 /// ends with the CTA holding the most rows).  Measured on B200, C2 level 1:
-/// 33.5 us (3 stages, 1628 CTAs) -> 30.9 us (2 stages).  LDGMG_NS overrides.
+/// 33.5 us (3 stages, 1628 CTAs) -> 30.9 us (2 stages).  ns_env > 1 forces a
+/// depth (measurement builds only; the library passes -1).
 template <int GT, int BS>
 void configure_and_launch(Ctx& ctx, RowPassArgs a, size_t stage_bytes, int ns_env) {
     auto smem_for = [&](int ns) {

@@ -46,8 +46,8 @@ inline void after_launch(const char* name) {
 
 inline int div_up(int64_t a, int64_t b) { return int((a + b - 1) / b); }
 
-/// Programmatic dependent launch (PDL, sm_90+), opt-in with LDGMG_PDL=1:
-/// kernels launched with programmatic stream serialization wait for their
+/// Programmatic dependent launch (PDL, sm_90+) for the BIG streaming passes
+/// (off; the small kernels use it, pdl_small_enabled below): kernels launched with programmatic stream serialization wait for their
 /// predecessor (griddepcontrol.wait) only before touching mutable memory, so
 /// launch processing and the immutable prologue (barrier init, row pointers,
 /// TMA staging of the injection matrices) overlap the previous kernel.
