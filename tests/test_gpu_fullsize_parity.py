@@ -48,7 +48,10 @@ BARS = {  # measured (profiles/r02/fullsize_parity.jsonl) -> bar
     "C1": dict(hist=1e-12, x=1e-10, eta=1e-12),            # 4.9e-15, 3.5e-14, 2.3e-14
     "C2": dict(hist=1e-12, x=1e-10, eta=1e-12),            # 7.3e-16, 5.6e-15, 1.7e-14
     "C3-box-GS": dict(hist=3e-9, x=1.5e-8, eta=2e-10),     # 9.2e-10, 4.1e-9, 5.1e-11
-    "C3-box-SAI": dict(hist=1e-9, x=5e-10, eta=5e-9),      # 3.3e-10, 1.3e-10, 1.7e-9
+    # x: 1.3e-10 with round 2a's QR panel, 3.0e-9 with round 2b's -- the two
+    # SAI builds differ from LAPACK's by the same 7e-15 (test_gpu_sai), the 1e4
+    # contrast amplifies it: the same bar as the GS smoother's factors get
+    "C3-box-SAI": dict(hist=1e-9, x=1.5e-8, eta=5e-9),     # 3.1e-10, 3.0e-9, 1.7e-9
     "C3-ball-GS": dict(hist_rel=1e-10),                    # 2.6e-12 (x 9.6e-13)
     "C3-ball-SAI": dict(hist_rel=1e-10),                   # 1.3e-12 (x 1.5e-12)
     "C4": dict(hist_rel=1e-10),                            # 4.4e-13 (x 1.4e-13)
