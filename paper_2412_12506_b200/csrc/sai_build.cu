@@ -702,22 +702,29 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
 /// T(0:i,i) = -tau_i T(0:i,0:i) G(0:i,i).  One CTA per problem, column-major.
 __global__ void qr_wide_t_kernel(const double* __restrict__ G, int64_t gstride, const double* __restrict__ taus,
                                  int taustride, double* __restrict__ T, int w, int64_t mstride) {
+    extern __shared__ double sgt[];  // G then T, w x w each, column-major (ld w)
+    double* sG = sgt;
+    double* sT = sgt + w * w;
     const int p = blockIdx.x;
     const double* Gp = G + size_t(p) * gstride;  // w x w, ld w, problem stride gstride
     const double* tp = taus + size_t(p) * taustride;
     double* Tp = T + size_t(p) * mstride;
-    for (int t = threadIdx.x; t < w * w; t += blockDim.x) Tp[t] = 0.0;
+    for (int t = threadIdx.x; t < w * w; t += blockDim.x) {
+        sG[t] = Gp[t];
+        sT[t] = 0.0;
+    }
     __syncthreads();
     for (int i = 0; i < w; ++i) {
         const double ti = tp[i];
         for (int a = threadIdx.x; a < i; a += blockDim.x) {
             double s = 0.0;
-            for (int b = a; b < i; ++b) s += Tp[size_t(b) * w + a] * Gp[size_t(i) * w + b];
-            Tp[size_t(i) * w + a] = -ti * s;
+            for (int b = a; b < i; ++b) s += sT[b * w + a] * sG[i * w + b];
+            sT[i * w + a] = -ti * s;
         }
-        if (threadIdx.x == 0) Tp[size_t(i) * w + i] = ti;
+        if (threadIdx.x == 0) sT[i * w + i] = ti;
         __syncthreads();
     }
+    for (int t = threadIdx.x; t < w * w; t += blockDim.x) Tp[t] = sT[t];
 }
 
 /// Row-major copy of the wide panel's reflectors (VT(r, c) at r * ldt + c
@@ -1101,7 +1108,9 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
             gy.nsplit2 = w + nM;
         }
         dgemm_nt_batched(ctx, gy, nb);
-        qr_wide_t_kernel<<<nb, 64, 0, ctx.stream>>>(Y, sY, d_tau.as<double>(), WB, d_Tb.as<double>(), w, sG);
+        ensure_dyn_smem(qr_wide_t_kernel, sizeof(double) * 2 * w * w);
+        qr_wide_t_kernel<<<nb, 64, sizeof(double) * 2 * w * w, ctx.stream>>>(Y, sY, d_tau.as<double>(), WB,
+                                                                             d_Tb.as<double>(), w, sG);
         after_launch("qr_wide_t_kernel");
         transpose_panel_kernel<<<dim3(div_up(mrb, 32), div_up(WB, 32), nb), 256, 0, ctx.stream>>>(
             Vb, sV, mrb, w, d_VbT.as<double>(), WB, sV, m);
