@@ -1568,6 +1568,20 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         std::vector<DevBuf> slot_M(nslots), slot_W(nslots);
         std::vector<cudaStream_t> slot_s(nslots, nullptr);
         cudaEvent_t ev_ready = nullptr;
+        // streams and the event go away on every exit path (an error in one
+        // slot leaves the others' work queued: drain before destroying)
+        struct SlotGuard {
+            std::vector<cudaStream_t>& s;
+            cudaEvent_t& e;
+            ~SlotGuard() {
+                for (cudaStream_t st : s)
+                    if (st) {
+                        cudaStreamSynchronize(st);
+                        cudaStreamDestroy(st);
+                    }
+                if (e) cudaEventDestroy(e);
+            }
+        } slot_guard{slot_s, ev_ready};
         LDGMG_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
         LDGMG_CUDA(cudaEventRecord(ev_ready, ctx.stream));  // d_At, d_X, the index arrays are ready
         for (int sl = 0; sl < nslots; ++sl) {
@@ -1580,15 +1594,26 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         // the batches' stream-ordered temporaries stay in the device's default
         // pool until the end of the QR (a release at every synchronisation
         // would unmap and remap them), then go back in one trim
-        cudaMemPool_t pool = nullptr;
-        uint64_t pool_thr_old = 0;
+        struct PoolKeep {  // restores the threshold and trims on every exit path
+            cudaMemPool_t pool = nullptr;
+            uint64_t old = 0;
+            bool active = false;
+            void release() {
+                if (!active) return;
+                active = false;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
+                cudaMemPoolTrimTo(pool, 0);
+            }
+            ~PoolKeep() { release(); }
+        } pool_keep;
         {
             int dev = 0;
             LDGMG_CUDA(cudaGetDevice(&dev));
-            LDGMG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-            LDGMG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &pool_thr_old));
+            LDGMG_CUDA(cudaDeviceGetDefaultMemPool(&pool_keep.pool, dev));
+            LDGMG_CUDA(cudaMemPoolGetAttribute(pool_keep.pool, cudaMemPoolAttrReleaseThreshold, &pool_keep.old));
             uint64_t keep = UINT64_MAX;
-            LDGMG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            LDGMG_CUDA(cudaMemPoolSetAttribute(pool_keep.pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            pool_keep.active = true;
         }
         // LDGMG_SAI_TIMING: per-batch start / end on the device clock
         std::vector<cudaEvent_t> tev;
@@ -1673,8 +1698,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         }
         for (cudaStream_t st : slot_s) LDGMG_CUDA(cudaStreamSynchronize(st));
         stamp("QR least squares (device work)");
-        LDGMG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &pool_thr_old));
-        LDGMG_CUDA(cudaMemPoolTrimTo(pool, 0));
+        pool_keep.release();
         stamp("QR temporaries released");
         if (timing) {
             for (size_t bi = 0; bi < batches.size(); ++bi) {
@@ -1740,12 +1764,7 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             }
             for (int i = 0; i < nb; ++i) deficient[bord[p0 + i]] = def[i];
         }
-        states.clear();  // stream-ordered frees on the batch streams
-        for (cudaStream_t st : slot_s) {
-            cudaStreamSynchronize(st);
-            cudaStreamDestroy(st);
-        }
-        cudaEventDestroy(ev_ready);
+        states.clear();  // stream-ordered frees on the batch streams (streams: slot_guard)
     }
 
     // cache inserts (device copies of the fresh solutions), one slab per build
