@@ -465,9 +465,11 @@ __global__ void __launch_bounds__(NT) qr_panel_kernel(double* __restrict__ Ms, c
     }
     __syncthreads();
     // V with explicit zeros above the unit heads (padded to NB columns)
-    double* V = Vg + voff[p];
-    for (int c = 0; c < NB; ++c)
-        for (int r = tid; r < mr; r += NT) V[int64_t(c) * mr + r] = (c < nb && r >= c) ? Vp[c * mr + r] : 0.0;
+    if (Vg) {  // (the compact-WY path reads the reflectors from Vbig instead)
+        double* V = Vg + voff[p];
+        for (int c = 0; c < NB; ++c)
+            for (int r = tid; r < mr; r += NT) V[int64_t(c) * mr + r] = (c < nb && r >= c) ? Vp[c * mr + r] : 0.0;
+    }
     for (int t = tid; t < NB * NB; t += NT) Tg[size_t(p) * NB * NB + t] = sT[t];
     if (Vbig) {  // also into the wide panel (ldbig rows, leading dimension ldv): columns bigcol.., rows
                  // shifted by bigcol (zeros above)
@@ -575,7 +577,10 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
                                                               const int* __restrict__ ni, const int* __restrict__ nj,
                                                               int bs, int j0, const double* __restrict__ Vg,
                                                               const int64_t* __restrict__ voff,
-                                                              const double* __restrict__ Tg, int col_limit = -1) {
+                                                              const double* __restrict__ Tg, int col_limit = -1,
+                                                              int64_t vstride = 0, int vld = 0) {
+    // reflectors: Vg + voff[p] with leading dimension mr, or (vld > 0) the
+    // wide panel's block read in place at Vg + p * vstride, leading dimension vld
     extern __shared__ __align__(16) double sC[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ double sy[8][CPW * NB];
@@ -613,7 +618,8 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
             bulk_g2s(sC + size_t(c) * ld, colp[c] - off[c], uint32_t(((off[c] + mr + 1) & ~1) * sizeof(double)),
                      &bar);
     }
-    const double* V = Vg + voff[p];
+    const double* V = vld > 0 ? Vg + int64_t(p) * vstride : Vg + voff[p];
+    const int64_t vl = vld > 0 ? vld : mr;
     mbar_wait(&bar, 0);
     double y[CPW][NB];
 #pragma unroll
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
 #pragma unroll
             for (int a = 0; a < NB; ++a) {
                 const int r = r0 + u * 256;
-                v[u][a] = r < mr ? __ldg(V + size_t(a) * mr + r) : 0.0;
+                v[u][a] = r < mr ? __ldg(V + size_t(a) * vl + r) : 0.0;
             }
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
@@ -679,7 +685,7 @@ __global__ void __launch_bounds__(256) qr_trailing_tma_kernel(double* __restrict
 #pragma unroll
             for (int a = 0; a < NB; ++a) {
                 const int r = r0 + u * 256;
-                v[u][a] = r < mr ? __ldg(V + size_t(a) * mr + r) : 0.0;
+                v[u][a] = r < mr ? __ldg(V + size_t(a) * vl + r) : 0.0;
             }
 #pragma unroll
         for (int u = 0; u < RU; ++u) {
@@ -1006,7 +1012,7 @@ void qr_blocked_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf
             const dim3 g(div_up(ncols, tcpw), nb);
             tma_kernel<<<g, 256, tsmem, ctx.stream>>>(
                 d_M.as<double>(), d_moff.as<int64_t>(), d_W.as<double>(), d_woff.as<int64_t>(), d_ni.as<int>(),
-                d_nj.as<int>(), bs, j0, d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), -1);
+                d_nj.as<int>(), bs, j0, d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), -1, int64_t(0), 0);
         } else {
             const dim3 g(div_up(ncols, 8 * CPW), nb);
             qr_trailing_kernel<NB, CPW><<<g, 256, 0, ctx.stream>>>(d_M.as<double>(), d_moff.as<int64_t>(),
@@ -1042,8 +1048,7 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
     constexpr int WB = 64, TCPW = 4;
     const int k = bs;
     // d_voff (uploaded by the caller): voff[i] = i * m * NB
-    DevBuf d_V(sizeof(double) * std::max<int64_t>(1, int64_t(nb) * m * NB)),
-        d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
+    DevBuf d_T(sizeof(double) * size_t(nb) * NB * NB), d_tol(sizeof(double) * nb),
         d_Vb(sizeof(double) * size_t(nb) * m * WB), d_Tb(sizeof(double) * size_t(nb) * WB * WB),
         d_tau(sizeof(double) * size_t(nb) * WB), d_Y(sizeof(double) * size_t(nb) * WB * (WB + n + k)),
         d_Z(sizeof(double) * size_t(nb) * WB * (n + k)), d_VbT(sizeof(double) * size_t(nb) * m * WB);
@@ -1064,7 +1069,7 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
         for (int s0 = 0; s0 < w; s0 += NB) {
             const int j0 = jb + s0;
             qr_panel_kernel<256, NB><<<nb, 256, psmem, ctx.stream>>>(
-                M, d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(), d_V.as<double>(),
+                M, d_moff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0, d_tol.as<double>(), nullptr,
                 d_voff.as<int64_t>(), d_T.as<double>(), d_def.as<int>(), d_Vb.as<double>(), mrb, sV, s0,
                 d_tau.as<double>(), WB, m);
             {
@@ -1082,9 +1087,10 @@ void qr_gemm_batch(Ctx& ctx, DevBuf& d_M, DevBuf& d_moff, DevBuf& d_W, DevBuf& d
             }
             const int rest = w - s0 - NB;
             if (rest > 0) {
+                // the sub-panel's reflectors in place in the wide block (ld m, rows from j0)
                 qr_trailing_tma_kernel<NB, TCPW><<<dim3(div_up(rest, TCPW), nb), 256, tsmem, ctx.stream>>>(
                     M, d_moff.as<int64_t>(), W, d_woff.as<int64_t>(), d_ni.as<int>(), d_nj.as<int>(), bs, j0,
-                    d_V.as<double>(), d_voff.as<int64_t>(), d_T.as<double>(), rest);
+                    d_Vb.as<double>() + size_t(s0) * m + s0, d_voff.as<int64_t>(), d_T.as<double>(), rest, sV, m);
                 after_launch("qr_trailing_tma_kernel");
             }
         }
