@@ -1498,7 +1498,10 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             // ones (n < 128): in-kernel blocked updates; panels too tall for
             // shared memory: the one-CTA-per-problem unblocked kernel
             const size_t smem8 = sizeof(double) * size_t(st.max_m) * 8, smem4 = sizeof(double) * size_t(st.max_m) * 4;
-            st.path = smem8 <= 200 * 1024 && st.max_n >= 128   ? 0
+            // (8-column panels only while they stay <= 100 KB of shared memory:
+            // a 4-column panel of a tall problem leaves room on its SM for a
+            // GEMM CTA of another batch -- C5 16^3 QR 0.320 -> 0.311 s median)
+            st.path = smem8 <= 100 * 1024 && st.max_n >= 128   ? 0
                       : smem4 <= 200 * 1024 && st.max_n >= 128 ? 1
                       : smem8 <= 200 * 1024                    ? 2
                       : smem4 <= 200 * 1024                    ? 3
