@@ -1635,8 +1635,6 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
         std::vector<double> slot_host_s(nslots, 0.0);
         auto run_slot = [&](int sl) {
             const auto h0 = std::chrono::steady_clock::now();
-            int dev = 0;
-            LDGMG_CUDA(cudaGetDevice(&dev));
             Ctx bctx = ctx;
             bctx.stream = slot_s[sl];
             DevAsyncScope async_scope(bctx.stream);
@@ -1678,7 +1676,6 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
                 }
                 if (timing) LDGMG_CUDA(cudaEventRecord(tev[2 + 2 * bi], bctx.stream));
             }
-            (void)dev;
             slot_host_s[sl] = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         };
         {
@@ -1686,15 +1683,20 @@ SaiResult build_sai_gpu(Ctx& ctx, const Bsr& A, int system_kind, int n_velocity,
             std::vector<std::thread> th;
             int dev = 0;
             LDGMG_CUDA(cudaGetDevice(&dev));
-            for (int sl = 0; sl < nslots; ++sl)
-                th.emplace_back([&, sl] {
-                    try {
-                        LDGMG_CUDA(cudaSetDevice(dev));
-                        run_slot(sl);
-                    } catch (...) {
-                        errs[sl] = std::current_exception();
-                    }
-                });
+            try {
+                for (int sl = 0; sl < nslots; ++sl)
+                    th.emplace_back([&, sl] {
+                        try {
+                            LDGMG_CUDA(cudaSetDevice(dev));
+                            run_slot(sl);
+                        } catch (...) {
+                            errs[sl] = std::current_exception();
+                        }
+                    });
+            } catch (...) {  // a thread could not be started: join the others first
+                for (auto& t : th) t.join();
+                throw;
+            }
             for (auto& t : th) t.join();
             if (timing)
                 fprintf(stderr, "[sai] host enqueue per slot (s):%s\n", [&] {
